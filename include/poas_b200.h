@@ -1,0 +1,223 @@
+/*
+ * poas_b200.h -- C ABI of the B200-native POAS co-executed GEMM.
+ *
+ * The reference (arXiv 2209.10245, /root/reference/proj) is a C++20 library
+ * with no FFI of its own; these entry points are what a foreign caller (or
+ * the reference's own CLI) binds to reach the same
+ * predict -> optimize -> adapt -> schedule -> execute path. Each entry point
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain C types only; no exceptions cross the boundary.
+ *  - Every int-returning function returns POAS_OK (0) or an error code;
+ *    poas_b200_last_error() then holds a thread-local message.
+ *  - Strings returned through char** are malloc'ed by the library and must
+ *    be released with poas_b200_free().
+ *  - Matrices are row-major: A[m x k] (lda), B[k x n] (ldb), C[m x n] (ldc).
+ */
+#ifndef POAS_B200_H
+#define POAS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes: poas::errc (reference proj/include/poas/error.hpp:8-21) in
+ * declaration order, shifted by one so that 0 means success. */
+enum {
+  POAS_OK = 0,
+  POAS_E_INVALID_ARGUMENT = 1,
+  POAS_E_DEGENERATE_SAMPLES = 2,
+  POAS_E_NON_POSITIVE_TIME = 3,
+  POAS_E_BACKEND_FAILURE = 4,
+  POAS_E_PARSE_FAILURE = 5,
+  POAS_E_NOT_ROW_ALIGNED = 6,
+  POAS_E_UNALIGNABLE_K = 7,
+  POAS_E_NO_FEASIBLE_TILING = 8,
+  POAS_E_TOO_MANY_DEVICES = 9,
+  POAS_E_MISSING_DEVICE = 10,
+  POAS_E_NUMERICAL_FAILURE = 11,
+  POAS_E_HASH_MISMATCH = 12,
+  POAS_E_IO_FAILURE = 13,
+  POAS_E_CUDA = 100,    /* CUDA runtime / driver error (message has details) */
+  POAS_E_INTERNAL = 101 /* any other C++ exception */
+};
+
+enum { POAS_DTYPE_F32 = 0, POAS_DTYPE_F16 = 1, POAS_DTYPE_BF16 = 2 };
+
+const char* poas_b200_last_error(void);
+void poas_b200_free(void* p);
+const char* poas_b200_version(void);
+
+/* ------------------------------------------------------------------------
+ * Plan (Optimize -> Adapt -> Schedule). Pure host code, byte-identical to
+ * the reference for the same profile.
+ * --------------------------------------------------------------------- */
+
+/* solve_split -> build_tile_plan -> build_schedule -> format_schedule.
+ * Replaces cmd_plan (proj/tools/poas.cpp:66-83) over solve_split
+ * (proj/include/poas/optimizer.hpp:67), build_tile_plan (adapter.hpp:71-72),
+ * build_schedule (scheduler.hpp:35), format_schedule (scheduler.hpp:45).
+ * `profile_text` is a "poas-profile v1" file body. */
+int poas_b200_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                   char** schedule_json);
+
+/* standalone_schedule (proj/include/poas/scheduler.hpp:40-41). */
+int poas_b200_plan_standalone(const char* profile_text, const char* device_id, int64_t m,
+                              int64_t n, int64_t k, char** schedule_json);
+
+/* The intermediate WorkloadSplit of solve_split (optimizer.hpp:30-35) as
+ * JSON with %.17g doubles: {"makespan","lp_objective","lp_iterations",
+ * "shares":[{"id","rows","ops","fraction","copy_in":[s,e],"compute":[s,e],
+ * "copy_out":[s,e],"finish"}]}. */
+int poas_b200_split(const char* profile_text, int64_t m, int64_t n, int64_t k, char** split_json);
+
+/* oracle_grid_search / _serial (optimizer.hpp:77-80): same JSON as above. */
+int poas_b200_oracle_split(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                           int64_t resolution, int parallel, char** split_json);
+
+/* build_tile_plan (adapter.hpp:71-72) for a given whole-row assignment
+ * (evaluate_rows, optimizer.hpp:62-63) in machine order:
+ * {"devices":[{"id","rows","k_prime","sq","window_fallback","tiles":[[m,k,n],...]}]} */
+int poas_b200_tile_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                        const int64_t* rows, size_t count, char** plan_json);
+
+/* parse_schedule -> format_schedule (scheduler.hpp:45-46): canonical bytes,
+ * or an error for a malformed schedule. */
+int poas_b200_schedule_roundtrip(const char* schedule_json, char** canonical_json);
+
+/* parse_profile -> format_profile (profiler.hpp:71-72). */
+int poas_b200_profile_roundtrip(const char* profile_text, char** canonical_text);
+
+/* machine_hash (device_model.hpp:135) of a profile, 16 hex chars + NUL. */
+int poas_b200_machine_hash(const char* profile_text, char out[17]);
+
+/* fit_linear (device_model.hpp:77): centred OLS in long double. */
+int poas_b200_fit_linear(const uint64_t* ops, const double* seconds, size_t count,
+                         double* slope, double* intercept);
+
+/* transfer_bytes (device_model.hpp:93) for device `device_id` of a profile. */
+int poas_b200_transfer_bytes(const char* profile_text, const char* device_id, uint64_t ops,
+                             int64_t m, int64_t n, int64_t k, uint64_t* in_bytes,
+                             uint64_t* out_bytes);
+
+/* Dense two-phase Bland simplex (simplex.hpp:25): minimise c.x s.t.
+ * Aeq x = beq, Age x >= bge, x >= 0. Matrices row-major. */
+int poas_b200_simplex(int num_vars, const double* objective, int n_eq, const double* eq_a,
+                      const double* eq_b, int n_ge, const double* ge_a, const double* ge_b,
+                      double* x_out, double* objective_out, long* iterations_out);
+
+/* ------------------------------------------------------------------------
+ * Predict: compute units and the profiler. A unit is one concurrently
+ * running share of the machine: the host CPU cores, the CUDA cores of one
+ * GPU (SIMT fp32 kernel) or its tensor cores (tcgen05 kernel).
+ *
+ * Unit spec strings: "<id>=<kind>[:key=value]*" with kind cpu|gpu|xpu
+ *   cpu : threads=<n>                       (0 = all online cores)
+ *   gpu : dev=<cuda ordinal>, sms=<n>       (SM budget, 0 = all), exclusive=0|1
+ *   xpu : dev=<ordinal>, sms=<n>, dtype=bf16|f16, elem=<bytes on the link>
+ * --------------------------------------------------------------------- */
+typedef struct poas_unit_s* poas_unit_t;
+
+int poas_b200_unit_create(const char* spec, poas_unit_t* out);
+void poas_b200_unit_destroy(poas_unit_t unit);
+/* DeviceBackend::time_gemm (proj/include/poas/backend.hpp:15-17). */
+int poas_b200_time_gemm(poas_unit_t unit, int64_t side, double* seconds);
+/* DeviceBackend::time_transfer (backend.hpp:19-21): pinned host -> device. */
+int poas_b200_time_transfer(poas_unit_t unit, uint64_t bytes, double* seconds);
+/* DeviceBackend::has_transfers (backend.hpp:23). */
+int poas_b200_has_transfers(poas_unit_t unit);
+
+/* profile_machine (proj/include/poas/simulator.hpp:28) over real units:
+ * run_compute_probes + run_bandwidth_probe per unit, fit_machine, and
+ * format_profile. `units` is a ';'-separated list of unit specs;
+ * `profiling` is "probes=..,repetitions=..,cpu_min_side=..,cpu_max_side=..,
+ * accel_min_side=..,accel_max_side=..,bandwidth_payload=.." (any subset;
+ * defaults as ProfilingConfig, profiler.hpp:28-38). `bus` is 1 or 0. */
+int poas_b200_profile_machine(const char* units, const char* profiling, int bus,
+                              char** profile_text);
+
+/* ------------------------------------------------------------------------
+ * Execute: the real replacement of simulate() (simulator.hpp:68-69).
+ * --------------------------------------------------------------------- */
+typedef struct poas_executor_s* poas_executor_t;
+
+typedef struct {
+  int64_t m, n, k;
+  /* Host fp32 operands (pinned memory recommended). Required when
+   * resident == 0 -- every GPU unit then copies its A rows and all of B over
+   * its link, computes, and copies its C rows back, inside execute() -- and
+   * whenever a CPU unit has rows (it computes in place on these). */
+  const float* a_host;
+  int64_t lda_host;
+  const float* b_host;
+  int64_t ldb_host;
+  float* c_host;
+  int64_t ldc_host;
+  /* resident == 1: operands already in HBM of the GPU the units run on.
+   * CUDA-core units read a_dev/b_dev (fp32); tensor units read a16/b16
+   * (bf16 or fp16, row pitch a multiple of 8 elements) when given, else
+   * convert a_dev/b_dev on the device. GPU units write c_dev rows. */
+  const float* a_dev;
+  int64_t lda_dev;
+  const float* b_dev;
+  int64_t ldb_dev;
+  const void* a16_dev;
+  int64_t lda16_dev;
+  const void* b16_dev;
+  int64_t ldb16_dev;
+  float* c_dev;
+  int64_t ldc_dev;
+  int resident;
+} poas_gemm_io;
+
+/* One executor per process per machine description (same unit specs as
+ * the profile that produced the schedule; "bus=0|1" token for the link
+ * topology, default shared). */
+int poas_b200_executor_create(const char* units, poas_executor_t* out);
+void poas_b200_executor_destroy(poas_executor_t ex);
+/* machine_identity_hash over the executor's units (device_model.hpp:130). */
+int poas_b200_executor_hash(poas_executor_t ex, char out[17]);
+
+/* Runs the schedule `repeats` times, every unit's share concurrently (one
+ * CUDA stream per GPU unit, host threads for the CPU unit), each phase
+ * timed on a common clock. report_json (optional) has the shape of the
+ * reference's simulate report (proj/tools/poas.cpp:85-114): per device
+ * copy_in/compute/copy_out/copy/finish {measured, predicted, error_pct},
+ * makespans and RMSE. Rows are contiguous in schedule order. */
+int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_gemm_io* io,
+                      int repeats, char** report_json);
+
+/* ------------------------------------------------------------------------
+ * Raw unit kernels (device pointers, caller's cudaStream_t or NULL).
+ * --------------------------------------------------------------------- */
+int poas_b200_tc_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                      const void* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
+                      int num_ctas, void* stream);
+int poas_b200_simt_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
+                        const float* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
+                        int num_ctas, int exclusive_sm, void* stream);
+/* Host CPU unit (AVX-512/AVX2 + threads), host pointers. */
+int poas_b200_host_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
+                        const float* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
+                        int threads);
+int poas_b200_fill_uniform(int dtype, void* dst, int64_t ld, int64_t rows, int64_t cols,
+                           int64_t row0, int64_t col0, int64_t total_cols, uint64_t seed,
+                           void* stream);
+/* Host twin of the device generator (fp32). */
+int poas_b200_fill_uniform_host(float* dst, int64_t ld, int64_t rows, int64_t cols,
+                                int64_t row0, int64_t col0, int64_t total_cols, uint64_t seed);
+int poas_b200_convert_f32(int dtype, const float* src, int64_t ld_src, void* dst, int64_t ld_dst,
+                          int64_t rows, int64_t cols, void* stream);
+int poas_b200_sm_count(void);
+/* Rng::for_stream(master, name).state (proj/include/poas/rng.hpp:43-50). */
+uint64_t poas_b200_stream_seed(uint64_t master_seed, const char* name);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POAS_B200_H */

@@ -1,0 +1,173 @@
+/*
+ * TEST INFRASTRUCTURE ONLY -- the CPU checker for C = A.B, never on the
+ * product path. Only tests/, bench.py (cpu_baseline and --impl reference)
+ * and __graft_entry__.smoke() may load liboracle.so.
+ *
+ * The reference (arXiv 2209.10245, /root/reference/proj) executes no GEMM:
+ * device time is a synthetic law (proj/src/simulator.cpp:30-34). So the
+ * arithmetic of C has no reference implementation -- C-value parity is
+ * "unpinned by the reference" and these routines restate only:
+ *   - the input generator: the reference's counter-based splitmix64 Rng
+ *     (proj/include/poas/rng.hpp:17-25: state += 0x9e3779b97f4a7c15, two
+ *     xor-shift-multiplies, next_unit = (u64 >> 11) * 2^-53), value 2u-1;
+ *     pinned by the known answer Rng::for_stream(20261017,"A").next_u64()
+ *     = 14442304120711173584 (rng.hpp:43-50, checked in tests);
+ *   - the plan semantics the executor must honour: rows are contiguous in
+ *     schedule order, each unit computes its rows with its own operand
+ *     precision (fp32 for cpu/gpu units, RNE bf16/fp16 for xpu units);
+ *   - a tile-by-tile CPU execution of a plan (split-K over the reference
+ *     tiling, proj/src/adapter.cpp:159-167) used as the timed CPU baseline.
+ * Products are accumulated in double ("fp64 oracle on the same rounded
+ * inputs").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- rng */
+
+static inline uint64_t splitmix_at(uint64_t seed, uint64_t index) {
+  uint64_t z = seed + (index + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t oracle_stream_seed(uint64_t master, const char* name) {
+  uint64_t h = 1469598103934665603ULL; /* the reference's (19-digit) FNV offset */
+  for (const unsigned char* p = (const unsigned char*)name; *p; ++p) {
+    h ^= (uint64_t)*p;
+    h *= 1099511628211ULL;
+  }
+  return master ^ h;
+}
+
+uint64_t oracle_draw(uint64_t seed, uint64_t index) { return splitmix_at(seed, index); }
+
+void oracle_fill_uniform(float* dst, int64_t ld, int64_t rows, int64_t cols, int64_t row0,
+                         int64_t col0, int64_t total_cols, uint64_t seed) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t c = 0; c < cols; ++c) {
+      const uint64_t z = splitmix_at(seed, (uint64_t)((row0 + r) * total_cols + col0 + c));
+      const double u = (double)(z >> 11) * 0x1.0p-53;
+      dst[r * ld + c] = (float)(2.0 * u - 1.0);
+    }
+  }
+}
+
+/* ------------------------------------------------- 16-bit rounding (RNE) */
+
+static inline float bf16_round(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x; /* inf / nan unchanged */
+  const uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7fffu + lsb;
+  u &= 0xffff0000u;
+  float y;
+  memcpy(&y, &u, 4);
+  return y;
+}
+
+/* IEEE binary16 round-to-nearest-even, returned as float. */
+static inline float fp16_round(float x) {
+  if (!isfinite(x)) return x;
+  const float ax = fabsf(x);
+  if (ax >= 65520.0f) return copysignf(INFINITY, x);
+  if (ax < 0x1.0p-25f) return copysignf(0.0f, x);
+  int e;
+  frexpf(ax, &e);               /* ax = f * 2^e, f in [0.5, 1) */
+  int exp_unit = e - 11;        /* 11 significant bits */
+  if (exp_unit < -24) exp_unit = -24; /* subnormal spacing 2^-24 */
+  const float q = ldexpf(ax, -exp_unit);
+  const float r = nearbyintf(q); /* default rounding mode: nearest-even */
+  return copysignf(ldexpf(r, exp_unit), x);
+}
+
+/* mode: 0 = none (fp32), 1 = fp16, 2 = bf16 (matches POAS_DTYPE_*). */
+void oracle_round(float* x, int64_t n, int mode) {
+  if (mode == 0) return;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) x[i] = mode == 2 ? bf16_round(x[i]) : fp16_round(x[i]);
+}
+
+/* --------------------------------------------------------- fp64 checker */
+
+/* C[rows x n] = round(A)[rows x k] . round(B)[k x n], double accumulation,
+ * where round() is the unit's operand precision `mode`. */
+void oracle_gemm_rows_f64(int64_t rows, int64_t n, int64_t k, const float* A, int64_t lda,
+                          const float* B, int64_t ldb, double* C, int64_t ldc, int mode) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < rows; ++i) {
+    double* c = C + i * ldc;
+    for (int64_t j = 0; j < n; ++j) c[j] = 0.0;
+    for (int64_t p = 0; p < k; ++p) {
+      float a = A[i * lda + p];
+      if (mode == 2) a = bf16_round(a);
+      else if (mode == 1) a = fp16_round(a);
+      const double ad = (double)a;
+      const float* b = B + p * ldb;
+      if (mode == 0) {
+        for (int64_t j = 0; j < n; ++j) c[j] += ad * (double)b[j];
+      } else {
+        for (int64_t j = 0; j < n; ++j) {
+          const float bj = mode == 2 ? bf16_round(b[j]) : fp16_round(b[j]);
+          c[j] += ad * (double)bj;
+        }
+      }
+    }
+  }
+}
+
+/* Relative Frobenius error ||C - R|| / ||R|| of an fp32 result. */
+double oracle_rel_frobenius(int64_t rows, int64_t n, const float* C, int64_t ldc, const double* R,
+                            int64_t ldr) {
+  double num = 0.0, den = 0.0;
+#pragma omp parallel for reduction(+ : num, den) schedule(static)
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const double d = (double)C[i * ldc + j] - R[i * ldr + j];
+      num += d * d;
+      den += R[i * ldr + j] * R[i * ldr + j];
+    }
+  return den > 0.0 ? sqrt(num / den) : sqrt(num);
+}
+
+/* ----------------------------------------------- CPU baseline (timed leg) */
+
+/* Executes one unit's tile list on the host: tiles are strip-major
+ * (strips of k' columns, each split into `parts` row blocks); tile t covers
+ * rows [off, off+m') of the unit's slice and columns [s*k', (s+1)*k') of A,
+ * accumulating A_tile . B_strip into C (split-K). fp32 accumulation, cache
+ * blocked, OpenMP over row blocks within a tile. */
+void oracle_exec_tiles_f32(int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                           int64_t ldb, float* C, int64_t ldc, const int64_t* tile_m,
+                           int64_t num_tiles, int64_t k_prime, int64_t rows) {
+  const int64_t strips = k / k_prime;
+  const int64_t parts = num_tiles / (strips > 0 ? strips : 1);
+  for (int64_t i = 0; i < rows; ++i) memset(C + i * ldc, 0, (size_t)n * sizeof(float));
+  for (int64_t s = 0; s < strips; ++s) {
+    int64_t off = 0;
+    for (int64_t p = 0; p < parts; ++p) {
+      const int64_t mt = tile_m[s * parts + p];
+      const int64_t k0 = s * k_prime;
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int64_t i = off; i < off + mt; i += 4) {
+        const int64_t ie = i + 4 < off + mt ? i + 4 : off + mt;
+        for (int64_t p0 = k0; p0 < k0 + k_prime; p0 += 256) {
+          const int64_t pe = p0 + 256 < k0 + k_prime ? p0 + 256 : k0 + k_prime;
+          for (int64_t ii = i; ii < ie; ++ii) {
+            float* c = C + ii * ldc;
+            for (int64_t pp = p0; pp < pe; ++pp) {
+              const float a = A[ii * lda + pp];
+              const float* b = B + pp * ldb;
+              for (int64_t j = 0; j < n; ++j) c[j] += a * b[j];
+            }
+          }
+        }
+      }
+      off += mt;
+    }
+  }
+}

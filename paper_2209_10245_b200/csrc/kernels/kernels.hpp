@@ -1,0 +1,39 @@
+// Host-side launch entry points for the sm_100a unit kernels. All pointers
+// are device pointers; all launches are asynchronous on `stream`.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace poas_b200 {
+
+enum class AbType : int { f32 = 0, f16 = 1, bf16 = 2 };
+
+// Tensor-core unit: C[M x N] (=|+=) A[M x K] * B[K x N], A and B row-major
+// 16-bit (bf16 or fp16), fp32 accumulate, fp32 C. `num_ctas` bounds the
+// persistent grid (the unit's SM budget); 0 = every SM.
+// Returns a cudaError_t (cudaSuccess = 0).
+cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                    int num_ctas, cudaStream_t stream);
+
+// CUDA-core unit: fp32 SIMT GEMM, same conventions.
+cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                      int num_ctas, bool exclusive_sm, cudaStream_t stream);
+
+// Counter-based uniform [-1, 1) fill, bit-identical to the host generator:
+// element (r, c) of a rows x cols block at (row0, col0) inside a matrix of
+// `total_cols` columns takes splitmix64 draw number (row0+r)*total_cols+col0+c
+// of Rng(seed). Written as fp32 or rounded (RNE) to bf16/fp16.
+cudaError_t fill_uniform(AbType t, void* dst, int64_t ld, int64_t rows, int64_t cols,
+                         int64_t row0, int64_t col0, int64_t total_cols, uint64_t seed,
+                         cudaStream_t stream);
+
+// fp32 -> bf16/fp16 (RNE) of a rows x cols block.
+cudaError_t convert_f32(AbType t, const float* src, int64_t ld_src, void* dst, int64_t ld_dst,
+                        int64_t rows, int64_t cols, cudaStream_t stream);
+
+int device_sm_count();
+
+}  // namespace poas_b200

@@ -1,0 +1,220 @@
+// CUDA-core unit of one B200: fp32 SIMT GEMM (FFMA pipe).
+//
+//   C[M x N] (=|+=) A[M x K] . B[K x N]     all fp32, row-major
+//
+// Replaces the GPU-kind synthetic law of the reference (SyntheticBackend::
+// time_gemm, /root/reference/proj/src/simulator.cpp:30-34).
+//
+// 128 x 128 x 16 CTA tile, 256 threads, 8 x 8 register micro-tile per thread
+// (two 4 x 4 quadrants 64 apart so the float4 shared-memory reads stay
+// conflict-free), 128-bit coalesced global loads prefetched into registers
+// one K-step ahead, shared memory double buffered (one barrier per K-step).
+// Persistent over tiles so the grid size is the unit's SM budget.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "kernels.hpp"
+
+namespace poas_b200 {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+constexpr int kBK = 16;
+constexpr int kThreads = 256;
+constexpr int kPad = 4;  // As row padding keeps the transposed stores spread over banks
+constexpr int kSmemFloats = 2 * kBK * (kBM + kPad) + 2 * kBK * kBN;
+
+struct SimtArgs {
+  int M, N, K;
+  const float* A;
+  long long lda;
+  const float* B;
+  long long ldb;
+  float* C;
+  long long ldc;
+  int accumulate;
+  int tiles_m, tiles_n;
+};
+
+template <bool kVec>
+__global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p) {
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  float* As = smem;                          // [2][kBK][kBM + kPad]  (A transposed)
+  float* Bs = smem + 2 * kBK * (kBM + kPad);  // [2][kBK][kBN]
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15;  // column group
+  const int ty = tid >> 4;  // row group
+
+  // Global-load assignment: A tile 128 x 16 -> two float4 per thread along K;
+  // B tile 16 x 128 -> two float4 per thread along N.
+  const int a_row = tid >> 1;          // 0..127
+  const int a_k = (tid & 1) * 8;       // 0 or 8 (two float4: +0, +4)
+  const int b_k = tid >> 4;            // 0..15
+  const int b_col = (tid & 15) * 8;    // two float4: +0, +4
+
+  const int total = p.tiles_m * p.tiles_n;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int mb = t / p.tiles_n;
+    const int nb = t % p.tiles_n;
+    const int m0 = mb * kBM;
+    const int n0 = nb * kBN;
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    float ra[8], rb[8];
+    auto load_global = [&](int k0) {
+      const int gr = m0 + a_row;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gk = k0 + a_k + h * 4;
+        if (kVec && gr < p.M && gk + 3 < p.K) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(p.A + (long long)gr * p.lda + gk));
+          ra[4 * h] = v.x; ra[4 * h + 1] = v.y; ra[4 * h + 2] = v.z; ra[4 * h + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            ra[4 * h + e] = (gr < p.M && gk + e < p.K) ? p.A[(long long)gr * p.lda + gk + e] : 0.f;
+        }
+      }
+      const int gk = k0 + b_k;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gc = n0 + b_col + h * 4;
+        if (kVec && gk < p.K && gc + 3 < p.N) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(p.B + (long long)gk * p.ldb + gc));
+          rb[4 * h] = v.x; rb[4 * h + 1] = v.y; rb[4 * h + 2] = v.z; rb[4 * h + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            rb[4 * h + e] = (gk < p.K && gc + e < p.N) ? p.B[(long long)gk * p.ldb + gc + e] : 0.f;
+        }
+      }
+    };
+    auto store_shared = [&](int buf) {
+      float* as = As + buf * kBK * (kBM + kPad);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) as[(a_k + e) * (kBM + kPad) + a_row] = ra[e];
+      float* bs = Bs + buf * kBK * kBN + b_k * kBN + b_col;
+      reinterpret_cast<float4*>(bs)[0] = make_float4(rb[0], rb[1], rb[2], rb[3]);
+      reinterpret_cast<float4*>(bs)[1] = make_float4(rb[4], rb[5], rb[6], rb[7]);
+    };
+
+    const int k_steps = (p.K + kBK - 1) / kBK;
+    load_global(0);
+    __syncthreads();  // previous tile's readers are done with both buffers
+    store_shared(0);
+    __syncthreads();
+
+    for (int ks = 0; ks < k_steps; ++ks) {
+      const int buf = ks & 1;
+      if (ks + 1 < k_steps) load_global((ks + 1) * kBK);
+      const float* as = As + buf * kBK * (kBM + kPad);
+      const float* bs = Bs + buf * kBK * kBN;
+#pragma unroll
+      for (int k = 0; k < kBK; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + ty * 4);
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + 64 + ty * 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(bs + k * kBN + tx * 4);
+        const float4 b1 = *reinterpret_cast<const float4*>(bs + k * kBN + 64 + tx * 4);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      if (ks + 1 < k_steps) store_shared(buf ^ 1);
+      __syncthreads();
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+      if (r >= p.M) continue;
+      float* crow = p.C + (long long)r * p.ldc;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = n0 + h * 64 + tx * 4;
+        if (kVec && c + 3 < p.N) {
+          float4 o = make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2],
+                                 acc[i][4 * h + 3]);
+          if (p.accumulate) {
+            const float4 q = *reinterpret_cast<const float4*>(crow + c);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4*>(crow + c) = o;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c + e < p.N) {
+              float o = acc[i][4 * h + e];
+              if (p.accumulate) o += crow[c + e];
+              crow[c + e] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                      int num_ctas, bool exclusive_sm, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return cudaErrorInvalidValue;
+  if (K <= 0) {
+    if (accumulate) return cudaSuccess;
+    return cudaMemset2DAsync(C, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(N) * 4,
+                             static_cast<size_t>(M), stream);
+  }
+  SimtArgs p;
+  p.M = static_cast<int>(M);
+  p.N = static_cast<int>(N);
+  p.K = static_cast<int>(K);
+  p.A = A;
+  p.lda = lda;
+  p.B = B;
+  p.ldb = ldb;
+  p.C = C;
+  p.ldc = ldc;
+  p.accumulate = accumulate ? 1 : 0;
+  p.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
+  p.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
+  const bool vec = lda % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+                     reinterpret_cast<uintptr_t>(C)) & 15) == 0;
+  // An "exclusive" CTA requests enough shared memory that nothing else (in
+  // particular a tensor-core CTA) can share its SM: the unit owns whole SMs.
+  const size_t smem = exclusive_sm ? 120 * 1024 : kSmemFloats * sizeof(float);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(simt_gemm_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(simt_gemm_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  int grid = num_ctas > 0 ? num_ctas : device_sm_count();
+  const int tiles = p.tiles_m * p.tiles_n;
+  if (grid > tiles) grid = tiles;
+  if (vec)
+    simt_gemm_kernel<true><<<grid, kThreads, smem, stream>>>(p);
+  else
+    simt_gemm_kernel<false><<<grid, kThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace poas_b200

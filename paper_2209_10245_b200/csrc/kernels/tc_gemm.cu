@@ -1,0 +1,320 @@
+// Tensor-core unit of one B200: persistent tcgen05 GEMM.
+//
+//   C[M x N] (=|+=) A[M x K] . B[K x N]     A, B row-major bf16/fp16, C fp32
+//
+// Replaces the XPU-kind synthetic law of the reference (SyntheticBackend::
+// time_gemm, /root/reference/proj/src/simulator.cpp:30-34) with real work.
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0  lane 0 : TMA producer  -- A tile [128 x 64] K-major, B tile
+//                    [64 x 256] N-major, both 128B-swizzled, STAGES-deep ring
+//   warp 1  lane 0 : MMA issuer    -- tcgen05.mma.cta_group::1.kind::f16
+//                    128x256x16, accumulator in TMEM (2 x 256 columns, double
+//                    buffered so the epilogue of tile i overlaps tile i+1)
+//   warps 2..5     : epilogue      -- tcgen05.ld 32x32b -> registers -> fp32 C
+// M/N/K tails come from TMA out-of-bounds zero fill plus masked stores.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "kernels.hpp"
+#include "sm100_ptx.cuh"
+
+namespace poas_b200 {
+namespace {
+
+using namespace ptx;
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBK = 64;  // one 128-byte swizzle row of 16-bit elements
+constexpr int kStages = 4;
+constexpr int kUmmaK = 16;
+constexpr int kABytes = kBM * kBK * 2;       // 16 KiB
+constexpr int kBBytes = kBN * kBK * 2;       // 32 KiB
+constexpr int kBChunkBytes = 64 * kBK * 2;   // one 64-column N chunk: 8 KiB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+constexpr int kTmemCols = 512;  // two 256-column fp32 accumulators
+constexpr int kGroupM = 16;     // tile raster: 16 M-tiles per group for L2 reuse
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
+
+struct TcArgs {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  float* C;
+  long long ldc;
+  int accumulate;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
+  const int per_group = kGroupM * tiles_n;
+  const int g = t / per_group;
+  const int first_m = g * kGroupM;
+  const int gm = min(tiles_m - first_m, kGroupM);
+  const int r = t - g * per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* s_a = smem;
+  uint8_t* s_b = smem + kStages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total = args.tiles_m * args.tiles_n;
+  const int k_blocks = (args.K + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          tma_load_2d(s_a + stage * kABytes, &map_a, &full[stage], kb * kBK, mb * kBM,
+                      kEvictNormal);
+#pragma unroll
+          for (int j = 0; j < kBN / 64; ++j)
+            tma_load_2d(s_b + stage * kBBytes + j * kBChunkBytes, &map_b, &full[stage],
+                        nb * kBN + j * 64, kb * kBK, kEvictNormal);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_addr(s_a + stage * kABytes);
+          const uint32_t b0 = smem_addr(s_b + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / kUmmaK; ++k) {
+            // A (K-major): advance 16 elements = 32 bytes inside the swizzle row.
+            const uint64_t ad = sdesc_sw128(a0 + k * kUmmaK * 2, 16, 1024);
+            // B (N-major): 16 K-rows = two 8-row (1024 B) swizzle atoms;
+            // 64-column N chunks sit kBChunkBytes apart.
+            const uint64_t bd = sdesc_sw128(b0 + k * 2 * 1024, kBChunkBytes, 1024);
+            umma_f16(d_tmem, ad, bd, args.idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&acc_full[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // Epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * kBM + quad * 32 + lane;
+      float* crow = args.C + static_cast<long long>(row) * args.ldc;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                               static_cast<uint32_t>(acc * kBN + c * 32),
+                           v);
+        tmem_wait_ld();
+        if (row < args.M) {
+          const int col0 = nb * kBN + c * 32;
+          if (vec && col0 + 32 <= args.N) {
+            float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 o = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                     __uint_as_float(v[4 * j + 2]),
+                                     __uint_as_float(v[4 * j + 3]));
+              if (args.accumulate) {
+                const float4 p = dst[j];
+                o.x += p.x;
+                o.y += p.y;
+                o.z += p.z;
+                o.w += p.w;
+              }
+              dst[j] = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = col0 + j;
+              if (col < args.N) {
+                float o = __uint_as_float(v[j]);
+                if (args.accumulate) o += crow[col];
+                crow[col] = o;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D map over a row-major [rows x cols] 16-bit matrix with leading dim `ld`.
+bool make_map(CUtensorMap* map, AbType t, const void* base, int64_t rows, int64_t cols,
+              int64_t ld, uint32_t box_cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r =
+      fn(map, t == AbType::bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+         2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int device_sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                    int num_ctas, cudaStream_t stream) {
+  if (t != AbType::bf16 && t != AbType::f16) return cudaErrorInvalidValue;
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (K <= 0) {
+    if (accumulate) return cudaSuccess;
+    return cudaMemset2DAsync(C, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(N) * 4,
+                             static_cast<size_t>(M), stream);
+  }
+  // TMA: 16-byte aligned base and row pitch.
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
+      (lda * 2) % 16 || (ldb * 2) % 16 || lda < K || ldb < N || ldc < N)
+    return cudaErrorInvalidValue;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return cudaErrorInvalidValue;
+
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, t, A, M, K, lda, kBK, kBM)) return cudaErrorInvalidValue;
+  if (!make_map(&mb, t, B, K, N, ldb, 64, kBK)) return cudaErrorInvalidValue;
+
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemBytes));
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+
+  TcArgs args;
+  args.M = static_cast<int>(M);
+  args.N = static_cast<int>(N);
+  args.K = static_cast<int>(K);
+  args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
+  args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
+  args.C = C;
+  args.ldc = ldc;
+  args.accumulate = accumulate ? 1 : 0;
+  args.idesc = idesc_f16(t == AbType::bf16, kBM, kBN, false, true);
+
+  const int sms = device_sm_count();
+  int grid = num_ctas > 0 ? num_ctas : sms;
+  const int tiles = args.tiles_m * args.tiles_n;
+  if (grid > tiles) grid = tiles;
+  tc_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
+  return cudaGetLastError();
+}
+
+}  // namespace poas_b200

@@ -1,0 +1,397 @@
+// C-ABI: plan, predict and execute entry points (include/poas_b200.h).
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "capi_util.hpp"
+#include "host_gemm.hpp"
+#include "host_rng.hpp"
+#include "poas/adapter.hpp"
+#include "poas/error.hpp"
+#include "poas/executor.hpp"
+#include "poas/optimizer.hpp"
+#include "poas/profiler.hpp"
+#include "poas/scheduler.hpp"
+#include "poas_b200.h"
+#include "units.hpp"
+
+using poas_b200::capi::dup_string;
+using poas_b200::capi::guard;
+using poas_b200::capi::raise;
+
+struct poas_unit_s {
+  std::unique_ptr<poas_b200::Unit> unit;
+};
+
+struct poas_executor_s {
+  std::unique_ptr<poas::Executor> ex;
+};
+
+namespace {
+
+poas::MatrixDims dims_of(int64_t m, int64_t n, int64_t k) {
+  poas::MatrixDims d{m, n, k};
+  poas::validate_dims(d);
+  return d;
+}
+
+std::string need_str(const char* s, const char* what) {
+  if (!s) raise(POAS_E_INVALID_ARGUMENT, std::string(what) + " is NULL");
+  return s;
+}
+
+template <class P>
+void need_ptr(P* p, const char* what) {
+  if (!p) raise(POAS_E_INVALID_ARGUMENT, std::string(what) + " is NULL");
+}
+
+std::string g17(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+std::string iv(const poas::Interval& i) { return "[" + g17(i.start) + ", " + g17(i.end) + "]"; }
+
+std::string split_json(const poas::WorkloadSplit& s) {
+  std::string o = "{\"makespan\": " + g17(s.makespan) + ", \"lp_objective\": " +
+                  g17(s.lp_objective) + ", \"lp_iterations\": " + std::to_string(s.lp_iterations) +
+                  ", \"shares\": [";
+  for (std::size_t i = 0; i < s.shares.size(); ++i) {
+    const poas::DeviceShare& d = s.shares[i];
+    o += (i ? ", " : "");
+    o += "{\"id\": \"" + d.device_id + "\", \"rows\": " + std::to_string(d.rows) +
+         ", \"ops\": " + std::to_string(d.ops) + ", \"fraction\": " + g17(d.fraction) +
+         ", \"copy_in\": " + iv(d.timeline.copy_in) + ", \"compute\": " + iv(d.timeline.compute) +
+         ", \"copy_out\": " + iv(d.timeline.copy_out) + ", \"finish\": " + g17(d.timeline.finish) +
+         "}";
+  }
+  return o + "]}";
+}
+
+std::string tile_plan_json(const poas::TilePlan& p) {
+  std::string o = "{\"devices\": [";
+  for (std::size_t i = 0; i < p.devices.size(); ++i) {
+    const poas::PlannedDevice& d = p.devices[i];
+    o += (i ? ", " : "");
+    o += "{\"id\": \"" + d.device_id + "\", \"rows\": " + std::to_string(d.rows) +
+         ", \"k_prime\": " + std::to_string(d.tiling.k_prime) + ", \"sq\": " + g17(d.tiling.sq) +
+         ", \"window_fallback\": " + (d.window_fallback ? "true" : "false") + ", \"tiles\": [";
+    for (std::size_t t = 0; t < d.tiling.tiles.size(); ++t) {
+      const poas::Tile& x = d.tiling.tiles[t];
+      o += (t ? ", " : "");
+      o += "[" + std::to_string(x.m) + ", " + std::to_string(x.k) + ", " + std::to_string(x.n) + "]";
+    }
+    o += "]}";
+  }
+  return o + "]}";
+}
+
+poas::ProfilingConfig parse_profiling(const char* text) {
+  poas::ProfilingConfig c;
+  if (!text) return c;
+  std::stringstream in(text);
+  std::string item;
+  while (std::getline(in, item, ',')) {
+    if (item.empty()) continue;
+    const auto eq = item.find('=');
+    if (eq == std::string::npos) poas::fail(poas::errc::invalid_argument, "profiling: bad item " + item);
+    const std::string k = item.substr(0, eq);
+    const long long v = std::stoll(item.substr(eq + 1));
+    if (k == "probes") c.probes = static_cast<int>(v);
+    else if (k == "repetitions") c.repetitions = static_cast<int>(v);
+    else if (k == "cpu_min_side") c.cpu_range.min_side = v;
+    else if (k == "cpu_max_side") c.cpu_range.max_side = v;
+    else if (k == "accel_min_side") c.accel_range.min_side = v;
+    else if (k == "accel_max_side") c.accel_range.max_side = v;
+    else if (k == "bandwidth_payload") c.bandwidth_payload = static_cast<std::uint64_t>(v);
+    else poas::fail(poas::errc::invalid_argument, "profiling: unknown key " + k);
+  }
+  poas::validate_profiling_config(c);
+  return c;
+}
+
+std::uint64_t llc_bytes() {
+  const long v = sysconf(_SC_LEVEL3_CACHE_SIZE);
+  return v > 0 ? static_cast<std::uint64_t>(v) : (32ULL << 20);
+}
+
+}  // namespace
+
+namespace poas_b200 {
+
+// profile_machine (reference proj/src/simulator.cpp:53-74) over real units.
+poas::MachineProfile profile_units(const std::vector<std::unique_ptr<Unit>>& units,
+                                   const poas::ProfilingConfig& cfg, bool bus) {
+  std::vector<poas::DeviceProbeData> probes;
+  for (const auto& u : units) {
+    poas::DeviceProbeData p;
+    p.id = u->spec().id;
+    p.kind = u->spec().kind;
+    p.elem_size = u->spec().elem;
+    p.samples = poas::run_compute_probes(*u, cfg.range_for(p.kind), cfg.probes, cfg.repetitions);
+    if (u->has_transfers())
+      p.bandwidth = poas::run_bandwidth_probe(*u, cfg.bandwidth_payload, cfg.repetitions);
+    if (p.kind == poas::DeviceKind::xpu) p.align = u->spec().align;
+    if (p.kind == poas::DeviceKind::cpu) p.cache_bytes = llc_bytes();
+    probes.push_back(std::move(p));
+  }
+  return poas::fit_machine(probes, bus, cfg);
+}
+
+}  // namespace poas_b200
+
+extern "C" {
+
+int poas_b200_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                   char** schedule_json) {
+  return guard([&] {
+    need_ptr(schedule_json, "schedule_json");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    const poas::MatrixDims d = dims_of(m, n, k);
+    const poas::WorkloadSplit split = poas::solve_split(machine, d);
+    const poas::TilePlan plan = poas::build_tile_plan(machine, d, split);
+    *schedule_json = dup_string(poas::format_schedule(poas::build_schedule(plan, machine)));
+  });
+}
+
+int poas_b200_plan_standalone(const char* profile_text, const char* device_id, int64_t m,
+                              int64_t n, int64_t k, char** schedule_json) {
+  return guard([&] {
+    need_ptr(schedule_json, "schedule_json");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    *schedule_json = dup_string(poas::format_schedule(
+        poas::standalone_schedule(machine, need_str(device_id, "device_id"), dims_of(m, n, k))));
+  });
+}
+
+int poas_b200_split(const char* profile_text, int64_t m, int64_t n, int64_t k, char** out) {
+  return guard([&] {
+    need_ptr(out, "out");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    *out = dup_string(split_json(poas::solve_split(machine, dims_of(m, n, k))));
+  });
+}
+
+int poas_b200_oracle_split(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                           int64_t resolution, int parallel, char** out) {
+  return guard([&] {
+    need_ptr(out, "out");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    const poas::MatrixDims d = dims_of(m, n, k);
+    *out = dup_string(split_json(parallel ? poas::oracle_grid_search(machine, d, resolution)
+                                          : poas::oracle_grid_search_serial(machine, d, resolution)));
+  });
+}
+
+int poas_b200_tile_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                        const int64_t* rows, size_t count, char** out) {
+  return guard([&] {
+    need_ptr(out, "out");
+    need_ptr(rows, "rows");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    const poas::MatrixDims d = dims_of(m, n, k);
+    const std::vector<std::int64_t> r(rows, rows + count);
+    const poas::WorkloadSplit split = poas::evaluate_rows(machine, d, r);
+    *out = dup_string(tile_plan_json(poas::build_tile_plan(machine, d, split)));
+  });
+}
+
+int poas_b200_schedule_roundtrip(const char* schedule_json, char** canonical_json) {
+  return guard([&] {
+    need_ptr(canonical_json, "out");
+    *canonical_json = dup_string(
+        poas::format_schedule(poas::parse_schedule(need_str(schedule_json, "schedule"))));
+  });
+}
+
+int poas_b200_profile_roundtrip(const char* profile_text, char** canonical_text) {
+  return guard([&] {
+    need_ptr(canonical_text, "out");
+    *canonical_text =
+        dup_string(poas::format_profile(poas::parse_profile(need_str(profile_text, "profile"))));
+  });
+}
+
+int poas_b200_machine_hash(const char* profile_text, char out[17]) {
+  return guard([&] {
+    need_ptr(out, "out");
+    const std::string h = poas::machine_hash(poas::parse_profile(need_str(profile_text, "profile")));
+    std::memcpy(out, h.c_str(), 17);
+  });
+}
+
+int poas_b200_fit_linear(const uint64_t* ops, const double* seconds, size_t count, double* slope,
+                         double* intercept) {
+  return guard([&] {
+    need_ptr(slope, "slope");
+    need_ptr(intercept, "intercept");
+    if (count && (!ops || !seconds)) raise(POAS_E_INVALID_ARGUMENT, "samples are NULL");
+    std::vector<poas::ModelSample> s;
+    for (size_t i = 0; i < count; ++i) s.push_back({ops[i], seconds[i]});
+    const poas::LinearModel mdl = poas::fit_linear(s);
+    *slope = mdl.slope;
+    *intercept = mdl.intercept;
+  });
+}
+
+int poas_b200_transfer_bytes(const char* profile_text, const char* device_id, uint64_t ops,
+                             int64_t m, int64_t n, int64_t k, uint64_t* in_bytes,
+                             uint64_t* out_bytes) {
+  return guard([&] {
+    need_ptr(in_bytes, "in_bytes");
+    need_ptr(out_bytes, "out_bytes");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    const poas::DeviceProfile* dev = machine.find(need_str(device_id, "device_id"));
+    if (!dev) poas::fail(poas::errc::missing_device, "no device '" + std::string(device_id) + "'");
+    const poas::TransferBytes tb = poas::transfer_bytes(*dev, ops, dims_of(m, n, k));
+    *in_bytes = tb.in;
+    *out_bytes = tb.out;
+  });
+}
+
+int poas_b200_simplex(int num_vars, const double* objective, int n_eq, const double* eq_a,
+                      const double* eq_b, int n_ge, const double* ge_a, const double* ge_b,
+                      double* x_out, double* objective_out, long* iterations_out) {
+  return guard([&] {
+    if (num_vars < 0 || n_eq < 0 || n_ge < 0) raise(POAS_E_INVALID_ARGUMENT, "negative sizes");
+    need_ptr(objective, "objective");
+    need_ptr(x_out, "x_out");
+    poas::SimplexProblem p;
+    p.num_vars = num_vars;
+    p.objective.assign(objective, objective + num_vars);
+    for (int i = 0; i < n_eq; ++i) {
+      p.eq_a.emplace_back(eq_a + static_cast<size_t>(i) * num_vars,
+                          eq_a + static_cast<size_t>(i + 1) * num_vars);
+      p.eq_b.push_back(eq_b[i]);
+    }
+    for (int i = 0; i < n_ge; ++i) {
+      p.ge_a.emplace_back(ge_a + static_cast<size_t>(i) * num_vars,
+                          ge_a + static_cast<size_t>(i + 1) * num_vars);
+      p.ge_b.push_back(ge_b[i]);
+    }
+    const poas::SimplexSolution s = poas::solve_simplex(p);
+    std::memcpy(x_out, s.x.data(), sizeof(double) * static_cast<size_t>(num_vars));
+    if (objective_out) *objective_out = s.objective;
+    if (iterations_out) *iterations_out = s.iterations;
+  });
+}
+
+int poas_b200_unit_create(const char* spec, poas_unit_t* out) {
+  return guard([&] {
+    need_ptr(out, "out");
+    auto h = std::make_unique<poas_unit_s>();
+    h->unit = std::make_unique<poas_b200::Unit>(poas_b200::parse_unit_spec(need_str(spec, "spec")));
+    *out = h.release();
+  });
+}
+
+void poas_b200_unit_destroy(poas_unit_t unit) { delete unit; }
+
+int poas_b200_time_gemm(poas_unit_t unit, int64_t side, double* seconds) {
+  return guard([&] {
+    need_ptr(unit, "unit");
+    need_ptr(seconds, "seconds");
+    *seconds = unit->unit->time_gemm(side);
+  });
+}
+
+int poas_b200_time_transfer(poas_unit_t unit, uint64_t bytes, double* seconds) {
+  return guard([&] {
+    need_ptr(unit, "unit");
+    need_ptr(seconds, "seconds");
+    *seconds = unit->unit->time_transfer(bytes);
+  });
+}
+
+int poas_b200_has_transfers(poas_unit_t unit) { return unit && unit->unit->has_transfers() ? 1 : 0; }
+
+int poas_b200_profile_machine(const char* units, const char* profiling, int bus,
+                              char** profile_text) {
+  return guard([&] {
+    need_ptr(profile_text, "profile_text");
+    std::vector<std::unique_ptr<poas_b200::Unit>> us;
+    for (const auto& s : poas_b200::parse_unit_list(need_str(units, "units")))
+      us.push_back(std::make_unique<poas_b200::Unit>(s));
+    const poas::MachineProfile m = poas_b200::profile_units(us, parse_profiling(profiling), bus != 0);
+    *profile_text = dup_string(poas::format_profile(m));
+  });
+}
+
+int poas_b200_executor_create(const char* units, poas_executor_t* out) {
+  return guard([&] {
+    need_ptr(out, "out");
+    auto h = std::make_unique<poas_executor_s>();
+    h->ex = std::make_unique<poas::Executor>(need_str(units, "units"));
+    *out = h.release();
+  });
+}
+
+void poas_b200_executor_destroy(poas_executor_t ex) { delete ex; }
+
+int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_gemm_io* io,
+                      int repeats, char** report_json) {
+  return guard([&] {
+    need_ptr(ex, "executor");
+    need_ptr(io, "io");
+    const poas::Schedule s = poas::parse_schedule(need_str(schedule_json, "schedule"));
+    poas::GemmOperands op;
+    op.m = io->m;
+    op.n = io->n;
+    op.k = io->k;
+    op.a_host = io->a_host;
+    op.lda_host = io->lda_host;
+    op.b_host = io->b_host;
+    op.ldb_host = io->ldb_host;
+    op.c_host = io->c_host;
+    op.ldc_host = io->ldc_host;
+    op.a_dev = io->a_dev;
+    op.lda_dev = io->lda_dev;
+    op.b_dev = io->b_dev;
+    op.ldb_dev = io->ldb_dev;
+    op.a16_dev = io->a16_dev;
+    op.lda16_dev = io->lda16_dev;
+    op.b16_dev = io->b16_dev;
+    op.ldb16_dev = io->ldb16_dev;
+    op.c_dev = io->c_dev;
+    op.ldc_dev = io->ldc_dev;
+    op.resident = io->resident != 0;
+    const poas::SimulationResult r = ex->ex->run(s, op, repeats);
+    if (report_json) *report_json = dup_string(poas::format_execution_report(s, r));
+  });
+}
+
+int poas_b200_executor_hash(poas_executor_t ex, char out[17]) {
+  return guard([&] {
+    need_ptr(ex, "executor");
+    need_ptr(out, "out");
+    std::memcpy(out, ex->ex->machine_hash().c_str(), 17);
+  });
+}
+
+int poas_b200_host_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
+                        const float* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
+                        int threads) {
+  return guard([&] {
+    if (m > 0 && n > 0 && k > 0 && (!a || !b || !c))
+      raise(POAS_E_INVALID_ARGUMENT, "host_gemm: NULL operand");
+    poas_b200::host_gemm(m, n, k, a, lda, b, ldb, c, ldc, accumulate != 0, threads);
+  });
+}
+
+int poas_b200_fill_uniform_host(float* dst, int64_t ld, int64_t rows, int64_t cols, int64_t row0,
+                                int64_t col0, int64_t total_cols, uint64_t seed) {
+  return guard([&] {
+    if (rows > 0 && cols > 0) need_ptr(dst, "dst");
+    poas_b200::fill_uniform_host(dst, ld, rows, cols, row0, col0, total_cols, seed);
+  });
+}
+
+uint64_t poas_b200_stream_seed(uint64_t master_seed, const char* name) {
+  return poas::Rng::for_stream(master_seed, name ? name : "").state();
+}
+
+}  // extern "C"

@@ -1,0 +1,461 @@
+// The co-execution engine: runs a schedule's shares concurrently on real
+// units and measures every phase (replaces the reference's discrete-event
+// simulate(), proj/src/simulator.cpp:104-209, with the same result shape).
+//
+// Per repeat:
+//   t0          one event per GPU (on every unit stream's critical path) and
+//               a host steady_clock stamp: the common clock origin
+//   cpu unit    a host thread runs host_gemm on its rows from t0
+//   copy-in     GPU units in schedule (priority) order; on a shared bus each
+//               copy-in waits for the previous unit's copy-in (link order)
+//   compute     right after the unit's own copy-in, on its SM budget
+//   copy-out    schedule order; the first waits for the last copy-in, each
+//               later one for the previous copy-out (shared bus)
+// Resident runs (operands already in HBM) skip both copy phases.
+// Rows are contiguous in schedule order (poas::row_offsets).
+#include "poas/executor.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <thread>
+
+#include "capi_util.hpp"
+#include "poas/error.hpp"
+#include "units.hpp"
+
+namespace poas {
+
+using poas_b200::AbType;
+using poas_b200::DeviceGuard;
+using poas_b200::Unit;
+using poas_b200::capi::cuda_check;
+
+double rel_err_pct(double measured, double predicted) {
+  if (measured == 0.0 && predicted == 0.0) return 0.0;
+  return 100.0 * (measured - predicted) / measured;
+}
+
+namespace {
+
+double rms(const std::vector<double>& v) {
+  if (v.empty()) return 0.0;
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s / static_cast<double>(v.size()));
+}
+
+std::int64_t round_up(std::int64_t x, std::int64_t a) { return (x + a - 1) / a * a; }
+
+struct PhaseEvents {
+  cudaEvent_t ci0 = nullptr, ci1 = nullptr, cp0 = nullptr, cp1 = nullptr, co0 = nullptr,
+              co1 = nullptr;
+  void create() {
+    for (cudaEvent_t* e : {&ci0, &ci1, &cp0, &cp1, &co0, &co1})
+      if (!*e) cuda_check(cudaEventCreate(e), "cudaEventCreate");
+  }
+  void destroy() {
+    for (cudaEvent_t* e : {&ci0, &ci1, &cp0, &cp1, &co0, &co1})
+      if (*e) cudaEventDestroy(*e);
+  }
+};
+
+void copy2d(void* dst, std::int64_t ld_dst, const void* src, std::int64_t ld_src,
+            std::int64_t rows, std::int64_t cols, std::size_t esz, cudaMemcpyKind kind,
+            cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  if (ld_dst == cols && ld_src == cols)
+    cuda_check(cudaMemcpyAsync(dst, src, static_cast<std::size_t>(rows * cols) * esz, kind, s),
+               "cudaMemcpyAsync");
+  else
+    cuda_check(cudaMemcpy2DAsync(dst, static_cast<std::size_t>(ld_dst) * esz, src,
+                                 static_cast<std::size_t>(ld_src) * esz,
+                                 static_cast<std::size_t>(cols) * esz,
+                                 static_cast<std::size_t>(rows), kind, s),
+               "cudaMemcpy2DAsync");
+}
+
+}  // namespace
+
+Executor::Executor(const std::string& spec) {
+  const std::vector<poas_b200::UnitSpec> specs = poas_b200::parse_unit_list(spec, &bus_);
+  std::vector<DeviceIdentity> ids;
+  for (const auto& s : specs) {
+    if (find(s.id)) fail(errc::invalid_argument, "duplicate unit id '" + s.id + "'");
+    units_.push_back(std::make_unique<Unit>(s));
+    ids.push_back({s.id, s.kind, s.elem});
+  }
+  hash_ = machine_identity_hash(ids, bus_);
+}
+
+Executor::~Executor() = default;
+
+Unit* Executor::find(const std::string& id) const {
+  for (const auto& u : units_)
+    if (u->spec().id == id) return u.get();
+  return nullptr;
+}
+
+SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io, int repeats) {
+  if (repeats < 1) fail(errc::invalid_argument, "repeats must be positive");
+  if (schedule.devices.empty()) fail(errc::invalid_argument, "schedule has no devices");
+  if (schedule.machine_hash != hash_)
+    fail(errc::hash_mismatch, "schedule was planned for machine " + schedule.machine_hash +
+                                  ", executor units describe " + hash_);
+  const MatrixDims& d = schedule.dims;
+  if (io.m != d.m || io.n != d.n || io.k != d.k)
+    fail(errc::invalid_argument, "operand dims do not match the schedule dims");
+
+  const std::size_t nd = schedule.devices.size();
+  std::vector<Unit*> unit(nd);
+  std::int64_t covered = 0;
+  for (std::size_t i = 0; i < nd; ++i) {
+    unit[i] = find(schedule.devices[i].id);
+    if (!unit[i]) fail(errc::missing_device, "no unit '" + schedule.devices[i].id + "'");
+    covered += schedule.devices[i].rows;
+  }
+  if (covered != d.m) fail(errc::invalid_argument, "schedule rows do not cover m");
+  const std::vector<std::int64_t> row0 = row_offsets(schedule);
+
+  // Operand availability checks, up front (no partial launches).
+  bool any_cpu = false;
+  for (std::size_t i = 0; i < nd; ++i) {
+    if (schedule.devices[i].rows == 0) continue;
+    if (!unit[i]->on_gpu()) any_cpu = true;
+  }
+  if ((any_cpu || !io.resident) && (!io.a_host || !io.b_host || !io.c_host))
+    fail(errc::invalid_argument, "host operands (a_host, b_host, c_host) are required");
+  if (io.resident) {
+    for (std::size_t i = 0; i < nd; ++i) {
+      if (schedule.devices[i].rows == 0 || !unit[i]->on_gpu()) continue;
+      if (!io.c_dev) fail(errc::invalid_argument, "resident run needs c_dev");
+      const bool tensor = unit[i]->spec().kind == DeviceKind::xpu;
+      if (tensor && !(io.a16_dev && io.b16_dev) && !(io.a_dev && io.b_dev))
+        fail(errc::invalid_argument, "resident tensor unit needs a16/b16 or a/b device operands");
+      if (!tensor && !(io.a_dev && io.b_dev))
+        fail(errc::invalid_argument, "resident CUDA-core unit needs a_dev/b_dev");
+    }
+  }
+
+  // Per-device t0 events and per-unit phase events.
+  std::map<int, cudaEvent_t> t0;
+  std::vector<PhaseEvents> ev(nd);
+  for (std::size_t i = 0; i < nd; ++i) {
+    if (!unit[i]->on_gpu()) continue;
+    const int dev = unit[i]->spec().device;
+    DeviceGuard g(dev);
+    if (!t0.count(dev)) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      t0[dev] = e;
+    }
+    ev[i].create();
+  }
+  struct Cleanup {
+    std::map<int, cudaEvent_t>& t0;
+    std::vector<PhaseEvents>& ev;
+    std::vector<Unit*>& unit;
+    ~Cleanup() {
+      for (std::size_t i = 0; i < ev.size(); ++i) {
+        if (!unit[i]->on_gpu()) continue;
+        DeviceGuard g(unit[i]->spec().device);
+        ev[i].destroy();
+      }
+      for (auto& [dev, e] : t0) {
+        DeviceGuard g(dev);
+        cudaEventDestroy(e);
+      }
+    }
+  } cleanup{t0, ev, unit};
+
+  SimulationResult res;
+  res.repeats = repeats;
+  std::vector<double> sum_in(nd, 0.0), sum_cp(nd, 0.0), sum_out(nd, 0.0), sum_fin(nd, 0.0);
+  double sum_makespan = 0.0, sum_wall = 0.0;
+
+  for (int rep = 0; rep < repeats; ++rep) {
+    // Quiesce so t0 is a true common origin.
+    for (std::size_t i = 0; i < nd; ++i)
+      if (unit[i]->on_gpu()) {
+        DeviceGuard g(unit[i]->spec().device);
+        cuda_check(cudaStreamSynchronize(unit[i]->stream()), "cudaStreamSynchronize");
+      }
+    for (auto& [dev, e] : t0) {
+      DeviceGuard g(dev);
+      cuda_check(cudaEventRecord(e, nullptr), "cudaEventRecord");
+    }
+    const auto host_t0 = std::chrono::steady_clock::now();
+
+    // CPU unit(s): host threads, started first so they begin at ~t0.
+    std::vector<std::thread> host_jobs;
+    std::vector<double> cpu_start(nd, 0.0), cpu_end(nd, 0.0);
+    std::vector<std::exception_ptr> cpu_err(nd);
+    for (std::size_t i = 0; i < nd; ++i) {
+      const ScheduledDevice& sd = schedule.devices[i];
+      if (unit[i]->on_gpu() || sd.rows == 0) continue;
+      host_jobs.emplace_back([&, i] {
+        try {
+          const ScheduledDevice& s = schedule.devices[i];
+          const auto a = std::chrono::steady_clock::now();
+          unit[i]->gemm(s.rows, d.n, d.k, io.a_host + row0[i] * io.lda_host, io.lda_host,
+                        io.b_host, io.ldb_host, io.c_host + row0[i] * io.ldc_host, io.ldc_host,
+                        false);
+          const auto b = std::chrono::steady_clock::now();
+          cpu_start[i] = std::chrono::duration<double>(a - host_t0).count();
+          cpu_end[i] = std::chrono::duration<double>(b - host_t0).count();
+        } catch (...) {
+          cpu_err[i] = std::current_exception();
+        }
+      });
+    }
+
+    // GPU units: make every unit stream start after its device's t0.
+    for (std::size_t i = 0; i < nd; ++i) {
+      if (!unit[i]->on_gpu()) continue;
+      DeviceGuard g(unit[i]->spec().device);
+      cuda_check(cudaStreamWaitEvent(unit[i]->stream(), t0[unit[i]->spec().device], 0),
+                 "cudaStreamWaitEvent");
+    }
+
+    // Copy-in + compute, in schedule order.
+    std::size_t prev_in = nd;  // previous busy bus unit (link order)
+    for (std::size_t i = 0; i < nd; ++i) {
+      const ScheduledDevice& sd = schedule.devices[i];
+      Unit* u = unit[i];
+      if (!u->on_gpu() || sd.rows == 0) continue;
+      DeviceGuard g(u->spec().device);
+      cudaStream_t s = u->stream();
+      const bool tensor = u->spec().kind == DeviceKind::xpu;
+      const std::int64_t r = sd.rows, r0 = row0[i];
+
+      const void* a = nullptr;
+      const void* b = nullptr;
+      std::int64_t lda = 0, ldb = 0;
+      float* c = nullptr;
+      std::int64_t ldc = 0;
+
+      if (!io.resident) {
+        if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(s, ev[prev_in].ci1, 0), "wait");
+        cuda_check(cudaEventRecord(ev[i].ci0, s), "cudaEventRecord");
+        float* da = static_cast<float*>(u->scratch(0).ensure(static_cast<std::size_t>(r * d.k) * 4));
+        float* db = static_cast<float*>(u->scratch(1).ensure(static_cast<std::size_t>(d.k * d.n) * 4));
+        copy2d(da, d.k, io.a_host + r0 * io.lda_host, io.lda_host, r, d.k, 4,
+               cudaMemcpyHostToDevice, s);
+        copy2d(db, d.n, io.b_host, io.ldb_host, d.k, d.n, 4, cudaMemcpyHostToDevice, s);
+        a = da;
+        b = db;
+        lda = d.k;
+        ldb = d.n;
+        c = static_cast<float*>(u->scratch(4).ensure(static_cast<std::size_t>(r * d.n) * 4));
+        ldc = d.n;
+        prev_in = i;
+      } else {
+        cuda_check(cudaEventRecord(ev[i].ci0, s), "cudaEventRecord");
+        c = io.c_dev + r0 * io.ldc_dev;
+        ldc = io.ldc_dev;
+        if (tensor && io.a16_dev && io.b16_dev) {
+          a = static_cast<const char*>(io.a16_dev) + r0 * io.lda16_dev * 2;
+          b = io.b16_dev;
+          lda = io.lda16_dev;
+          ldb = io.ldb16_dev;
+        } else {
+          a = io.a_dev + r0 * io.lda_dev;
+          b = io.b_dev;
+          lda = io.lda_dev;
+          ldb = io.ldb_dev;
+        }
+      }
+      cuda_check(cudaEventRecord(ev[i].ci1, s), "cudaEventRecord");
+
+      cuda_check(cudaEventRecord(ev[i].cp0, s), "cudaEventRecord");
+      const bool need_convert = tensor && !(io.resident && io.a16_dev && io.b16_dev);
+      if (need_convert) {
+        const AbType t = u->spec().dtype;
+        const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
+        void* a16 = u->scratch(2).ensure(static_cast<std::size_t>(r * lda16) * 2);
+        void* b16 = u->scratch(3).ensure(static_cast<std::size_t>(d.k * ldb16) * 2);
+        cuda_check(poas_b200::convert_f32(t, static_cast<const float*>(a), lda, a16, lda16, r, d.k, s),
+                   "convert A");
+        cuda_check(poas_b200::convert_f32(t, static_cast<const float*>(b), ldb, b16, ldb16, d.k, d.n, s),
+                   "convert B");
+        a = a16;
+        b = b16;
+        lda = lda16;
+        ldb = ldb16;
+      }
+      u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false);
+      cuda_check(cudaEventRecord(ev[i].cp1, s), "cudaEventRecord");
+    }
+
+    // Copy-outs, in schedule order.
+    const std::size_t last_in = prev_in;
+    std::size_t prev_out = nd;
+    for (std::size_t i = 0; i < nd; ++i) {
+      const ScheduledDevice& sd = schedule.devices[i];
+      Unit* u = unit[i];
+      if (!u->on_gpu() || sd.rows == 0) continue;
+      DeviceGuard g(u->spec().device);
+      cudaStream_t s = u->stream();
+      if (!io.resident) {
+        if (bus_) {
+          if (prev_out == nd) {
+            if (last_in != nd && last_in != i)
+              cuda_check(cudaStreamWaitEvent(s, ev[last_in].ci1, 0), "wait");
+          } else {
+            cuda_check(cudaStreamWaitEvent(s, ev[prev_out].co1, 0), "wait");
+          }
+        }
+        cuda_check(cudaEventRecord(ev[i].co0, s), "cudaEventRecord");
+        copy2d(io.c_host + row0[i] * io.ldc_host, io.ldc_host, u->scratch(4).get(), d.n, sd.rows,
+               d.n, 4, cudaMemcpyDeviceToHost, s);
+        prev_out = i;
+      } else {
+        cuda_check(cudaEventRecord(ev[i].co0, s), "cudaEventRecord");
+      }
+      cuda_check(cudaEventRecord(ev[i].co1, s), "cudaEventRecord");
+    }
+
+    // Join.
+    for (std::thread& t : host_jobs) t.join();
+    for (std::size_t i = 0; i < nd; ++i)
+      if (unit[i]->on_gpu()) {
+        DeviceGuard g(unit[i]->spec().device);
+        cuda_check(cudaStreamSynchronize(unit[i]->stream()), "unit stream");
+      }
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
+    for (auto& e : cpu_err)
+      if (e) std::rethrow_exception(e);
+
+    // Measured timeline of this repeat.
+    std::vector<DeviceTimeline> tl(nd);
+    double makespan = 0.0;
+    for (std::size_t i = 0; i < nd; ++i) {
+      const ScheduledDevice& sd = schedule.devices[i];
+      DeviceTimeline& t = tl[i];
+      if (sd.rows == 0) {
+        t = sd.timeline;  // idle: nothing to measure, keep the plan's placement
+        continue;
+      }
+      if (!unit[i]->on_gpu()) {
+        t.copy_in = {0.0, 0.0};
+        t.compute = {cpu_start[i], cpu_end[i]};
+        t.copy_out = {cpu_end[i], cpu_end[i]};
+        t.finish = cpu_end[i];
+      } else {
+        DeviceGuard g(unit[i]->spec().device);
+        cudaEvent_t z = t0[unit[i]->spec().device];
+        const auto at = [&](cudaEvent_t e) {
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, z, e), "cudaEventElapsedTime");
+          return static_cast<double>(ms) * 1e-3;
+        };
+        t.copy_in = {at(ev[i].ci0), at(ev[i].ci1)};
+        t.compute = {at(ev[i].cp0), at(ev[i].cp1)};
+        t.copy_out = {at(ev[i].co0), at(ev[i].co1)};
+        t.finish = t.copy_out.end;
+      }
+      makespan = std::max(makespan, t.finish);
+    }
+    for (std::size_t i = 0; i < nd; ++i) {
+      sum_in[i] += tl[i].copy_in.duration();
+      sum_cp[i] += tl[i].compute.duration();
+      sum_out[i] += tl[i].copy_out.duration();
+      sum_fin[i] += tl[i].finish;
+    }
+    sum_makespan += makespan;
+    sum_wall += wall;
+    res.repeat_timelines.push_back(std::move(tl));
+  }
+
+  const double inv = 1.0 / repeats;
+  std::vector<double> e_cp, e_copy, e_fin;
+  for (std::size_t i = 0; i < nd; ++i) {
+    const ScheduledDevice& sd = schedule.devices[i];
+    const bool link = unit[i]->on_gpu();
+    DeviceOutcome o;
+    o.id = sd.id;
+    o.rows = sd.rows;
+    o.copy_in = {sum_in[i] * inv, sd.timeline.copy_in.duration(), 0.0};
+    o.compute = {sum_cp[i] * inv, sd.timeline.compute.duration(), 0.0};
+    o.copy_out = {sum_out[i] * inv, sd.timeline.copy_out.duration(), 0.0};
+    o.copy = {(sum_in[i] + sum_out[i]) * inv,
+              sd.timeline.copy_in.duration() + sd.timeline.copy_out.duration(), 0.0};
+    o.finish = {sum_fin[i] * inv, link ? sd.timeline.copy_out.end : sd.timeline.compute.end, 0.0};
+    for (PhaseError* p : {&o.copy_in, &o.compute, &o.copy_out, &o.copy, &o.finish})
+      p->error_pct = rel_err_pct(p->measured, p->predicted);
+    if (sd.rows > 0) {
+      e_cp.push_back(o.compute.error_pct);
+      e_fin.push_back(o.finish.error_pct);
+      if (link && !io.resident) e_copy.push_back(o.copy.error_pct);
+    }
+    res.devices.push_back(std::move(o));
+  }
+  res.measured_makespan = sum_makespan * inv;
+  res.predicted_makespan = schedule.makespan;
+  res.makespan_error_pct = rel_err_pct(res.measured_makespan, res.predicted_makespan);
+  res.rmse_compute = rms(e_cp);
+  res.rmse_copy = rms(e_copy);
+  res.rmse_finish = rms(e_fin);
+  res.measured_wall = sum_wall * inv;
+  return res;
+}
+
+namespace {
+
+std::string num(double v) {
+  if (!std::isfinite(v)) return "null";
+  char buf[40];
+  for (int prec = 15; prec <= 17; ++prec) {
+    std::snprintf(buf, sizeof buf, "%.*g", prec, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  return buf;
+}
+
+std::string phase_json(const PhaseError& p) {
+  return "{\"measured\": " + num(p.measured) + ", \"predicted\": " + num(p.predicted) +
+         ", \"error_pct\": " + num(p.error_pct) + "}";
+}
+
+}  // namespace
+
+std::string format_execution_report(const Schedule& s, const SimulationResult& r) {
+  std::string o = "{\n";
+  o += "  \"machine_hash\": \"" + s.machine_hash + "\",\n";
+  o += "  \"dims\": {\"m\": " + std::to_string(s.dims.m) + ", \"n\": " + std::to_string(s.dims.n) +
+       ", \"k\": " + std::to_string(s.dims.k) + "},\n";
+  o += "  \"seed\": " + std::to_string(r.seed) + ",\n";
+  o += "  \"repeats\": " + std::to_string(r.repeats) + ",\n";
+  o += "  \"predicted_makespan\": " + num(r.predicted_makespan) + ",\n";
+  o += "  \"measured_makespan\": " + num(r.measured_makespan) + ",\n";
+  o += "  \"makespan_error_pct\": " + num(r.makespan_error_pct) + ",\n";
+  o += "  \"devices\": [\n";
+  for (std::size_t i = 0; i < r.devices.size(); ++i) {
+    const DeviceOutcome& d = r.devices[i];
+    o += "    {\"id\": \"" + d.id + "\", \"rows\": " + std::to_string(d.rows) +
+         ",\n     \"copy_in\": " + phase_json(d.copy_in) + ",\n     \"compute\": " +
+         phase_json(d.compute) + ",\n     \"copy_out\": " + phase_json(d.copy_out) +
+         ",\n     \"copy\": " + phase_json(d.copy) + ",\n     \"finish\": " +
+         phase_json(d.finish) + "}";
+    o += i + 1 < r.devices.size() ? ",\n" : "\n";
+  }
+  o += "  ],\n";
+  o += "  \"rmse\": {\"finish\": " + num(r.rmse_finish) + ", \"compute\": " + num(r.rmse_compute) +
+       ", \"copy\": " + num(r.rmse_copy) + "},\n";
+  o += "  \"measured_wall\": " + num(r.measured_wall) + ",\n";
+  o += "  \"repeat_makespans\": [";
+  for (std::size_t k = 0; k < r.repeat_timelines.size(); ++k) {
+    double m = 0.0;
+    for (const DeviceTimeline& t : r.repeat_timelines[k]) m = std::max(m, t.finish);
+    o += (k ? ", " : "") + num(m);
+  }
+  o += "]\n}\n";
+  return o;
+}
+
+}  // namespace poas

@@ -1,0 +1,240 @@
+#include "units.hpp"
+
+#include <chrono>
+#include <cstdlib>
+#include <sstream>
+
+#include "capi_util.hpp"
+#include "host_gemm.hpp"
+#include "host_rng.hpp"
+#include "poas/error.hpp"
+
+namespace poas_b200 {
+
+using capi::cuda_check;
+
+namespace {
+
+std::vector<std::string> split(const std::string& s, char sep) {
+  std::vector<std::string> out;
+  std::string cur;
+  std::istringstream in(s);
+  while (std::getline(in, cur, sep)) {
+    // trim spaces
+    const auto b = cur.find_first_not_of(" \t\n");
+    const auto e = cur.find_last_not_of(" \t\n");
+    if (b == std::string::npos) continue;
+    out.push_back(cur.substr(b, e - b + 1));
+  }
+  return out;
+}
+
+long to_long(const std::string& v, const std::string& key) {
+  char* end = nullptr;
+  const long x = std::strtol(v.c_str(), &end, 10);
+  if (v.empty() || *end != '\0')
+    poas::fail(poas::errc::invalid_argument, "unit spec: bad integer for '" + key + "': " + v);
+  return x;
+}
+
+std::int64_t round_up(std::int64_t x, std::int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+UnitSpec parse_unit_spec(const std::string& text) {
+  const auto eq = text.find('=');
+  if (eq == std::string::npos || eq == 0)
+    poas::fail(poas::errc::invalid_argument, "unit spec '" + text + "': expected <id>=<kind>[:k=v]*");
+  UnitSpec u;
+  u.id = text.substr(0, eq);
+  const std::vector<std::string> parts = split(text.substr(eq + 1), ':');
+  if (parts.empty()) poas::fail(poas::errc::invalid_argument, "unit spec '" + text + "': no kind");
+  const auto kind = poas::kind_from_name(parts[0]);
+  if (!kind) poas::fail(poas::errc::invalid_argument, "unit spec '" + text + "': unknown kind");
+  u.kind = *kind;
+  u.elem = 4;
+  for (size_t i = 1; i < parts.size(); ++i) {
+    const auto kv = parts[i].find('=');
+    if (kv == std::string::npos)
+      poas::fail(poas::errc::invalid_argument, "unit spec '" + text + "': bad option " + parts[i]);
+    const std::string k = parts[i].substr(0, kv), v = parts[i].substr(kv + 1);
+    if (k == "dev") u.device = static_cast<int>(to_long(v, k));
+    else if (k == "sms") u.sms = static_cast<int>(to_long(v, k));
+    else if (k == "exclusive") u.exclusive = to_long(v, k) != 0;
+    else if (k == "threads") u.threads = static_cast<int>(to_long(v, k));
+    else if (k == "elem") u.elem = static_cast<std::uint32_t>(to_long(v, k));
+    else if (k == "align") u.align = to_long(v, k);
+    else if (k == "dtype") {
+      if (v == "bf16") u.dtype = AbType::bf16;
+      else if (v == "f16" || v == "fp16") u.dtype = AbType::f16;
+      else poas::fail(poas::errc::invalid_argument, "unit spec: dtype must be bf16 or f16");
+    } else if (k == "link") {
+      if (v == "pcie") u.link = Link::pcie;
+      else if (v == "hbm") u.link = Link::hbm;
+      else poas::fail(poas::errc::invalid_argument, "unit spec: link must be pcie or hbm");
+    } else {
+      poas::fail(poas::errc::invalid_argument, "unit spec '" + text + "': unknown option " + k);
+    }
+  }
+  if (u.kind == poas::DeviceKind::cpu && u.link == Link::hbm) u.link = Link::pcie;
+  return u;
+}
+
+std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus) {
+  std::vector<UnitSpec> out;
+  if (bus) *bus = true;
+  for (const std::string& item : split(text, ';')) {
+    if (item.rfind("bus=", 0) == 0) {
+      if (bus) *bus = item.substr(4) != "0" && item.substr(4) != "false";
+      continue;
+    }
+    out.push_back(parse_unit_spec(item));
+  }
+  if (out.empty()) poas::fail(poas::errc::invalid_argument, "no units in '" + text + "'");
+  return out;
+}
+
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr_) cudaFree(ptr_);
+}
+
+void* DeviceBuffer::ensure(std::size_t bytes) {
+  if (bytes <= bytes_ && ptr_) return ptr_;
+  if (ptr_) cudaFree(ptr_);
+  ptr_ = nullptr;
+  bytes_ = 0;
+  cuda_check(cudaMalloc(&ptr_, bytes), "cudaMalloc");
+  bytes_ = bytes;
+  return ptr_;
+}
+
+PinnedBuffer::~PinnedBuffer() {
+  if (ptr_) cudaFreeHost(ptr_);
+}
+
+void* PinnedBuffer::ensure(std::size_t bytes) {
+  if (bytes <= bytes_ && ptr_) return ptr_;
+  if (ptr_) cudaFreeHost(ptr_);
+  ptr_ = nullptr;
+  bytes_ = 0;
+  cuda_check(cudaMallocHost(&ptr_, bytes), "cudaMallocHost");
+  bytes_ = bytes;
+  return ptr_;
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  cudaGetDevice(&prev_);
+  if (dev != prev_) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+}
+
+DeviceGuard::~DeviceGuard() { cudaSetDevice(prev_); }
+
+Unit::Unit(UnitSpec spec) : spec_(std::move(spec)) {
+  if (on_gpu()) {
+    DeviceGuard g(spec_.device);
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreate(&ev0_), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&ev1_), "cudaEventCreate");
+  }
+}
+
+Unit::~Unit() {
+  if (on_gpu()) {
+    DeviceGuard g(spec_.device);
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (stream_) cudaStreamDestroy(stream_);
+  }
+}
+
+void Unit::gemm(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, std::int64_t lda,
+                const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate) {
+  switch (spec_.kind) {
+    case poas::DeviceKind::cpu:
+      host_gemm(m, n, k, static_cast<const float*>(a), lda, static_cast<const float*>(b), ldb, c,
+                ldc, accumulate, spec_.threads);
+      return;
+    case poas::DeviceKind::gpu:
+      cuda_check(simt_gemm(m, n, k, static_cast<const float*>(a), lda,
+                           static_cast<const float*>(b), ldb, c, ldc, accumulate, spec_.sms,
+                           spec_.exclusive, stream_),
+                 "simt_gemm");
+      return;
+    case poas::DeviceKind::xpu:
+      cuda_check(tc_gemm(spec_.dtype, m, n, k, a, lda, b, ldb, c, ldc, accumulate, spec_.sms,
+                         stream_),
+                 "tc_gemm");
+      return;
+  }
+}
+
+double Unit::time_gemm(std::int64_t side) {
+  if (side < 1) poas::fail(poas::errc::invalid_argument, "time_gemm: side must be positive");
+  if (!on_gpu()) {
+    const std::size_t elems = static_cast<std::size_t>(side) * static_cast<std::size_t>(side);
+    if (probe_side_ != side) {
+      host_a_.resize(elems);
+      host_b_.resize(elems);
+      host_c_.resize(elems);
+      fill_uniform_host(host_a_.data(), side, side, side, 0, 0, side, 0x5eedA);
+      fill_uniform_host(host_b_.data(), side, side, side, 0, 0, side, 0x5eedB);
+      probe_side_ = side;
+      gemm(side, side, side, host_a_.data(), side, host_b_.data(), side, host_c_.data(), side,
+           false);  // warm-up: page in, spin up threads
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    gemm(side, side, side, host_a_.data(), side, host_b_.data(), side, host_c_.data(), side, false);
+    const auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double>(t1 - t0).count();
+  }
+
+  DeviceGuard g(spec_.device);
+  const bool tensor = spec_.kind == poas::DeviceKind::xpu;
+  // 16-bit operands need a 16-byte row pitch for TMA: pad the leading dim.
+  const std::int64_t ld = tensor ? round_up(side, 8) : side;
+  const std::size_t esz = tensor ? 2 : 4;
+  if (probe_side_ != side) {
+    const std::size_t bytes = static_cast<std::size_t>(side) * ld * esz;
+    void* a = probe_a_.ensure(bytes);
+    void* b = probe_b_.ensure(bytes);
+    probe_c_.ensure(static_cast<std::size_t>(side) * side * 4);
+    const AbType t = tensor ? spec_.dtype : AbType::f32;
+    cuda_check(fill_uniform(t, a, ld, side, side, 0, 0, side, 0x5eedA, stream_), "fill");
+    cuda_check(fill_uniform(t, b, ld, side, side, 0, 0, side, 0x5eedB, stream_), "fill");
+    probe_side_ = side;
+    gemm(side, side, side, a, ld, b, ld, static_cast<float*>(probe_c_.get()), side, false);
+  }
+  cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+  gemm(side, side, side, probe_a_.get(), ld, probe_b_.get(), ld,
+       static_cast<float*>(probe_c_.get()), side, false);
+  cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+  cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "cudaEventElapsedTime");
+  return static_cast<double>(ms) * 1e-3;
+}
+
+double Unit::time_transfer(std::uint64_t bytes) {
+  if (!on_gpu()) poas::fail(poas::errc::backend_failure, "cpu unit has no link");
+  DeviceGuard g(spec_.device);
+  void* dst = xfer_dev_.ensure(bytes);
+  const void* src = nullptr;
+  cudaMemcpyKind kind;
+  if (spec_.link == Link::pcie) {
+    src = xfer_host_.ensure(bytes);
+    kind = cudaMemcpyHostToDevice;
+  } else {
+    src = xfer_dev2_.ensure(bytes);
+    kind = cudaMemcpyDeviceToDevice;
+  }
+  cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+  cuda_check(cudaMemcpyAsync(dst, src, bytes, kind, stream_), "cudaMemcpyAsync");
+  cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+  cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "cudaEventElapsedTime");
+  return static_cast<double>(ms) * 1e-3;
+}
+
+}  // namespace poas_b200

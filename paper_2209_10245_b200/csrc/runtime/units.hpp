@@ -1,0 +1,117 @@
+// Compute units of a B200 box and their DeviceBackend plugins.
+//
+// A unit is one concurrently running share of the machine:
+//   cpu : the host cores                 (host_gemm, no link)
+//   gpu : the CUDA cores of one B200      (simt_gemm fp32 on an SM budget)
+//   xpu : the tensor cores of one B200    (tc_gemm bf16/fp16 -> fp32 on an SM budget)
+// Each unit implements poas::DeviceBackend (reference
+// proj/include/poas/backend.hpp:11-24) with real timed work, so the
+// reference's profiler drives it unchanged.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.hpp"
+#include "poas/backend.hpp"
+#include "poas/device_model.hpp"
+
+namespace poas_b200 {
+
+enum class Link { pcie, hbm };
+
+struct UnitSpec {
+  std::string id;
+  poas::DeviceKind kind = poas::DeviceKind::cpu;
+  int device = 0;         // CUDA ordinal (gpu/xpu)
+  int sms = 0;            // SM budget = persistent grid size (0 = all SMs)
+  bool exclusive = true;  // gpu: own whole SMs (no co-residency with xpu CTAs)
+  AbType dtype = AbType::bf16;  // xpu operand type
+  std::uint32_t elem = 4;       // bytes per element crossing the link
+  int threads = 0;              // cpu: OpenMP threads (0 = all cores)
+  std::int64_t align = 8;       // xpu row alignment (16-byte TMA pitch for 16-bit)
+  Link link = Link::pcie;       // what time_transfer measures
+};
+
+// "<id>=<kind>[:key=value]*"
+UnitSpec parse_unit_spec(const std::string& text);
+// ';'-separated unit specs, optionally with a "bus=0|1" token.
+std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus = nullptr);
+
+// Device scratch that grows on demand and is reused across calls.
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  ~DeviceBuffer();
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  void* ensure(std::size_t bytes);
+  void* get() const { return ptr_; }
+
+ private:
+  void* ptr_ = nullptr;
+  std::size_t bytes_ = 0;
+};
+
+class PinnedBuffer {
+ public:
+  PinnedBuffer() = default;
+  ~PinnedBuffer();
+  PinnedBuffer(const PinnedBuffer&) = delete;
+  PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  void* ensure(std::size_t bytes);
+
+ private:
+  void* ptr_ = nullptr;
+  std::size_t bytes_ = 0;
+};
+
+class Unit : public poas::DeviceBackend {
+ public:
+  explicit Unit(UnitSpec spec);
+  ~Unit() override;
+
+  const UnitSpec& spec() const { return spec_; }
+  bool on_gpu() const { return spec_.kind != poas::DeviceKind::cpu; }
+  cudaStream_t stream() const { return stream_; }
+
+  // Probe plugin (DeviceBackend).
+  double time_gemm(std::int64_t side) override;
+  double time_transfer(std::uint64_t bytes) override;
+  bool has_transfers() const override { return on_gpu(); }
+
+  // The unit's GEMM on already-placed operands (device pointers for GPU
+  // units -- 16-bit for xpu -- host pointers for cpu). Asynchronous on
+  // stream() for GPU units, synchronous for cpu.
+  void gemm(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, std::int64_t lda,
+            const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate);
+
+  // Scratch owned by the unit (staging for link copies in execute()).
+  DeviceBuffer& scratch(int slot) { return scratch_[slot]; }
+
+ private:
+  UnitSpec spec_;
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  DeviceBuffer probe_a_, probe_b_, probe_c_, xfer_dev_, xfer_dev2_;
+  PinnedBuffer xfer_host_;
+  std::vector<float> host_a_, host_b_, host_c_;
+  std::int64_t probe_side_ = 0;
+  DeviceBuffer scratch_[6];
+};
+
+// RAII device selection.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+
+ private:
+  int prev_ = 0;
+};
+
+}  // namespace poas_b200

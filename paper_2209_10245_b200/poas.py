@@ -1,0 +1,225 @@
+"""Python mirror of the POAS plan / predict / execute API over the C ABI.
+
+Names and argument meaning follow the reference C++ API (namespace poas,
+/root/reference/proj/include/poas/*.hpp); errors raise PoasError whose
+`.errc` is the reference's poas::errc name. Every function calls into
+libpoas_b200.so -- there is no Python implementation of any of it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass
+from typing import Sequence
+
+from ._lib import DTYPE_BF16, DTYPE_F16, DTYPE_F32, PoasError, call_str, check, lib
+
+__all__ = [
+    "PoasError", "plan", "plan_standalone", "solve_split", "oracle_grid_search", "build_tile_plan",
+    "schedule_roundtrip", "profile_roundtrip", "machine_hash", "fit_linear", "transfer_bytes",
+    "solve_simplex", "Unit", "profile_machine", "Executor", "GemmIO", "stream_seed",
+    "DTYPE_F32", "DTYPE_F16", "DTYPE_BF16",
+]
+
+
+def _b(s: str) -> bytes:
+    return s.encode()
+
+
+# ------------------------------------------------------------------ planning
+def plan(profile: str, m: int, n: int, k: int) -> str:
+    """solve_split -> build_tile_plan -> build_schedule -> format_schedule
+    (reference proj/tools/poas.cpp:66-83). Returns the schedule JSON text."""
+    return call_str(lib.poas_b200_plan, _b(profile), m, n, k)
+
+
+def plan_standalone(profile: str, device_id: str, m: int, n: int, k: int) -> str:
+    """standalone_schedule (reference proj/src/scheduler.cpp:59-74)."""
+    return call_str(lib.poas_b200_plan_standalone, _b(profile), _b(device_id), m, n, k)
+
+
+def solve_split(profile: str, m: int, n: int, k: int) -> dict:
+    """solve_split (reference proj/src/optimizer.cpp:238-325) as a dict."""
+    return json.loads(call_str(lib.poas_b200_split, _b(profile), m, n, k))
+
+
+def oracle_grid_search(profile: str, m: int, n: int, k: int, resolution: int,
+                       parallel: bool = True) -> dict:
+    """oracle_grid_search(_serial) (reference proj/src/optimizer.cpp:431-439)."""
+    return json.loads(call_str(lib.poas_b200_oracle_split, _b(profile), m, n, k, resolution,
+                               int(parallel)))
+
+
+def build_tile_plan(profile: str, m: int, n: int, k: int, rows: Sequence[int]) -> dict:
+    """build_tile_plan over evaluate_rows(rows) (reference proj/src/adapter.cpp:171-215)."""
+    arr = (C.c_int64 * len(rows))(*rows)
+    return json.loads(call_str(lib.poas_b200_tile_plan, _b(profile), m, n, k, arr, len(rows)))
+
+
+def schedule_roundtrip(text: str) -> str:
+    """parse_schedule -> format_schedule (reference proj/src/scheduler.cpp:147-242)."""
+    return call_str(lib.poas_b200_schedule_roundtrip, _b(text))
+
+
+def profile_roundtrip(text: str) -> str:
+    """parse_profile -> format_profile (reference proj/src/profiler.cpp:139-209)."""
+    return call_str(lib.poas_b200_profile_roundtrip, _b(text))
+
+
+def machine_hash(profile: str) -> str:
+    buf = C.create_string_buffer(17)
+    check(lib.poas_b200_machine_hash(_b(profile), buf))
+    return buf.value.decode()
+
+
+def fit_linear(ops: Sequence[int], seconds: Sequence[float]) -> tuple[float, float]:
+    """fit_linear (reference proj/src/device_model.cpp:97-131): (slope, intercept)."""
+    n = len(ops)
+    o = (C.c_uint64 * n)(*ops)
+    s = (C.c_double * n)(*seconds)
+    slope, icpt = C.c_double(), C.c_double()
+    check(lib.poas_b200_fit_linear(o, s, n, C.byref(slope), C.byref(icpt)))
+    return slope.value, icpt.value
+
+
+def transfer_bytes(profile: str, device_id: str, ops: int, m: int, n: int, k: int) -> tuple[int, int]:
+    i, o = C.c_uint64(), C.c_uint64()
+    check(lib.poas_b200_transfer_bytes(_b(profile), _b(device_id), ops, m, n, k, C.byref(i),
+                                       C.byref(o)))
+    return i.value, o.value
+
+
+def solve_simplex(objective, eq_a=(), eq_b=(), ge_a=(), ge_b=()):
+    """solve_simplex (reference proj/src/simplex.cpp:86-187): (x, objective, iterations)."""
+    nv = len(objective)
+
+    def mat(rows):
+        flat = [float(v) for r in rows for v in r]
+        return (C.c_double * max(1, len(flat)))(*flat)
+
+    x = (C.c_double * max(1, nv))()
+    obj, it = C.c_double(), C.c_long()
+    check(lib.poas_b200_simplex(nv, (C.c_double * nv)(*objective), len(eq_a), mat(eq_a),
+                                (C.c_double * max(1, len(eq_b)))(*eq_b), len(ge_a), mat(ge_a),
+                                (C.c_double * max(1, len(ge_b)))(*ge_b), x, C.byref(obj),
+                                C.byref(it)))
+    return list(x)[:nv], obj.value, it.value
+
+
+def stream_seed(master: int, name: str) -> int:
+    """Rng::for_stream(master, name) seed (reference proj/include/poas/rng.hpp:43-50)."""
+    return lib.poas_b200_stream_seed(master, _b(name))
+
+
+# ------------------------------------------------------------------- predict
+class Unit:
+    """One compute unit as a DeviceBackend (reference proj/include/poas/backend.hpp).
+
+    spec: "<id>=<kind>[:key=value]*", e.g. "gpu0.tc=xpu:dev=0:sms=146:dtype=bf16".
+    """
+
+    def __init__(self, spec: str):
+        self._h = C.c_void_p()
+        check(lib.poas_b200_unit_create(_b(spec), C.byref(self._h)))
+
+    def time_gemm(self, side: int) -> float:
+        s = C.c_double()
+        check(lib.poas_b200_time_gemm(self._h, side, C.byref(s)))
+        return s.value
+
+    def time_transfer(self, nbytes: int) -> float:
+        s = C.c_double()
+        check(lib.poas_b200_time_transfer(self._h, nbytes, C.byref(s)))
+        return s.value
+
+    def has_transfers(self) -> bool:
+        return bool(lib.poas_b200_has_transfers(self._h))
+
+    def close(self):
+        if self._h:
+            lib.poas_b200_unit_destroy(self._h)
+            self._h = C.c_void_p()
+
+    __del__ = close
+
+
+def profile_machine(units: str, profiling: str = "", bus: bool = True) -> str:
+    """profile_machine over real units -> "poas-profile v1" text
+    (reference proj/src/simulator.cpp:53-74 + proj/src/profiler.cpp:75-135)."""
+    return call_str(lib.poas_b200_profile_machine, _b(units), _b(profiling), int(bus))
+
+
+# ------------------------------------------------------------------- execute
+class GemmIO(C.Structure):
+    """poas_gemm_io (include/poas_b200.h)."""
+    _fields_ = [
+        ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+        ("a_host", C.c_void_p), ("lda_host", C.c_int64),
+        ("b_host", C.c_void_p), ("ldb_host", C.c_int64),
+        ("c_host", C.c_void_p), ("ldc_host", C.c_int64),
+        ("a_dev", C.c_void_p), ("lda_dev", C.c_int64),
+        ("b_dev", C.c_void_p), ("ldb_dev", C.c_int64),
+        ("a16_dev", C.c_void_p), ("lda16_dev", C.c_int64),
+        ("b16_dev", C.c_void_p), ("ldb16_dev", C.c_int64),
+        ("c_dev", C.c_void_p), ("ldc_dev", C.c_int64),
+        ("resident", C.c_int),
+    ]
+
+
+class Executor:
+    """The real replacement of simulate() (reference proj/src/simulator.cpp:104-209)."""
+
+    def __init__(self, units: str):
+        self._h = C.c_void_p()
+        check(lib.poas_b200_executor_create(_b(units), C.byref(self._h)))
+
+    @property
+    def machine_hash(self) -> str:
+        buf = C.create_string_buffer(17)
+        check(lib.poas_b200_executor_hash(self._h, buf))
+        return buf.value.decode()
+
+    def execute(self, schedule: str, io: GemmIO, repeats: int = 1) -> dict:
+        out = C.c_void_p()
+        check(lib.poas_b200_execute(self._h, _b(schedule), C.byref(io), repeats, C.byref(out)))
+        from ._lib import take_string
+        return json.loads(take_string(out))
+
+    def close(self):
+        if self._h:
+            lib.poas_b200_executor_destroy(self._h)
+            self._h = C.c_void_p()
+
+    __del__ = close
+
+
+# --------------------------------------------------------------- raw kernels
+def tc_gemm(dtype: int, m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, num_ctas=0, stream=None):
+    check(lib.poas_b200_tc_gemm(dtype, m, n, k, a, lda, b, ldb, c, ldc, int(accumulate), num_ctas,
+                                stream))
+
+
+def simt_gemm(m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, num_ctas=0, exclusive=False,
+              stream=None):
+    check(lib.poas_b200_simt_gemm(m, n, k, a, lda, b, ldb, c, ldc, int(accumulate), num_ctas,
+                                  int(exclusive), stream))
+
+
+def host_gemm(m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, threads=0):
+    check(lib.poas_b200_host_gemm(m, n, k, a, lda, b, ldb, c, ldc, int(accumulate), threads))
+
+
+def fill_uniform(dtype, dst, ld, rows, cols, row0, col0, total_cols, seed, stream=None):
+    check(lib.poas_b200_fill_uniform(dtype, dst, ld, rows, cols, row0, col0, total_cols, seed, stream))
+
+
+def fill_uniform_host(dst, ld, rows, cols, row0, col0, total_cols, seed):
+    check(lib.poas_b200_fill_uniform_host(dst, ld, rows, cols, row0, col0, total_cols, seed))
+
+
+def convert_f32(dtype, src, ld_src, dst, ld_dst, rows, cols, stream=None):
+    check(lib.poas_b200_convert_f32(dtype, src, ld_src, dst, ld_dst, rows, cols, stream))
+
+
+def sm_count() -> int:
+    return lib.poas_b200_sm_count()
