@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""POAS co-executed GEMM benchmark on B200 (driver contract: one JSON line).
+
+Metric (BASELINE.json): co-executed GEMM TFLOP/s at N=16384 on 1/2/4/8 B200,
+plus speedup vs the best single unit.
+
+Per rank (one process per GPU, torchrun for N > 1; weak scaling):
+  units      gpu<r>.tc   tensor cores (tcgen05 bf16 -> fp32) on TC_SMS SMs
+             gpu<r>.simt CUDA cores (fp32 FFMA) on SIMT_SMS whole SMs
+  predict    the POAS profiler probes both units on this box (C++, real
+             kernels) -> "poas-profile v1"
+  optimize/adapt/schedule   the reference-identical planner -> schedule JSON
+  step       one co-executed GEMM of this rank's M=16384 rows x N=K=16384:
+             every unit's share concurrently through the executor (C ABI);
+             at N > 1 rank 0's B (bf16 + fp32) is broadcast with NCCL inside
+             the step
+  value      whole-job TFLOP/s = 2*M_total*N*K / max-over-ranks device time
+  e2e        the same GEMM through poas_b200_execute with HOST pinned fp32
+             buffers: H2D copy-in, compute, D2H copy-out inside the timed step
+
+`--impl reference` times the reference's own CPU path for this workload on
+the host cores (the reference planner from oracle/_ref planning a CPU-only
+run, executed tile by tile by the oracle port) and prints the same line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SEED = 20261017
+N_DEFAULT = 16384
+TC_SMS = 146
+SIMT_SMS = 2
+PROFILING = "probes=9,repetitions=3,bandwidth_payload=268435456"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", 0) or 0), "measured"
+        except Exception:
+            pass
+    return 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- reference
+def reference_cpu_path(n: int, sample_rows: int | None = None, reps: int = 1):
+    """The reference's CPU path for an N^3 GEMM on this host: the reference
+    planner (oracle/_ref/libpoasref.so, compiled from /root/reference) plans
+    a CPU-only machine; the oracle port executes a bounded sample of that
+    plan's tiles (the first m-part of every k'-strip, split-K). Returns
+    (TFLOP/s, seconds per rep, sample description, cores)."""
+    import numpy as np
+    import oracle
+
+    cores = os.cpu_count() or 1
+    # CPU-only machine, reference ProfilingConfig defaults (cpu sides 1000-2000).
+    cfg = ("poas-machine v1\n\nbus true\n\ndevice cpu0\nkind cpu\ntrue_slope 2e-12\n"
+           "true_intercept 0.0005\nelem_size 4\nnoise 0\ndrift 0\ncache_bytes 33554432\n")
+    profile = oracle.ref.exact_profile(cfg)
+    t0 = time.perf_counter()
+    sched = json.loads(oracle.ref.plan(profile, n, n, n))
+    plan_s = time.perf_counter() - t0
+    dev = sched["devices"][0]
+    tiles = dev["tiles"]
+    kp = tiles[0]["k"]
+    strips = n // kp
+    parts = len(tiles) // strips
+    rows = tiles[0]["m"] if sample_rows is None else sample_rows
+    tile_m = [rows] * strips  # one m-part per strip: rows x k, split-K over strips
+    A = oracle.fill_uniform(rows, n, oracle.stream_seed(SEED, "A"), total_cols=n)
+    B = oracle.fill_uniform(n, n, oracle.stream_seed(SEED, "B"))
+    oracle.exec_tiles_f32(A[:8], B, [8] * strips, kp)  # warm-up (page-in, thread spin-up)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.exec_tiles_f32(A, B, tile_m, kp)
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    tflops = 2.0 * rows * n * n / sec / 1e12
+    sample = (f"reference CPU-only plan of {n}^3 ({len(tiles)} tiles {parts}x{strips}, k'={kp}) "
+              f"planned by oracle/_ref in {plan_s * 1e6:.0f} us; timed: {rows} rows x full K "
+              f"({strips} split-K tiles of {rows}x{kp}x{n}) by the oracle port, fp32, {cores} threads")
+    return tflops, sec, sample, cores
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    n = args.n
+    rows = args.ref_rows
+    reps_w, reps_k = args.warmup, args.steps
+    # warm-up steps
+    for _ in range(max(0, reps_w)):
+        reference_cpu_path(n, sample_rows=rows, reps=1)
+    tfl, sec, sample, cores = reference_cpu_path(n, sample_rows=rows, reps=max(1, reps_k))
+    line = {
+        "metric": "co-executed GEMM TFLOP/s at N=16384 (1/2/4/8 B200); speedup vs best single unit",
+        "value": round(tfl, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": reps_k,
+        "warmup": reps_w, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"C3 GEMM N={n} (reference CPU path: reference planner + oracle port "
+                               f"executing its CPU-only plan, bounded sample)", "m": n, "n": n, "k": n},
+        "cpu_baseline": {"value": round(tfl, 4), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(tfl, 4), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------- ours
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--tc-sms", type=int, default=TC_SMS)
+    ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=None)
+    ap.add_argument("--save", default=None, help="directory for profile/schedule/report artefacts")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_10245_b200 import poas
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    n = k = args.n
+    m = args.n  # rows per rank (weak scaling)
+    save = Path(args.save) if args.save else None
+    if save and rank == 0:
+        save.mkdir(parents=True, exist_ok=True)
+
+    g = local  # CUDA ordinal inside this process (CUDA_VISIBLE_DEVICES respected)
+    tc_id, simt_id = f"gpu{rank}.tc", f"gpu{rank}.simt"
+    units_res = (f"{tc_id}=xpu:dev={g}:sms={args.tc_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384;"
+                 f"{simt_id}=gpu:dev={g}:sms={args.simt_sms}:exclusive=1:elem=4:link=hbm:probe=512-2048")
+
+    # ---- predict -> optimize -> adapt -> schedule (resident operands)
+    t0 = time.perf_counter()
+    profile = poas.profile_machine(units_res, PROFILING, bus=True)
+    t_prof = time.perf_counter() - t0
+    schedule = poas.plan(profile, m, n, k)
+    sched = json.loads(schedule)
+    rows = {d["id"]: d["rows"] for d in sched["devices"]}
+    log(f"rank {rank}: profiled in {t_prof:.1f}s; plan rows {rows}; predicted {sched['makespan']*1e3:.3f} ms")
+    if save and rank == 0:
+        (save / "profile_resident.txt").write_text(profile)
+        (save / "schedule_resident.json").write_text(schedule)
+
+    # ---- resident operands (counter-based generator, identical to host/oracle)
+    sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
+    A32 = torch.empty(m, k, device=dev, dtype=torch.float32)
+    A16 = torch.empty(m, k, device=dev, dtype=torch.bfloat16)
+    C = torch.empty(m, n, device=dev, dtype=torch.float32)
+    B32 = torch.empty(k, n, device=dev, dtype=torch.float32)
+    B16 = torch.empty(k, n, device=dev, dtype=torch.bfloat16)
+    row0 = rank * m  # this rank's rows of the global A (M_total = m * world)
+    poas.fill_uniform(poas.DTYPE_F32, A32.data_ptr(), k, m, k, row0, 0, k, sa)
+    poas.fill_uniform(poas.DTYPE_BF16, A16.data_ptr(), k, m, k, row0, 0, k, sa)
+    if rank == 0:
+        poas.fill_uniform(poas.DTYPE_F32, B32.data_ptr(), n, k, n, 0, 0, n, sb)
+        poas.fill_uniform(poas.DTYPE_BF16, B16.data_ptr(), n, k, n, 0, 0, n, sb)
+    else:
+        B32.zero_()
+        B16.zero_()
+    torch.cuda.synchronize()
+
+    ex = poas.Executor(units_res)
+    io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=n,
+                     a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=n,
+                     c_dev=C.data_ptr(), ldc_dev=n, resident=1)
+    need_b32 = rows.get(simt_id, 0) > 0
+
+    def step(repeats=1):
+        if world > 1:  # B lives on rank 0: broadcast over NVLink inside the step
+            dist.broadcast(B16, src=0)
+            if need_b32:
+                dist.broadcast(B32, src=0)
+        return ex.execute(schedule, io, repeats)
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reports = []
+    with ClockSampler(g) as clk:
+        e0.record()
+        if world > 1:
+            for _ in range(args.steps):
+                reports.append(step())
+        else:
+            reports.append(ex.execute(schedule, io, args.steps))
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    t = torch.tensor([ms_total], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    flops_step_total = 2.0 * m * world * n * k
+    value = flops_step_total / (ms_step * 1e-3) / 1e12
+    clocks = clk.summary()
+
+    # per-unit measured vs predicted (mean over the timed reports)
+    def unit_mean(key, field="measured"):
+        vals = []
+        for r in reports:
+            for d in r["devices"]:
+                if d["id"] == key:
+                    vals.append(d["compute"][field] * (1 if len(reports) > 1 else 1))
+        return sum(vals) / len(vals) if vals else 0.0
+
+    rep_last = reports[-1]
+    meas_make = sum(r["measured_makespan"] for r in reports) / len(reports)
+    pred_make = rep_last["predicted_makespan"]
+    tc_compute = unit_mean(tc_id)
+    tc_rows = rows.get(tc_id, 0)
+    peak_burst, peak_sust, peak_kind = measured_peaks()
+    achieved = 2.0 * tc_rows * n * k / tc_compute / 1e12 if tc_compute > 0 else 0.0
+    traffic = None
+    tp = ROOT / "profiles" / "tc_gemm_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(str(args.n))
+        except Exception:
+            traffic = None
+
+    # ---- speedup vs best single unit (the tensor unit; the 2-SM CUDA-core
+    # unit alone is predicted ~3 orders of magnitude slower)
+    standalone = {}
+    for uid in (tc_id,):
+        s_sched = poas.plan_standalone(profile, uid, m, n, k)
+        for _ in range(2):
+            ex.execute(s_sched, io, 1)
+        r = ex.execute(s_sched, io, max(3, args.steps // 2))
+        standalone[uid] = r["measured_makespan"]
+    simt_alone_pred = json.loads(poas.plan_standalone(profile, simt_id, m, n, k))["makespan"]
+    best_single = min(standalone.values())
+    speedup = best_single / meas_make if meas_make > 0 else None
+
+    # tensor-core-only on every SM (what a non-POAS caller would run)
+    sms_all = poas.sm_count()
+    tc_all_ms = None
+    if world == 1:
+        s = torch.cuda.current_stream().cuda_stream
+        for _ in range(3):
+            poas.tc_gemm(poas.DTYPE_BF16, m, n, k, A16.data_ptr(), k, B16.data_ptr(), n, C.data_ptr(), n,
+                         stream=s)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            poas.tc_gemm(poas.DTYPE_BF16, m, n, k, A16.data_ptr(), k, B16.data_ptr(), n, C.data_ptr(), n,
+                         stream=s)
+        e1.record()
+        torch.cuda.synchronize()
+        tc_all_ms = e0.elapsed_time(e1) / 5
+
+    # ---- e2e through the C ABI with host buffers (fp32 over PCIe)
+    e2e = None
+    if not args.no_e2e:
+        units_e2e = units_res.replace("elem=2:link=hbm", "elem=4:link=pcie").replace(
+            "elem=4:link=hbm", "elem=4:link=pcie")
+        prof_e2e = poas.profile_machine(units_e2e, PROFILING, bus=True)
+        sched_e2e = poas.plan(prof_e2e, m, n, k)
+        se = json.loads(sched_e2e)
+        if save and rank == 0:
+            (save / "profile_e2e.txt").write_text(prof_e2e)
+            (save / "schedule_e2e.json").write_text(sched_e2e)
+        hA = torch.empty(m, k, dtype=torch.float32, pin_memory=True)
+        hB = torch.empty(k, n, dtype=torch.float32, pin_memory=True)
+        hC = torch.empty(m, n, dtype=torch.float32, pin_memory=True)
+        poas.fill_uniform_host(hA.data_ptr(), k, m, k, row0, 0, k, sa)
+        poas.fill_uniform_host(hB.data_ptr(), n, k, n, 0, 0, n, sb)
+        ex_e2e = poas.Executor(units_e2e)
+        io_h = poas.GemmIO(m=m, n=n, k=k, a_host=hA.data_ptr(), lda_host=k, b_host=hB.data_ptr(),
+                           ldb_host=n, c_host=hC.data_ptr(), ldc_host=n, resident=0)
+        ex_e2e.execute(sched_e2e, io_h, 1)
+        if world > 1:
+            dist.barrier()
+        steps_e2e = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        r_e2e = ex_e2e.execute(sched_e2e, io_h, steps_e2e)
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall], device=dev)
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        wall = float(tw.item())
+        h2d = sum(4 * (d["rows"] * k + k * n) for d in se["devices"] if d["rows"] > 0)
+        d2h = sum(4 * d["rows"] * n for d in se["devices"] if d["rows"] > 0)
+        e2e = {"value": round(2.0 * m * world * n * k / (wall / steps_e2e) / 1e12, 3), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "ms_per_step": round(wall / steps_e2e * 1e3, 3),
+               "plan_rows": {d["id"]: d["rows"] for d in se["devices"]},
+               "predicted_makespan_ms": round(r_e2e["predicted_makespan"] * 1e3, 4),
+               "measured_makespan_ms": round(r_e2e["measured_makespan"] * 1e3, 4),
+               "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
+               "path": "poas_b200_execute (C ABI), pinned host fp32 A/B/C, H2D+compute+D2H in step"}
+        if save and rank == 0:
+            (save / "report_e2e.json").write_text(json.dumps(r_e2e, indent=1))
+
+    # ---- CPU baseline (rank 0 at N=1 only)
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            tfl, sec, sample, cores = reference_cpu_path(args.n, sample_rows=args.ref_rows, reps=1)
+            cpu_baseline = {"value": round(tfl, 4), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                            "sample": sample}
+        except Exception as exc:  # reported, never fatal
+            cpu_baseline = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                            "sample": f"unavailable: {exc}"}
+
+    launches_per_step = sum(1 for d in sched["devices"] if d["rows"] > 0)
+    if save and rank == 0:
+        (save / "report_resident.json").write_text(json.dumps(rep_last, indent=1))
+    if rank == 0:
+        line = {
+            "metric": "co-executed GEMM TFLOP/s at N=16384 (1/2/4/8 B200); speedup vs best single unit",
+            "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {
+                "workload": f"C3: square GEMM N={args.n} per GPU (M={m}*{world}), bf16 tensor-core + fp32 "
+                            f"CUDA-core co-execution planned by POAS; B broadcast from rank 0 (NCCL) at N>1",
+                "m": m * world, "n": n, "k": k, "parallelism": f"POAS row split x {world} GPU(s)",
+                "units": {tc_id: f"tcgen05 bf16->fp32 on {args.tc_sms} SMs",
+                          simt_id: f"fp32 SIMT on {args.simt_sms} SMs"},
+                "plan_rows": rows, "l2": "inputs larger than L2 (A,B bf16 512 MiB each; fp32 1 GiB each)",
+                "predicted_makespan_ms": round(pred_make * 1e3, 4),
+                "measured_makespan_ms": round(meas_make * 1e3, 4),
+                "makespan_error_pct": round(100.0 * (meas_make - pred_make) / meas_make, 3),
+                "speedup_vs_best_single_unit": round(speedup, 4) if speedup else None,
+                "best_single_unit": {"id": tc_id, "measured_makespan_ms": round(best_single * 1e3, 4)},
+                "simt_standalone_predicted_ms": round(simt_alone_pred * 1e3, 2),
+                "tc_only_all_sms_tflops": round(2.0 * m * n * k / (tc_all_ms * 1e-3) / 1e12, 2)
+                if tc_all_ms else None,
+                "sm_count": sms_all, "profile_seconds": round(t_prof, 2),
+            },
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst,
+                         "unit": "TFLOP/s", "frac": round(achieved / peak_burst, 4),
+                         "traffic": traffic, "kernel": "tc_gemm_kernel",
+                         "peak_kind": f"{peak_kind} bf16 burst (sustained {peak_sust})"},
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -166,6 +166,114 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p
   }
 }
 
+// Skinny-M path (M < 128: a co-executed CUDA-core share is often a handful
+// of rows). A 16 x 1024 output block per CTA: each thread keeps all 16 rows
+// x 4 columns in registers, streams its B columns straight from global
+// memory (one coalesced 128-bit load per k, 8 k-steps in flight), and reads
+// the 16 x kSkBK A panel from shared memory as warp-broadcast float4s.
+constexpr int kSkCols = 1024;
+constexpr int kSkBK = 32;
+
+template <bool kVec, int kSkRows>
+__global__ void __launch_bounds__(kThreads, 1) simt_skinny_kernel(const SimtArgs p) {
+  __shared__ __align__(16) float As[kSkBK][kSkRows];  // A panel, transposed
+  const int tid = threadIdx.x;
+  const int row_groups = (p.M + kSkRows - 1) / kSkRows;
+  const int col_blocks = (p.N + kSkCols - 1) / kSkCols;
+  const int total = row_groups * col_blocks;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int r0 = (t % row_groups) * kSkRows;
+    const int c = (t / row_groups) * kSkCols + tid * 4;
+    float acc[kSkRows][4];
+#pragma unroll
+    for (int i = 0; i < kSkRows; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    const bool col_vec = kVec && c + 3 < p.N;
+    for (int k0 = 0; k0 < p.K; k0 += kSkBK) {
+      __syncthreads();
+      // 256 threads stage 16 x 32 A values (2 each), transposed.
+      for (int e = tid; e < kSkRows * kSkBK; e += kThreads) {
+        const int rr = e / kSkBK, kk = e % kSkBK;
+        const int gr = r0 + rr, gk = k0 + kk;
+        As[kk][rr] = (gr < p.M && gk < p.K) ? p.A[(long long)gr * p.lda + gk] : 0.f;
+      }
+      __syncthreads();
+      const int kn = min(kSkBK, p.K - k0);
+#pragma unroll 8
+      for (int kk = 0; kk < kSkBK; ++kk) {
+        if (kk >= kn) break;
+        const float* brow = p.B + (long long)(k0 + kk) * p.ldb;
+        float4 b;
+        if (col_vec) {
+          b = __ldg(reinterpret_cast<const float4*>(brow + c));
+        } else {
+          b.x = c < p.N ? brow[c] : 0.f;
+          b.y = c + 1 < p.N ? brow[c + 1] : 0.f;
+          b.z = c + 2 < p.N ? brow[c + 2] : 0.f;
+          b.w = c + 3 < p.N ? brow[c + 3] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < kSkRows / 4; ++q) {
+          const float4 a = *reinterpret_cast<const float4*>(&As[kk][4 * q]);
+          const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            acc[4 * q + i][0] = fmaf(av[i], b.x, acc[4 * q + i][0]);
+            acc[4 * q + i][1] = fmaf(av[i], b.y, acc[4 * q + i][1]);
+            acc[4 * q + i][2] = fmaf(av[i], b.z, acc[4 * q + i][2]);
+            acc[4 * q + i][3] = fmaf(av[i], b.w, acc[4 * q + i][3]);
+          }
+        }
+      }
+    }
+    if (c >= p.N) continue;
+#pragma unroll
+    for (int i = 0; i < kSkRows; ++i) {
+      const int r = r0 + i;
+      if (r >= p.M) break;
+      float* crow = p.C + (long long)r * p.ldc;
+      if (col_vec) {
+        float4 o = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (p.accumulate) {
+          const float4 q = *reinterpret_cast<const float4*>(crow + c);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(crow + c) = o;
+      } else {
+        for (int e = 0; e < 4 && c + e < p.N; ++e) {
+          float o = acc[i][e];
+          if (p.accumulate) o += crow[c + e];
+          crow[c + e] = o;
+        }
+      }
+    }
+  }
+}
+
+template <bool kVec, int kRows>
+cudaError_t launch_skinny_t(int grid, size_t dyn, cudaStream_t stream, const SimtArgs& p) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(simt_skinny_kernel<kVec, kRows>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  });
+  if (err != cudaSuccess) return err;
+  simt_skinny_kernel<kVec, kRows><<<grid, kThreads, dyn, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_skinny(bool vec, int rows, int grid, size_t dyn, cudaStream_t s,
+                          const SimtArgs& p) {
+  if (vec) {
+    if (rows == 4) return launch_skinny_t<true, 4>(grid, dyn, s, p);
+    if (rows == 8) return launch_skinny_t<true, 8>(grid, dyn, s, p);
+    return launch_skinny_t<true, 16>(grid, dyn, s, p);
+  }
+  if (rows == 4) return launch_skinny_t<false, 4>(grid, dyn, s, p);
+  if (rows == 8) return launch_skinny_t<false, 8>(grid, dyn, s, p);
+  return launch_skinny_t<false, 16>(grid, dyn, s, p);
+}
+
 }  // namespace
 
 cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
@@ -208,6 +316,16 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
   });
   if (attr_err != cudaSuccess) return attr_err;
   int grid = num_ctas > 0 ? num_ctas : device_sm_count();
+  if (M < kBM) {
+    // Row-group height: smallest of 4/8/16 covering M (no padded FMAs for
+    // the common 4- or 8-row shares).
+    const int rg = M <= 4 ? 4 : (M <= 8 ? 8 : 16);
+    const int tiles = static_cast<int>(((M + rg - 1) / rg) * ((N + kSkCols - 1) / kSkCols));
+    if (grid > tiles) grid = tiles;
+    // Exclusive units pad dynamic shared memory so no tensor CTA shares the SM.
+    const size_t dyn = exclusive_sm ? 100 * 1024 : 0;
+    return launch_skinny(vec, rg, grid, dyn, stream, p);
+  }
   const int tiles = p.tiles_m * p.tiles_n;
   if (grid > tiles) grid = tiles;
   if (vec)

@@ -127,19 +127,23 @@ namespace poas_b200 {
 poas::MachineProfile profile_units(const std::vector<std::unique_ptr<Unit>>& units,
                                    const poas::ProfilingConfig& cfg, bool bus) {
   std::vector<poas::DeviceProbeData> probes;
+  std::vector<poas::SideRange> ranges;
   for (const auto& u : units) {
     poas::DeviceProbeData p;
     p.id = u->spec().id;
     p.kind = u->spec().kind;
     p.elem_size = u->spec().elem;
-    p.samples = poas::run_compute_probes(*u, cfg.range_for(p.kind), cfg.probes, cfg.repetitions);
+    poas::SideRange range = cfg.range_for(p.kind);
+    if (u->spec().probe_min > 0) range = {u->spec().probe_min, u->spec().probe_max};
+    ranges.push_back(range);
+    p.samples = poas::run_compute_probes(*u, range, cfg.probes, cfg.repetitions);
     if (u->has_transfers())
       p.bandwidth = poas::run_bandwidth_probe(*u, cfg.bandwidth_payload, cfg.repetitions);
     if (p.kind == poas::DeviceKind::xpu) p.align = u->spec().align;
     if (p.kind == poas::DeviceKind::cpu) p.cache_bytes = llc_bytes();
     probes.push_back(std::move(p));
   }
-  return poas::fit_machine(probes, bus, cfg);
+  return poas::fit_machine_ranges(probes, bus, cfg, ranges);
 }
 
 }  // namespace poas_b200

@@ -68,6 +68,14 @@ UnitSpec parse_unit_spec(const std::string& text) {
       if (v == "bf16") u.dtype = AbType::bf16;
       else if (v == "f16" || v == "fp16") u.dtype = AbType::f16;
       else poas::fail(poas::errc::invalid_argument, "unit spec: dtype must be bf16 or f16");
+    } else if (k == "probe") {
+      const auto dash = v.find('-');
+      if (dash == std::string::npos)
+        poas::fail(poas::errc::invalid_argument, "unit spec: probe must be MIN-MAX");
+      u.probe_min = to_long(v.substr(0, dash), k);
+      u.probe_max = to_long(v.substr(dash + 1), k);
+      if (u.probe_min < 1 || u.probe_max < u.probe_min)
+        poas::fail(poas::errc::invalid_argument, "unit spec: bad probe range " + v);
     } else if (k == "link") {
       if (v == "pcie") u.link = Link::pcie;
       else if (v == "hbm") u.link = Link::hbm;
@@ -191,6 +199,10 @@ double Unit::time_gemm(std::int64_t side) {
 
   DeviceGuard g(spec_.device);
   const bool tensor = spec_.kind == poas::DeviceKind::xpu;
+  // A tensor unit whose link carries fp32 (elem 4) receives fp32 operands
+  // and converts them to 16-bit inside its compute phase (executor.cpp);
+  // the probe times exactly that.
+  const bool converts = tensor && spec_.elem == 4;
   // 16-bit operands need a 16-byte row pitch for TMA: pad the leading dim.
   const std::int64_t ld = tensor ? round_up(side, 8) : side;
   const std::size_t esz = tensor ? 2 : 4;
@@ -202,10 +214,23 @@ double Unit::time_gemm(std::int64_t side) {
     const AbType t = tensor ? spec_.dtype : AbType::f32;
     cuda_check(fill_uniform(t, a, ld, side, side, 0, 0, side, 0x5eedA, stream_), "fill");
     cuda_check(fill_uniform(t, b, ld, side, side, 0, 0, side, 0x5eedB, stream_), "fill");
+    if (converts) {
+      const std::size_t f32 = static_cast<std::size_t>(side) * side * 4;
+      cuda_check(fill_uniform(AbType::f32, probe_a32_.ensure(f32), side, side, side, 0, 0, side,
+                              0x5eedA, stream_), "fill");
+      cuda_check(fill_uniform(AbType::f32, probe_b32_.ensure(f32), side, side, side, 0, 0, side,
+                              0x5eedB, stream_), "fill");
+    }
     probe_side_ = side;
     gemm(side, side, side, a, ld, b, ld, static_cast<float*>(probe_c_.get()), side, false);
   }
   cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+  if (converts) {
+    cuda_check(convert_f32(spec_.dtype, static_cast<const float*>(probe_a32_.get()), side,
+                           probe_a_.get(), ld, side, side, stream_), "convert");
+    cuda_check(convert_f32(spec_.dtype, static_cast<const float*>(probe_b32_.get()), side,
+                           probe_b_.get(), ld, side, side, stream_), "convert");
+  }
   gemm(side, side, side, probe_a_.get(), ld, probe_b_.get(), ld,
        static_cast<float*>(probe_c_.get()), side, false);
   cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");

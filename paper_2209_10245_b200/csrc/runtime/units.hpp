@@ -35,6 +35,8 @@ struct UnitSpec {
   int threads = 0;              // cpu: OpenMP threads (0 = all cores)
   std::int64_t align = 8;       // xpu row alignment (16-byte TMA pitch for 16-bit)
   Link link = Link::pcie;       // what time_transfer measures
+  std::int64_t probe_min = 0;   // own probe side range ("probe=MIN-MAX"); 0 = config's
+  std::int64_t probe_max = 0;
 };
 
 // "<id>=<kind>[:key=value]*"
@@ -97,7 +99,7 @@ class Unit : public poas::DeviceBackend {
   UnitSpec spec_;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
-  DeviceBuffer probe_a_, probe_b_, probe_c_, xfer_dev_, xfer_dev2_;
+  DeviceBuffer probe_a_, probe_b_, probe_c_, probe_a32_, probe_b32_, xfer_dev_, xfer_dev2_;
   PinnedBuffer xfer_host_;
   std::vector<float> host_a_, host_b_, host_c_;
   std::int64_t probe_side_ = 0;

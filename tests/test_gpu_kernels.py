@@ -1,0 +1,175 @@
+"""GPU parity of the unit kernels against the fp64 CPU oracle
+(oracle/gemm_oracle.c) on the same (rounded) inputs.
+
+Tolerances (stated here): relative Frobenius error against the
+fp64 oracle on the SAME rounded inputs <= 2e-5 for every unit; generator and
+RNE conversions bit-exact.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+def _dev_fill(torch, poas, rows, cols, seed, dtype=None, ld=None):
+    ld = ld or cols
+    t = torch.empty(rows, ld, device="cuda", dtype=torch.float32)
+    poas.fill_uniform(poas.DTYPE_F32, t.data_ptr(), ld, rows, cols, 0, 0, cols, seed)
+    return t
+
+
+def test_device_generator_bit_identical_to_oracle(torch_cuda, poas):
+    import oracle
+
+    torch = torch_cuda
+    seed = poas.stream_seed(20261017, "A")
+    assert seed == oracle.stream_seed(20261017, "A")
+    for rows, cols, r0, c0, tot in [(37, 53, 0, 0, 53), (64, 64, 5, 7, 1000), (1, 4096, 3, 0, 4096)]:
+        t = torch.empty(rows, cols, device="cuda")
+        poas.fill_uniform(poas.DTYPE_F32, t.data_ptr(), cols, rows, cols, r0, c0, tot, seed)
+        ref = oracle.fill_uniform(rows, cols, seed, r0, c0, tot)
+        assert np.array_equal(t.cpu().numpy(), ref)
+        host = np.empty((rows, cols), dtype=np.float32)
+        poas.fill_uniform_host(host.ctypes.data, cols, rows, cols, r0, c0, tot, seed)
+        assert np.array_equal(host, ref)
+        for dt, mode in ((poas.DTYPE_BF16, 2), (poas.DTYPE_F16, 1)):
+            td = torch.bfloat16 if dt == poas.DTYPE_BF16 else torch.float16
+            h = torch.empty(rows, cols, device="cuda", dtype=td)
+            poas.fill_uniform(dt, h.data_ptr(), cols, rows, cols, r0, c0, tot, seed)
+            assert np.array_equal(h.float().cpu().numpy(), oracle.round_to(ref, mode))
+
+
+def test_convert_rne_bit_identical(torch_cuda, poas):
+    import oracle
+
+    torch = torch_cuda
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal((257, 129)) * 10.0 ** rng.integers(-6, 4, (257, 129))).astype(np.float32)
+    src = torch.from_numpy(x).cuda()
+    for dt, mode, td in ((poas.DTYPE_BF16, 2, torch.bfloat16), (poas.DTYPE_F16, 1, torch.float16)):
+        out = torch.empty(257, 136, device="cuda", dtype=td)
+        poas.convert_f32(dt, src.data_ptr(), 129, out.data_ptr(), 136, 257, 129)
+        torch.cuda.synchronize()
+        got = out[:, :129].float().cpu().numpy()
+        assert np.array_equal(got, oracle.round_to(x, mode))
+
+
+TC_SHAPES = [(128, 256, 64), (1000, 1000, 1000), (129, 300, 72), (64, 4096, 512), (4096, 64, 1024),
+             (1, 1, 8), (7, 1000, 24), (255, 257, 136), (2048, 2048, 2048), (333, 1536, 4104)]
+
+
+@pytest.mark.parametrize("shape", TC_SHAPES)
+@pytest.mark.parametrize("dtype,mode", [(2, 2), (1, 1)])
+def test_tc_gemm_vs_oracle(torch_cuda, poas, shape, dtype, mode):
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = shape
+    A = oracle.fill_uniform(m, k, 11)
+    B = oracle.fill_uniform(k, n, 12)
+    lda, ldb = (k + 7) // 8 * 8, (n + 7) // 8 * 8
+    td = torch.bfloat16 if dtype == 2 else torch.float16
+    a = torch.zeros(m, lda, device="cuda", dtype=td)
+    b = torch.zeros(k, ldb, device="cuda", dtype=td)
+    a[:, :k] = torch.from_numpy(A).cuda().to(td)
+    b[:, :n] = torch.from_numpy(B).cuda().to(td)
+    c = torch.full((m, n), float("nan"), device="cuda")
+    poas.tc_gemm(dtype, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), n)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_rows_f64(A, B, mode)
+    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 7, 146])
+def test_tc_gemm_sm_budget_and_accumulate(torch_cuda, poas, ctas):
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = 700, 900, 264
+    A, B = oracle.fill_uniform(m, k, 3), oracle.fill_uniform(k, n, 4)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(np.pad(B, ((0, 0), (0, 4)))).cuda().bfloat16()
+    c0 = oracle.fill_uniform(m, n, 5)
+    c = torch.from_numpy(c0).cuda()
+    poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n + 4, c.data_ptr(), n, accumulate=True,
+                 num_ctas=ctas)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_rows_f64(A, B, 2) + c0.astype(np.float64)
+    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+
+
+def test_tc_gemm_rejects_misaligned_pitch(torch_cuda, poas):
+    from paper_2209_10245_b200 import PoasError
+
+    torch = torch_cuda
+    a = torch.zeros(16, 20, device="cuda", dtype=torch.bfloat16)
+    c = torch.zeros(16, 20, device="cuda")
+    with pytest.raises(PoasError) as e:  # 20 bf16 = 40 B row pitch: not a TMA 16 B multiple
+        poas.tc_gemm(2, 16, 20, 20, a.data_ptr(), 20, a.data_ptr(), 20, c.data_ptr(), 20)
+    assert e.value.errc == "cuda"
+
+
+SIMT_SHAPES = [(128, 128, 16), (1000, 1000, 1000), (129, 300, 72), (77, 33, 5), (1, 5000, 777),
+               (3, 4096, 1024), (8, 16384, 256), (16, 1030, 64), (17, 999, 33), (127, 513, 100),
+               (2048, 2048, 2048)]
+
+
+@pytest.mark.parametrize("shape", SIMT_SHAPES)
+@pytest.mark.parametrize("ctas", [0, 2])
+def test_simt_gemm_vs_oracle(torch_cuda, poas, shape, ctas):
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = shape
+    A, B = oracle.fill_uniform(m, k, 21), oracle.fill_uniform(k, n, 22)
+    a, b = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    c = torch.full((m, n), float("nan"), device="cuda")
+    poas.simt_gemm(m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n, num_ctas=ctas,
+                   exclusive=ctas > 0)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_rows_f64(A, B, 0)
+    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+
+
+def test_simt_accumulate_and_strided(torch_cuda, poas):
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = 300, 500, 96
+    A, B, C0 = oracle.fill_uniform(m, k + 3, 1), oracle.fill_uniform(k, n + 5, 2), oracle.fill_uniform(m, n, 3)
+    a, b, c = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), torch.from_numpy(C0).cuda()
+    poas.simt_gemm(m, n, k, a.data_ptr(), k + 3, b.data_ptr(), n + 5, c.data_ptr(), n, accumulate=True)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_rows_f64(A[:, :k], B[:, :n], 0) + C0
+    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+
+
+def test_full_size_tc_property(torch_cuda, poas):
+    """BASELINE size (16384^3): size-independent check C.x == A.(B.x) for a
+    random x, in fp64 on the device, on the rounded bf16 inputs."""
+    torch = torch_cuda
+    n = 16384
+    sa, sb = poas.stream_seed(20261017, "A"), poas.stream_seed(20261017, "B")
+    a = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
+    b = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
+    poas.fill_uniform(poas.DTYPE_BF16, a.data_ptr(), n, n, n, 0, 0, n, sa)
+    poas.fill_uniform(poas.DTYPE_BF16, b.data_ptr(), n, n, n, 0, 0, n, sb)
+    c = torch.empty(n, n, device="cuda")
+    poas.tc_gemm(2, n, n, n, a.data_ptr(), n, b.data_ptr(), n, c.data_ptr(), n)
+    torch.cuda.synchronize()
+    x = torch.randn(n, 4, device="cuda", dtype=torch.float64)
+    lhs = c.double() @ x
+    rhs = a.double() @ (b.double() @ x)
+    rel = ((lhs - rhs).norm() / rhs.norm()).item()
+    assert rel <= TOL, rel
