@@ -218,7 +218,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2209_10245_b200 import poas
+    from paper_2209_10245_b200 import poas, shard
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
@@ -272,14 +272,16 @@ def main():
     io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=n,
                      a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=n,
                      c_dev=C.data_ptr(), ldc_dev=n, resident=1)
-    need_b32 = rows.get(simt_id, 0) > 0
+    # B in every precision a busy unit consumes is what crosses NVLink.
+    b_needed = [B16] + ([B32] if rows.get(simt_id, 0) > 0 else [])
+    # Level-1 (per-GPU) split of the whole job by the same planner: equal
+    # shards of `m` rows for identical GPUs (weak scaling).
+    l1_rows = shard.shard_rows(world, m * world, n, k, profile) if world > 1 else [m]
+    assert l1_rows == [m] * world, l1_rows
 
     def step(repeats=1):
-        if world > 1:  # B lives on rank 0: broadcast over NVLink inside the step
-            dist.broadcast(B16, src=0)
-            if need_b32:
-                dist.broadcast(B32, src=0)
-        return ex.execute(schedule, io, repeats)
+        # B lives on rank 0: NCCL broadcast over NVLink inside the step (N > 1)
+        return shard.sharded_step(ex, schedule, io, b_needed, repeats)
 
     for _ in range(args.warmup):
         step()
@@ -430,6 +432,7 @@ def main():
                 "workload": f"C3: square GEMM N={args.n} per GPU (M={m}*{world}), bf16 tensor-core + fp32 "
                             f"CUDA-core co-execution planned by POAS; B broadcast from rank 0 (NCCL) at N>1",
                 "m": m * world, "n": n, "k": k, "parallelism": f"POAS row split x {world} GPU(s)",
+                "level1_rows_per_gpu": l1_rows,
                 "units": {tc_id: f"tcgen05 bf16->fp32 on {args.tc_sms} SMs",
                           simt_id: f"fp32 SIMT on {args.simt_sms} SMs"},
                 "plan_rows": rows, "l2": "inputs larger than L2 (A,B bf16 512 MiB each; fp32 1 GiB each)",

@@ -34,6 +34,11 @@ cudaError_t fill_uniform(AbType t, void* dst, int64_t ld, int64_t rows, int64_t 
 cudaError_t convert_f32(AbType t, const float* src, int64_t ld_src, void* dst, int64_t ld_dst,
                         int64_t rows, int64_t cols, cudaStream_t stream);
 
+// Streaming read of `bytes` (multiple of 16) by `num_ctas` CTAs of 512
+// threads (0 = one per SM): the HBM bandwidth a unit on that SM budget sees.
+cudaError_t stream_read(const void* src, size_t bytes, int num_ctas, float* sink,
+                        cudaStream_t stream);
+
 int device_sm_count();
 
 }  // namespace poas_b200

@@ -249,6 +249,142 @@ __global__ void __launch_bounds__(kThreads, 1) simt_skinny_kernel(const SimtArgs
   }
 }
 
+// Pipelined skinny path for 16-byte aligned operands. A skinny share is
+// bound by streaming B (each B element feeds only `kRows` FMAs), so the
+// kernel is built around bytes in flight: every thread cp.async's its own
+// 4 columns of `kPipeK` consecutive B rows per stage into a `stages`-deep
+// shared-memory ring (up to ~190 KB in flight per SM on an exclusive SM).
+// A thread only ever reads the smem it filled itself, so the ring needs no
+// block barrier -- only per-thread cp.async group waits. A values come
+// through L1 as warp-uniform 128-bit loads.
+constexpr int kPipeK = 8;  // B rows per stage: 8 x 1024 x 4 B = 32 KB per stage
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int kN>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
+}
+
+template <int kRows>
+__global__ void __launch_bounds__(kThreads, 1) simt_skinny_pipe_kernel(const SimtArgs p,
+                                                                         int stages) {
+  // Ring slot = B part [kPipeK][kThreads] float4 (thread-private columns)
+  //           + A part [kRows][kPipeK] floats (shared, filled by 2*kRows threads).
+  constexpr int kSlotB = kPipeK * kThreads;            // float4s
+  constexpr int kSlotA = kRows * kPipeK / 4;           // float4s
+  constexpr int kSlot = kSlotB + kSlotA;
+  extern __shared__ float4 ring[];
+  const int tid = threadIdx.x;
+  const int row_groups = (p.M + kRows - 1) / kRows;
+  const int col_blocks = (p.N + kSkCols - 1) / kSkCols;
+  const int total = row_groups * col_blocks;
+  const int steps = (p.K + kPipeK - 1) / kPipeK;
+  constexpr int kAhead = 5;  // wait depth below is compile-time: stages must be kAhead + 1
+
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int r0 = (t % row_groups) * kRows;
+    const int c = (t / row_groups) * kSkCols + tid * 4;
+    const int col_bytes = c < p.N ? min(16, (p.N - c) * 4) : 0;
+    const float* bcol = p.B + (c < p.N ? c : 0);
+    // A staging role: threads [0, 2*kRows) copy 4 floats each per stage.
+    const int a_row = tid >> 1, a_half = tid & 1;
+    const bool a_loader = tid < 2 * kRows;
+    const bool a_row_ok = a_loader && r0 + a_row < p.M;
+    const float* arow = p.A + (long long)(a_row_ok ? r0 + a_row : 0) * p.lda;
+
+    auto issue = [&](int step) {
+      if (step < steps) {
+        float4* slot = ring + (step % stages) * kSlot;
+        const int k0 = step * kPipeK;
+#pragma unroll
+        for (int kk = 0; kk < kPipeK; ++kk) {
+          const bool in = k0 + kk < p.K;
+          cp_async16(slot + kk * kThreads + tid, in ? bcol + (long long)(k0 + kk) * p.ldb : bcol,
+                     in ? col_bytes : 0);
+        }
+        if (a_loader) {
+          const int ka = k0 + a_half * 4;
+          const int bytes = a_row_ok ? max(0, min(16, (p.K - ka) * 4)) : 0;
+          cp_async16(slot + kSlotB + a_row * (kPipeK / 4) + a_half, bytes ? arow + ka : arow, bytes);
+        }
+      }
+      cp_async_commit();  // empty groups keep the wait arithmetic uniform
+    };
+
+    float acc[kRows][4];
+#pragma unroll
+    for (int i = 0; i < kRows; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+    __syncthreads();  // the previous tile's readers are done with every slot
+    for (int s = 0; s < kAhead; ++s) issue(s);
+    for (int step = 0; step < steps; ++step) {
+      cp_async_wait<kAhead - 1>();  // this thread's copies for `step` have landed
+      __syncthreads();               // ... and every thread's (the shared A part)
+      issue(step + kAhead);          // refills the slot everyone finished last step
+      const float4* slot = ring + (step % stages) * kSlot;
+      const float* As = reinterpret_cast<const float*>(slot + kSlotB);
+#pragma unroll
+      for (int kk = 0; kk < kPipeK; ++kk) {
+        const float4 b = slot[kk * kThreads + tid];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+          const float a = As[i * kPipeK + kk];  // warp-uniform: broadcast
+          acc[i][0] = fmaf(a, b.x, acc[i][0]);
+          acc[i][1] = fmaf(a, b.y, acc[i][1]);
+          acc[i][2] = fmaf(a, b.z, acc[i][2]);
+          acc[i][3] = fmaf(a, b.w, acc[i][3]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    if (c >= p.N) continue;
+#pragma unroll
+    for (int i = 0; i < kRows; ++i) {
+      const int r = r0 + i;
+      if (r >= p.M) break;
+      float* crow = p.C + (long long)r * p.ldc;
+      if (c + 3 < p.N) {
+        float4 o = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (p.accumulate) {
+          const float4 q = *reinterpret_cast<const float4*>(crow + c);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(crow + c) = o;
+      } else {
+        for (int e = 0; e < 4 && c + e < p.N; ++e) {
+          float o = acc[i][e];
+          if (p.accumulate) o += crow[c + e];
+          crow[c + e] = o;
+        }
+      }
+    }
+  }
+}
+
+template <int kRows>
+cudaError_t launch_pipe_t(int grid, cudaStream_t stream, const SimtArgs& p) {
+  constexpr int stages = 6;  // kAhead + 1
+  const size_t smem =
+      static_cast<size_t>(stages) * (kPipeK * kThreads + kRows * kPipeK / 4) * sizeof(float4);
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [smem] {
+    err = cudaFuncSetAttribute(simt_skinny_pipe_kernel<kRows>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  });
+  if (err != cudaSuccess) return err;
+  simt_skinny_pipe_kernel<kRows><<<grid, kThreads, smem, stream>>>(p, stages);
+  return cudaGetLastError();
+}
+
 template <bool kVec, int kRows>
 cudaError_t launch_skinny_t(int grid, size_t dyn, cudaStream_t stream, const SimtArgs& p) {
   static std::once_flag once;
@@ -322,6 +458,11 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
     const int rg = M <= 4 ? 4 : (M <= 8 ? 8 : 16);
     const int tiles = static_cast<int>(((M + rg - 1) / rg) * ((N + kSkCols - 1) / kSkCols));
     if (grid > tiles) grid = tiles;
+    if (vec && exclusive_sm) {  // the unit owns its SMs: spend their smem on bytes in flight
+      if (rg == 4) return launch_pipe_t<4>(grid, stream, p);
+      if (rg == 8) return launch_pipe_t<8>(grid, stream, p);
+      return launch_pipe_t<16>(grid, stream, p);
+    }
     // Exclusive units pad dynamic shared memory so no tensor CTA shares the SM.
     const size_t dyn = exclusive_sm ? 100 * 1024 : 0;
     return launch_skinny(vec, rg, grid, dyn, stream, p);

@@ -243,18 +243,22 @@ double Unit::time_gemm(std::int64_t side) {
 double Unit::time_transfer(std::uint64_t bytes) {
   if (!on_gpu()) poas::fail(poas::errc::backend_failure, "cpu unit has no link");
   DeviceGuard g(spec_.device);
-  void* dst = xfer_dev_.ensure(bytes);
-  const void* src = nullptr;
-  cudaMemcpyKind kind;
-  if (spec_.link == Link::pcie) {
-    src = xfer_host_.ensure(bytes);
-    kind = cudaMemcpyHostToDevice;
-  } else {
-    src = xfer_dev2_.ensure(bytes);
-    kind = cudaMemcpyDeviceToDevice;
-  }
   cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
-  cuda_check(cudaMemcpyAsync(dst, src, bytes, kind, stream_), "cudaMemcpyAsync");
+  if (spec_.link == Link::pcie) {
+    // Pinned host -> device over the unit's PCIe link (what execute() copies).
+    void* dst = xfer_dev_.ensure(bytes);
+    const void* src = xfer_host_.ensure(bytes);
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "cudaMemcpyAsync");
+  } else {
+    // Resident operands: the unit's "link" is its own path from HBM into its
+    // SMs -- a streaming read on exactly its SM budget. A 2-SM CUDA-core
+    // unit sees ~1/70 of what the 146-SM tensor unit sees, which is what
+    // makes receiving all of B (the model's copy-in) expensive for it.
+    const std::size_t rounded = (bytes + 15) / 16 * 16;
+    void* src = xfer_dev2_.ensure(rounded);
+    float* sink = static_cast<float*>(xfer_dev_.ensure(64));
+    cuda_check(stream_read(src, rounded, spec_.sms, sink, stream_), "stream_read");
+  }
   cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
   cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
   float ms = 0.f;

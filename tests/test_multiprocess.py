@@ -1,0 +1,97 @@
+"""N > 1 host logic on CPU: world_size-2 gloo processes run the sharded
+POAS step end to end with CPU units (the executor's host path), B broadcast
+from rank 0, and the gathered C checked against the fp64 oracle. Also the
+level-1 (per-GPU) split of BASELINE config C4 across 2/4/8 GPUs."""
+import json
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2209_10245_b200 import poas, shard
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m_total, n, k = 520, 192, 160
+    units = f"cpu{rank}=cpu:threads=2"
+    prof = poas.profile_machine(units, "probes=3,repetitions=1,cpu_min_side=48,cpu_max_side=128")
+    # level-1 split: planned on rank 0, shared (every rank could plan it too:
+    # the planner is deterministic given the profile)
+    obj = [None]
+    if rank == 0:
+        gpu_like = prof.replace("kind cpu", "kind gpu").replace("cache_bytes", "bandwidth_x")
+        gpu_like = "\n".join(l for l in gpu_like.splitlines() if not l.startswith("bandwidth_x"))
+        gpu_like = gpu_like.replace("bandwidth 0", "bandwidth 1e11")
+        obj = [shard.shard_rows(world, m_total, n, k, gpu_like, 1e11)]
+    dist.broadcast_object_list(obj, src=0)
+    rows = obj[0]
+    r0 = shard.row_offsets(rows)[rank]
+    m = rows[rank]
+    sched = poas.plan(prof, m, n, k)
+    assert sched == oracle.ref.plan(prof, m, n, k)
+
+    sa, sb = poas.stream_seed(20261017, "A"), poas.stream_seed(20261017, "B")
+    A = oracle.fill_uniform(m, k, sa, row0=r0, total_cols=k)  # this rank's rows only
+    B = torch.zeros(k, n) if rank else torch.from_numpy(oracle.fill_uniform(k, n, sb))
+    C = np.full((m, n), np.nan, dtype=np.float32)
+    io = poas.GemmIO(m=m, n=n, k=k, a_host=A.ctypes.data, lda_host=k, b_host=B.data_ptr(),
+                     ldb_host=n, c_host=C.ctypes.data, ldc_host=n, resident=1)
+    ex = poas.Executor(units)
+    rep = shard.sharded_step(ex, sched, io, [B])
+    assert rep["devices"][0]["rows"] == m
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (r0, C))
+    if rank == 0:
+        full = np.concatenate([c for _, c in sorted(gathered, key=lambda t: t[0])])
+        Afull = oracle.fill_uniform(m_total, k, sa)
+        ref = oracle.gemm_rows_f64(Afull, oracle.fill_uniform(k, n, sb), 0)
+        err = oracle.rel_frobenius(full, ref)
+        Path(out_dir, "result.json").write_text(json.dumps({"rows": rows, "err": err}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_gemm(tmp_path, ref):
+    port = _free_port()
+    mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    res = json.loads((tmp_path / "result.json").read_text())
+    assert sum(res["rows"]) == 520 and len(res["rows"]) == 2
+    assert res["err"] <= 2e-5
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_level1_split_config_c4(poas, world):
+    """C4: 65536 x 8192 x 8192 over G identical B200s -> equal shards (SURVEY
+    Appendix B: 32768x2 / 16384x4 / 8192x8)."""
+    from paper_2209_10245_b200 import shard
+
+    per_gpu = ("poas-profile v1\n\nbus true\n\ndevice gpu0.tc\nkind xpu\nslope 1.45e-15\n"
+               "intercept 2.0000000000000002e-05\nbandwidth 6500000000000\nelem_size 2\npriority 0\n"
+               "align 8\nops_min 549755813888\nops_max 4398046511104\n\ndevice gpu0.simt\nkind gpu\n"
+               "slope 3.5e-14\nintercept 2.0000000000000002e-05\nbandwidth 6500000000000\n"
+               "elem_size 4\npriority 1\nops_min 134217728\nops_max 8589934592\n")
+    rows = shard.shard_rows(world, 65536, 8192, 8192, per_gpu, 9e11)
+    assert rows == [65536 // world] * world
