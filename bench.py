@@ -205,6 +205,9 @@ def main():
     ap.add_argument("--tc-sms", type=int, default=TC_SMS)
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--policy", default="best-subset", choices=["reference", "best-subset"],
+                    help="planner policy: the reference algorithm (byte-identical plans) or the "
+                         "opt-in best-subset B200 extension")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=None)
     ap.add_argument("--save", default=None, help="directory for profile/schedule/report artefacts")
@@ -242,7 +245,8 @@ def main():
     t0 = time.perf_counter()
     profile = poas.profile_machine(units_res, PROFILING, bus=True)
     t_prof = time.perf_counter() - t0
-    schedule = poas.plan(profile, m, n, k)
+    schedule = poas.plan_policy(profile, m, n, k, args.policy)
+    ref_policy_makespan = json.loads(poas.plan(profile, m, n, k))["makespan"]
     sched = json.loads(schedule)
     rows = {d["id"]: d["rows"] for d in sched["devices"]}
     log(f"rank {rank}: profiled in {t_prof:.1f}s; plan rows {rows}; predicted {sched['makespan']*1e3:.3f} ms")
@@ -371,7 +375,8 @@ def main():
         units_e2e = units_res.replace("elem=2:link=hbm", "elem=4:link=pcie").replace(
             "elem=4:link=hbm", "elem=4:link=pcie")
         prof_e2e = poas.profile_machine(units_e2e, PROFILING, bus=True)
-        sched_e2e = poas.plan(prof_e2e, m, n, k)
+        sched_e2e = poas.plan_policy(prof_e2e, m, n, k, args.policy)
+        ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
         se = json.loads(sched_e2e)
         if save and rank == 0:
             (save / "profile_e2e.txt").write_text(prof_e2e)
@@ -401,6 +406,8 @@ def main():
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                "ms_per_step": round(wall / steps_e2e * 1e3, 3),
                "plan_rows": {d["id"]: d["rows"] for d in se["devices"]},
+               "reference_policy_plan_rows": {d["id"]: d["rows"] for d in ref_e2e["devices"]},
+               "reference_policy_predicted_ms": round(ref_e2e["makespan"] * 1e3, 4),
                "predicted_makespan_ms": round(r_e2e["predicted_makespan"] * 1e3, 4),
                "measured_makespan_ms": round(r_e2e["measured_makespan"] * 1e3, 4),
                "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
@@ -435,6 +442,8 @@ def main():
                 "level1_rows_per_gpu": l1_rows,
                 "units": {tc_id: f"tcgen05 bf16->fp32 on {args.tc_sms} SMs",
                           simt_id: f"fp32 SIMT on {args.simt_sms} SMs"},
+                "planner_policy": args.policy,
+                "reference_policy_predicted_ms": round(ref_policy_makespan * 1e3, 4),
                 "plan_rows": rows, "l2": "inputs larger than L2 (A,B bf16 512 MiB each; fp32 1 GiB each)",
                 "predicted_makespan_ms": round(pred_make * 1e3, 4),
                 "measured_makespan_ms": round(meas_make * 1e3, 4),

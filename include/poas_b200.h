@@ -65,6 +65,13 @@ const char* poas_b200_version(void);
 int poas_b200_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
                    char** schedule_json);
 
+/* poas_b200_plan with a planner policy: "reference" (== poas_b200_plan) or
+ * "best-subset" -- an opt-in B200 extension that also plans every subset of
+ * units and keeps the smallest predicted makespan (the reference LP charges
+ * every unit the full B transfer; proj/src/optimizer.cpp:21-32,257-275). */
+int poas_b200_plan_policy(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                          const char* policy, char** schedule_json);
+
 /* standalone_schedule (proj/include/poas/scheduler.hpp:40-41). */
 int poas_b200_plan_standalone(const char* profile_text, const char* device_id, int64_t m,
                               int64_t n, int64_t k, char** schedule_json);

@@ -17,7 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "kernels.hpp"
 #include "sm100_ptx.cuh"
@@ -223,6 +225,198 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------- 2-SM (cta_group::2) kernel
+// A CTA pair (cluster of 2 on one TPC) owns a 256 x 256 output tile. Each
+// CTA stages 128 rows of A and 128 columns of B per 64-deep K block (32 KB
+// per stage per CTA, 6 stages); the leader's single thread issues
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads both CTAs'
+// shared memory and writes both CTAs' TMEM (each holds its 128 rows x 256
+// fp32 columns, double buffered). Versus two independent 128 x 256 CTAs this
+// moves 1/3 fewer operand bytes from L2 into shared memory per MAC.
+constexpr int k2Stages = 6;
+constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
+constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
+constexpr int k2StageBytes = k2ABytes + k2BBytes;
+constexpr int kGroupM2 = 8;  // 8 x 256 rows per raster group
+constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + 256;
+
+__device__ __forceinline__ void tile_coords2(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
+  const int per_group = kGroupM2 * tiles_n;
+  const int g = t / per_group;
+  const int first_m = g * kGroupM2;
+  const int gm = min(tiles_m - first_m, kGroupM2);
+  const int r = t - g * per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* s_a = smem;
+  uint8_t* s_b = smem + k2Stages * k2ABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * k2StageBytes);
+  uint64_t* empty = full + k2Stages;
+  uint64_t* acc_full = empty + k2Stages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(&full[s], 1);   // leader: its expect_tx arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, kTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total = args.tiles_m * args.tiles_n;
+  const int k_blocks = (args.K + kBK - 1) / kBK;
+  const int first = static_cast<int>(cluster_id_x());
+  const int step = static_cast<int>(num_clusters_x());
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = first; t < total; t += step) {
+        int mb, nb;
+        tile_coords2(t, args.tiles_m, args.tiles_n, mb, nb);
+        const int row0 = mb * 256 + static_cast<int>(rank) * 128;
+        const int col0 = nb * 256 + static_cast<int>(rank) * 128;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
+          tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kb * kBK, row0,
+                           kEvictNormal);
+          tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK,
+                           kEvictNormal);
+          tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage], col0 + 64,
+                           kb * kBK, kEvictNormal);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = first; t < total; t += step) {
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_addr(s_a + stage * k2ABytes);
+          const uint32_t b0 = smem_addr(s_b + stage * k2BBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / kUmmaK; ++k) {
+            const uint64_t ad = sdesc_sw128(a0 + k * kUmmaK * 2, 16, 1024);
+            const uint64_t bd = sdesc_sw128(b0 + k * 2 * 1024, kBChunkBytes, 1024);
+            umma_f16_pair(d_tmem, ad, bd, args.idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[stage], 0x3);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&acc_full[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
+    for (int t = first; t < total; t += step) {
+      int mb, nb;
+      tile_coords2(t, args.tiles_m, args.tiles_n, mb, nb);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + static_cast<int>(rank) * 128 + quad * 32 + lane;
+      float* crow = args.C + static_cast<long long>(row) * args.ldc;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                               static_cast<uint32_t>(acc * kBN + c * 32),
+                           v);
+        tmem_wait_ld();
+        if (row < args.M) {
+          const int col0 = nb * kBN + c * 32;
+          if (vec && col0 + 32 <= args.N) {
+            float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 o = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                     __uint_as_float(v[4 * j + 2]),
+                                     __uint_as_float(v[4 * j + 3]));
+              if (args.accumulate) {
+                const float4 p = dst[j];
+                o.x += p.x;
+                o.y += p.y;
+                o.z += p.z;
+                o.w += p.w;
+              }
+              dst[j] = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = col0 + j;
+              if (col < args.N) {
+                float o = __uint_as_float(v[j]);
+                if (args.accumulate) o += crow[col];
+                crow[col] = o;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer may still be reading TMEM / signalling the leader
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -295,22 +489,41 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   std::call_once(once, [] {
     attr_err = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmemBytes));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(k2SmemBytes));
   });
   if (attr_err != cudaSuccess) return attr_err;
+  // POAS_TC_KERNEL=1cta selects the single-SM kernel (A/B comparisons, tests).
+  const char* variant = std::getenv("POAS_TC_KERNEL");
+  const bool force_1cta = variant && std::string(variant) == "1cta";
 
+  const int sms = device_sm_count();
+  const int budget = num_ctas > 0 ? num_ctas : sms;
   TcArgs args;
   args.M = static_cast<int>(M);
   args.N = static_cast<int>(N);
   args.K = static_cast<int>(K);
-  args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
-  args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
   args.C = C;
   args.ldc = ldc;
   args.accumulate = accumulate ? 1 : 0;
-  args.idesc = idesc_f16(t == AbType::bf16, kBM, kBN, false, true);
 
-  const int sms = device_sm_count();
-  int grid = num_ctas > 0 ? num_ctas : sms;
+  if (!force_1cta && budget >= 2) {
+    // CTA pairs: 256 x 256 tiles, grid = even SM budget (one pair per TPC).
+    args.tiles_m = static_cast<int>((M + 255) / 256);
+    args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
+    args.idesc = idesc_f16(t == AbType::bf16, 256, kBN, false, true);
+    const int tiles = args.tiles_m * args.tiles_n;
+    int pairs = budget / 2;
+    if (pairs > tiles) pairs = tiles;
+    tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, args);
+    return cudaGetLastError();
+  }
+  args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
+  args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
+  args.idesc = idesc_f16(t == AbType::bf16, kBM, kBN, false, true);
+  int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
   tc_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);

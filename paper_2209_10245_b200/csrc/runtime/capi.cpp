@@ -13,6 +13,7 @@
 #include "poas/error.hpp"
 #include "poas/executor.hpp"
 #include "poas/optimizer.hpp"
+#include "poas/policy.hpp"
 #include "poas/profiler.hpp"
 #include "poas/scheduler.hpp"
 #include "poas_b200.h"
@@ -159,6 +160,16 @@ int poas_b200_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
     const poas::WorkloadSplit split = poas::solve_split(machine, d);
     const poas::TilePlan plan = poas::build_tile_plan(machine, d, split);
     *schedule_json = dup_string(poas::format_schedule(poas::build_schedule(plan, machine)));
+  });
+}
+
+int poas_b200_plan_policy(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                          const char* policy, char** schedule_json) {
+  return guard([&] {
+    need_ptr(schedule_json, "schedule_json");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    *schedule_json = dup_string(poas::format_schedule(
+        poas::plan_with_policy(machine, dims_of(m, n, k), policy ? policy : "")));
   });
 }
 

@@ -243,11 +243,12 @@ double Unit::time_gemm(std::int64_t side) {
 double Unit::time_transfer(std::uint64_t bytes) {
   if (!on_gpu()) poas::fail(poas::errc::backend_failure, "cpu unit has no link");
   DeviceGuard g(spec_.device);
-  cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+  // Buffers first: allocation must stay outside the timed interval.
   if (spec_.link == Link::pcie) {
     // Pinned host -> device over the unit's PCIe link (what execute() copies).
     void* dst = xfer_dev_.ensure(bytes);
     const void* src = xfer_host_.ensure(bytes);
+    cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
     cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "cudaMemcpyAsync");
   } else {
     // Resident operands: the unit's "link" is its own path from HBM into its
@@ -257,6 +258,7 @@ double Unit::time_transfer(std::uint64_t bytes) {
     const std::size_t rounded = (bytes + 15) / 16 * 16;
     void* src = xfer_dev2_.ensure(rounded);
     float* sink = static_cast<float*>(xfer_dev_.ensure(64));
+    cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
     cuda_check(stream_read(src, rounded, spec_.sms, sink, stream_), "stream_read");
   }
   cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");

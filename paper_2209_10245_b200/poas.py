@@ -33,6 +33,12 @@ def plan(profile: str, m: int, n: int, k: int) -> str:
     return call_str(lib.poas_b200_plan, _b(profile), m, n, k)
 
 
+def plan_policy(profile: str, m: int, n: int, k: int, policy: str = "reference") -> str:
+    """plan() under a planner policy: "reference" (byte-identical to the
+    reference) or the opt-in "best-subset" B200 extension."""
+    return call_str(lib.poas_b200_plan_policy, _b(profile), m, n, k, _b(policy))
+
+
 def plan_standalone(profile: str, device_id: str, m: int, n: int, k: int) -> str:
     """standalone_schedule (reference proj/src/scheduler.cpp:59-74)."""
     return call_str(lib.poas_b200_plan_standalone, _b(profile), _b(device_id), m, n, k)

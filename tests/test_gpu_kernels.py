@@ -173,3 +173,26 @@ def test_full_size_tc_property(torch_cuda, poas):
     rhs = a.double() @ (b.double() @ x)
     rel = ((lhs - rhs).norm() / rhs.norm()).item()
     assert rel <= TOL, rel
+
+
+@pytest.mark.parametrize("variant", ["1cta", "2cta"])
+@pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
+def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape):
+    """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) agree
+    with the oracle, including partial pair tiles and odd SM budgets."""
+    import oracle
+
+    torch = torch_cuda
+    monkeypatch.setenv("POAS_TC_KERNEL", variant)
+    m, n, k = shape
+    A, B = oracle.fill_uniform(m, k, 31), oracle.fill_uniform(k, n, 32)
+    ldb = (n + 7) // 8 * 8
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.zeros(k, ldb, device="cuda", dtype=torch.bfloat16)
+    b[:, :n] = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    for ctas in (0, 3, 10):
+        c = torch.full((m, n), float("nan"), device="cuda")
+        poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), ldb, c.data_ptr(), n, num_ctas=ctas)
+        torch.cuda.synchronize()
+        assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, (variant, ctas)

@@ -33,7 +33,9 @@ def _worker(rank, world, port, out_dir):
     import oracle
     from paper_2209_10245_b200 import poas, shard
 
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no port races between concurrently running suites
+    dist.init_process_group("gloo", init_method=f"file://{out_dir}/rdzv", rank=rank,
+                            world_size=world)
     m_total, n, k = 520, 192, 160
     units = f"cpu{rank}=cpu:threads=2"
     prof = poas.profile_machine(units, "probes=3,repetitions=1,cpu_min_side=48,cpu_max_side=128")

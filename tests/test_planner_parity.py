@@ -144,6 +144,30 @@ def test_b200_like_profile_matches_survey(poas, ref):
     assert poas.plan(prof, 16384, 16384, 16384) == ref.plan(prof, 16384, 16384, 16384)
 
 
+def test_policy_reference_is_the_reference_and_best_subset_never_worse(poas, ref):
+    """The default planner policy is byte-identical to the reference; the
+    opt-in best-subset policy (B200 extension) never predicts a longer
+    makespan, and on the survey's B200-like profile it recovers the
+    no-CPU plan (8.553 ms -> 6.448 ms)."""
+    prof = (GOLDEN / "profiles" / "b200_like.profile").read_text()
+    s = json.loads(poas.plan_policy(prof, 16384, 16384, 16384, "best-subset"))
+    assert {d["id"]: d["rows"] for d in s["devices"]} == {"gpu0.tc": 15736, "gpu0.simt": 648, "cpu0": 0}
+    assert abs(s["makespan"] - 0.006448) < 1e-6
+    rng = random.Random(99)
+    for _ in range(150):
+        nd = rng.randint(1, 4)
+        prof = random_profile(rng, nd, with_cpu=rng.random() < 0.5, bus=rng.random() < 0.8)
+        m, n, k = random_dims(rng)
+        a, b = both(lambda *x: poas.plan_policy(*x, "reference"), ref.plan, prof, m, n, k)
+        assert a == b
+        if a[0] != "ok":
+            continue
+        best = json.loads(poas.plan_policy(prof, m, n, k, "best-subset"))
+        assert best["makespan"] <= json.loads(a[1])["makespan"] + 1e-9
+        assert sum(d["rows"] for d in best["devices"]) == m
+        assert best["machine_hash"] == json.loads(a[1])["machine_hash"]
+
+
 def test_standalone_plans(poas, ref):
     for name in ("mach2_exact", "mach2_seed7", "b200_like"):
         prof = (GOLDEN / "profiles" / f"{name}.profile").read_text()

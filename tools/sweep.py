@@ -1,0 +1,136 @@
+"""BASELINE configs C2 and C5 on one B200 (writes JSON to stdout).
+
+C5: N = 1024 .. 32768 square GEMMs: the POAS co-executed plan (tensor +
+    CUDA cores, resident operands) vs tensor-core-only on every SM vs the
+    cuBLAS timing reference (torch.matmul bf16, timing only) vs the host
+    CPU unit (N <= 4096).
+C2: N = 8192 co-executed by host CPU + fp32 CUDA cores + fp16 tensor cores.
+
+    python tools/sweep.py [--quick]
+"""
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+from paper_2209_10245_b200 import poas  # noqa: E402
+
+SEED = 20261017
+PROF = "probes=9,repetitions=3,bandwidth_payload=268435456"
+
+
+def ev_time(fn, iters):
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters * 1e-3
+
+
+def operands(n, with_host=False):
+    sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
+    d = {}
+    for name, seed in (("A", sa), ("B", sb)):
+        t32 = torch.empty(n, n, device="cuda")
+        t16 = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
+        poas.fill_uniform(poas.DTYPE_F32, t32.data_ptr(), n, n, n, 0, 0, n, seed)
+        poas.fill_uniform(poas.DTYPE_BF16, t16.data_ptr(), n, n, n, 0, 0, n, seed)
+        d[name + "32"], d[name + "16"] = t32, t16
+    d["C"] = torch.empty(n, n, device="cuda")
+    if with_host:
+        for name in ("A", "B"):
+            d["h" + name] = d[name + "32"].cpu().pin_memory()
+        d["hC"] = torch.empty(n, n).pin_memory()
+    torch.cuda.synchronize()
+    return d
+
+
+def io_for(n, d, with_host=False):
+    kw = dict(m=n, n=n, k=n, a_dev=d["A32"].data_ptr(), lda_dev=n, b_dev=d["B32"].data_ptr(), ldb_dev=n,
+              a16_dev=d["A16"].data_ptr(), lda16_dev=n, b16_dev=d["B16"].data_ptr(), ldb16_dev=n,
+              c_dev=d["C"].data_ptr(), ldc_dev=n, resident=1)
+    if with_host:
+        kw.update(a_host=d["hA"].data_ptr(), lda_host=n, b_host=d["hB"].data_ptr(), ldb_host=n,
+                  c_host=d["hC"].data_ptr(), ldc_host=n)
+    return poas.GemmIO(**kw)
+
+
+def c5(sizes):
+    units = ("gpu0.tc=xpu:dev=0:sms=146:dtype=bf16:elem=2:link=hbm:probe=8192-16384;"
+             "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048")
+    profile = poas.profile_machine(units, PROF, True)
+    ex = poas.Executor(units)
+    out = {"profile": profile, "rows": []}
+    for n in sizes:
+        d = operands(n)
+        io = io_for(n, d)
+        sched = poas.plan(profile, n, n, n)
+        s = json.loads(sched)
+        it = max(2, min(50, int(2e12 / (2 * n ** 3)) + 1))
+        ex.execute(sched, io, 2)
+        rep = ex.execute(sched, io, it)
+        poas_s = rep["measured_makespan"]
+        st = torch.cuda.current_stream().cuda_stream
+        tc_fn = lambda: poas.tc_gemm(2, n, n, n, d["A16"].data_ptr(), n, d["B16"].data_ptr(), n,  # noqa: E731
+                                     d["C"].data_ptr(), n, stream=st)
+        tc_fn()
+        tc_s = ev_time(tc_fn, it)
+        cublas_fn = lambda: torch.matmul(d["A16"], d["B16"])  # noqa: E731
+        cublas_fn()
+        cb_s = ev_time(cublas_fn, it)
+        row = {"n": n, "plan_rows": {x["id"]: x["rows"] for x in s["devices"]},
+               "poas_tflops": 2 * n ** 3 / poas_s / 1e12, "poas_pred_ms": rep["predicted_makespan"] * 1e3,
+               "poas_meas_ms": poas_s * 1e3, "makespan_error_pct": rep["makespan_error_pct"],
+               "tc_only_148sm_tflops": 2 * n ** 3 / tc_s / 1e12,
+               "cublas_bf16_out_tflops": 2 * n ** 3 / cb_s / 1e12}
+        if n <= 4096:
+            A, B = d["A32"].cpu(), d["B32"].cpu()
+            C = torch.empty(n, n)
+            poas.host_gemm(n, n, n, A.data_ptr(), n, B.data_ptr(), n, C.data_ptr(), n)
+            t0 = time.perf_counter()
+            poas.host_gemm(n, n, n, A.data_ptr(), n, B.data_ptr(), n, C.data_ptr(), n)
+            row["host_cpu_tflops"] = 2 * n ** 3 / (time.perf_counter() - t0) / 1e12
+            row["host_cores"] = os.cpu_count()
+        out["rows"].append(row)
+        print(json.dumps(row), file=sys.stderr, flush=True)
+        del d
+        torch.cuda.empty_cache()
+    return out
+
+
+def c2(n=8192):
+    threads = max(1, (os.cpu_count() or 2) - 2)
+    units = (f"cpu0=cpu:threads={threads};"
+             "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048;"
+             "gpu0.tc=xpu:dev=0:sms=146:dtype=f16:elem=2:link=hbm:probe=4096-8192")
+    profile = poas.profile_machine(units, PROF + ",cpu_min_side=512,cpu_max_side=1536", True)
+    d = operands(n, with_host=True)
+    # fp16 operands for the fp16 tensor unit
+    d["A16"] = d["A32"].half().view(torch.bfloat16)
+    d["B16"] = d["B32"].half().view(torch.bfloat16)
+    io = io_for(n, d, with_host=True)
+    sched = poas.plan(profile, n, n, n)
+    ex = poas.Executor(units)
+    ex.execute(sched, io, 1)
+    rep = ex.execute(sched, io, 5)
+    s = json.loads(sched)
+    return {"n": n, "profile": profile, "plan_rows": {x["id"]: x["rows"] for x in s["devices"]},
+            "predicted_ms": rep["predicted_makespan"] * 1e3, "measured_ms": rep["measured_makespan"] * 1e3,
+            "makespan_error_pct": rep["makespan_error_pct"],
+            "tflops": 2 * n ** 3 / rep["measured_makespan"] / 1e12,
+            "devices": rep["devices"]}
+
+
+if __name__ == "__main__":
+    quick = "--quick" in sys.argv
+    sizes = [1024, 2048, 4096, 8192, 16384] + ([] if quick else [32768])
+    res = {"gpu": torch.cuda.get_device_name(), "c5": c5(sizes), "c2": c2()}
+    print(json.dumps(res, indent=1))
