@@ -25,6 +25,7 @@ run, executed tile by tile by the oracle port) and prints the same line.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -205,6 +206,8 @@ def main():
     ap.add_argument("--tc-sms", type=int, default=TC_SMS)
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--b-panels", type=int, default=4,
+                    help="N > 1: B column panels broadcast separately (overlap with compute)")
     ap.add_argument("--policy", default="best-subset", choices=["reference", "best-subset"],
                     help="planner policy: the reference algorithm (byte-identical plans) or the "
                          "opt-in best-subset B200 extension")
@@ -259,33 +262,58 @@ def main():
     A32 = torch.empty(m, k, device=dev, dtype=torch.float32)
     A16 = torch.empty(m, k, device=dev, dtype=torch.bfloat16)
     C = torch.empty(m, n, device=dev, dtype=torch.float32)
-    B32 = torch.empty(k, n, device=dev, dtype=torch.float32)
-    B16 = torch.empty(k, n, device=dev, dtype=torch.bfloat16)
+    # B is stored panel-major ([P][K][N/P]): at N > 1 each column panel is
+    # broadcast separately and the units start on panel p as soon as it
+    # lands (executor b_ready events), overlapping the rest of the broadcast.
+    P = args.b_panels if world > 1 else 1
+    np_ = n // P
+    B32 = torch.empty(P, k, np_, device=dev, dtype=torch.float32)
+    B16 = torch.empty(P, k, np_, device=dev, dtype=torch.bfloat16)
     row0 = rank * m  # this rank's rows of the global A (M_total = m * world)
     poas.fill_uniform(poas.DTYPE_F32, A32.data_ptr(), k, m, k, row0, 0, k, sa)
     poas.fill_uniform(poas.DTYPE_BF16, A16.data_ptr(), k, m, k, row0, 0, k, sa)
     if rank == 0:
-        poas.fill_uniform(poas.DTYPE_F32, B32.data_ptr(), n, k, n, 0, 0, n, sb)
-        poas.fill_uniform(poas.DTYPE_BF16, B16.data_ptr(), n, k, n, 0, 0, n, sb)
+        for p in range(P):
+            poas.fill_uniform(poas.DTYPE_F32, B32[p].data_ptr(), np_, k, np_, 0, p * np_, n, sb)
+            poas.fill_uniform(poas.DTYPE_BF16, B16[p].data_ptr(), np_, k, np_, 0, p * np_, n, sb)
     else:
         B32.zero_()
         B16.zero_()
     torch.cuda.synchronize()
 
     ex = poas.Executor(units_res)
-    io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=n,
-                     a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=n,
-                     c_dev=C.data_ptr(), ldc_dev=n, resident=1)
+    io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=np_,
+                     a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=np_,
+                     c_dev=C.data_ptr(), ldc_dev=n, resident=1, b_panels=P)
     # B in every precision a busy unit consumes is what crosses NVLink.
-    b_needed = [B16] + ([B32] if rows.get(simt_id, 0) > 0 else [])
+    simt_busy = rows.get(simt_id, 0) > 0
+    ready = [torch.cuda.Event() for _ in range(P)]
+    comm_side = torch.cuda.Stream()
+    if world > 1 and rank != 0:
+        handles = (ctypes.c_void_p * P)()
+        io.b_ready = ctypes.cast(handles, ctypes.POINTER(ctypes.c_void_p))
     # Level-1 (per-GPU) split of the whole job by the same planner: equal
     # shards of `m` rows for identical GPUs (weak scaling).
     l1_rows = shard.shard_rows(world, m * world, n, k, profile) if world > 1 else [m]
     assert l1_rows == [m] * world, l1_rows
 
     def step(repeats=1):
-        # B lives on rank 0: NCCL broadcast over NVLink inside the step (N > 1)
-        return shard.sharded_step(ex, schedule, io, b_needed, repeats)
+        if world > 1:
+            # B lives on rank 0: NCCL broadcast over NVLink inside the step,
+            # one async broadcast per panel; panel p's event fires when it lands.
+            works = []
+            for p in range(P):
+                works.append([dist.broadcast(B16[p], src=0, async_op=True)] +
+                             ([dist.broadcast(B32[p], src=0, async_op=True)] if simt_busy else []))
+            if rank != 0:
+                with torch.cuda.stream(comm_side):
+                    for p in range(P):
+                        for w in works[p]:
+                            w.wait()
+                        ready[p].record(comm_side)
+                for p in range(P):
+                    handles[p] = ready[p].cuda_event
+        return ex.execute(schedule, io, repeats)
 
     for _ in range(args.warmup):
         step()

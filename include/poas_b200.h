@@ -179,6 +179,15 @@ typedef struct {
   float* c_dev;
   int64_t ldc_dev;
   int resident;
+  /* Optional (resident == 1): B arrives in `b_panels` column panels (e.g.
+   * chunks of a broadcast). Panel p = columns [p*n/P, (p+1)*n/P) stored
+   * contiguously as a [k x n/P] matrix at b_dev + p*k*(n/P) (and likewise
+   * b16_dev); each GPU unit waits on b_ready[p] (a cudaEvent_t recorded on
+   * the same GPU after the panel landed) before computing that panel, so the
+   * transfer of later panels overlaps compute on earlier ones. n must be a
+   * multiple of b_panels. b_panels <= 1: B is one row-major matrix. */
+  int b_panels;
+  void* const* b_ready;
 } poas_gemm_io;
 
 /* One executor per process per machine description (same unit specs as

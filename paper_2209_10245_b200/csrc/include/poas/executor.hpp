@@ -70,6 +70,9 @@ struct GemmOperands {
   float* c_dev = nullptr;
   std::int64_t ldc_dev = 0;
   bool resident = false;
+  // Panel-major B with per-panel readiness events (see poas_gemm_io).
+  int b_panels = 0;
+  void* const* b_ready = nullptr;
 };
 
 double rel_err_pct(double measured, double predicted);

@@ -50,13 +50,18 @@ struct TcArgs {
   long long ldc;
   int accumulate;
   uint32_t idesc;
+  int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  const int per_group = kGroupM * tiles_n;
+// Grouped raster: consecutive tile ids walk `group` M-tiles down a column of
+// N-tiles, so one wave of the persistent grid shares A row panels and B
+// column panels through L2.
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int& mb,
+                                            int& nb) {
+  const int per_group = group * tiles_n;
   const int g = t / per_group;
-  const int first_m = g * kGroupM;
-  const int gm = min(tiles_m - first_m, kGroupM);
+  const int first_m = g * group;
+  const int gm = min(tiles_m - first_m, group);
   const int r = t - g * per_group;
   mb = first_m + r % gm;
   nb = r / gm;
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
+        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int mb, nb;
-      tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
+      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * kBM + quad * 32 + lane;
@@ -237,18 +242,9 @@ constexpr int k2Stages = 6;
 constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
 constexpr int k2StageBytes = k2ABytes + k2BBytes;
-constexpr int kGroupM2 = 8;  // 8 x 256 rows per raster group
+constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
 constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + 256;
 
-__device__ __forceinline__ void tile_coords2(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  const int per_group = kGroupM2 * tiles_n;
-  const int g = t / per_group;
-  const int first_m = g * kGroupM2;
-  const int gm = min(tiles_m - first_m, kGroupM2);
-  const int r = t - g * per_group;
-  mb = first_m + r % gm;
-  nb = r / gm;
-}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -299,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = first; t < total; t += step) {
         int mb, nb;
-        tile_coords2(t, args.tiles_m, args.tiles_n, mb, nb);
+        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
         const int col0 = nb * 256 + static_cast<int>(rank) * 128;
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -357,7 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     for (int t = first; t < total; t += step) {
       int mb, nb;
-      tile_coords2(t, args.tiles_m, args.tiles_n, mb, nb);
+      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + quad * 32 + lane;
@@ -498,6 +494,8 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   // POAS_TC_KERNEL=1cta selects the single-SM kernel (A/B comparisons, tests).
   const char* variant = std::getenv("POAS_TC_KERNEL");
   const bool force_1cta = variant && std::string(variant) == "1cta";
+  const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
+  const int group_override = group_env ? std::atoi(group_env) : 0;
 
   const int sms = device_sm_count();
   const int budget = num_ctas > 0 ? num_ctas : sms;
@@ -514,6 +512,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
     args.tiles_m = static_cast<int>((M + 255) / 256);
     args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
     args.idesc = idesc_f16(t == AbType::bf16, 256, kBN, false, true);
+    args.group = group_override > 0 ? group_override : kGroupM2;
     const int tiles = args.tiles_m * args.tiles_n;
     int pairs = budget / 2;
     if (pairs > tiles) pairs = tiles;
@@ -523,6 +522,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
   args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
   args.idesc = idesc_f16(t == AbType::bf16, kBM, kBN, false, true);
+  args.group = group_override > 0 ? group_override : kGroupM;
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;

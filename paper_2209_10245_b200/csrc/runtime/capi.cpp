@@ -374,6 +374,8 @@ int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_
     op.c_dev = io->c_dev;
     op.ldc_dev = io->ldc_dev;
     op.resident = io->resident != 0;
+    op.b_panels = io->b_panels;
+    op.b_ready = io->b_ready;
     const poas::SimulationResult r = ex->ex->run(s, op, repeats);
     if (report_json) *report_json = dup_string(poas::format_execution_report(s, r));
   });

@@ -129,6 +129,16 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
   }
   if ((any_cpu || !io.resident) && (!io.a_host || !io.b_host || !io.c_host))
     fail(errc::invalid_argument, "host operands (a_host, b_host, c_host) are required");
+  const int panels = io.b_panels > 1 ? io.b_panels : 1;
+  if (panels > 1) {
+    if (!io.resident) fail(errc::invalid_argument, "B panels need resident operands");
+    if (d.n % panels != 0 || (d.n / panels) % 8 != 0)
+      fail(errc::invalid_argument, "n must split into b_panels panels of a multiple of 8 columns");
+    for (std::size_t i = 0; i < nd; ++i)
+      if (schedule.devices[i].rows > 0 && unit[i]->spec().kind == DeviceKind::xpu &&
+          !(io.a16_dev && io.b16_dev))
+        fail(errc::invalid_argument, "B panels with a tensor unit need a16/b16 operands");
+  }
   if (io.resident) {
     for (std::size_t i = 0; i < nd; ++i) {
       if (schedule.devices[i].rows == 0 || !unit[i]->on_gpu()) continue;
@@ -287,7 +297,21 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         lda = lda16;
         ldb = ldb16;
       }
-      u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false);
+      if (panels > 1) {
+        // Panel-major B arriving panel by panel: compute each column panel
+        // as soon as it has landed (overlaps e.g. a chunked broadcast).
+        const std::int64_t np = d.n / panels;
+        const std::size_t esz = (tensor && !need_convert) ? 2 : 4;
+        for (int p = 0; p < panels; ++p) {
+          if (io.b_ready && io.b_ready[p])
+            cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(io.b_ready[p]), 0),
+                       "wait B panel");
+          const void* bp = static_cast<const char*>(b) + static_cast<std::size_t>(p) * d.k * np * esz;
+          u->gemm(r, np, d.k, a, lda, bp, np, c + p * np, ldc, false);
+        }
+      } else {
+        u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false);
+      }
       cuda_check(cudaEventRecord(ev[i].cp1, s), "cudaEventRecord");
     }
 

@@ -95,6 +95,48 @@ void micro_portable(int64_t mr, int64_t nr, int64_t kc, const float* A, int64_t 
     for (int64_t j = 0; j < nr; ++j) C[i * ldc + j] = (load_c ? C[i * ldc + j] : 0.f) + acc[i][j];
 }
 
+// Skinny-M path (a co-executed CPU share is often a handful of residue rows):
+// no packing -- every B element is streamed from memory exactly once per
+// 8-row group. Threads split the columns in 1024-wide strips (one 4 KB page
+// of each B row per k, so the walk down B stays page-friendly); a strip
+// keeps its 8 x 1024 partial C in an L1-resident buffer.
+constexpr int64_t kSkinnyRows = 8;
+constexpr int64_t kSkinnyCols = 1024;
+
+__attribute__((target("avx512f,fma"))) void skinny_block_avx512(
+    int64_t mr, int64_t c0, int64_t nc, int64_t k, const float* A, int64_t lda, const float* B,
+    int64_t ldb, float* C, int64_t ldc, bool accumulate) {
+  alignas(64) float acc[kSkinnyRows][kSkinnyCols];
+  const int64_t vecs = (nc + 15) / 16;
+  const __mmask16 tail =
+      nc % 16 == 0 ? static_cast<__mmask16>(0xFFFF) : static_cast<__mmask16>((1u << (nc % 16)) - 1);
+  for (int64_t i = 0; i < mr; ++i)
+    for (int64_t v = 0; v < vecs; ++v) _mm512_store_ps(&acc[i][16 * v], _mm512_setzero_ps());
+  for (int64_t kk = 0; kk < k; ++kk) {
+    const float* b = B + kk * ldb + c0;
+    __m512 av[kSkinnyRows];
+    for (int64_t i = 0; i < mr; ++i) av[i] = _mm512_set1_ps(A[i * lda + kk]);
+    for (int64_t v = 0; v < vecs; ++v) {
+      const __m512 bv = _mm512_maskz_loadu_ps(v + 1 == vecs ? tail : 0xFFFF, b + 16 * v);
+#pragma GCC unroll 8
+      for (int64_t i = 0; i < kSkinnyRows; ++i) {
+        if (i >= mr) break;
+        _mm512_store_ps(&acc[i][16 * v],
+                        _mm512_fmadd_ps(av[i], bv, _mm512_load_ps(&acc[i][16 * v])));
+      }
+    }
+  }
+  for (int64_t i = 0; i < mr; ++i) {
+    float* c = C + i * ldc + c0;
+    for (int64_t v = 0; v < vecs; ++v) {
+      const __mmask16 mk = v + 1 == vecs ? tail : 0xFFFF;
+      __m512 x = _mm512_load_ps(&acc[i][16 * v]);
+      if (accumulate) x = _mm512_add_ps(x, _mm512_maskz_loadu_ps(mk, c + 16 * v));
+      _mm512_mask_storeu_ps(c + 16 * v, mk, x);
+    }
+  }
+}
+
 bool have_avx512() {
   static const bool yes = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("fma");
   return yes;
@@ -114,6 +156,19 @@ void host_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, con
   }
   const int nt = threads > 0 ? threads : omp_get_num_procs();
   const bool wide = have_avx512();
+  if (wide && m <= 4 * kSkinnyRows) {
+    const int64_t groups = (m + kSkinnyRows - 1) / kSkinnyRows;
+    const int64_t blocks = (n + kSkinnyCols - 1) / kSkinnyCols;
+#pragma omp parallel for num_threads(nt) schedule(static) collapse(2)
+    for (int64_t g = 0; g < groups; ++g)
+      for (int64_t cb = 0; cb < blocks; ++cb) {
+        const int64_t r0 = g * kSkinnyRows;
+        const int64_t c0 = cb * kSkinnyCols;
+        skinny_block_avx512(std::min(kSkinnyRows, m - r0), c0, std::min(kSkinnyCols, n - c0), k,
+                            A + r0 * lda, lda, B, ldb, C + r0 * ldc, ldc, accumulate);
+      }
+    return;
+  }
   const int64_t nc_max = std::min<int64_t>(kNC, (n + kNR - 1) / kNR * kNR);
   std::unique_ptr<float[]> packed(new float[static_cast<size_t>(kKC * nc_max)]);
   float* Bp = packed.get();

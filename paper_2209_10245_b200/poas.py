@@ -169,6 +169,7 @@ class GemmIO(C.Structure):
         ("b16_dev", C.c_void_p), ("ldb16_dev", C.c_int64),
         ("c_dev", C.c_void_p), ("ldc_dev", C.c_int64),
         ("resident", C.c_int),
+        ("b_panels", C.c_int), ("b_ready", C.POINTER(C.c_void_p)),
     ]
 
 

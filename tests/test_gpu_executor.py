@@ -167,6 +167,46 @@ def test_cpu_unit_coexecution_config_c2(torch_cuda, poas, ref):
     assert oracle.rel_frobenius(got, exp) <= TOL
 
 
+def test_b_panels_with_ready_events(torch_cuda, poas):
+    """Panel-major B arriving panel by panel (the N > 1 broadcast overlap):
+    each unit waits on its panel's event; C must be exact regardless."""
+    import ctypes
+
+    import oracle
+
+    torch = torch_cuda
+    m, n, k, P = 1536, 2048, 512, 4
+    np_ = n // P
+    profile = poas.profile_machine(UNITS, PROF, True)
+    sched = json.loads(poas.plan(profile, m, n, k))
+    for dv in sched["devices"]:  # both units busy
+        dv["rows"] = 1024 if dv["id"] == "gpu0.tc" else m - 1024
+    sched_text = json.dumps(sched)
+    d = operands(torch, poas, m, n, k)
+    src32, src16 = d["B32"], d["B16"][:, :n]
+    B32p = torch.zeros(P, k, np_, device="cuda")
+    B16p = torch.zeros(P, k, np_, device="cuda", dtype=torch.bfloat16)
+    side = torch.cuda.Stream()
+    events = [torch.cuda.Event() for _ in range(P)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):  # "broadcast": panels land one by one
+        for p in range(P):
+            torch.cuda._sleep(2_000_000)
+            B32p[p].copy_(src32[:, p * np_:(p + 1) * np_])
+            B16p[p].copy_(src16[:, p * np_:(p + 1) * np_])
+            events[p].record(side)
+    handles = (ctypes.c_void_p * P)(*[e.cuda_event for e in events])
+    io = poas.GemmIO(m=m, n=n, k=k, a_dev=d["A32"].data_ptr(), lda_dev=k, b_dev=B32p.data_ptr(),
+                     ldb_dev=np_, a16_dev=d["A16"].data_ptr(), lda16_dev=d["A16"].shape[1],
+                     b16_dev=B16p.data_ptr(), ldb16_dev=np_, c_dev=d["C"].data_ptr(), ldc_dev=n,
+                     resident=1, b_panels=P, b_ready=ctypes.cast(handles, ctypes.POINTER(ctypes.c_void_p)))
+    ex = poas.Executor(UNITS)
+    ex.execute(sched_text, io, 1)
+    torch.cuda.synchronize()
+    exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2, "gpu0.simt": 0})
+    assert oracle.rel_frobenius(d["C"].cpu().numpy(), exp) <= TOL
+
+
 def test_execute_error_paths(torch_cuda, poas):
     from paper_2209_10245_b200 import PoasError
 
