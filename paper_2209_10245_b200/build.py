@@ -18,6 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libpoas_b200.so"
+CLI = PKG / "bin" / "poas"
 
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
@@ -85,6 +86,20 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         if r.returncode != 0:
             raise RuntimeError(f"link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, LIB)
+    # The `poas` CLI: its own main, linked against the same objects.
+    cli_src = CSRC / "tools" / "poas_cli.cpp"
+    cli_obj = obj_for(cli_src)
+    if force or not cli_obj.exists() or cli_obj.stat().st_mtime < max(cli_src.stat().st_mtime, newest_hdr):
+        compile_one(cli_src)
+    if not CLI.exists() or CLI.stat().st_mtime < max(o.stat().st_mtime for o in [*objs, cli_obj]):
+        CLI.parent.mkdir(exist_ok=True)
+        tmp = CLI.with_suffix(".tmp")
+        cmd = [NVCC, *ARCH, "-o", str(tmp), str(cli_obj), *map(str, objs),
+               "-Xcompiler", "-fopenmp", "-lgomp", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, CLI)
     return LIB
 
 

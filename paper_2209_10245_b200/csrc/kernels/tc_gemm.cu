@@ -51,7 +51,20 @@ struct TcArgs {
   int accumulate;
   uint32_t idesc;
   int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
+  unsigned* start_sync;  // optional zeroed counter: all producers start K in step
 };
+
+// One-time start barrier of the producers (persistent grid, all CTAs
+// co-resident): CTAs that share A/B panels through L2 then sweep K in step
+// instead of inheriting the launch stagger of cluster scheduling.
+__device__ __forceinline__ void start_barrier(unsigned* counter, unsigned expected) {
+  if (!counter) return;
+  atomicAdd(counter, 1u);
+  unsigned seen = 0;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+  } while (seen < expected);
+}
 
 // Grouped raster: consecutive tile ids walk `group` M-tiles down a column of
 // N-tiles, so one wave of the persistent grid shares A row panels and B
@@ -108,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      start_barrier(args.start_sync, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -291,6 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      start_barrier(args.start_sync, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = first; t < total; t += step) {
@@ -460,6 +475,28 @@ int device_sm_count() {
   return n;
 }
 
+namespace {
+// Per-device ring of start-barrier counters: concurrent launches (other
+// streams) get distinct counters; each is zeroed on the launch's stream.
+unsigned* next_sync_counter() {
+  constexpr int kRing = 256;
+  static std::mutex mu;
+  static unsigned* ring[64] = {};
+  static int next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ring[dev] && cudaMalloc(&ring[dev], kRing * 32 * sizeof(unsigned)) != cudaSuccess) {
+    ring[dev] = nullptr;
+    return nullptr;
+  }
+  unsigned* c = ring[dev] + (next[dev] % kRing) * 32;  // 128 B apart
+  ++next[dev];
+  return c;
+}
+}  // namespace
+
 cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                     int num_ctas, cudaStream_t stream) {
@@ -506,6 +543,16 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.C = C;
   args.ldc = ldc;
   args.accumulate = accumulate ? 1 : 0;
+  args.start_sync = nullptr;
+  // Start barrier (POAS_TC_SYNC=0 disables): needs every CTA co-resident,
+  // which a persistent grid within the unit's SM budget guarantees.
+  const char* sync_env = std::getenv("POAS_TC_SYNC");
+  if (!(sync_env && sync_env[0] == '0') && budget <= sms) {
+    args.start_sync = next_sync_counter();
+    if (!args.start_sync) return cudaErrorMemoryAllocation;
+    const cudaError_t e = cudaMemsetAsync(args.start_sync, 0, sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+  }
 
   if (!force_1cta && budget >= 2) {
     // CTA pairs: 256 x 256 tiles, grid = even SM budget (one pair per TPC).

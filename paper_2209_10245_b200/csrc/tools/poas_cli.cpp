@@ -1,0 +1,488 @@
+// poas -- command-line front end of the B200 POAS path.
+//
+// Mirrors the reference CLI (proj/tools/poas.cpp:47-262) over real units:
+//   poas profile  --units SPEC [--profiling k=v,..] [--bus true|false] --out FILE
+//   poas plan     --profile FILE --dims MxNxK --out FILE [--policy reference|best-subset]
+//   poas run      --schedule FILE --units SPEC [--repeats N] [--seed S] [--host]
+//   poas evaluate --units SPEC [--inputs FILE] [--repeats N] [--seed S]
+//                 [--policy P] [--profiling k=v,..] --out-dir DIR
+// Exit codes as the reference: 0 success, 1 domain or usage error, 2 internal.
+// `run` replaces `simulate` (poas.cpp:116-151): it executes the schedule on
+// the box (inputs from the seeded counter generator) and writes
+// <schedule>.report.json in the simulate report's shape.
+#include <cuda_runtime.h>
+#include <sys/stat.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.hpp"
+#include "../planner/json_lite.hpp"
+#include "../runtime/capi_util.hpp"
+#include "../runtime/host_rng.hpp"
+#include "../runtime/units.hpp"
+#include "poas/error.hpp"
+#include "poas/executor.hpp"
+#include "poas/log.hpp"
+#include "poas/policy.hpp"
+#include "poas/profiler.hpp"
+#include "poas/rng.hpp"
+#include "poas/scheduler.hpp"
+
+namespace poas_b200 {
+poas::MachineProfile profile_units(const std::vector<std::unique_ptr<Unit>>& units,
+                                   const poas::ProfilingConfig& cfg, bool bus);
+}
+
+namespace {
+
+using poas::errc;
+using poas::fail;
+using poas_b200::AbType;
+using poas_b200::parse_unit_list;
+using poas_b200::Unit;
+using poas_b200::UnitSpec;
+
+struct Args {
+  std::string cmd;
+  std::map<std::string, std::string> kv;
+  bool has(const std::string& k) const { return kv.count(k) != 0; }
+  std::string get(const std::string& k, const std::string& def = "") const {
+    const auto it = kv.find(k);
+    return it == kv.end() ? def : it->second;
+  }
+  std::string need(const std::string& k) const {
+    if (!has(k)) fail(errc::invalid_argument, "missing required option --" + k);
+    return kv.at(k);
+  }
+};
+
+Args parse_args(int argc, char** argv) {
+  Args a;
+  if (argc < 2) fail(errc::invalid_argument, "usage: poas {profile|plan|run|evaluate} [options]");
+  a.cmd = argv[1];
+  static const std::map<std::string, bool> flags = {{"host", true}};
+  for (int i = 2; i < argc; ++i) {
+    std::string s = argv[i];
+    if (s.rfind("--", 0) != 0) fail(errc::invalid_argument, "unexpected argument '" + s + "'");
+    s = s.substr(2);
+    if (flags.count(s)) {
+      a.kv[s] = "1";
+      continue;
+    }
+    if (i + 1 >= argc) fail(errc::invalid_argument, "option --" + s + " needs a value");
+    a.kv[s] = argv[++i];
+  }
+  return a;
+}
+
+std::string read_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(errc::io_failure, "cannot open '" + path + "'");
+  std::ostringstream b;
+  b << in.rdbuf();
+  return b.str();
+}
+
+// tmp + rename, as the reference's report writer (poas.cpp:164-179).
+void write_atomic(const std::string& path, const std::string& text) {
+  const std::string tmp = path + ".tmp";
+  {
+    std::ofstream out(tmp, std::ios::binary);
+    if (!out) fail(errc::io_failure, "cannot open '" + tmp + "' for writing");
+    out << text;
+    out.flush();
+    if (!out) {
+      std::remove(tmp.c_str());
+      fail(errc::io_failure, "failed writing '" + tmp + "'");
+    }
+  }
+  if (std::rename(tmp.c_str(), path.c_str()) != 0) {
+    std::remove(tmp.c_str());
+    fail(errc::io_failure, "cannot rename '" + tmp + "' to '" + path + "'");
+  }
+}
+
+poas::ProfilingConfig profiling_from(const std::string& text) {
+  poas::ProfilingConfig c;
+  std::stringstream in(text);
+  std::string item;
+  while (std::getline(in, item, ',')) {
+    if (item.empty()) continue;
+    const auto eq = item.find('=');
+    if (eq == std::string::npos) fail(errc::invalid_argument, "profiling: bad item " + item);
+    const std::string k = item.substr(0, eq);
+    const long long v = std::atoll(item.c_str() + eq + 1);
+    if (k == "probes") c.probes = static_cast<int>(v);
+    else if (k == "repetitions") c.repetitions = static_cast<int>(v);
+    else if (k == "cpu_min_side") c.cpu_range.min_side = v;
+    else if (k == "cpu_max_side") c.cpu_range.max_side = v;
+    else if (k == "accel_min_side") c.accel_range.min_side = v;
+    else if (k == "accel_max_side") c.accel_range.max_side = v;
+    else if (k == "bandwidth_payload") c.bandwidth_payload = static_cast<std::uint64_t>(v);
+    else fail(errc::invalid_argument, "profiling: unknown key " + k);
+  }
+  poas::validate_profiling_config(c);
+  return c;
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Operands of one run: generated in place from the seeded counter stream,
+// resident in HBM (default) or in pinned host memory (--host).
+struct Operands {
+  poas::GemmOperands io;
+  std::vector<void*> dev, pinned, heap;
+  ~Operands() {
+    for (void* p : dev) cudaFree(p);
+    for (void* p : pinned) cudaFreeHost(p);
+    for (void* p : heap) std::free(p);
+  }
+};
+
+std::unique_ptr<Operands> make_operands(const poas::MatrixDims& d, std::uint64_t seed, bool host,
+                                        bool need_host, bool need_dev, bool need16, AbType t16) {
+  auto o = std::make_unique<Operands>();
+  const std::uint64_t sa = poas::Rng::for_stream(seed, "A").state();
+  const std::uint64_t sb = poas::Rng::for_stream(seed, "B").state();
+  poas::GemmOperands& io = o->io;
+  io.m = d.m;
+  io.n = d.n;
+  io.k = d.k;
+  io.resident = !host;
+  auto dmalloc = [&](std::size_t bytes) {
+    void* p = nullptr;
+    cuda_ok(cudaMalloc(&p, bytes), "cudaMalloc");
+    o->dev.push_back(p);
+    return p;
+  };
+  auto hmalloc = [&](std::size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) == cudaSuccess) {
+      o->pinned.push_back(p);
+      return p;
+    }
+    cudaGetLastError();  // no GPU/driver: a CPU-only run works on pageable memory
+    p = std::aligned_alloc(64, (bytes + 63) / 64 * 64);
+    if (!p) throw std::bad_alloc();
+    o->heap.push_back(p);
+    return p;
+  };
+  const std::size_t mk = static_cast<std::size_t>(d.m) * d.k, kn = static_cast<std::size_t>(d.k) * d.n,
+                    mn = static_cast<std::size_t>(d.m) * d.n;
+  if (host || need_host) {
+    float* a = static_cast<float*>(hmalloc(mk * 4));
+    float* b = static_cast<float*>(hmalloc(kn * 4));
+    poas_b200::fill_uniform_host(a, d.k, d.m, d.k, 0, 0, d.k, sa);
+    poas_b200::fill_uniform_host(b, d.n, d.k, d.n, 0, 0, d.n, sb);
+    io.a_host = a;
+    io.lda_host = d.k;
+    io.b_host = b;
+    io.ldb_host = d.n;
+    io.c_host = static_cast<float*>(hmalloc(mn * 4));
+    io.ldc_host = d.n;
+  }
+  if (!host && need_dev) {
+    float* a = static_cast<float*>(dmalloc(mk * 4));
+    float* b = static_cast<float*>(dmalloc(kn * 4));
+    cuda_ok(poas_b200::fill_uniform(AbType::f32, a, d.k, d.m, d.k, 0, 0, d.k, sa, nullptr), "fill");
+    cuda_ok(poas_b200::fill_uniform(AbType::f32, b, d.n, d.k, d.n, 0, 0, d.n, sb, nullptr), "fill");
+    io.a_dev = a;
+    io.lda_dev = d.k;
+    io.b_dev = b;
+    io.ldb_dev = d.n;
+    io.c_dev = static_cast<float*>(dmalloc(mn * 4));
+    io.ldc_dev = d.n;
+    if (need16) {
+      const std::int64_t lda = (d.k + 7) / 8 * 8, ldb = (d.n + 7) / 8 * 8;
+      void* a16 = dmalloc(static_cast<std::size_t>(d.m) * lda * 2);
+      void* b16 = dmalloc(static_cast<std::size_t>(d.k) * ldb * 2);
+      cuda_ok(poas_b200::fill_uniform(t16, a16, lda, d.m, d.k, 0, 0, d.k, sa, nullptr), "fill");
+      cuda_ok(poas_b200::fill_uniform(t16, b16, ldb, d.k, d.n, 0, 0, d.n, sb, nullptr), "fill");
+      io.a16_dev = a16;
+      io.lda16_dev = lda;
+      io.b16_dev = b16;
+      io.ldb16_dev = ldb;
+    }
+    cuda_ok(cudaDeviceSynchronize(), "fill sync");
+  }
+  return o;
+}
+
+std::unique_ptr<Operands> operands_for(const poas::Executor& ex, const poas::Schedule& s,
+                                       std::uint64_t seed, bool host) {
+  bool need_host = false, need_dev = false, need16 = false;
+  AbType t16 = AbType::bf16;
+  for (const poas::ScheduledDevice& d : s.devices) {
+    if (d.rows == 0) continue;
+    const Unit* u = ex.find(d.id);
+    if (!u) fail(errc::missing_device, "no unit '" + d.id + "'");
+    if (!u->on_gpu()) need_host = true;
+    else need_dev = true;
+    if (u->spec().kind == poas::DeviceKind::xpu) {
+      need16 = true;
+      t16 = u->spec().dtype;
+    }
+  }
+  return make_operands(s.dims, seed, host, need_host, need_dev, need16, t16);
+}
+
+int cmd_profile(const Args& a) {
+  bool bus = true;
+  std::vector<std::unique_ptr<Unit>> units;
+  for (const UnitSpec& s : parse_unit_list(a.need("units"), &bus)) units.push_back(std::make_unique<Unit>(s));
+  if (a.has("bus")) bus = a.get("bus") == "true";
+  const poas::MachineProfile m = poas_b200::profile_units(units, profiling_from(a.get("profiling")), bus);
+  const std::string out = a.need("out");
+  poas::save_profile(out, m);
+  std::printf("profiled %zu unit(s), bus %s\n", m.devices.size(), m.bus ? "true" : "false");
+  for (const poas::DeviceProfile& d : m.devices) {
+    std::printf("%s (%s): slope %.6g s/op (%.1f TFLOP/s), intercept %.3g s", d.id.c_str(),
+                poas::kind_name(d.kind), d.compute.slope, 2.0 / d.compute.slope / 1e12,
+                d.compute.intercept);
+    if (d.uses_bus()) std::printf(", link %.1f GB/s", d.bandwidth / 1e9);
+    std::printf("\n");
+  }
+  std::printf("wrote %s\n", out.c_str());
+  return 0;
+}
+
+int cmd_plan(const Args& a) {
+  const poas::MachineProfile m = poas::load_profile(a.need("profile"));
+  const poas::MatrixDims d = poas::parse_dims(a.need("dims"));
+  const poas::Schedule s = poas::plan_with_policy(m, d, a.get("policy", "reference"));
+  const std::string out = a.need("out");
+  poas::save_schedule(out, s);
+  std::printf("split:");
+  for (std::size_t i = 0; i < s.devices.size(); ++i)
+    std::printf("%s %s %.2f%%", i ? "," : "", s.devices[i].id.c_str(),
+                100.0 * static_cast<double>(s.devices[i].rows) / static_cast<double>(d.m));
+  std::printf("\npredicted makespan: %.9f s\nwrote %s\n", s.makespan, out.c_str());
+  return 0;
+}
+
+void print_result(const poas::SimulationResult& r) {
+  std::printf("%-14s %-9s %14s %14s %9s\n", "device", "phase", "predicted s", "measured s", "err %");
+  for (const poas::DeviceOutcome& d : r.devices) {
+    const struct {
+      const char* n;
+      const poas::PhaseError* p;
+    } ph[] = {{"copy-in", &d.copy_in}, {"compute", &d.compute}, {"copy-out", &d.copy_out},
+              {"finish", &d.finish}};
+    for (const auto& x : ph)
+      std::printf("%-14s %-9s %14.9f %14.9f %9.2f\n", d.id.c_str(), x.n, x.p->predicted,
+                  x.p->measured, x.p->error_pct);
+  }
+  std::printf("makespan: predicted %.9f s, measured %.9f s, err %.2f%%\n", r.predicted_makespan,
+              r.measured_makespan, r.makespan_error_pct);
+  std::printf("rmse %%: finish %.2f, compute %.2f, copy %.2f\n", r.rmse_finish, r.rmse_compute,
+              r.rmse_copy);
+}
+
+int cmd_run(const Args& a) {
+  const std::string path = a.need("schedule");
+  const poas::Schedule s = poas::load_schedule(path);
+  poas::Executor ex(a.need("units"));
+  if (s.machine_hash != ex.machine_hash())  // as cmd_simulate, proj/tools/poas.cpp:120-122
+    fail(errc::hash_mismatch, "schedule was planned for machine " + s.machine_hash +
+                                  ", the units describe " + ex.machine_hash());
+  const int repeats = std::atoi(a.get("repeats", "3").c_str());
+  const std::uint64_t seed = std::strtoull(a.get("seed", "20261017").c_str(), nullptr, 10);
+  auto ops = operands_for(ex, s, seed, a.has("host"));
+  ex.run(s, ops->io, 1);  // warm-up
+  poas::SimulationResult r = ex.run(s, ops->io, repeats);
+  r.seed = seed;
+  std::printf("machine %s, seed %llu, repeats %d, %s operands\n", s.machine_hash.c_str(),
+              static_cast<unsigned long long>(seed), repeats, a.has("host") ? "host" : "resident");
+  print_result(r);
+  std::string report = path;
+  const auto dot = report.rfind('.');
+  if (dot != std::string::npos && report.find('/', dot) == std::string::npos) report.resize(dot);
+  report += ".report.json";
+  write_atomic(report, poas::format_execution_report(s, r));
+  std::printf("%.3f TFLOP/s\nwrote %s\n",
+              2.0 * static_cast<double>(s.dims.total_ops()) / r.measured_makespan / 1e12,
+              report.c_str());
+  return 0;
+}
+
+struct EvalInput {
+  std::string name;
+  poas::MatrixDims dims;
+};
+
+std::vector<EvalInput> load_inputs(const std::string& path) {
+  const poas::json::Value j = poas::json::parse(read_file(path), "inputs");
+  if (!j.is_array() || j.items.empty()) fail(errc::parse_failure, "inputs: expected a non-empty array");
+  std::vector<EvalInput> out;
+  for (const poas::json::Value& e : j.items) {
+    if (!e.is_object() || e.size() != 4 || !e.get("name") || !e.get("m") || !e.get("n") || !e.get("k"))
+      fail(errc::parse_failure, "inputs: each entry needs exactly name/m/n/k");
+    if (!e.get("name")->is_string() || !e.get("m")->is_integer() || !e.get("n")->is_integer() ||
+        !e.get("k")->is_integer())
+      fail(errc::parse_failure, "inputs: name must be a string and m/n/k integers");
+    EvalInput in{e.get("name")->s, {e.get("m")->as_int64(), e.get("n")->as_int64(), e.get("k")->as_int64()}};
+    poas::validate_dims(in.dims);
+    out.push_back(in);
+  }
+  return out;
+}
+
+std::string g(double v) {
+  char b[40];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+
+// evaluate_inputs over real hardware (reference proj/src/simulator.cpp:213-291):
+// co-executed run per input, standalone run per unit (skipped when its
+// predicted standalone makespan exceeds --max-standalone seconds), shares,
+// speedups, per-device RMSE.
+int cmd_evaluate(const Args& a) {
+  const std::string units = a.need("units");
+  const std::string out_dir = a.need("out-dir");
+  const int repeats = std::atoi(a.get("repeats", "3").c_str());
+  const std::uint64_t seed = std::strtoull(a.get("seed", "20261017").c_str(), nullptr, 10);
+  const double max_alone = std::atof(a.get("max-standalone", "2.0").c_str());
+  const std::string policy = a.get("policy", "reference");
+  std::vector<EvalInput> inputs;
+  if (a.has("inputs")) {
+    inputs = load_inputs(a.get("inputs"));
+  } else {  // the reference's Table 3 shapes scaled to one B200 (1/4 per side)
+    inputs = {{"i1", {7500, 7500, 7504}},   {"i2", {15000, 5000, 8752}},
+              {"i3", {32496, 5000, 5000}},  {"i4", {10000, 20000, 5000}},
+              {"i5", {10000, 7504, 15000}}, {"i6", {14000, 10000, 10000}}};
+  }
+  bool bus = true;
+  std::vector<std::unique_ptr<Unit>> probe_units;
+  for (const UnitSpec& s : parse_unit_list(units, &bus)) probe_units.push_back(std::make_unique<Unit>(s));
+  const poas::MachineProfile prof = poas_b200::profile_units(probe_units, profiling_from(a.get("profiling")), bus);
+  probe_units.clear();
+  poas::Executor ex(units);
+
+  std::string j = "{\n  \"machine_hash\": \"" + ex.machine_hash() + "\",\n  \"seed\": " +
+                  std::to_string(seed) + ",\n  \"repeats\": " + std::to_string(repeats) +
+                  ",\n  \"policy\": \"" + policy + "\",\n  \"devices\": [";
+  for (std::size_t i = 0; i < prof.devices.size(); ++i)
+    j += (i ? ", " : "") + std::string("\"") + prof.devices[i].id + "\"";
+  j += "],\n  \"inputs\": [\n";
+  std::string txt = "machine " + ex.machine_hash() + "  seed " + std::to_string(seed) +
+                    "  repeats " + std::to_string(repeats) + "  policy " + policy + "\n\n";
+  char line[512];
+  std::snprintf(line, sizeof line, "%-6s %-22s %8s %12s %12s %8s %10s %8s\n", "input", "dims",
+                "TOps", "predicted s", "measured s", "err %", "TFLOP/s", "speedup");
+  txt += line;
+  std::map<std::string, std::vector<double>> e_fin, e_cp;
+  for (std::size_t ii = 0; ii < inputs.size(); ++ii) {
+    const EvalInput& in = inputs[ii];
+    const poas::Schedule s = poas::plan_with_policy(prof, in.dims, policy);
+    auto ops = operands_for(ex, s, seed + ii, false);
+    ex.run(s, ops->io, 1);
+    const poas::SimulationResult r = ex.run(s, ops->io, repeats);
+    double best_alone = 0.0;
+    std::string alone_json;
+    for (const poas::DeviceProfile& d : prof.devices) {
+      const poas::Schedule sa = poas::standalone_schedule(prof, d.id, in.dims);
+      double meas = -1.0;
+      if (sa.makespan <= max_alone) {
+        auto oa = operands_for(ex, sa, seed + ii, false);
+        ex.run(sa, oa->io, 1);
+        meas = ex.run(sa, oa->io, repeats).measured_makespan;
+        if (best_alone == 0.0 || meas < best_alone) best_alone = meas;
+      }
+      alone_json += (alone_json.empty() ? "" : ", ") + std::string("{\"id\": \"") + d.id +
+                    "\", \"predicted\": " + g(sa.makespan) + ", \"measured\": " +
+                    (meas < 0 ? "null" : g(meas)) + "}";
+    }
+    const double tops = static_cast<double>(in.dims.total_ops()) / 1e12;
+    const double speedup = best_alone > 0 ? best_alone / r.measured_makespan : 0.0;
+    std::snprintf(line, sizeof line, "%-6s %-22s %8.2f %12.6f %12.6f %8.2f %10.1f %7.3fx\n",
+                  in.name.c_str(),
+                  (std::to_string(in.dims.m) + "x" + std::to_string(in.dims.n) + "x" +
+                   std::to_string(in.dims.k)).c_str(),
+                  tops, r.predicted_makespan, r.measured_makespan, r.makespan_error_pct,
+                  2 * tops / r.measured_makespan, speedup);
+    txt += line;
+    j += std::string(ii ? ",\n" : "") + "    {\"name\": \"" + in.name + "\", \"dims\": {\"m\": " +
+         std::to_string(in.dims.m) + ", \"n\": " + std::to_string(in.dims.n) + ", \"k\": " +
+         std::to_string(in.dims.k) + "}, \"tops\": " + g(tops) + ", \"predicted_makespan\": " +
+         g(r.predicted_makespan) + ", \"measured_makespan\": " + g(r.measured_makespan) +
+         ", \"makespan_error_pct\": " + g(r.makespan_error_pct) + ", \"speedup_vs_best_single\": " +
+         g(speedup) + ", \"standalone\": [" + alone_json + "], \"devices\": [";
+    for (std::size_t k = 0; k < r.devices.size(); ++k) {
+      const poas::DeviceOutcome& d = r.devices[k];
+      j += std::string(k ? ", " : "") + "{\"id\": \"" + d.id + "\", \"rows\": " +
+           std::to_string(d.rows) + ", \"share_pct\": " +
+           g(100.0 * static_cast<double>(d.rows) / static_cast<double>(in.dims.m)) +
+           ", \"finish_error_pct\": " + g(d.finish.error_pct) + ", \"compute_error_pct\": " +
+           g(d.compute.error_pct) + ", \"copy_error_pct\": " + g(d.copy.error_pct) + "}";
+      if (d.rows > 0) {
+        e_fin[d.id].push_back(d.finish.error_pct);
+        e_cp[d.id].push_back(d.compute.error_pct);
+      }
+    }
+    j += "]}";
+  }
+  j += "\n  ],\n  \"rmse\": [";
+  txt += "\nRMSE % across inputs, finish (compute)\n";
+  std::size_t idx = 0;
+  for (const poas::DeviceProfile& d : prof.devices) {
+    auto rms = [](const std::vector<double>& v) {
+      double s = 0;
+      for (double x : v) s += x * x;
+      return v.empty() ? 0.0 : std::sqrt(s / static_cast<double>(v.size()));
+    };
+    const double f = rms(e_fin[d.id]), c = rms(e_cp[d.id]);
+    j += std::string(idx++ ? ", " : "") + "{\"id\": \"" + d.id + "\", \"finish\": " + g(f) +
+         ", \"compute\": " + g(c) + "}";
+    std::snprintf(line, sizeof line, "%-14s %.2f (%.2f)\n", d.id.c_str(), f, c);
+    txt += line;
+  }
+  j += "]\n}\n";
+  mkdir(out_dir.c_str(), 0755);
+  write_atomic(out_dir + "/report.json", j);
+  write_atomic(out_dir + "/report.txt", txt);
+  std::fputs(txt.c_str(), stdout);
+  std::printf("wrote %s/report.txt\nwrote %s/report.json\n", out_dir.c_str(), out_dir.c_str());
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (const char* env = std::getenv("POAS_LOG"); env && !poas::parse_log_level(env)) {
+    std::fprintf(stderr, "poas: error: POAS_LOG must be quiet, info, or debug (got '%s')\n", env);
+    return 1;
+  }
+  try {
+    const Args a = parse_args(argc, argv);
+    if (a.cmd == "profile") return cmd_profile(a);
+    if (a.cmd == "plan") return cmd_plan(a);
+    if (a.cmd == "run") return cmd_run(a);
+    if (a.cmd == "evaluate") return cmd_evaluate(a);
+    fail(errc::invalid_argument, "unknown subcommand '" + a.cmd + "' (profile|plan|run|evaluate)");
+  } catch (const poas::Error& e) {
+    std::fprintf(stderr, "poas: error: %s\n", e.what());
+    return 1;
+  } catch (const poas_b200::capi::AbiError& e) {
+    std::fprintf(stderr, "poas: error: %s\n", e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "poas: internal error: %s\n", e.what());
+    return 2;
+  } catch (...) {
+    std::fprintf(stderr, "poas: internal error\n");
+    return 2;
+  }
+  return 2;
+}

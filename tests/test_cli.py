@@ -1,0 +1,68 @@
+"""The `poas` CLI: profile -> plan -> run on CPU units,
+exit codes 0/1/2 as the reference CLI (proj/tools/poas.cpp:251-260), and
+plan files byte-identical to the reference planner for the same profile."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+CLI = ROOT / "paper_2209_10245_b200" / "bin" / "poas"
+
+
+def run(*args, cwd=None):
+    return subprocess.run([str(CLI), *args], capture_output=True, text=True, cwd=cwd)
+
+
+@pytest.fixture(scope="module")
+def cli():
+    if not CLI.exists():
+        pytest.skip("poas CLI not built")
+    return CLI
+
+
+def test_plan_matches_reference(cli, ref, tmp_path):
+    prof = GOLDEN / "profiles" / "mach2_seed7.profile"
+    out = tmp_path / "s.json"
+    r = run("plan", "--profile", str(prof), "--dims", "16000x16000x16000", "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    assert out.read_text() == ref.plan(prof.read_text(), 16000, 16000, 16000)
+    assert "predicted makespan: 0.2" in r.stdout
+    out2 = tmp_path / "s2.json"
+    r = run("plan", "--profile", str(GOLDEN / "profiles" / "b200_like.profile"), "--dims",
+            "16384x16384x16384", "--policy", "best-subset", "--out", str(out2))
+    assert r.returncode == 0
+    assert json.loads(out2.read_text())["makespan"] == pytest.approx(0.006448, abs=1e-6)
+
+
+def test_profile_plan_run_cpu(cli, tmp_path):
+    prof, sched = tmp_path / "p.profile", tmp_path / "s.json"
+    r = run("profile", "--units", "cpu0=cpu:threads=2", "--profiling",
+            "probes=3,repetitions=3,cpu_min_side=256,cpu_max_side=640", "--out", str(prof))
+    assert r.returncode == 0, r.stderr
+    r = run("plan", "--profile", str(prof), "--dims", "300x200x100", "--out", str(sched))
+    assert r.returncode == 0, r.stderr
+    r = run("run", "--schedule", str(sched), "--units", "cpu0=cpu:threads=2", "--repeats", "2")
+    assert r.returncode == 0, r.stderr
+    rep = json.loads((tmp_path / "s.report.json").read_text())
+    assert rep["repeats"] == 2 and rep["devices"][0]["rows"] == 300
+    assert not (tmp_path / "s.report.json.tmp").exists()
+
+
+def test_exit_codes(cli, tmp_path):
+    assert run("bogus").returncode == 1
+    assert run().returncode == 1
+    assert run("plan", "--profile", "/nonexistent", "--dims", "1x1x1", "--out", "x").returncode == 1
+    bad = tmp_path / "bad.profile"
+    bad.write_text("poas-profile v2\n")
+    assert run("plan", "--profile", str(bad), "--dims", "1x1x1", "--out", "x").returncode == 1
+    sched = tmp_path / "s.json"
+    r = run("plan", "--profile", str(GOLDEN / "profiles" / "cpu_only.profile"), "--dims", "64x64x64",
+            "--out", str(sched))
+    assert r.returncode == 0
+    r = run("run", "--schedule", str(sched), "--units", "cpuX=cpu:threads=1")
+    assert r.returncode == 1 and "planned for machine" in r.stderr  # hash mismatch
+    r = subprocess.run([str(CLI), "plan"], capture_output=True, text=True, env={"POAS_LOG": "loud"})
+    assert r.returncode == 1 and "POAS_LOG" in r.stderr

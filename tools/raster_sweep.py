@@ -1,9 +1,13 @@
-"""Raster-group / kernel-variant sweep of the tensor unit (dev tool).
+"""Tensor-unit variant / raster-group comparison with clock sampling (dev tool).
 
-    python tools/raster_sweep.py  ->  JSON {variant: {N: {group: TFLOP/s}}}
+Variants are interleaved in rounds so power/thermal drift hits all of them
+alike; each timing records the SM clock and throttle reasons (pynvml).
+
+    python tools/raster_sweep.py [N ...]  ->  JSON
 """
 import json
 import os
+import statistics
 import sys
 from pathlib import Path
 
@@ -13,41 +17,64 @@ import torch  # noqa: E402
 
 from paper_2209_10245_b200 import poas  # noqa: E402
 
+try:
+    import pynvml
 
-def run(n, iters=6):
+    pynvml.nvmlInit()
+    NV = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+except Exception:  # pragma: no cover
+    NV = None
+
+
+def clocks():
+    if NV is None:
+        return None, None
+    return (pynvml.nvmlDeviceGetClockInfo(NV, pynvml.NVML_CLOCK_SM),
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(NV))
+
+
+VARIANTS = [("2cta", 8, 1), ("2cta", 8, 0), ("2cta", 16, 1), ("1cta", 16, 1), ("1cta", 16, 0), ("cublas", 0, 0)]
+
+
+def bench(n, rounds=3, iters=8):
     a = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
     b = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
     c = torch.empty(n, n, device="cuda")
     poas.fill_uniform(poas.DTYPE_BF16, a.data_ptr(), n, n, n, 0, 0, n, 1)
     poas.fill_uniform(poas.DTYPE_BF16, b.data_ptr(), n, n, n, 0, 0, n, 2)
     s = torch.cuda.current_stream().cuda_stream
-    res = {}
-    for variant in ("2cta", "1cta"):
-        os.environ["POAS_TC_KERNEL"] = variant
-        res[variant] = {}
-        for group in (1, 2, 4, 8, 16, 32, 64):
-            os.environ["POAS_TC_GROUP"] = str(group)
-            f = lambda: poas.tc_gemm(2, n, n, n, a.data_ptr(), n, b.data_ptr(), n, c.data_ptr(), n,  # noqa
-                                     stream=s)
-            f()
+    res = {f"{v}:{g}:s{y}": [] for v, g, y in VARIANTS}
+    for _ in range(rounds):
+        for v, g, y in VARIANTS:
+            if v == "cublas":
+                f = lambda: torch.matmul(a, b)  # noqa: E731
+            else:
+                os.environ["POAS_TC_KERNEL"] = v
+                os.environ["POAS_TC_GROUP"] = str(g)
+                os.environ["POAS_TC_SYNC"] = str(y)
+                f = lambda: poas.tc_gemm(2, n, n, n, a.data_ptr(), n, b.data_ptr(), n,  # noqa: E731
+                                         c.data_ptr(), n, stream=s)
+            for _ in range(2):
+                f()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record()
-            for _ in range(iters):
+            for i in range(iters):
                 f()
             e1.record()
-            torch.cuda.synchronize()
+            e1.synchronize()
+            clk, why = clocks()
             ms = e0.elapsed_time(e1) / iters
-            res[variant][group] = round(2 * n ** 3 / ms / 1e9, 1)
+            res[f"{v}:{g}:s{y}"].append((round(2 * n ** 3 / ms / 1e9, 1), clk, why))
     os.environ.pop("POAS_TC_GROUP", None)
     os.environ.pop("POAS_TC_KERNEL", None)
-    return res
+    return {k: {"tflops_median": statistics.median(x[0] for x in v), "runs": v} for k, v in res.items()}
 
 
 if __name__ == "__main__":
     sizes = [int(x) for x in sys.argv[1:]] or [8192, 16384, 32768]
     out = {}
     for n in sizes:
-        out[n] = run(n)
-        print(n, json.dumps(out[n]), file=sys.stderr, flush=True)
+        out[n] = bench(n)
+        print(n, json.dumps({k: v["tflops_median"] for k, v in out[n].items()}), file=sys.stderr, flush=True)
     print(json.dumps(out, indent=1))
