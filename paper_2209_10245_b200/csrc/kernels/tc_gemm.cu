@@ -320,8 +320,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                            kEvictNormal);
           tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK,
                            kEvictNormal);
-          tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage], col0 + 64,
-                           kb * kBK, kEvictNormal);
+          tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
+                           col0 + 64, kb * kBK, kEvictNormal);
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
@@ -528,9 +528,16 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
                                       static_cast<int>(k2SmemBytes));
   });
   if (attr_err != cudaSuccess) return attr_err;
-  // POAS_TC_KERNEL=1cta selects the single-SM kernel (A/B comparisons, tests).
+  // Kernel choice. The CTA-pair kernel moves 1/3 fewer operand bytes into
+  // shared memory per MAC and wins while the GPU runs near max clocks, but
+  // it re-reads ~2x more from DRAM (profiles/r01_*); once one launch is long
+  // enough to sit under the power cap (measured: 32768^3) the single-SM
+  // kernel's lower DRAM traffic buys higher clocks and wins. Threshold from
+  // tools/raster_sweep.py under sustained load: 2^44 MACs (~26000^3).
+  // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const char* variant = std::getenv("POAS_TC_KERNEL");
-  const bool force_1cta = variant && std::string(variant) == "1cta";
+  const double macs = static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K);
+  const bool force_1cta = variant ? std::string(variant) == "1cta" : macs >= 17592186044416.0;
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -544,10 +551,11 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.ldc = ldc;
   args.accumulate = accumulate ? 1 : 0;
   args.start_sync = nullptr;
-  // Start barrier (POAS_TC_SYNC=0 disables): needs every CTA co-resident,
-  // which a persistent grid within the unit's SM budget guarantees.
+  // Optional start barrier (POAS_TC_SYNC=1; off by default: measured no DRAM
+  // or time benefit, and it needs every CTA co-resident, which concurrent
+  // kernels -- e.g. NCCL's during an overlapped broadcast -- can break).
   const char* sync_env = std::getenv("POAS_TC_SYNC");
-  if (!(sync_env && sync_env[0] == '0') && budget <= sms) {
+  if (sync_env && sync_env[0] == '1' && budget <= sms) {
     args.start_sync = next_sync_counter();
     if (!args.start_sync) return cudaErrorMemoryAllocation;
     const cudaError_t e = cudaMemsetAsync(args.start_sync, 0, sizeof(unsigned), stream);
