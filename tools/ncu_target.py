@@ -64,7 +64,7 @@ if __name__ == "__main__":
         rows = int(sys.argv[2])
         n = int(sys.argv[3]) if len(sys.argv) > 3 else 16384
         sms = int(sys.argv[4]) if len(sys.argv) > 4 else 2
-        print(simt(rows, n, sms))
+        print(simt(rows, n, sms, exclusive=sms > 0))
     else:
         out = {"tc": {}, "simt_2sm": {}, "simt_all": {}}
         for n in (4096, 8192, 16384):
