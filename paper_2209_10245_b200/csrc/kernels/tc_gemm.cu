@@ -581,6 +581,25 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
+  // Experiment knob (POAS_TC_CLUSTER1=1): launch the single-SM kernel as
+  // clusters of 2 -- same work, cluster scheduling -- to separate placement
+  // effects from the pair MMA in the DRAM-traffic comparison.
+  const char* cl_env = std::getenv("POAS_TC_CLUSTER1");
+  if (cl_env && cl_env[0] == '1' && grid % 2 == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel, ma, mb, args);
+  }
   tc_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
   return cudaGetLastError();
 }

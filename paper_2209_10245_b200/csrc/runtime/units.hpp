@@ -33,7 +33,13 @@ struct UnitSpec {
   AbType dtype = AbType::bf16;  // xpu operand type
   std::uint32_t elem = 4;       // bytes per element crossing the link
   int threads = 0;              // cpu: OpenMP threads (0 = all cores)
-  std::int64_t align = 8;       // xpu row alignment (16-byte TMA pitch for 16-bit)
+  // xpu row alignment written to the profile (the adapter floors the unit's
+  // rows to it and requires k % align == 0). The tcgen05 kernel needs none:
+  // M/N/K tails are TMA out-of-bounds fills and the 16-byte row-pitch rule
+  // is met by padded leading dimensions, so the default is 1 -- an align of
+  // 8 (the paper's tensor cores) would push shaved rows onto a 25x slower
+  // unit. "align=8" reproduces the reference's setting.
+  std::int64_t align = 1;
   Link link = Link::pcie;       // what time_transfer measures
   std::int64_t probe_min = 0;   // own probe side range ("probe=MIN-MAX"); 0 = config's
   std::int64_t probe_max = 0;
