@@ -243,6 +243,7 @@ def main():
     ap.add_argument("--tc-sms", type=int, default=TC_SMS)
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-cpu", action="store_true", help="e2e without the host-CPU unit")
     ap.add_argument("--b-panels", type=int, default=4,
                     help="N > 1: B column panels broadcast separately (overlap with compute)")
     ap.add_argument("--policy", default="best-subset", choices=["reference", "best-subset"],
@@ -439,7 +440,12 @@ def main():
     if not args.no_e2e:
         units_e2e = units_res.replace("elem=2:link=hbm", "elem=4:link=pcie").replace(
             "elem=4:link=hbm", "elem=4:link=pcie")
-        prof_e2e = poas.profile_machine(units_e2e, PROFILING, bus=True)
+        if not args.no_e2e_cpu:
+            # With host-resident operands the host cores are a unit too: they
+            # compute rows in place while the GPU units' copies hold the link.
+            units_e2e += f";cpu{rank}=cpu:threads={max(1, (os.cpu_count() or 2) - 2)}"
+        prof_e2e = poas.profile_machine(units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048",
+                                        bus=True)
         sched_e2e = poas.plan_policy(prof_e2e, m, n, k, args.policy)
         ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
         se = json.loads(sched_e2e)
@@ -465,8 +471,9 @@ def main():
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         wall = float(tw.item())
-        h2d = sum(4 * (d["rows"] * k + k * n) for d in se["devices"] if d["rows"] > 0)
-        d2h = sum(4 * d["rows"] * n for d in se["devices"] if d["rows"] > 0)
+        linked = [d for d in se["devices"] if d["rows"] > 0 and not d["id"].startswith("cpu")]
+        h2d = sum(4 * (d["rows"] * k + k * n) for d in linked)  # A rows + all of B, fp32
+        d2h = sum(4 * d["rows"] * n for d in linked)            # C rows, fp32
         e2e = {"value": round(2.0 * m * world * n * k / (wall / steps_e2e) / 1e12, 3), "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                "ms_per_step": round(wall / steps_e2e * 1e3, 3),
@@ -476,6 +483,7 @@ def main():
                "predicted_makespan_ms": round(r_e2e["predicted_makespan"] * 1e3, 4),
                "measured_makespan_ms": round(r_e2e["measured_makespan"] * 1e3, 4),
                "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
+               "units": units_e2e,
                "path": "poas_b200_execute (C ABI), pinned host fp32 A/B/C, H2D+compute+D2H in step"}
         if save and rank == 0:
             (save / "report_e2e.json").write_text(json.dumps(r_e2e, indent=1))

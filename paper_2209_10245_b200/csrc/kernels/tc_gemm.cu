@@ -51,6 +51,8 @@ struct TcArgs {
   int accumulate;
   uint32_t idesc;
   int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
+  int raster_n;        // 1: groups run along N instead of M (experiments)
+  uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   unsigned* start_sync;  // optional zeroed counter: all producers start K in step
 };
 
@@ -70,7 +72,17 @@ __device__ __forceinline__ void start_barrier(unsigned* counter, unsigned expect
 // N-tiles, so one wave of the persistent grid shares A row panels and B
 // column panels through L2.
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int& mb,
-                                            int& nb) {
+                                            int& nb, int raster_n = 0) {
+  if (raster_n) {  // transpose the raster: groups of N-tiles walk down M
+    const int per_group_n = group * tiles_m;
+    const int gn_idx = t / per_group_n;
+    const int first_n = gn_idx * group;
+    const int gn = min(tiles_n - first_n, group);
+    const int rn = t - gn_idx * per_group_n;
+    nb = first_n + rn % gn;
+    mb = rn / gn;
+    return;
+  }
   const int per_group = group * tiles_n;
   const int g = t / per_group;
   const int first_m = g * group;
@@ -126,16 +138,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
+        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
           tma_load_2d(s_a + stage * kABytes, &map_a, &full[stage], kb * kBK, mb * kBM,
-                      kEvictNormal);
+                      args.hint_a);
 #pragma unroll
           for (int j = 0; j < kBN / 64; ++j)
             tma_load_2d(s_b + stage * kBBytes + j * kBChunkBytes, &map_b, &full[stage],
-                        nb * kBN + j * 64, kb * kBK, kEvictNormal);
+                        nb * kBN + j * 64, kb * kBK, args.hint_b);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int mb, nb;
-      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
+      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * kBM + quad * 32 + lane;
@@ -310,18 +322,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int t = first; t < total; t += step) {
         int mb, nb;
-        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
+        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
         const int col0 = nb * 256 + static_cast<int>(rank) * 128;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
           tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kb * kBK, row0,
-                           kEvictNormal);
+                           args.hint_a);
           tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK,
-                           kEvictNormal);
+                           args.hint_b);
           tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
-                           col0 + 64, kb * kBK, kEvictNormal);
+                           col0 + 64, kb * kBK, args.hint_b);
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
@@ -368,7 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     for (int t = first; t < total; t += step) {
       int mb, nb;
-      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb);
+      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + quad * 32 + lane;
@@ -551,6 +563,16 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.ldc = ldc;
   args.accumulate = accumulate ? 1 : 0;
   args.start_sync = nullptr;
+  auto hint = [](const char* name) {
+    const char* v = std::getenv(name);
+    if (v && std::string(v) == "first") return kEvictFirst;
+    if (v && std::string(v) == "last") return kEvictLast;
+    return kEvictNormal;
+  };
+  args.hint_a = hint("POAS_TC_HINT_A");  // experiment knobs; default evict_normal
+  args.hint_b = hint("POAS_TC_HINT_B");
+  const char* raster_env = std::getenv("POAS_TC_RASTER");
+  args.raster_n = raster_env && std::string(raster_env) == "n";
   // Optional start barrier (POAS_TC_SYNC=1; off by default: measured no DRAM
   // or time benefit, and it needs every CTA co-resident, which concurrent
   // kernels -- e.g. NCCL's during an overlapped broadcast -- can break).
