@@ -185,7 +185,8 @@ typedef struct {
    * b16_dev); each GPU unit waits on b_ready[p] (a cudaEvent_t recorded on
    * the same GPU after the panel landed) before computing that panel, so the
    * transfer of later panels overlaps compute on earlier ones. n must be a
-   * multiple of b_panels. b_panels <= 1: B is one row-major matrix. */
+   * multiple of b_panels. b_panels <= 1: B is one row-major matrix and, if
+   * b_ready is given, every GPU unit waits on b_ready[0] before computing. */
   int b_panels;
   void* const* b_ready;
 } poas_gemm_io;

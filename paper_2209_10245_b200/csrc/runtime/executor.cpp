@@ -310,6 +310,10 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
           u->gemm(r, np, d.k, a, lda, bp, np, c + p * np, ldc, false);
         }
       } else {
+        // One readiness event for the whole of B (e.g. a single broadcast).
+        if (io.resident && io.b_ready && io.b_ready[0])
+          cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(io.b_ready[0]), 0),
+                     "wait B");
         u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false);
       }
       cuda_check(cudaEventRecord(ev[i].cp1, s), "cudaEventRecord");
