@@ -209,11 +209,34 @@ int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_
                       int repeats, char** report_json);
 
 /* ------------------------------------------------------------------------
+ * Dynamic scheduling (paper §3.4.2; the reference has only
+ * the static scheduler -- B200 extension).
+ * --------------------------------------------------------------------- */
+/* The profile with every unit of an execution report (poas_b200_execute's
+ * report_json) re-fitted: slope and intercept scaled by 1 + alpha (r - 1),
+ * r = measured/predicted compute; link bandwidth likewise from the copy
+ * phases. alpha in (0, 1]. Identity (and machine hash) unchanged. */
+int poas_b200_refit_profile(const char* profile_text, const char* report_json, double alpha,
+                            char** out_profile);
+/* `iterations` executions of an m x n x k GEMM with re-planning: plan from
+ * the profile with `policy` (NULL = "reference"), execute once, re-fit,
+ * re-plan when |makespan error| > replan_threshold_pct, repeat. out_json:
+ * {"iterations": [{iteration, replanned, rows{id: n}, predicted_makespan,
+ * measured_makespan, makespan_error_pct}], "replans", "profile" (final,
+ * poas-profile v1 text), "schedule" (final)}. */
+int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t m, int64_t n,
+                          int64_t k, const char* policy, const poas_gemm_io* io, int iterations,
+                          double alpha, double replan_threshold_pct, char** out_json);
+
+/* ------------------------------------------------------------------------
  * Raw unit kernels (device pointers, caller's cudaStream_t or NULL).
  * --------------------------------------------------------------------- */
 int poas_b200_tc_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
                       const void* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
                       int num_ctas, void* stream);
+/* Name of the kernel poas_b200_tc_gemm launches for this shape
+ * ("tc_gemm_2cta_kernel" or "tc_gemm_kernel"; static string). */
+const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k);
 int poas_b200_simt_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
                         const float* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
                         int num_ctas, int exclusive_sm, void* stream);

@@ -157,6 +157,30 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
       "r"(rank)
       : "memory");
 }
+// 32-bit store to the same smem offset in CTA `rank` of the cluster (DSMEM).
+__device__ __forceinline__ void st_shared_cluster(const void* p, uint32_t rank, int v) {
+  asm volatile(
+      "{\n\t.reg .b32 remote;\n\t"
+      "mapa.shared::cluster.u32 remote, %0, %1;\n\t"
+      "st.shared::cluster.u32 [remote], %2;\n\t}" ::"r"(smem_addr(p)),
+      "r"(rank), "r"(v)
+      : "memory");
+}
+// Parity wait with cluster-scope acquire: pairs with arrivals released by
+// another CTA of the cluster (mbar_arrive_cluster).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 // Both CTAs of a pair load their half; completion bytes go to the even
 // (leader) CTA's barrier (peer bit cleared).
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,

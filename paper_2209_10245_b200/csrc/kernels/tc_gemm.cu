@@ -54,7 +54,37 @@ struct TcArgs {
   int raster_n;        // 1: groups run along N instead of M (experiments)
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   unsigned* start_sync;  // optional zeroed counter: all producers start K in step
+  int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
 };
+
+// ---------------------------------------------------------- tile scheduler
+// The producer thread (of the CTA, or of the pair's leader) owns the tile
+// sequence and hands each tile id to the other roles through a small smem
+// ring (tile_full / tile_empty mbarriers; -1 ends the sequence).
+//
+// Dynamic mode: tiles are claimed with one global atomicAdd per tile, so the
+// tiles in flight are always a contiguous window of the raster order however
+// far individual CTAs drift (launch stagger, far-die L2 latency, co-running
+// kernels taking SMs). With a static round-robin a lagging CTA works on a
+// tile of an older wave whose A/B panels have already left L2. The counter
+// resets itself: the last worker to finish zeroes it for the next launch.
+constexpr int kTileSlots = 4;
+
+__device__ __forceinline__ int claim_tile(const TcArgs& a, int& next_static, int step) {
+  if (a.tile_counter) return atomicAdd(a.tile_counter, 1);
+  const int t = next_static;
+  next_static += step;
+  return t;
+}
+
+__device__ __forceinline__ void release_counter(const TcArgs& a, int workers) {
+  if (!a.tile_counter) return;
+  __threadfence();  // this worker's claims precede its "done"
+  if (atomicAdd(a.tile_counter + 1, 1) == workers - 1) {
+    atomicExch(a.tile_counter, 0);
+    atomicExch(a.tile_counter + 1, 0);
+  }
+}
 
 // One-time start barrier of the producers (persistent grid, all CTAs
 // co-resident): CTAs that share A/B panels through L2 then sweep K in step
@@ -104,7 +134,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* tile_full = acc_empty + 2;
+  uint64_t* tile_empty = tile_full + kTileSlots;
+  int* tile_ring = reinterpret_cast<int*>(tile_empty + kTileSlots);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -119,6 +152,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 4);  // one arrive per epilogue warp
+    }
+    for (int s = 0; s < kTileSlots; ++s) {
+      mbar_init(&tile_full[s], 1);
+      mbar_init(&tile_empty[s], 5);  // MMA thread + 4 epilogue warps
     }
     fence_mbar_init();
   }
@@ -136,7 +173,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       start_barrier(args.start_sync, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int next_static = blockIdx.x;
+      int slot = 0;
+      uint32_t tphase = 0;
+      int t = claim_tile(args, next_static, gridDim.x);
+      while (true) {
+        const int tt = t < total ? t : -1;
+        mbar_wait(&tile_empty[slot], tphase ^ 1);
+        tile_ring[slot] = tt;
+        mbar_arrive(&tile_full[slot]);
+        if (++slot == kTileSlots) {
+          slot = 0;
+          tphase ^= 1;
+        }
+        if (tt < 0) break;
+        const int t_next = claim_tile(args, next_static, gridDim.x);  // latency hidden by the loads
         int mb, nb;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -153,7 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
+        t = t_next;
       }
+      release_counter(args, gridDim.x);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -161,7 +214,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int slot = 0;
+      uint32_t tphase = 0;
+      while (true) {
+        mbar_wait(&tile_full[slot], tphase);
+        const int t = tile_ring[slot];
+        mbar_arrive(&tile_empty[slot]);
+        if (++slot == kTileSlots) {
+          slot = 0;
+          tphase ^= 1;
+        }
+        if (t < 0) break;
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
@@ -196,7 +259,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    int slot = 0;
+    uint32_t tphase = 0;
+    while (true) {
+      mbar_wait(&tile_full[slot], tphase);
+      const int t = tile_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[slot]);
+      if (++slot == kTileSlots) {
+        slot = 0;
+        tphase ^= 1;
+      }
+      if (t < 0) break;
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
@@ -284,7 +358,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + k2Stages;
   uint64_t* acc_full = empty + k2Stages;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* tile_full = acc_empty + 2;
+  uint64_t* tile_empty = tile_full + kTileSlots;
+  int* tile_ring = reinterpret_cast<int*>(tile_empty + kTileSlots);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -301,6 +378,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    for (int s = 0; s < kTileSlots; ++s) {
+      mbar_init(&tile_full[s], 1);    // the leader's producer (local or remote arrive)
+      mbar_init(&tile_empty[s], 10);  // leader: its MMA thread + peer producer + 2 x 4 epilogue warps
     }
     fence_mbar_init();
   }
@@ -320,7 +401,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       start_barrier(args.start_sync, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = first; t < total; t += step) {
+      int next_static = first;
+      int slot = 0;
+      uint32_t tphase = 0;
+      // The leader claims tiles and publishes them to both CTAs' rings; the
+      // peer's producer follows its own ring.
+      int t = leader ? claim_tile(args, next_static, step) : 0;
+      while (true) {
+        if (leader) {
+          t = t < total ? t : -1;
+          mbar_wait_cluster(&tile_empty[slot], tphase ^ 1);
+          tile_ring[slot] = t;
+          st_shared_cluster(&tile_ring[slot], 1, t);
+          mbar_arrive(&tile_full[slot]);
+          mbar_arrive_cluster(&tile_full[slot], 1);
+        } else {
+          mbar_wait_cluster(&tile_full[slot], tphase);
+          t = tile_ring[slot];
+          mbar_arrive_cluster(&tile_empty[slot], 0);
+        }
+        if (++slot == kTileSlots) {
+          slot = 0;
+          tphase ^= 1;
+        }
+        if (t < 0) break;
+        const int t_next = leader ? claim_tile(args, next_static, step) : 0;
         int mb, nb;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
@@ -339,7 +444,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
+        t = t_next;
       }
+      if (leader) release_counter(args, step);
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
@@ -347,7 +454,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = first; t < total; t += step) {
+      int slot = 0;
+      uint32_t tphase = 0;
+      while (true) {
+        mbar_wait_cluster(&tile_full[slot], tphase);
+        const int t = tile_ring[slot];
+        mbar_arrive(&tile_empty[slot]);
+        if (++slot == kTileSlots) {
+          slot = 0;
+          tphase ^= 1;
+        }
+        if (t < 0) break;
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
@@ -378,7 +495,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
-    for (int t = first; t < total; t += step) {
+    int slot = 0;
+    uint32_t tphase = 0;
+    while (true) {
+      mbar_wait_cluster(&tile_full[slot], tphase);
+      const int t = tile_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tile_empty[slot], 0);  // the leader's barrier
+      if (++slot == kTileSlots) {
+        slot = 0;
+        tphase ^= 1;
+      }
+      if (t < 0) break;
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
@@ -507,7 +635,42 @@ unsigned* next_sync_counter() {
   ++next[dev];
   return c;
 }
+
+// Per-device ring of tile-scheduler counters {next, done}. Zeroed once at
+// allocation; every launch leaves its counter zero again (release_counter),
+// so no per-launch memset. Launches in flight at the same time (other
+// streams) take distinct slots.
+int* next_tile_counter() {
+  constexpr int kRing = 256;
+  static std::mutex mu;
+  static int* ring[64] = {};
+  static int next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ring[dev]) {
+    int* p = nullptr;
+    const size_t bytes = kRing * 32 * sizeof(int);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      cudaFree(p);
+      return nullptr;
+    }
+    ring[dev] = p;
+  }
+  int* c = ring[dev] + (next[dev] % kRing) * 32;  // 128 B apart
+  ++next[dev];
+  return c;
+}
 }  // namespace
+
+const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t K) {
+  if (const char* v = std::getenv("POAS_TC_KERNEL"))
+    return std::string(v) == "1cta" ? "tc_gemm_kernel" : "tc_gemm_2cta_kernel";
+  const double macs = static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K);
+  return macs >= 17592186044416.0 ? "tc_gemm_kernel" : "tc_gemm_2cta_kernel";
+}
 
 cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
@@ -547,9 +710,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   // kernel's lower DRAM traffic buys higher clocks and wins. Threshold from
   // tools/raster_sweep.py under sustained load: 2^44 MACs (~26000^3).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
-  const char* variant = std::getenv("POAS_TC_KERNEL");
-  const double macs = static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K);
-  const bool force_1cta = variant ? std::string(variant) == "1cta" : macs >= 17592186044416.0;
+  const bool force_1cta = std::string(tc_gemm_kernel_name(M, N, K)) == "tc_gemm_kernel";
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -582,6 +743,13 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
     if (!args.start_sync) return cudaErrorMemoryAllocation;
     const cudaError_t e = cudaMemsetAsync(args.start_sync, 0, sizeof(unsigned), stream);
     if (e != cudaSuccess) return e;
+  }
+  // Dynamic tile scheduler (default; POAS_TC_SCHED=static: round-robin).
+  const char* sched_env = std::getenv("POAS_TC_SCHED");
+  args.tile_counter = nullptr;
+  if (!(sched_env && std::string(sched_env) == "static")) {
+    args.tile_counter = next_tile_counter();
+    if (!args.tile_counter) return cudaErrorMemoryAllocation;
   }
 
   if (!force_1cta && budget >= 2) {

@@ -1,0 +1,121 @@
+// Dynamic scheduling: model re-fit from measured executions and re-planning
+// (see poas/dynamic.hpp).
+#include "poas/dynamic.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <utility>
+
+#include "json_lite.hpp"
+#include "poas/error.hpp"
+#include "poas/policy.hpp"
+
+namespace poas {
+namespace {
+
+// EWMA update of a measured/predicted ratio, clamped to one step.
+bool update_factor(const PhaseError& e, const RefitOptions& o, double* g) {
+  if (!(e.measured > 0.0) || !(e.predicted > 0.0) || !std::isfinite(e.measured) ||
+      !std::isfinite(e.predicted))
+    return false;
+  const double r = e.measured / e.predicted;
+  *g = std::clamp(1.0 + o.alpha * (r - 1.0), 1.0 / o.max_step, o.max_step);
+  return true;
+}
+
+[[noreturn]] void bad_report(const std::string& what) {
+  fail(errc::parse_failure, "execution report: " + what);
+}
+
+const json::Value& member(const json::Value& obj, const std::string& key) {
+  const json::Value* v = obj.is_object() ? obj.get(key) : nullptr;
+  if (!v) bad_report("missing \"" + key + "\"");
+  return *v;
+}
+
+// A measured/predicted number; JSON null (a non-finite value) reads as 0,
+// which the re-fit ignores.
+double number(const json::Value& obj, const std::string& key) {
+  const json::Value& v = member(obj, key);
+  if (v.type == json::Value::Type::null) return 0.0;
+  if (!v.is_number()) bad_report("\"" + key + "\" is not a number");
+  return v.as_double();
+}
+
+PhaseError phase(const json::Value& dev, const std::string& key) {
+  const json::Value& p = member(dev, key);
+  return {number(p, "measured"), number(p, "predicted"), number(p, "error_pct")};
+}
+
+}  // namespace
+
+SimulationResult parse_execution_report(const std::string& report_json) {
+  const json::Value root = json::parse(report_json, "execution report");
+  SimulationResult r;
+  r.measured_makespan = number(root, "measured_makespan");
+  r.predicted_makespan = number(root, "predicted_makespan");
+  r.makespan_error_pct = number(root, "makespan_error_pct");
+  const json::Value& devs = member(root, "devices");
+  if (!devs.is_array()) bad_report("\"devices\" is not an array");
+  for (const json::Value& d : devs.items) {
+    DeviceOutcome o;
+    const json::Value& id = member(d, "id");
+    if (!id.is_string()) bad_report("device id is not a string");
+    o.id = id.s;
+    const json::Value& rows = member(d, "rows");
+    if (!rows.is_integer()) bad_report("device rows is not an integer");
+    o.rows = rows.as_int64();
+    o.copy_in = phase(d, "copy_in");
+    o.compute = phase(d, "compute");
+    o.copy_out = phase(d, "copy_out");
+    r.devices.push_back(std::move(o));
+  }
+  return r;
+}
+
+MachineProfile refit_profile(const MachineProfile& prior, const std::vector<DeviceOutcome>& observed,
+                             const RefitOptions& options) {
+  if (!(options.alpha > 0.0 && options.alpha <= 1.0))
+    fail(errc::invalid_argument, "refit alpha must be in (0, 1]");
+  if (!(options.max_step >= 1.0) || !std::isfinite(options.max_step))
+    fail(errc::invalid_argument, "refit max_step must be a finite number >= 1");
+  MachineProfile out = prior;
+  for (const DeviceOutcome& o : observed) {
+    DeviceProfile* d = nullptr;
+    for (DeviceProfile& c : out.devices)
+      if (c.id == o.id) d = &c;
+    if (!d) fail(errc::missing_device, "refit: unit '" + o.id + "' is not in the profile");
+    if (o.rows <= 0) continue;
+    double g = 1.0;
+    if (update_factor(o.compute, options, &g)) {
+      d->compute.slope *= g;
+      d->compute.intercept *= g;
+    }
+    if (d->uses_bus() && d->bandwidth > 0.0) {
+      PhaseError link;
+      link.measured = o.copy_in.measured + o.copy_out.measured;
+      link.predicted = o.copy_in.predicted + o.copy_out.predicted;
+      if (update_factor(link, options, &g)) d->bandwidth /= g;
+    }
+  }
+  validate_machine(out);
+  return out;
+}
+
+DynamicScheduler::DynamicScheduler(MachineProfile prior, MatrixDims dims, DynamicOptions options)
+    : profile_(std::move(prior)), dims_(dims), options_(std::move(options)) {
+  if (!(options_.replan_threshold_pct >= 0.0))
+    fail(errc::invalid_argument, "replan threshold must be >= 0");
+  schedule_ = plan_with_policy(profile_, dims_, options_.policy);
+}
+
+bool DynamicScheduler::observe(const SimulationResult& result) {
+  profile_ = refit_profile(profile_, result.devices, options_.refit);
+  ++observations_;
+  if (!(std::fabs(result.makespan_error_pct) > options_.replan_threshold_pct)) return false;
+  schedule_ = plan_with_policy(profile_, dims_, options_.policy);
+  ++replans_;
+  return true;
+}
+
+}  // namespace poas

@@ -10,6 +10,7 @@
 #include "host_gemm.hpp"
 #include "host_rng.hpp"
 #include "poas/adapter.hpp"
+#include "poas/dynamic.hpp"
 #include "poas/error.hpp"
 #include "poas/executor.hpp"
 #include "poas/optimizer.hpp"
@@ -89,6 +90,52 @@ std::string tile_plan_json(const poas::TilePlan& p) {
     o += "]}";
   }
   return o + "]}";
+}
+
+std::string json_escape(const std::string& s) {
+  std::string o;
+  for (const char c : s) {
+    if (c == '"' || c == '\\') {
+      o += '\\';
+      o += c;
+    } else if (c == '\n') {
+      o += "\\n";
+    } else if (static_cast<unsigned char>(c) < 0x20) {
+      char buf[8];
+      std::snprintf(buf, sizeof buf, "\\u%04x", c);
+      o += buf;
+    } else {
+      o += c;
+    }
+  }
+  return o;
+}
+
+poas::GemmOperands operands_of(const poas_gemm_io& io) {
+  poas::GemmOperands op;
+  op.m = io.m;
+  op.n = io.n;
+  op.k = io.k;
+  op.a_host = io.a_host;
+  op.lda_host = io.lda_host;
+  op.b_host = io.b_host;
+  op.ldb_host = io.ldb_host;
+  op.c_host = io.c_host;
+  op.ldc_host = io.ldc_host;
+  op.a_dev = io.a_dev;
+  op.lda_dev = io.lda_dev;
+  op.b_dev = io.b_dev;
+  op.ldb_dev = io.ldb_dev;
+  op.a16_dev = io.a16_dev;
+  op.lda16_dev = io.lda16_dev;
+  op.b16_dev = io.b16_dev;
+  op.ldb16_dev = io.ldb16_dev;
+  op.c_dev = io.c_dev;
+  op.ldc_dev = io.ldc_dev;
+  op.resident = io.resident != 0;
+  op.b_panels = io.b_panels;
+  op.b_ready = io.b_ready;
+  return op;
 }
 
 poas::ProfilingConfig parse_profiling(const char* text) {
@@ -353,31 +400,58 @@ int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_
     need_ptr(ex, "executor");
     need_ptr(io, "io");
     const poas::Schedule s = poas::parse_schedule(need_str(schedule_json, "schedule"));
-    poas::GemmOperands op;
-    op.m = io->m;
-    op.n = io->n;
-    op.k = io->k;
-    op.a_host = io->a_host;
-    op.lda_host = io->lda_host;
-    op.b_host = io->b_host;
-    op.ldb_host = io->ldb_host;
-    op.c_host = io->c_host;
-    op.ldc_host = io->ldc_host;
-    op.a_dev = io->a_dev;
-    op.lda_dev = io->lda_dev;
-    op.b_dev = io->b_dev;
-    op.ldb_dev = io->ldb_dev;
-    op.a16_dev = io->a16_dev;
-    op.lda16_dev = io->lda16_dev;
-    op.b16_dev = io->b16_dev;
-    op.ldb16_dev = io->ldb16_dev;
-    op.c_dev = io->c_dev;
-    op.ldc_dev = io->ldc_dev;
-    op.resident = io->resident != 0;
-    op.b_panels = io->b_panels;
-    op.b_ready = io->b_ready;
-    const poas::SimulationResult r = ex->ex->run(s, op, repeats);
+    const poas::SimulationResult r = ex->ex->run(s, operands_of(*io), repeats);
     if (report_json) *report_json = dup_string(poas::format_execution_report(s, r));
+  });
+}
+
+int poas_b200_refit_profile(const char* profile_text, const char* report_json, double alpha,
+                            char** out_profile) {
+  return guard([&] {
+    need_ptr(out_profile, "out_profile");
+    const poas::MachineProfile prior = poas::parse_profile(need_str(profile_text, "profile"));
+    const poas::SimulationResult r =
+        poas::parse_execution_report(need_str(report_json, "report_json"));
+    poas::RefitOptions opt;
+    opt.alpha = alpha;
+    *out_profile = dup_string(poas::format_profile(poas::refit_profile(prior, r.devices, opt)));
+  });
+}
+
+int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t m, int64_t n,
+                          int64_t k, const char* policy, const poas_gemm_io* io, int iterations,
+                          double alpha, double replan_threshold_pct, char** out_json) {
+  return guard([&] {
+    need_ptr(ex, "executor");
+    need_ptr(io, "io");
+    need_ptr(out_json, "out_json");
+    if (iterations < 1) raise(POAS_E_INVALID_ARGUMENT, "iterations must be >= 1");
+    poas::DynamicOptions opt;
+    opt.refit.alpha = alpha;
+    opt.replan_threshold_pct = replan_threshold_pct;
+    if (policy) opt.policy = policy;
+    poas::DynamicScheduler dyn(poas::parse_profile(need_str(profile_text, "profile")),
+                               dims_of(m, n, k), opt);
+    const poas::GemmOperands op = operands_of(*io);
+    std::string o = "{\n  \"iterations\": [\n";
+    bool replanned = false;
+    for (int it = 0; it < iterations; ++it) {
+      const poas::SimulationResult r = ex->ex->run(dyn.schedule(), op, 1);
+      o += "    {\"iteration\": " + std::to_string(it) +
+           ", \"replanned\": " + (replanned ? "true" : "false") + ", \"rows\": {";
+      for (std::size_t i = 0; i < r.devices.size(); ++i)
+        o += (i ? ", \"" : "\"") + json_escape(r.devices[i].id) +
+             "\": " + std::to_string(r.devices[i].rows);
+      o += "}, \"predicted_makespan\": " + g17(r.predicted_makespan) +
+           ", \"measured_makespan\": " + g17(r.measured_makespan) +
+           ", \"makespan_error_pct\": " + g17(r.makespan_error_pct) + "}";
+      o += it + 1 < iterations ? ",\n" : "\n";
+      replanned = dyn.observe(r);
+    }
+    o += "  ],\n  \"replans\": " + std::to_string(dyn.replans()) + ",\n";
+    o += "  \"profile\": \"" + json_escape(poas::format_profile(dyn.profile())) + "\",\n";
+    o += "  \"schedule\": " + poas::format_schedule(dyn.schedule()) + "}\n";
+    *out_json = dup_string(o);
   });
 }
 

@@ -6,6 +6,9 @@
 //   poas run      --schedule FILE --units SPEC [--repeats N] [--seed S] [--host]
 //   poas evaluate --units SPEC [--inputs FILE] [--repeats N] [--seed S]
 //                 [--policy P] [--profiling k=v,..] --out-dir DIR
+//   poas adapt    --profile FILE --units SPEC --dims MxNxK [--iterations N]
+//                 [--alpha A] [--threshold PCT] [--policy P] [--seed S] [--host]
+//                 [--out-profile FILE] [--out FILE]
 // Exit codes as the reference: 0 success, 1 domain or usage error, 2 internal.
 // `run` replaces `simulate` (poas.cpp:116-151): it executes the schedule on
 // the box (inputs from the seeded counter generator) and writes
@@ -29,6 +32,7 @@
 #include "../runtime/capi_util.hpp"
 #include "../runtime/host_rng.hpp"
 #include "../runtime/units.hpp"
+#include "poas/dynamic.hpp"
 #include "poas/error.hpp"
 #include "poas/executor.hpp"
 #include "poas/log.hpp"
@@ -67,7 +71,7 @@ struct Args {
 
 Args parse_args(int argc, char** argv) {
   Args a;
-  if (argc < 2) fail(errc::invalid_argument, "usage: poas {profile|plan|run|evaluate} [options]");
+  if (argc < 2) fail(errc::invalid_argument, "usage: poas {profile|plan|run|evaluate|adapt} [options]");
   a.cmd = argv[1];
   static const std::map<std::string, bool> flags = {{"host", true}};
   for (int i = 2; i < argc; ++i) {
@@ -219,14 +223,13 @@ std::unique_ptr<Operands> make_operands(const poas::MatrixDims& d, std::uint64_t
   return o;
 }
 
-std::unique_ptr<Operands> operands_for(const poas::Executor& ex, const poas::Schedule& s,
-                                       std::uint64_t seed, bool host) {
+// Operands every unit in `busy` can read.
+std::unique_ptr<Operands> operands_for_units(const std::vector<const Unit*>& busy,
+                                             const poas::MatrixDims& dims, std::uint64_t seed,
+                                             bool host) {
   bool need_host = false, need_dev = false, need16 = false;
   AbType t16 = AbType::bf16;
-  for (const poas::ScheduledDevice& d : s.devices) {
-    if (d.rows == 0) continue;
-    const Unit* u = ex.find(d.id);
-    if (!u) fail(errc::missing_device, "no unit '" + d.id + "'");
+  for (const Unit* u : busy) {
     if (!u->on_gpu()) need_host = true;
     else need_dev = true;
     if (u->spec().kind == poas::DeviceKind::xpu) {
@@ -234,7 +237,19 @@ std::unique_ptr<Operands> operands_for(const poas::Executor& ex, const poas::Sch
       t16 = u->spec().dtype;
     }
   }
-  return make_operands(s.dims, seed, host, need_host, need_dev, need16, t16);
+  return make_operands(dims, seed, host, need_host, need_dev, need16, t16);
+}
+
+std::unique_ptr<Operands> operands_for(const poas::Executor& ex, const poas::Schedule& s,
+                                       std::uint64_t seed, bool host) {
+  std::vector<const Unit*> busy;
+  for (const poas::ScheduledDevice& d : s.devices) {
+    if (d.rows == 0) continue;
+    const Unit* u = ex.find(d.id);
+    if (!u) fail(errc::missing_device, "no unit '" + d.id + "'");
+    busy.push_back(u);
+  }
+  return operands_for_units(busy, s.dims, seed, host);
 }
 
 int cmd_profile(const Args& a) {
@@ -313,6 +328,52 @@ int cmd_run(const Args& a) {
   std::printf("%.3f TFLOP/s\nwrote %s\n",
               2.0 * static_cast<double>(s.dims.total_ops()) / r.measured_makespan / 1e12,
               report.c_str());
+  return 0;
+}
+
+// Dynamic scheduling (paper §3.4.2; poas/dynamic.hpp): plan from the
+// profile, run, re-fit the unit models from the measured phases, re-plan when
+// the makespan error exceeds the threshold; writes the adapted profile and the
+// last schedule.
+int cmd_adapt(const Args& a) {
+  poas::Executor ex(a.need("units"));
+  const poas::MachineProfile prior = poas::load_profile(a.need("profile"));
+  if (poas::machine_hash(prior) != ex.machine_hash())
+    fail(errc::hash_mismatch, "profile describes machine " + poas::machine_hash(prior) +
+                                  ", the units describe " + ex.machine_hash());
+  const poas::MatrixDims dims = poas::parse_dims(a.need("dims"));
+  const int iterations = std::atoi(a.get("iterations", "5").c_str());
+  if (iterations < 1) fail(errc::invalid_argument, "--iterations must be >= 1");
+  poas::DynamicOptions opt;
+  opt.refit.alpha = std::atof(a.get("alpha", "0.5").c_str());
+  opt.replan_threshold_pct = std::atof(a.get("threshold", "2").c_str());
+  opt.policy = a.get("policy", "reference");
+  const std::uint64_t seed = std::strtoull(a.get("seed", "20261017").c_str(), nullptr, 10);
+  poas::DynamicScheduler dyn(prior, dims, opt);
+  std::vector<const Unit*> all;
+  for (const auto& u : ex.units()) all.push_back(u.get());
+  auto ops = operands_for_units(all, dims, seed, a.has("host"));
+  std::printf("%-5s %-8s %14s %14s %9s  rows\n", "iter", "replan", "predicted s", "measured s",
+              "err %");
+  bool replanned = false;
+  for (int it = 0; it < iterations; ++it) {
+    const poas::SimulationResult r = ex.run(dyn.schedule(), ops->io, 1);
+    std::printf("%-5d %-8s %14.9f %14.9f %9.2f ", it, replanned ? "yes" : "no",
+                r.predicted_makespan, r.measured_makespan, r.makespan_error_pct);
+    for (const poas::DeviceOutcome& d : r.devices)
+      std::printf(" %s=%lld", d.id.c_str(), static_cast<long long>(d.rows));
+    std::printf("\n");
+    replanned = dyn.observe(r);
+  }
+  std::printf("%d re-plan(s) in %d iteration(s)\n", dyn.replans(), iterations);
+  if (a.has("out-profile")) {
+    poas::save_profile(a.get("out-profile"), dyn.profile());
+    std::printf("wrote %s\n", a.get("out-profile").c_str());
+  }
+  if (a.has("out")) {
+    poas::save_schedule(a.get("out"), dyn.schedule());
+    std::printf("wrote %s\n", a.get("out").c_str());
+  }
   return 0;
 }
 
@@ -470,7 +531,9 @@ int main(int argc, char** argv) {
     if (a.cmd == "plan") return cmd_plan(a);
     if (a.cmd == "run") return cmd_run(a);
     if (a.cmd == "evaluate") return cmd_evaluate(a);
-    fail(errc::invalid_argument, "unknown subcommand '" + a.cmd + "' (profile|plan|run|evaluate)");
+    if (a.cmd == "adapt") return cmd_adapt(a);
+    fail(errc::invalid_argument,
+         "unknown subcommand '" + a.cmd + "' (profile|plan|run|evaluate|adapt)");
   } catch (const poas::Error& e) {
     std::fprintf(stderr, "poas: error: %s\n", e.what());
     return 1;

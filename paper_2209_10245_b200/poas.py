@@ -39,6 +39,15 @@ def plan_policy(profile: str, m: int, n: int, k: int, policy: str = "reference")
     return call_str(lib.poas_b200_plan_policy, _b(profile), m, n, k, _b(policy))
 
 
+def refit_profile(profile: str, report: str | dict, alpha: float = 0.5) -> str:
+    """Dynamic-scheduling model update (paper §3.4.2; B200 extension): the
+    profile re-fitted from one execution report (Executor.execute's dict or
+    its JSON text)."""
+    if isinstance(report, dict):
+        report = json.dumps(report)
+    return call_str(lib.poas_b200_refit_profile, _b(profile), _b(report), float(alpha))
+
+
 def plan_standalone(profile: str, device_id: str, m: int, n: int, k: int) -> str:
     """standalone_schedule (reference proj/src/scheduler.cpp:59-74)."""
     return call_str(lib.poas_b200_plan_standalone, _b(profile), _b(device_id), m, n, k)
@@ -192,6 +201,19 @@ class Executor:
         from ._lib import take_string
         return json.loads(take_string(out))
 
+    def run_dynamic(self, profile: str, m: int, n: int, k: int, io: GemmIO, iterations: int,
+                    policy: str = "reference", alpha: float = 0.5,
+                    replan_threshold_pct: float = 2.0) -> dict:
+        """Dynamic scheduling loop (poas_b200_run_dynamic): plan, execute,
+        re-fit, re-plan when |makespan error| > threshold; per-iteration log,
+        the final profile and schedule."""
+        out = C.c_void_p()
+        check(lib.poas_b200_run_dynamic(self._h, _b(profile), m, n, k, _b(policy), C.byref(io),
+                                        iterations, float(alpha), float(replan_threshold_pct),
+                                        C.byref(out)))
+        from ._lib import take_string
+        return json.loads(take_string(out))
+
     def close(self):
         if self._h:
             lib.poas_b200_executor_destroy(self._h)
@@ -204,6 +226,11 @@ class Executor:
 def tc_gemm(dtype: int, m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, num_ctas=0, stream=None):
     check(lib.poas_b200_tc_gemm(dtype, m, n, k, a, lda, b, ldb, c, ldc, int(accumulate), num_ctas,
                                 stream))
+
+
+def tc_kernel_name(m: int, n: int, k: int) -> str:
+    """The tensor-core kernel tc_gemm launches for this shape."""
+    return lib.poas_b200_tc_kernel_name(m, n, k).decode()
 
 
 def simt_gemm(m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, num_ctas=0, exclusive=False,

@@ -66,3 +66,39 @@ def test_exit_codes(cli, tmp_path):
     assert r.returncode == 1 and "planned for machine" in r.stderr  # hash mismatch
     r = subprocess.run([str(CLI), "plan"], capture_output=True, text=True, env={"POAS_LOG": "loud"})
     assert r.returncode == 1 and "POAS_LOG" in r.stderr
+
+
+def test_adapt_cpu_units(cli, tmp_path):
+    """`poas adapt`: dynamic scheduling on two host units; a profile planted
+    8x too optimistic for cpuA is re-fitted and re-planned."""
+    units = "cpuA=cpu:threads=1;cpuB=cpu:threads=1"
+    prof = tmp_path / "p.profile"
+    r = run("profile", "--units", units, "--profiling",
+            "probes=3,repetitions=2,cpu_min_side=128,cpu_max_side=256", "--out", str(prof))
+    assert r.returncode == 0, r.stderr
+    lines, cur = [], None
+    for line in prof.read_text().splitlines():
+        parts = line.split()
+        if len(parts) == 2 and parts[0] == "device":
+            cur = parts[1]
+        if cur == "cpuA" and len(parts) == 2 and parts[0] in ("slope", "intercept"):
+            line = f"{parts[0]} {float(parts[1]) / 8.0!r}"
+        lines.append(line)
+    planted = tmp_path / "planted.profile"
+    planted.write_text("\n".join(lines) + "\n")
+    out_prof, out_sched = tmp_path / "adapted.profile", tmp_path / "adapted.json"
+    r = run("adapt", "--profile", str(planted), "--units", units, "--dims", "1024x256x256",
+            "--iterations", "5", "--alpha", "1", "--threshold", "5",
+            "--out-profile", str(out_prof), "--out", str(out_sched))
+    assert r.returncode == 0, r.stderr
+    assert "re-plan(s) in 5 iteration(s)" in r.stdout
+    assert not r.stdout.splitlines()[-3].startswith("0 re-plan")
+    s = json.loads(out_sched.read_text())
+    assert sum(d["rows"] for d in s["devices"]) == 1024
+    assert out_prof.read_text().startswith("poas-profile v1")
+    # a profile for other units is a hash mismatch (exit 1)
+    r = run("adapt", "--profile", str(planted), "--units", "cpuZ=cpu:threads=1", "--dims", "64x64x64")
+    assert r.returncode == 1 and "describes machine" in r.stderr
+    r = run("adapt", "--profile", str(planted), "--units", units, "--dims", "64x64x64",
+            "--iterations", "0")
+    assert r.returncode == 1

@@ -239,3 +239,38 @@ def test_unit_backend_plugin(torch_cuda, poas):
     c = poas.Unit("cpu0=cpu:threads=2")
     assert not c.has_transfers()
     assert c.time_gemm(64) > 0
+
+
+def test_dynamic_rescheduling_on_gpu_units(torch_cuda, poas):
+    """Dynamic scheduling (paper §3.4.2) on real units: the tensor unit's
+    profile is planted 3x too optimistic; the first (static) run misses the
+    prediction by ~2/3, the re-fitted plans converge and C stays exact."""
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = 3000, 1536, 1024
+    profile = poas.profile_machine(UNITS, PROF, True)
+    lines, cur = [], None
+    for line in profile.splitlines():
+        parts = line.split()
+        if len(parts) == 2 and parts[0] == "device":
+            cur = parts[1]
+        if cur == "gpu0.tc" and len(parts) == 2 and parts[0] in ("slope", "intercept"):
+            line = f"{parts[0]} {float(parts[1]) / 3.0!r}"
+        lines.append(line)
+    planted = "\n".join(lines) + "\n"
+    d = operands(torch, poas, m, n, k)
+    ex = poas.Executor(UNITS)
+    out = ex.run_dynamic(planted, m, n, k, d["io_res"], iterations=5, alpha=1.0,
+                         replan_threshold_pct=2.0)
+    torch.cuda.synchronize()
+    its = out["iterations"]
+    assert its[0]["makespan_error_pct"] > 30.0, its[0]
+    assert out["replans"] >= 1
+    assert min(abs(i["makespan_error_pct"]) for i in its[1:]) < 15.0, its
+    assert out["schedule"]["machine_hash"] == ex.machine_hash
+    # C holds the last executed plan (rows in schedule order)
+    sched = {"devices": [{"id": i, "rows": r} for i, r in its[-1]["rows"].items()]}
+    got = result_c(torch, sched, d, True)
+    exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2, "gpu0.simt": 0})
+    assert oracle.rel_frobenius(got, exp) <= TOL

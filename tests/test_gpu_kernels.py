@@ -175,15 +175,18 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= TOL, rel
 
 
+@pytest.mark.parametrize("sched", ["dynamic", "static"])
 @pytest.mark.parametrize("variant", ["1cta", "2cta"])
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
-def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape):
-    """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) agree
-    with the oracle, including partial pair tiles and odd SM budgets."""
+def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched):
+    """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) under
+    both tile schedulers agree with the oracle, including partial pair tiles
+    and odd SM budgets."""
     import oracle
 
     torch = torch_cuda
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
+    monkeypatch.setenv("POAS_TC_SCHED", sched)
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 31), oracle.fill_uniform(k, n, 32)
     ldb = (n + 7) // 8 * 8
@@ -196,3 +199,28 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape):
         poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), ldb, c.data_ptr(), n, num_ctas=ctas)
         torch.cuda.synchronize()
         assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, (variant, ctas)
+
+
+def test_tc_tile_counter_reuse_and_concurrency(torch_cuda, poas):
+    """The dynamic scheduler's self-resetting counters: more launches than
+    the counter ring holds, both kernels interleaved, and two streams
+    launching concurrently -- every result exact."""
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = 640, 768, 256
+    A, B = oracle.fill_uniform(m, k, 41), oracle.fill_uniform(k, n, 42)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    c1 = torch.full((m, n), float("nan"), device="cuda")
+    c2 = torch.full((m, n), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    for i in range(300):  # ring of 256 counters wraps
+        for st, c, ctas in ((s1, c1, 0), (s2, c2, 7 + (i % 5))):
+            poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n,
+                         num_ctas=ctas, stream=st.cuda_stream)
+    torch.cuda.synchronize()
+    for c in (c1, c2):
+        assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL

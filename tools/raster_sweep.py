@@ -33,7 +33,9 @@ def clocks():
             pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(NV))
 
 
-VARIANTS = [("2cta", 8, 1), ("2cta", 8, 0), ("2cta", 16, 1), ("1cta", 16, 1), ("1cta", 16, 0), ("cublas", 0, 0)]
+# (kernel, raster group, tile scheduler)
+VARIANTS = [("2cta", 8, "dynamic"), ("2cta", 8, "static"), ("2cta", 16, "dynamic"),
+            ("1cta", 16, "dynamic"), ("1cta", 16, "static"), ("cublas", 0, "")]
 
 
 def bench(n, rounds=3, iters=8):
@@ -43,15 +45,16 @@ def bench(n, rounds=3, iters=8):
     poas.fill_uniform(poas.DTYPE_BF16, a.data_ptr(), n, n, n, 0, 0, n, 1)
     poas.fill_uniform(poas.DTYPE_BF16, b.data_ptr(), n, n, n, 0, 0, n, 2)
     s = torch.cuda.current_stream().cuda_stream
-    res = {f"{v}:{g}:s{y}": [] for v, g, y in VARIANTS}
+    c16 = torch.empty(n, n, device="cuda")
+    res = {f"{v}:{g}:{y}": [] for v, g, y in VARIANTS}
     for _ in range(rounds):
         for v, g, y in VARIANTS:
             if v == "cublas":
-                f = lambda: torch.matmul(a, b)  # noqa: E731
+                f = lambda: torch.mm(a, b, out_dtype=torch.float32, out=c16)  # noqa: E731
             else:
                 os.environ["POAS_TC_KERNEL"] = v
                 os.environ["POAS_TC_GROUP"] = str(g)
-                os.environ["POAS_TC_SYNC"] = str(y)
+                os.environ["POAS_TC_SCHED"] = y
                 f = lambda: poas.tc_gemm(2, n, n, n, a.data_ptr(), n, b.data_ptr(), n,  # noqa: E731
                                          c.data_ptr(), n, stream=s)
             for _ in range(2):
@@ -65,9 +68,10 @@ def bench(n, rounds=3, iters=8):
             e1.synchronize()
             clk, why = clocks()
             ms = e0.elapsed_time(e1) / iters
-            res[f"{v}:{g}:s{y}"].append((round(2 * n ** 3 / ms / 1e9, 1), clk, why))
+            res[f"{v}:{g}:{y}"].append((round(2 * n ** 3 / ms / 1e9, 1), clk, why))
     os.environ.pop("POAS_TC_GROUP", None)
     os.environ.pop("POAS_TC_KERNEL", None)
+    os.environ.pop("POAS_TC_SCHED", None)
     return {k: {"tflops_median": statistics.median(x[0] for x in v), "runs": v} for k, v in res.items()}
 
 
