@@ -704,11 +704,11 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   });
   if (attr_err != cudaSuccess) return attr_err;
   // Kernel choice. The CTA-pair kernel moves 1/3 fewer operand bytes into
-  // shared memory per MAC and wins while the GPU runs near max clocks, but
-  // it re-reads ~2x more from DRAM (profiles/r01_*); once one launch is long
-  // enough to sit under the power cap (measured: 32768^3) the single-SM
-  // kernel's lower DRAM traffic buys higher clocks and wins. Threshold from
-  // tools/raster_sweep.py under sustained load: 2^44 MACs (~26000^3).
+  // shared memory per MAC and wins at 16384^3 under sustained load (+8% over
+  // the single-SM kernel with the dynamic scheduler, profiles/
+  // r01_tile_scheduler); at 32768^3 it drops to lower clocks under the power
+  // cap and the single-SM kernel wins (+14%). Threshold from
+  // tools/raster_sweep.py: 2^44 MACs (~26000^3).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const bool force_1cta = std::string(tc_gemm_kernel_name(M, N, K)) == "tc_gemm_kernel";
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
