@@ -372,7 +372,10 @@ def main():
     # models from its measured phases and re-plans. The first one runs the
     # static plan, so its error is the static model's prediction error.
     step()  # lands B on every rank (N > 1) before the loop
-    dyn = ex.run_dynamic(profile, m, n, k, io, iterations=args.warmup, policy=args.policy,
+    # at least ~0.3 s of work, so the power-capped clock has settled before
+    # the timed region (the adapted model then predicts it)
+    warm_iters = min(200, max(args.warmup, int(0.3 / max(sched["makespan"], 1e-6)) + 1))
+    dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
                          alpha=args.alpha, replan_threshold_pct=args.replan_threshold)
     schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
     sched = json.loads(schedule)
@@ -588,6 +591,7 @@ def main():
                               "static_plan = the profile-only plan's first run",
                 "static_plan": _static_summary(dyn),
                 "dynamic_replans": dyn["replans"],
+                "dynamic_warmup_iterations": len(dyn["iterations"]),
                 "speedup_vs_best_single_unit": round(speedup, 4) if speedup else None,
                 "best_single_unit": {"id": tc_id, "measured_makespan_ms": round(best_single * 1e3, 4),
                                      "coexec_paired_makespan_ms": round(co_median * 1e3, 4),

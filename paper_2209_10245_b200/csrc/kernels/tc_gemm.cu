@@ -55,7 +55,19 @@ struct TcArgs {
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   unsigned* start_sync;  // optional zeroed counter: all producers start K in step
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
+  int epi_backoff_ns;    // epilogue warps sleep between accumulator polls (0: spin)
 };
+
+// The epilogue warps wait a whole mainloop (~100 us) for each accumulator;
+// sleeping between polls keeps them from issuing millions of try_wait
+// instructions (power under the cap). The accumulator is double buffered, so
+// a late wake-up delays nothing on the tensor pipe.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, int ns) {
+  const uint32_t a = smem_addr(bar);
+  while (!mbar_try_wait(a, parity)) {
+    if (ns) __nanosleep(static_cast<unsigned>(ns));
+  }
+}
 
 // ---------------------------------------------------------- tile scheduler
 // The producer thread (of the CTA, or of the pair's leader) owns the tile
@@ -273,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t < 0) break;
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
-      mbar_wait(&acc_full[acc], acc_phase);
+      mbar_wait_backoff(&acc_full[acc], acc_phase, args.epi_backoff_ns);
       tc_fence_after();
       const int row = mb * kBM + quad * 32 + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
@@ -509,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (t < 0) break;
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
-      mbar_wait(&acc_full[acc], acc_phase);
+      mbar_wait_backoff(&acc_full[acc], acc_phase, args.epi_backoff_ns);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + quad * 32 + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
@@ -746,6 +758,8 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   }
   // Dynamic tile scheduler (default; POAS_TC_SCHED=static: round-robin).
   const char* sched_env = std::getenv("POAS_TC_SCHED");
+  const char* backoff_env = std::getenv("POAS_TC_BACKOFF");
+  args.epi_backoff_ns = backoff_env ? std::atoi(backoff_env) : 0;
   args.tile_counter = nullptr;
   if (!(sched_env && std::string(sched_env) == "static")) {
     args.tile_counter = next_tile_counter();
