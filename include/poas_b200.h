@@ -193,7 +193,8 @@ typedef struct {
 
 /* One executor per process per machine description (same unit specs as
  * the profile that produced the schedule; "bus=0|1" token for the link
- * topology, default shared). */
+ * topology, default shared; "lend=0|1": when a schedule leaves all but one
+ * unit of a GPU idle, the busy unit runs on their SMs too, default 1). */
 int poas_b200_executor_create(const char* units, poas_executor_t* out);
 void poas_b200_executor_destroy(poas_executor_t ex);
 /* machine_identity_hash over the executor's units (device_model.hpp:130). */

@@ -97,6 +97,7 @@ class Executor {
  private:
   std::vector<std::unique_ptr<poas_b200::Unit>> units_;
   bool bus_ = true;
+  bool lend_ = true;  // idle units' SMs go to the one busy unit on their GPU
   std::string hash_;
 };
 

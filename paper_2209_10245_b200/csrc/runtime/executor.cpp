@@ -82,7 +82,7 @@ void copy2d(void* dst, std::int64_t ld_dst, const void* src, std::int64_t ld_src
 }  // namespace
 
 Executor::Executor(const std::string& spec) {
-  const std::vector<poas_b200::UnitSpec> specs = poas_b200::parse_unit_list(spec, &bus_);
+  const std::vector<poas_b200::UnitSpec> specs = poas_b200::parse_unit_list(spec, &bus_, &lend_);
   std::vector<DeviceIdentity> ids;
   for (const auto& s : specs) {
     if (find(s.id)) fail(errc::invalid_argument, "duplicate unit id '" + s.id + "'");
@@ -148,6 +148,31 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         fail(errc::invalid_argument, "resident tensor unit needs a16/b16 or a/b device operands");
       if (!tensor && !(io.a_dev && io.b_dev))
         fail(errc::invalid_argument, "resident CUDA-core unit needs a_dev/b_dev");
+    }
+  }
+
+  // SM lending: when exactly one unit of a GPU has rows in this schedule,
+  // the SM budgets of its idle siblings are added to its launch (the plan
+  // left them nothing to do; a static partition would leave them dark).
+  std::vector<int> extra_sms(nd, 0);
+  if (lend_) {
+    std::map<int, std::vector<std::size_t>> by_dev;
+    for (std::size_t i = 0; i < nd; ++i)
+      if (unit[i]->on_gpu()) by_dev[unit[i]->spec().device].push_back(i);
+    for (const auto& [dev, idx] : by_dev) {
+      std::size_t busy = nd;
+      int busy_count = 0, idle_sms = 0;
+      bool budgets = true;
+      for (std::size_t i : idx) {
+        budgets = budgets && unit[i]->spec().sms > 0;
+        if (schedule.devices[i].rows > 0) {
+          busy = i;
+          ++busy_count;
+        } else {
+          idle_sms += unit[i]->spec().sms;
+        }
+      }
+      if (budgets && busy_count == 1) extra_sms[busy] = idle_sms;
     }
   }
 
@@ -307,14 +332,14 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
             cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(io.b_ready[p]), 0),
                        "wait B panel");
           const void* bp = static_cast<const char*>(b) + static_cast<std::size_t>(p) * d.k * np * esz;
-          u->gemm(r, np, d.k, a, lda, bp, np, c + p * np, ldc, false);
+          u->gemm(r, np, d.k, a, lda, bp, np, c + p * np, ldc, false, extra_sms[i]);
         }
       } else {
         // One readiness event for the whole of B (e.g. a single broadcast).
         if (io.resident && io.b_ready && io.b_ready[0])
           cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(io.b_ready[0]), 0),
                      "wait B");
-        u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false);
+        u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false, extra_sms[i]);
       }
       cuda_check(cudaEventRecord(ev[i].cp1, s), "cudaEventRecord");
     }

@@ -88,12 +88,17 @@ UnitSpec parse_unit_spec(const std::string& text) {
   return u;
 }
 
-std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus) {
+std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus, bool* lend) {
   std::vector<UnitSpec> out;
   if (bus) *bus = true;
+  if (lend) *lend = true;
   for (const std::string& item : split(text, ';')) {
     if (item.rfind("bus=", 0) == 0) {
       if (bus) *bus = item.substr(4) != "0" && item.substr(4) != "false";
+      continue;
+    }
+    if (item.rfind("lend=", 0) == 0) {
+      if (lend) *lend = item.substr(5) != "0" && item.substr(5) != "false";
       continue;
     }
     out.push_back(parse_unit_spec(item));
@@ -157,7 +162,9 @@ Unit::~Unit() {
 }
 
 void Unit::gemm(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, std::int64_t lda,
-                const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate) {
+                const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate,
+                int extra_sms) {
+  const int sms = spec_.sms > 0 ? spec_.sms + extra_sms : 0;
   switch (spec_.kind) {
     case poas::DeviceKind::cpu:
       host_gemm(m, n, k, static_cast<const float*>(a), lda, static_cast<const float*>(b), ldb, c,
@@ -165,13 +172,12 @@ void Unit::gemm(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, s
       return;
     case poas::DeviceKind::gpu:
       cuda_check(simt_gemm(m, n, k, static_cast<const float*>(a), lda,
-                           static_cast<const float*>(b), ldb, c, ldc, accumulate, spec_.sms,
+                           static_cast<const float*>(b), ldb, c, ldc, accumulate, sms,
                            spec_.exclusive, stream_),
                  "simt_gemm");
       return;
     case poas::DeviceKind::xpu:
-      cuda_check(tc_gemm(spec_.dtype, m, n, k, a, lda, b, ldb, c, ldc, accumulate, spec_.sms,
-                         stream_),
+      cuda_check(tc_gemm(spec_.dtype, m, n, k, a, lda, b, ldb, c, ldc, accumulate, sms, stream_),
                  "tc_gemm");
       return;
   }

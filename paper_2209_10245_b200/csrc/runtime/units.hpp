@@ -48,7 +48,11 @@ struct UnitSpec {
 // "<id>=<kind>[:key=value]*"
 UnitSpec parse_unit_spec(const std::string& text);
 // ';'-separated unit specs, optionally with a "bus=0|1" token.
-std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus = nullptr);
+// ';'-separated unit specs plus optional machine tokens: "bus=0|1" (shared
+// link, default 1) and "lend=0|1" (idle units lend their SMs to the one busy
+// unit on the same GPU during execute, default 1).
+std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus = nullptr,
+                                      bool* lend = nullptr);
 
 // Device scratch that grows on demand and is reused across calls.
 class DeviceBuffer {
@@ -94,9 +98,11 @@ class Unit : public poas::DeviceBackend {
 
   // The unit's GEMM on already-placed operands (device pointers for GPU
   // units -- 16-bit for xpu -- host pointers for cpu). Asynchronous on
-  // stream() for GPU units, synchronous for cpu.
+  // stream() for GPU units, synchronous for cpu. `extra_sms` widens a GPU
+  // unit's SM budget for this call (SMs lent by idle units on its GPU).
   void gemm(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, std::int64_t lda,
-            const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate);
+            const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate,
+            int extra_sms = 0);
 
   // Scratch owned by the unit (staging for link copies in execute()).
   DeviceBuffer& scratch(int slot) { return scratch_[slot]; }

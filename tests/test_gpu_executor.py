@@ -274,3 +274,26 @@ def test_dynamic_rescheduling_on_gpu_units(torch_cuda, poas):
     got = result_c(torch, sched, d, True)
     exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2, "gpu0.simt": 0})
     assert oracle.rel_frobenius(got, exp) <= TOL
+
+
+def test_sm_lending_idle_units(torch_cuda, poas):
+    """A schedule leaving the CUDA-core unit idle: the tensor unit borrows
+    its SMs (default) or keeps its own budget ("lend=0"); same identity,
+    same exact C."""
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = 1024, 768, 512
+    profile = poas.profile_machine(UNITS, PROF, True)
+    sched_text = poas.plan_standalone(profile, "gpu0.tc", m, n, k)
+    sched = json.loads(sched_text)
+    assert {d["id"]: d["rows"] for d in sched["devices"]}["gpu0.simt"] == 0
+    d = operands(torch, poas, m, n, k)
+    exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2, "gpu0.simt": 0})
+    for units in (UNITS, UNITS + ";lend=0"):
+        ex = poas.Executor(units)
+        assert ex.machine_hash == sched["machine_hash"]
+        d["C"].fill_(float("nan"))
+        ex.execute(sched_text, d["io_res"], 1)
+        torch.cuda.synchronize()
+        assert oracle.rel_frobenius(result_c(torch, sched, d, True), exp) <= TOL
