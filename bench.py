@@ -332,7 +332,9 @@ def main():
         B16.zero_()
     torch.cuda.synchronize()
 
-    ex = poas.Executor(units_res)
+    # N > 1: NCCL's broadcast kernels run beside the GEMM on the SMs the
+    # idle CUDA-core unit leaves free, so the tensor unit must not borrow them.
+    ex = poas.Executor(units_res + (";lend=0" if world > 1 else ""))
     io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=np_,
                      a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=np_,
                      c_dev=C.data_ptr(), ldc_dev=n, resident=1, b_panels=P)
@@ -565,7 +567,9 @@ def main():
             cpu_baseline = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                             "sample": f"unavailable: {exc}"}
 
-    launches_per_step = sum(1 for d in sched["devices"] if d["rows"] > 0)
+    # per step: one GEMM launch per busy unit and B panel, plus the
+    # executor's start-gate kernel on this GPU
+    launches_per_step = sum(P for d in sched["devices"] if d["rows"] > 0) + 1
     if save and rank == 0:
         (save / "report_resident.json").write_text(json.dumps(rep_last, indent=1))
     if rank == 0:

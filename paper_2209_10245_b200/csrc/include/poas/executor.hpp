@@ -98,6 +98,18 @@ class Executor {
   std::vector<std::unique_ptr<poas_b200::Unit>> units_;
   bool bus_ = true;
   bool lend_ = true;  // idle units' SMs go to the one busy unit on their GPU
+
+ public:
+  // Start-gate flags (mapped pinned ints, one per repeat; grown on demand,
+  // released with the executor). Used by run().
+  struct GateBuffer {
+    int* host = nullptr;
+    std::size_t capacity = 0;
+    std::vector<int*> retired;
+  };
+
+ private:
+  GateBuffer gates_;
   std::string hash_;
 };
 

@@ -94,6 +94,20 @@ __global__ void __launch_bounds__(512) stream_read_kernel(const float4* __restri
   if (acc == 1.2345678e-30f) sink[0] = acc;
 }
 
+// Start gate of one executor repeat: holds the stream until the host sets
+// *flag (mapped pinned memory), so the events recorded after it mark when
+// the whole repeat is queued. Gives up after `timeout_ns` (a host that died
+// mid-enqueue must not leave the GPU spinning).
+__global__ void gate_kernel(const volatile int* flag, unsigned long long timeout_ns) {
+  unsigned long long start, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  while (*flag == 0) {
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start > timeout_ns) break;
+  }
+}
+
 int grid_for(int64_t n) {
   const int64_t blocks = (n + 255) / 256;
   const int64_t cap = static_cast<int64_t>(device_sm_count()) * 16;
@@ -101,6 +115,11 @@ int grid_for(int64_t n) {
 }
 
 }  // namespace
+
+cudaError_t gate_wait(const int* flag, cudaStream_t stream) {
+  gate_kernel<<<1, 1, 0, stream>>>(flag, 10ull * 1000000000ull);
+  return cudaGetLastError();
+}
 
 cudaError_t stream_read(const void* src, size_t bytes, int num_ctas, float* sink,
                         cudaStream_t stream) {

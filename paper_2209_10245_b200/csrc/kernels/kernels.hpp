@@ -39,6 +39,10 @@ cudaError_t fill_uniform(AbType t, void* dst, int64_t ld, int64_t rows, int64_t 
 cudaError_t convert_f32(AbType t, const float* src, int64_t ld_src, void* dst, int64_t ld_dst,
                         int64_t rows, int64_t cols, cudaStream_t stream);
 
+// One-thread kernel that holds `stream` until the host writes a non-zero
+// value to *flag (mapped pinned memory); times out after 10 s.
+cudaError_t gate_wait(const int* flag, cudaStream_t stream);
+
 // Streaming read of `bytes` (multiple of 16) by `num_ctas` CTAs of 512
 // threads (0 = one per SM): the HBM bandwidth a unit on that SM budget sees.
 cudaError_t stream_read(const void* src, size_t bytes, int num_ctas, float* sink,

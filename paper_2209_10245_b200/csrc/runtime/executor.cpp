@@ -3,8 +3,15 @@
 // simulate(), proj/src/simulator.cpp:104-209, with the same result shape).
 //
 // Per repeat:
-//   t0          one event per GPU (on every unit stream's critical path) and
-//               a host steady_clock stamp: the common clock origin
+//   gate        the repeat is enqueued behind a one-thread kernel that waits
+//               for a host flag; the flag is set once everything is queued,
+//               so enqueue latency is not measured as GPU phase time
+//   t0          one event per GPU after the gate (on every unit stream's
+//               critical path) and a host steady_clock stamp when the gate
+//               opens: the common clock origin
+//   chaining    GPU-only repeats follow each other on the device (t0 of
+//               repeat r waits for repeat r-1's last events), no host sync;
+//               with host-CPU units every repeat is host-synchronous
 //   cpu unit    a host thread runs host_gemm on its rows from t0
 //   copy-in     GPU units in schedule (priority) order; on a shared bus each
 //               copy-in waits for the previous unit's copy-in (link order)
@@ -79,6 +86,43 @@ void copy2d(void* dst, std::int64_t ld_dst, const void* src, std::int64_t ld_src
                "cudaMemcpy2DAsync");
 }
 
+// The start gates of one run() (see gate_wait): flag r opens repeat r.
+// Every flag is opened on destruction, so an exception between a gate's
+// launch and its opening cannot leave a kernel waiting.
+class StartGates {
+ public:
+  StartGates(int repeats, Executor::GateBuffer* buf) : buf_(buf), n_(repeats) {
+    if (repeats <= 0) return;
+    const std::size_t need = static_cast<std::size_t>(repeats);
+    if (buf->capacity < need) {
+      void* p = nullptr;
+      cuda_check(cudaHostAlloc(&p, need * sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable),
+                 "cudaHostAlloc");
+      if (buf->host) buf->retired.push_back(buf->host);  // freed with the executor
+      buf->host = static_cast<int*>(p);
+      buf->capacity = need;
+    }
+    for (int r = 0; r < repeats; ++r) __atomic_store_n(buf->host + r, 0, __ATOMIC_SEQ_CST);
+    void* dp = nullptr;
+    cuda_check(cudaHostGetDevicePointer(&dp, buf->host, 0), "cudaHostGetDevicePointer");
+    dev_ = static_cast<const int*>(dp);
+  }
+  ~StartGates() {
+    for (int r = 0; r < n_; ++r) open(r);
+  }
+  StartGates(const StartGates&) = delete;
+  StartGates& operator=(const StartGates&) = delete;
+  const int* device_flag(int r) const { return dev_ + r; }
+  void open(int r) {
+    if (r < n_) __atomic_store_n(buf_->host + r, 1, __ATOMIC_SEQ_CST);
+  }
+
+ private:
+  Executor::GateBuffer* buf_;
+  int n_;
+  const int* dev_ = nullptr;
+};
+
 }  // namespace
 
 Executor::Executor(const std::string& spec) {
@@ -92,7 +136,10 @@ Executor::Executor(const std::string& spec) {
   hash_ = machine_identity_hash(ids, bus_);
 }
 
-Executor::~Executor() = default;
+Executor::~Executor() {
+  if (gates_.host) cudaFreeHost(gates_.host);
+  for (int* p : gates_.retired) cudaFreeHost(p);
+}
 
 Unit* Executor::find(const std::string& id) const {
   for (const auto& u : units_)
@@ -154,8 +201,10 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
   // SM lending: when exactly one unit of a GPU has rows in this schedule,
   // the SM budgets of its idle siblings are added to its launch (the plan
   // left them nothing to do; a static partition would leave them dark).
+  // Not while B arrives through readiness events: the idle SMs are where
+  // the collective's kernels run concurrently with the GEMM.
   std::vector<int> extra_sms(nd, 0);
-  if (lend_) {
+  if (lend_ && !io.b_ready) {
     std::map<int, std::vector<std::size_t>> by_dev;
     for (std::size_t i = 0; i < nd; ++i)
       if (unit[i]->on_gpu()) by_dev[unit[i]->spec().device].push_back(i);
@@ -176,84 +225,107 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     }
   }
 
-  // Per-device t0 events and per-unit phase events.
-  std::map<int, cudaEvent_t> t0;
-  std::vector<PhaseEvents> ev(nd);
-  for (std::size_t i = 0; i < nd; ++i) {
-    if (!unit[i]->on_gpu()) continue;
-    const int dev = unit[i]->spec().device;
-    DeviceGuard g(dev);
-    if (!t0.count(dev)) {
-      cudaEvent_t e;
-      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-      t0[dev] = e;
-    }
-    ev[i].create();
-  }
+  // Per GPU with work: its first busy unit (schedule order) hosts the start
+  // gate and t0 on its own stream; other busy units of that GPU wait on t0.
+  std::map<int, std::size_t> host_unit;
+  for (std::size_t i = 0; i < nd; ++i)
+    if (unit[i]->on_gpu() && schedule.devices[i].rows > 0 && !host_unit.count(unit[i]->spec().device))
+      host_unit[unit[i]->spec().device] = i;
+
+  // Events: per repeat, one t0 per GPU and one phase set per busy GPU unit;
+  // one entry event per GPU (orders the run after work already queued on the
+  // legacy default stream, e.g. the caller's input preparation).
+  std::map<int, std::vector<cudaEvent_t>> t0;  // device -> [repeat]
+  std::map<int, cudaEvent_t> entry;
+  std::vector<std::vector<PhaseEvents>> ev(static_cast<std::size_t>(repeats),
+                                           std::vector<PhaseEvents>(nd));
   struct Cleanup {
-    std::map<int, cudaEvent_t>& t0;
-    std::vector<PhaseEvents>& ev;
+    std::map<int, std::vector<cudaEvent_t>>& t0;
+    std::map<int, cudaEvent_t>& entry;
+    std::vector<std::vector<PhaseEvents>>& ev;
     std::vector<Unit*>& unit;
     ~Cleanup() {
-      for (std::size_t i = 0; i < ev.size(); ++i) {
-        if (!unit[i]->on_gpu()) continue;
-        DeviceGuard g(unit[i]->spec().device);
-        ev[i].destroy();
-      }
-      for (auto& [dev, e] : t0) {
+      for (auto& per_rep : ev)
+        for (std::size_t i = 0; i < per_rep.size(); ++i) {
+          if (!unit[i]->on_gpu()) continue;
+          DeviceGuard g(unit[i]->spec().device);
+          per_rep[i].destroy();
+        }
+      for (auto& [dev, v] : t0) {
         DeviceGuard g(dev);
-        cudaEventDestroy(e);
+        for (cudaEvent_t e : v)
+          if (e) cudaEventDestroy(e);
+        if (entry.count(dev) && entry[dev]) cudaEventDestroy(entry[dev]);
       }
     }
-  } cleanup{t0, ev, unit};
+  } cleanup{t0, entry, ev, unit};
+  for (const auto& [dev, h] : host_unit) {
+    DeviceGuard g(dev);
+    std::vector<cudaEvent_t>& v = t0[dev];
+    v.assign(static_cast<std::size_t>(repeats), nullptr);
+    for (cudaEvent_t& e : v) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    entry[dev] = nullptr;
+    cuda_check(cudaEventCreateWithFlags(&entry[dev], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  for (std::size_t i = 0; i < nd; ++i) {
+    if (!unit[i]->on_gpu() || schedule.devices[i].rows == 0) continue;
+    DeviceGuard g(unit[i]->spec().device);
+    for (auto& per_rep : ev) per_rep[i].create();
+  }
+  // Resident runs have no copy phases: only compute is bracketed by events.
+  const auto last_event = [&](std::size_t rep, std::size_t i) {
+    return io.resident ? ev[rep][i].cp1 : ev[rep][i].co1;
+  };
 
-  SimulationResult res;
-  res.repeats = repeats;
-  std::vector<double> sum_in(nd, 0.0), sum_cp(nd, 0.0), sum_out(nd, 0.0), sum_fin(nd, 0.0);
-  double sum_makespan = 0.0, sum_wall = 0.0;
+  // Start gates: each repeat's GPU work is enqueued behind a tiny kernel
+  // that waits for a host flag (gate_wait); t0 is recorded after it, so the
+  // host's enqueue latency is not charged to the measured phases.
+  StartGates gates(host_unit.empty() ? 0 : repeats, &gates_);
 
-  for (int rep = 0; rep < repeats; ++rep) {
-    // Quiesce so t0 is a true common origin.
+  // Repeats with host threads (CPU units) are host-synchronous: the threads
+  // start when the gate opens. GPU-only repeats are chained on the device
+  // (the next gate waits for the previous repeat's last events) so the GPU
+  // never idles between them.
+  const bool host_sync_repeats = any_cpu;
+  std::vector<std::vector<double>> cpu_start(static_cast<std::size_t>(repeats),
+                                             std::vector<double>(nd, 0.0));
+  std::vector<std::vector<double>> cpu_end = cpu_start;
+  double sum_wall = 0.0;
+  auto quiesce = [&] {
     for (std::size_t i = 0; i < nd; ++i)
       if (unit[i]->on_gpu()) {
         DeviceGuard g(unit[i]->spec().device);
         cuda_check(cudaStreamSynchronize(unit[i]->stream()), "cudaStreamSynchronize");
       }
-    for (auto& [dev, e] : t0) {
+  };
+  std::chrono::steady_clock::time_point first_open;
+
+  for (const auto& [dev, h] : host_unit) {
+    DeviceGuard g(dev);
+    cuda_check(cudaEventRecord(entry[dev], nullptr), "cudaEventRecord");
+    for (std::size_t i = 0; i < nd; ++i)
+      if (unit[i]->on_gpu() && schedule.devices[i].rows > 0 && unit[i]->spec().device == dev)
+        cuda_check(cudaStreamWaitEvent(unit[i]->stream(), entry[dev], 0), "cudaStreamWaitEvent");
+  }
+
+  for (int rep = 0; rep < repeats; ++rep) {
+    const std::size_t rr = static_cast<std::size_t>(rep);
+    std::vector<PhaseEvents>& evr = ev[rr];
+    if (host_sync_repeats) quiesce();
+    for (const auto& [dev, h] : host_unit) {
       DeviceGuard g(dev);
-      cuda_check(cudaEventRecord(e, nullptr), "cudaEventRecord");
-    }
-    const auto host_t0 = std::chrono::steady_clock::now();
-
-    // CPU unit(s): host threads, started first so they begin at ~t0.
-    std::vector<std::thread> host_jobs;
-    std::vector<double> cpu_start(nd, 0.0), cpu_end(nd, 0.0);
-    std::vector<std::exception_ptr> cpu_err(nd);
-    for (std::size_t i = 0; i < nd; ++i) {
-      const ScheduledDevice& sd = schedule.devices[i];
-      if (unit[i]->on_gpu() || sd.rows == 0) continue;
-      host_jobs.emplace_back([&, i] {
-        try {
-          const ScheduledDevice& s = schedule.devices[i];
-          const auto a = std::chrono::steady_clock::now();
-          unit[i]->gemm(s.rows, d.n, d.k, io.a_host + row0[i] * io.lda_host, io.lda_host,
-                        io.b_host, io.ldb_host, io.c_host + row0[i] * io.ldc_host, io.ldc_host,
-                        false);
-          const auto b = std::chrono::steady_clock::now();
-          cpu_start[i] = std::chrono::duration<double>(a - host_t0).count();
-          cpu_end[i] = std::chrono::duration<double>(b - host_t0).count();
-        } catch (...) {
-          cpu_err[i] = std::current_exception();
-        }
-      });
-    }
-
-    // GPU units: make every unit stream start after its device's t0.
-    for (std::size_t i = 0; i < nd; ++i) {
-      if (!unit[i]->on_gpu()) continue;
-      DeviceGuard g(unit[i]->spec().device);
-      cuda_check(cudaStreamWaitEvent(unit[i]->stream(), t0[unit[i]->spec().device], 0),
-                 "cudaStreamWaitEvent");
+      cudaStream_t hs = unit[h]->stream();
+      if (rep > 0 && !host_sync_repeats)  // chain after the other units' previous repeat
+        for (std::size_t j = 0; j < nd; ++j)
+          if (j != h && unit[j]->on_gpu() && schedule.devices[j].rows > 0 &&
+              unit[j]->spec().device == dev)
+            cuda_check(cudaStreamWaitEvent(hs, last_event(rr - 1, j), 0), "cudaStreamWaitEvent");
+      cuda_check(poas_b200::gate_wait(gates.device_flag(rep), hs), "gate_wait");
+      cuda_check(cudaEventRecord(t0[dev][rr], hs), "cudaEventRecord");
+      for (std::size_t i = 0; i < nd; ++i)
+        if (i != h && unit[i]->on_gpu() && schedule.devices[i].rows > 0 &&
+            unit[i]->spec().device == dev)
+          cuda_check(cudaStreamWaitEvent(unit[i]->stream(), t0[dev][rr], 0), "cudaStreamWaitEvent");
     }
 
     // Copy-in + compute, in schedule order.
@@ -274,8 +346,8 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       std::int64_t ldc = 0;
 
       if (!io.resident) {
-        if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(s, ev[prev_in].ci1, 0), "wait");
-        cuda_check(cudaEventRecord(ev[i].ci0, s), "cudaEventRecord");
+        if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(s, evr[prev_in].ci1, 0), "wait");
+        cuda_check(cudaEventRecord(evr[i].ci0, s), "cudaEventRecord");
         float* da = static_cast<float*>(u->scratch(0).ensure(static_cast<std::size_t>(r * d.k) * 4));
         float* db = static_cast<float*>(u->scratch(1).ensure(static_cast<std::size_t>(d.k * d.n) * 4));
         copy2d(da, d.k, io.a_host + r0 * io.lda_host, io.lda_host, r, d.k, 4,
@@ -289,7 +361,6 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         ldc = d.n;
         prev_in = i;
       } else {
-        cuda_check(cudaEventRecord(ev[i].ci0, s), "cudaEventRecord");
         c = io.c_dev + r0 * io.ldc_dev;
         ldc = io.ldc_dev;
         if (tensor && io.a16_dev && io.b16_dev) {
@@ -304,9 +375,9 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
           ldb = io.ldb_dev;
         }
       }
-      cuda_check(cudaEventRecord(ev[i].ci1, s), "cudaEventRecord");
+      if (!io.resident) cuda_check(cudaEventRecord(evr[i].ci1, s), "cudaEventRecord");
 
-      cuda_check(cudaEventRecord(ev[i].cp0, s), "cudaEventRecord");
+      cuda_check(cudaEventRecord(evr[i].cp0, s), "cudaEventRecord");
       const bool need_convert = tensor && !(io.resident && io.a16_dev && io.b16_dev);
       if (need_convert) {
         const AbType t = u->spec().dtype;
@@ -341,7 +412,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
                      "wait B");
         u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false, extra_sms[i]);
       }
-      cuda_check(cudaEventRecord(ev[i].cp1, s), "cudaEventRecord");
+      cuda_check(cudaEventRecord(evr[i].cp1, s), "cudaEventRecord");
     }
 
     // Copy-outs, in schedule order.
@@ -357,34 +428,62 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         if (bus_) {
           if (prev_out == nd) {
             if (last_in != nd && last_in != i)
-              cuda_check(cudaStreamWaitEvent(s, ev[last_in].ci1, 0), "wait");
+              cuda_check(cudaStreamWaitEvent(s, evr[last_in].ci1, 0), "wait");
           } else {
-            cuda_check(cudaStreamWaitEvent(s, ev[prev_out].co1, 0), "wait");
+            cuda_check(cudaStreamWaitEvent(s, evr[prev_out].co1, 0), "wait");
           }
         }
-        cuda_check(cudaEventRecord(ev[i].co0, s), "cudaEventRecord");
+        cuda_check(cudaEventRecord(evr[i].co0, s), "cudaEventRecord");
         copy2d(io.c_host + row0[i] * io.ldc_host, io.ldc_host, u->scratch(4).get(), d.n, sd.rows,
                d.n, 4, cudaMemcpyDeviceToHost, s);
         prev_out = i;
-      } else {
-        cuda_check(cudaEventRecord(ev[i].co0, s), "cudaEventRecord");
+        cuda_check(cudaEventRecord(evr[i].co1, s), "cudaEventRecord");
       }
-      cuda_check(cudaEventRecord(ev[i].co1, s), "cudaEventRecord");
     }
 
-    // Join.
-    for (std::thread& t : host_jobs) t.join();
-    for (std::size_t i = 0; i < nd; ++i)
-      if (unit[i]->on_gpu()) {
-        DeviceGuard g(unit[i]->spec().device);
-        cuda_check(cudaStreamSynchronize(unit[i]->stream()), "unit stream");
-      }
-    const double wall =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
-    for (auto& e : cpu_err)
-      if (e) std::rethrow_exception(e);
+    // Open the gate: the whole repeat is queued. Host threads start now.
+    gates.open(rep);
+    const auto host_t0 = std::chrono::steady_clock::now();
+    if (rep == 0) first_open = host_t0;
+    std::vector<std::thread> host_jobs;
+    std::vector<std::exception_ptr> cpu_err(nd);
+    for (std::size_t i = 0; i < nd; ++i) {
+      if (unit[i]->on_gpu() || schedule.devices[i].rows == 0) continue;
+      host_jobs.emplace_back([&, i, rep] {
+        try {
+          const ScheduledDevice& s = schedule.devices[i];
+          const auto a = std::chrono::steady_clock::now();
+          unit[i]->gemm(s.rows, d.n, d.k, io.a_host + row0[i] * io.lda_host, io.lda_host,
+                        io.b_host, io.ldb_host, io.c_host + row0[i] * io.ldc_host, io.ldc_host,
+                        false);
+          const auto b = std::chrono::steady_clock::now();
+          cpu_start[static_cast<std::size_t>(rep)][i] = std::chrono::duration<double>(a - host_t0).count();
+          cpu_end[static_cast<std::size_t>(rep)][i] = std::chrono::duration<double>(b - host_t0).count();
+        } catch (...) {
+          cpu_err[i] = std::current_exception();
+        }
+      });
+    }
+    if (host_sync_repeats) {
+      for (std::thread& t : host_jobs) t.join();
+      quiesce();
+      sum_wall += std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
+      for (auto& e : cpu_err)
+        if (e) std::rethrow_exception(e);
+    }
+  }
+  if (!host_sync_repeats) {
+    quiesce();
+    sum_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - first_open).count();
+  }
 
-    // Measured timeline of this repeat.
+  // Measured timelines, relative to each repeat's t0.
+  SimulationResult res;
+  res.repeats = repeats;
+  std::vector<double> sum_in(nd, 0.0), sum_cp(nd, 0.0), sum_out(nd, 0.0), sum_fin(nd, 0.0);
+  double sum_makespan = 0.0;
+  for (int rep = 0; rep < repeats; ++rep) {
+    const std::size_t r = static_cast<std::size_t>(rep);
     std::vector<DeviceTimeline> tl(nd);
     double makespan = 0.0;
     for (std::size_t i = 0; i < nd; ++i) {
@@ -396,20 +495,26 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       }
       if (!unit[i]->on_gpu()) {
         t.copy_in = {0.0, 0.0};
-        t.compute = {cpu_start[i], cpu_end[i]};
-        t.copy_out = {cpu_end[i], cpu_end[i]};
-        t.finish = cpu_end[i];
+        t.compute = {cpu_start[r][i], cpu_end[r][i]};
+        t.copy_out = {cpu_end[r][i], cpu_end[r][i]};
+        t.finish = cpu_end[r][i];
       } else {
         DeviceGuard g(unit[i]->spec().device);
-        cudaEvent_t z = t0[unit[i]->spec().device];
+        cudaEvent_t z = t0[unit[i]->spec().device][r];
         const auto at = [&](cudaEvent_t e) {
           float ms = 0.f;
           cuda_check(cudaEventElapsedTime(&ms, z, e), "cudaEventElapsedTime");
           return static_cast<double>(ms) * 1e-3;
         };
-        t.copy_in = {at(ev[i].ci0), at(ev[i].ci1)};
-        t.compute = {at(ev[i].cp0), at(ev[i].cp1)};
-        t.copy_out = {at(ev[i].co0), at(ev[i].co1)};
+        const PhaseEvents& e = ev[r][i];
+        t.compute = {at(e.cp0), at(e.cp1)};
+        if (io.resident) {
+          t.copy_in = {t.compute.start, t.compute.start};
+          t.copy_out = {t.compute.end, t.compute.end};
+        } else {
+          t.copy_in = {at(e.ci0), at(e.ci1)};
+          t.copy_out = {at(e.co0), at(e.co1)};
+        }
         t.finish = t.copy_out.end;
       }
       makespan = std::max(makespan, t.finish);
@@ -421,7 +526,6 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       sum_fin[i] += tl[i].finish;
     }
     sum_makespan += makespan;
-    sum_wall += wall;
     res.repeat_timelines.push_back(std::move(tl));
   }
 

@@ -135,6 +135,7 @@ class Unit:
 
     def __init__(self, spec: str):
         self._h = C.c_void_p()
+        self._destroy = lib.poas_b200_unit_destroy  # still bound at interpreter exit
         check(lib.poas_b200_unit_create(_b(spec), C.byref(self._h)))
 
     def time_gemm(self, side: int) -> float:
@@ -151,9 +152,9 @@ class Unit:
         return bool(lib.poas_b200_has_transfers(self._h))
 
     def close(self):
-        if self._h:
-            lib.poas_b200_unit_destroy(self._h)
-            self._h = C.c_void_p()
+        if getattr(self, "_h", None):
+            self._destroy(self._h)
+            self._h = None
 
     __del__ = close
 
@@ -187,6 +188,7 @@ class Executor:
 
     def __init__(self, units: str):
         self._h = C.c_void_p()
+        self._destroy = lib.poas_b200_executor_destroy  # still bound at interpreter exit
         check(lib.poas_b200_executor_create(_b(units), C.byref(self._h)))
 
     @property
@@ -215,9 +217,9 @@ class Executor:
         return json.loads(take_string(out))
 
     def close(self):
-        if self._h:
-            lib.poas_b200_executor_destroy(self._h)
-            self._h = C.c_void_p()
+        if getattr(self, "_h", None):
+            self._destroy(self._h)
+            self._h = None
 
     __del__ = close
 
