@@ -5,7 +5,7 @@
 //   poas plan     --profile FILE --dims MxNxK --out FILE [--policy reference|best-subset]
 //   poas run      --schedule FILE --units SPEC [--repeats N] [--seed S] [--host]
 //   poas evaluate --units SPEC [--inputs FILE] [--repeats N] [--seed S]
-//                 [--policy P] [--profiling k=v,..] --out-dir DIR
+//                 [--policy P] [--profiling k=v,..] [--adapt N] --out-dir DIR
 //   poas adapt    --profile FILE --units SPEC --dims MxNxK [--iterations N]
 //                 [--alpha A] [--threshold PCT] [--policy P] [--seed S] [--host]
 //                 [--out-profile FILE] [--out FILE]
@@ -416,6 +416,10 @@ int cmd_evaluate(const Args& a) {
   const std::uint64_t seed = std::strtoull(a.get("seed", "20261017").c_str(), nullptr, 10);
   const double max_alone = std::atof(a.get("max-standalone", "2.0").c_str());
   const std::string policy = a.get("policy", "reference");
+  // --adapt N: dynamic scheduling (paper §3.4.2) -- N warm-up executions per
+  // input re-fit the models (carried over to the next input) before the
+  // measured run; 0 (default) is the reference's static evaluation.
+  const int adapt = std::atoi(a.get("adapt", "0").c_str());
   std::vector<EvalInput> inputs;
   if (a.has("inputs")) {
     inputs = load_inputs(a.get("inputs"));
@@ -430,10 +434,14 @@ int cmd_evaluate(const Args& a) {
   const poas::MachineProfile prof = poas_b200::profile_units(probe_units, profiling_from(a.get("profiling")), bus);
   probe_units.clear();
   poas::Executor ex(units);
+  poas::MachineProfile live = prof;  // re-fitted across inputs with --adapt
+  std::vector<const Unit*> all_units;
+  for (const auto& u : ex.units()) all_units.push_back(u.get());
 
   std::string j = "{\n  \"machine_hash\": \"" + ex.machine_hash() + "\",\n  \"seed\": " +
                   std::to_string(seed) + ",\n  \"repeats\": " + std::to_string(repeats) +
-                  ",\n  \"policy\": \"" + policy + "\",\n  \"devices\": [";
+                  ",\n  \"policy\": \"" + policy + "\",\n  \"adapt\": " + std::to_string(adapt) +
+                  ",\n  \"devices\": [";
   for (std::size_t i = 0; i < prof.devices.size(); ++i)
     j += (i ? ", " : "") + std::string("\"") + prof.devices[i].id + "\"";
   j += "],\n  \"inputs\": [\n";
@@ -446,14 +454,30 @@ int cmd_evaluate(const Args& a) {
   std::map<std::string, std::vector<double>> e_fin, e_cp;
   for (std::size_t ii = 0; ii < inputs.size(); ++ii) {
     const EvalInput& in = inputs[ii];
-    const poas::Schedule s = poas::plan_with_policy(prof, in.dims, policy);
-    auto ops = operands_for(ex, s, seed + ii, false);
-    ex.run(s, ops->io, 1);
+    poas::Schedule s = poas::plan_with_policy(live, in.dims, policy);
+    auto ops = adapt > 0 ? operands_for_units(all_units, in.dims, seed + ii, false)
+                         : operands_for(ex, s, seed + ii, false);
+    double static_err = 0.0;
+    if (adapt > 0) {
+      poas::DynamicOptions o;
+      o.policy = policy;
+      o.refit.alpha = std::atof(a.get("alpha", "0.5").c_str());
+      poas::DynamicScheduler dyn(live, in.dims, o);
+      for (int it = 0; it < adapt; ++it) {
+        const poas::SimulationResult w = ex.run(dyn.schedule(), ops->io, 1);
+        if (it == 0) static_err = w.makespan_error_pct;
+        dyn.observe(w);
+      }
+      live = dyn.profile();
+      s = dyn.schedule();
+    } else {
+      ex.run(s, ops->io, 1);
+    }
     const poas::SimulationResult r = ex.run(s, ops->io, repeats);
     double best_alone = 0.0;
     std::string alone_json;
     for (const poas::DeviceProfile& d : prof.devices) {
-      const poas::Schedule sa = poas::standalone_schedule(prof, d.id, in.dims);
+      const poas::Schedule sa = poas::standalone_schedule(live, d.id, in.dims);
       double meas = -1.0;
       if (sa.makespan <= max_alone) {
         auto oa = operands_for(ex, sa, seed + ii, false);
@@ -478,7 +502,9 @@ int cmd_evaluate(const Args& a) {
          std::to_string(in.dims.m) + ", \"n\": " + std::to_string(in.dims.n) + ", \"k\": " +
          std::to_string(in.dims.k) + "}, \"tops\": " + g(tops) + ", \"predicted_makespan\": " +
          g(r.predicted_makespan) + ", \"measured_makespan\": " + g(r.measured_makespan) +
-         ", \"makespan_error_pct\": " + g(r.makespan_error_pct) + ", \"speedup_vs_best_single\": " +
+         ", \"makespan_error_pct\": " + g(r.makespan_error_pct) +
+         (adapt > 0 ? ", \"static_plan_error_pct\": " + g(static_err) : std::string()) +
+         ", \"speedup_vs_best_single\": " +
          g(speedup) + ", \"standalone\": [" + alone_json + "], \"devices\": [";
     for (std::size_t k = 0; k < r.devices.size(); ++k) {
       const poas::DeviceOutcome& d = r.devices[k];

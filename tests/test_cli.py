@@ -102,3 +102,21 @@ def test_adapt_cpu_units(cli, tmp_path):
     r = run("adapt", "--profile", str(planted), "--units", units, "--dims", "64x64x64",
             "--iterations", "0")
     assert r.returncode == 1
+
+
+def test_evaluate_adapt_cpu_units(cli, tmp_path):
+    """`poas evaluate --adapt N` on host units: report.json in the reference
+    evaluate shape plus the static plan's first-run error per input."""
+    inputs = tmp_path / "in.json"
+    inputs.write_text(json.dumps([{"name": "a", "m": 512, "n": 256, "k": 256},
+                                  {"name": "b", "m": 300, "n": 200, "k": 128}]))
+    out = tmp_path / "ev"
+    r = run("evaluate", "--units", "cpuA=cpu:threads=1;cpuB=cpu:threads=1", "--inputs", str(inputs),
+            "--profiling", "probes=3,repetitions=2,cpu_min_side=128,cpu_max_side=256",
+            "--repeats", "2", "--adapt", "3", "--out-dir", str(out))
+    assert r.returncode == 0, r.stderr
+    rep = json.loads((out / "report.json").read_text())
+    assert rep["adapt"] == 3 and len(rep["inputs"]) == 2
+    for e in rep["inputs"]:
+        assert "static_plan_error_pct" in e
+        assert sum(d["rows"] for d in e["devices"]) == e["dims"]["m"]
