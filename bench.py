@@ -262,6 +262,10 @@ def main():
                     help="dynamic scheduling: weight of the newest measurement in the model re-fit")
     ap.add_argument("--replan-threshold", type=float, default=2.0,
                     help="dynamic scheduling: re-plan when |makespan error| exceeds this (%%)")
+    ap.add_argument("--profile", default=None,
+                    help="reuse a poas-profile v1 file for the resident units instead of probing "
+                         "('{rank}' is replaced by the rank); probes timed under a profiler are "
+                         "meaningless")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=None)
     ap.add_argument("--save", default=None, help="directory for profile/schedule/report artefacts")
@@ -297,7 +301,10 @@ def main():
 
     # ---- predict -> optimize -> adapt -> schedule (resident operands)
     t0 = time.perf_counter()
-    profile = poas.profile_machine(units_res, PROFILING, bus=True)
+    if args.profile:  # a profile measured earlier on this box (e.g. for an ncu pass)
+        profile = Path(args.profile.replace("{rank}", str(rank))).read_text()
+    else:
+        profile = poas.profile_machine(units_res, PROFILING, bus=True)
     t_prof = time.perf_counter() - t0
     schedule = poas.plan_policy(profile, m, n, k, args.policy)
     ref_policy_makespan = json.loads(poas.plan(profile, m, n, k))["makespan"]
@@ -609,7 +616,8 @@ def main():
             },
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst,
                          "unit": "TFLOP/s", "frac": round(achieved / peak_burst, 4),
-                         "traffic": traffic, "kernel": poas.tc_kernel_name(tc_rows, n, k),
+                         "traffic": traffic, "kernel": f"{poas.tc_kernel_name(tc_rows, n, k)} "
+                                   f"({poas.tc_scheduler_name(tc_rows, n, k)} tile scheduler)",
                          "peak_kind": f"{peak_kind} bf16 burst (sustained {peak_sust})"},
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,

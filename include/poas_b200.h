@@ -238,6 +238,8 @@ int poas_b200_tc_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
 /* Name of the kernel poas_b200_tc_gemm launches for this shape
  * ("tc_gemm_2cta_kernel" or "tc_gemm_kernel"; static string). */
 const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k);
+/* Its tile scheduler for this shape: "dynamic" or "wave" (static string). */
+const char* poas_b200_tc_scheduler_name(int64_t m, int64_t n, int64_t k);
 int poas_b200_simt_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
                         const float* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
                         int num_ctas, int exclusive_sm, void* stream);

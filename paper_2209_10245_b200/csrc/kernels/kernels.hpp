@@ -17,10 +17,12 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
                     const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                     int num_ctas, cudaStream_t stream);
 
-// The kernel tc_gemm launches for an M x N x K problem: "tc_gemm_2cta_kernel"
-// (CTA pairs, cta_group::2) below 2^44 MACs, "tc_gemm_kernel" (single SM)
-// from there on; POAS_TC_KERNEL=1cta|2cta overrides.
+// The kernel tc_gemm launches: "tc_gemm_2cta_kernel" (CTA pairs,
+// cta_group::2); POAS_TC_KERNEL=1cta selects "tc_gemm_kernel" (single SM).
 const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t K);
+// Its tile scheduler: "dynamic" (atomic claiming) below 2^44 MACs, "wave"
+// (static order, per-wave barrier) from there on; POAS_TC_SCHED overrides.
+const char* tc_gemm_scheduler_name(int64_t M, int64_t N, int64_t K);
 
 // CUDA-core unit: fp32 SIMT GEMM, same conventions.
 cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,

@@ -55,6 +55,7 @@ struct TcArgs {
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   unsigned* start_sync;  // optional zeroed counter: all producers start K in step
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
+  int wave_sync;         // 1: static order + per-wave barrier on tile_counter[0]
   int epi_backoff_ns;    // epilogue warps sleep between accumulator polls (0: spin)
 };
 
@@ -83,7 +84,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 constexpr int kTileSlots = 4;
 
 __device__ __forceinline__ int claim_tile(const TcArgs& a, int& next_static, int step) {
-  if (a.tile_counter) return atomicAdd(a.tile_counter, 1);
+  if (a.tile_counter && !a.wave_sync) return atomicAdd(a.tile_counter, 1);
   const int t = next_static;
   next_static += step;
   return t;
@@ -95,6 +96,28 @@ __device__ __forceinline__ void release_counter(const TcArgs& a, int workers) {
   if (atomicAdd(a.tile_counter + 1, 1) == workers - 1) {
     atomicExch(a.tile_counter, 0);
     atomicExch(a.tile_counter + 1, 0);
+  }
+}
+
+// Wave mode (large problems, see tc_gemm): static round-robin order, and
+// before its i-th tile (i >= 1) a worker waits until every worker that has an
+// i-th tile has reached it, so the tiles of a wave sweep K in step and share
+// A/B panels through L2. `target` accumulates the arrivals expected by wave
+// i. The wait gives up after 200 us (a worker that is not resident -- SMs
+// held by another kernel -- must not stall the grid); the caller then stops
+// synchronising, and the others time out once and follow: plain static order.
+__device__ __forceinline__ bool wave_barrier(const TcArgs& a, int i, int workers, int total,
+                                             int& target) {
+  target += min(workers, total - i * workers);
+  atomicAdd(a.tile_counter, 1);
+  unsigned long long start, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  while (true) {
+    int seen;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(a.tile_counter) : "memory");
+    if (seen >= target) return true;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start > 200000ull) return false;  // 200 us: a worker is not resident
   }
 }
 
@@ -188,6 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int next_static = blockIdx.x;
       int slot = 0;
       uint32_t tphase = 0;
+      int wave = 0, wave_target = 0;
+      bool wave_on = args.wave_sync != 0;
       int t = claim_tile(args, next_static, gridDim.x);
       while (true) {
         const int tt = t < total ? t : -1;
@@ -199,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tphase ^= 1;
         }
         if (tt < 0) break;
+        if (wave_on && wave > 0) wave_on = wave_barrier(args, wave, gridDim.x, total, wave_target);
+        ++wave;
         const int t_next = claim_tile(args, next_static, gridDim.x);  // latency hidden by the loads
         int mb, nb;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
@@ -418,6 +445,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t tphase = 0;
       // The leader claims tiles and publishes them to both CTAs' rings; the
       // peer's producer follows its own ring.
+      int wave = 0, wave_target = 0;
+      bool wave_on = args.wave_sync != 0;
       int t = leader ? claim_tile(args, next_static, step) : 0;
       while (true) {
         if (leader) {
@@ -437,6 +466,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tphase ^= 1;
         }
         if (t < 0) break;
+        if (leader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
+        ++wave;
         const int t_next = leader ? claim_tile(args, next_static, step) : 0;
         int mb, nb;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
@@ -677,11 +708,19 @@ int* next_tile_counter() {
 }
 }  // namespace
 
-const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t K) {
-  if (const char* v = std::getenv("POAS_TC_KERNEL"))
-    return std::string(v) == "1cta" ? "tc_gemm_kernel" : "tc_gemm_2cta_kernel";
+const char* tc_gemm_kernel_name(int64_t, int64_t, int64_t) {
+  const char* v = std::getenv("POAS_TC_KERNEL");
+  return v && std::string(v) == "1cta" ? "tc_gemm_kernel" : "tc_gemm_2cta_kernel";
+}
+
+const char* tc_gemm_scheduler_name(int64_t M, int64_t N, int64_t K) {
+  if (const char* v = std::getenv("POAS_TC_SCHED")) {
+    const std::string s(v);
+    if (s == "static" || s == "wave" || s == "dynamic") return s == "static" ? "static"
+                                                               : s == "wave" ? "wave" : "dynamic";
+  }
   const double macs = static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K);
-  return macs >= 17592186044416.0 ? "tc_gemm_kernel" : "tc_gemm_2cta_kernel";
+  return macs >= 17592186044416.0 ? "wave" : "dynamic";
 }
 
 cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
@@ -715,12 +754,9 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
                                       static_cast<int>(k2SmemBytes));
   });
   if (attr_err != cudaSuccess) return attr_err;
-  // Kernel choice. The CTA-pair kernel moves 1/3 fewer operand bytes into
-  // shared memory per MAC and wins at 16384^3 under sustained load (+8% over
-  // the single-SM kernel with the dynamic scheduler, profiles/
-  // r01_tile_scheduler); at 32768^3 it drops to lower clocks under the power
-  // cap and the single-SM kernel wins (+14%). Threshold from
-  // tools/raster_sweep.py: 2^44 MACs (~26000^3).
+  // Kernel choice: the CTA-pair kernel (1/3 fewer operand bytes into shared
+  // memory per MAC than the single-SM kernel; faster at every size measured
+  // once its scheduler fits the size, profiles/r01_tile_scheduler).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const bool force_1cta = std::string(tc_gemm_kernel_name(M, N, K)) == "tc_gemm_kernel";
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
@@ -756,12 +792,17 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
     const cudaError_t e = cudaMemsetAsync(args.start_sync, 0, sizeof(unsigned), stream);
     if (e != cudaSuccess) return e;
   }
-  // Dynamic tile scheduler (default; POAS_TC_SCHED=static: round-robin).
-  const char* sched_env = std::getenv("POAS_TC_SCHED");
+  // Tile scheduler: dynamic claiming below 2^44 MACs; wave-synchronised
+  // static order from there on (a tile lasts long enough that the claim
+  // order's stagger spreads A-panel sharers over more than an L2 lifetime:
+  // 206 -> 69 GB DRAM and +25% sustained at 32768^3). POAS_TC_SCHED=
+  // dynamic|wave|static overrides.
+  const std::string sched = tc_gemm_scheduler_name(M, N, K);
   const char* backoff_env = std::getenv("POAS_TC_BACKOFF");
   args.epi_backoff_ns = backoff_env ? std::atoi(backoff_env) : 0;
   args.tile_counter = nullptr;
-  if (!(sched_env && std::string(sched_env) == "static")) {
+  args.wave_sync = sched == "wave";
+  if (sched != "static") {
     args.tile_counter = next_tile_counter();
     if (!args.tile_counter) return cudaErrorMemoryAllocation;
   }

@@ -86,7 +86,28 @@ MachineProfile refit_profile(const MachineProfile& prior, const std::vector<Devi
       if (c.id == o.id) d = &c;
     if (!d) fail(errc::missing_device, "refit: unit '" + o.id + "' is not in the profile");
     if (o.rows <= 0) continue;
+    const double pred_link = o.copy_in.predicted + o.copy_out.predicted;
+    const bool fused = d->uses_bus() && pred_link > 0.0 && o.copy_in.measured == 0.0 &&
+                       o.copy_out.measured == 0.0;
     double g = 1.0;
+    if (fused) {
+      // Operands resident where the unit computes: the modelled link phases
+      // happen inside the kernel (it streams its operands while computing),
+      // so the measured compute phase stands for copy-in + compute +
+      // copy-out. Move the compute model so the three predicted phases sum
+      // to the measurement; the link model is left as profiled.
+      PhaseError whole;
+      whole.measured = o.compute.measured;
+      whole.predicted = o.compute.predicted + pred_link;
+      double gw = 1.0;
+      if (update_factor(whole, options, &gw) && o.compute.predicted > 0.0) {
+        const double target = o.compute.predicted + (gw - 1.0) * whole.predicted;
+        g = std::clamp(target / o.compute.predicted, 1.0 / options.max_step, options.max_step);
+        d->compute.slope *= g;
+        d->compute.intercept *= g;
+      }
+      continue;
+    }
     if (update_factor(o.compute, options, &g)) {
       d->compute.slope *= g;
       d->compute.intercept *= g;

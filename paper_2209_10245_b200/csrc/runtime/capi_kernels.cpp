@@ -42,6 +42,10 @@ const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k) {
   return poas_b200::tc_gemm_kernel_name(m, n, k);
 }
 
+const char* poas_b200_tc_scheduler_name(int64_t m, int64_t n, int64_t k) {
+  return poas_b200::tc_gemm_scheduler_name(m, n, k);
+}
+
 int poas_b200_simt_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
                         const float* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
                         int num_ctas, int exclusive_sm, void* stream) {

@@ -607,8 +607,9 @@ std::string format_execution_report(const Schedule& s, const SimulationResult& r
   o += "  \"measured_wall\": " + num(r.measured_wall) + ",\n";
   o += "  \"repeat_makespans\": [";
   for (std::size_t k = 0; k < r.repeat_timelines.size(); ++k) {
-    double m = 0.0;
-    for (const DeviceTimeline& t : r.repeat_timelines[k]) m = std::max(m, t.finish);
+    double m = 0.0;  // busy units only, as measured_makespan
+    for (std::size_t i = 0; i < r.repeat_timelines[k].size() && i < s.devices.size(); ++i)
+      if (s.devices[i].rows > 0) m = std::max(m, r.repeat_timelines[k][i].finish);
     o += (k ? ", " : "") + num(m);
   }
   o += "]\n}\n";

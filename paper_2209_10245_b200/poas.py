@@ -235,6 +235,11 @@ def tc_kernel_name(m: int, n: int, k: int) -> str:
     return lib.poas_b200_tc_kernel_name(m, n, k).decode()
 
 
+def tc_scheduler_name(m: int, n: int, k: int) -> str:
+    """The tile scheduler tc_gemm uses for this shape ("dynamic" or "wave")."""
+    return lib.poas_b200_tc_scheduler_name(m, n, k).decode()
+
+
 def simt_gemm(m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, num_ctas=0, exclusive=False,
               stream=None):
     check(lib.poas_b200_simt_gemm(m, n, k, a, lda, b, ldb, c, ldc, int(accumulate), num_ctas,

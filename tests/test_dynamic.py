@@ -195,3 +195,26 @@ def test_dynamic_rejects_bad_arguments(poas):
     with pytest.raises(PoasError) as e:
         ex.run_dynamic(prof, 64, 64, 64, io, iterations=1, policy="nope")
     assert e.value.errc == "invalid_argument"
+
+
+def test_refit_resident_unit_folds_link_phases_into_compute(poas, b200_like):
+    """Resident operands: predicted copy phases, none measured -- the kernel
+    streamed its operands while computing. The compute model moves so the
+    three predicted phases add up to the measured compute; bandwidth stays."""
+    s = json.loads(poas.plan(b200_like, 16384, 16384, 16384))
+    rep = _fake_report(s)
+    tc = [d for d in rep["devices"] if d["id"] == "gpu0.tc"][0]
+    link = tc["copy_in"]["predicted"] + tc["copy_out"]["predicted"]
+    assert link > 0
+    whole = tc["compute"]["predicted"] + link
+    for ph in ("copy_in", "copy_out"):
+        tc[ph]["measured"] = 0.0
+    tc["compute"]["measured"] = 0.9 * whole
+    out = poas.refit_profile(b200_like, rep, 1.0)
+    before, after = _profile_fields(b200_like), _profile_fields(out)
+    # the same rows now predict copy-in + compute + copy-out == measured
+    g = (0.9 * whole - link) / tc["compute"]["predicted"]
+    for key in ("slope", "intercept"):
+        assert float(after["gpu0.tc"][key]) == pytest.approx(float(before["gpu0.tc"][key]) * g,
+                                                             rel=1e-12)
+    assert after["gpu0.tc"]["bandwidth"] == before["gpu0.tc"]["bandwidth"]

@@ -248,7 +248,7 @@ def test_dynamic_rescheduling_on_gpu_units(torch_cuda, poas):
     import oracle
 
     torch = torch_cuda
-    m, n, k = 3000, 1536, 1024
+    m, n, k = 6000, 3072, 2048  # ~0.7 ms on the test units: kernel time dominates launch latency
     profile = poas.profile_machine(UNITS, PROF, True)
     lines, cur = [], None
     for line in profile.splitlines():
@@ -270,7 +270,7 @@ def test_dynamic_rescheduling_on_gpu_units(torch_cuda, poas):
     # converges from ~2/3 off to the unmodelled remainder (launch and
     # cross-stream latency of a sub-millisecond co-executed step)
     best = min(abs(i["makespan_error_pct"]) for i in its[1:])
-    assert best < 25.0 and best < 0.5 * its[0]["makespan_error_pct"], its
+    assert best < 20.0 and best < 0.5 * its[0]["makespan_error_pct"], its
     assert out["schedule"]["machine_hash"] == ex.machine_hash
     # C holds the last executed plan (rows in schedule order)
     sched = {"devices": [{"id": i, "rows": r} for i, r in its[-1]["rows"].items()]}

@@ -175,7 +175,7 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= TOL, rel
 
 
-@pytest.mark.parametrize("sched", ["dynamic", "static"])
+@pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
 @pytest.mark.parametrize("variant", ["1cta", "2cta"])
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
 def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched):
@@ -224,3 +224,27 @@ def test_tc_tile_counter_reuse_and_concurrency(torch_cuda, poas):
     torch.cuda.synchronize()
     for c in (c1, c2):
         assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+
+
+def test_tc_wave_scheduler_survives_non_resident_workers(torch_cuda, poas, monkeypatch):
+    """Wave mode with more persistent workers than SMs (the late ones are not
+    resident until others exit): the per-wave barriers time out once and the
+    kernel finishes with exact results instead of hanging."""
+    import time
+
+    import oracle
+
+    torch = torch_cuda
+    monkeypatch.setenv("POAS_TC_SCHED", "wave")
+    m, n, k = 8192, 4096, 256  # 512 pair tiles; 400 CTAs = 200 pairs, 74 resident
+    A, B = oracle.fill_uniform(m, k, 51), oracle.fill_uniform(k, n, 52)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    for ctas in (0, 400):
+        c = torch.full((m, n), float("nan"), device="cuda")
+        t0 = time.perf_counter()
+        poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n, num_ctas=ctas)
+        torch.cuda.synchronize()
+        assert time.perf_counter() - t0 < 5.0
+        assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, ctas
