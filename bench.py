@@ -15,8 +15,10 @@ Per rank (one process per GPU, torchrun for N > 1; weak scaling):
              at N > 1 rank 0's B (bf16 + fp32) is broadcast with NCCL inside
              the step
   value      whole-job TFLOP/s = 2*M_total*N*K / max-over-ranks device time
-  e2e        the same GEMM through poas_b200_execute with HOST pinned fp32
-             buffers: H2D copy-in, compute, D2H copy-out inside the timed step
+  e2e        the same GEMM through poas_b200_execute with HOST pinned buffers
+             (bf16 A/B for the tensor unit, fp32 for the others, fp32 C):
+             H2D copy-in, compute, D2H copy-out inside the timed step;
+             e2e.fp32_host: the same with fp32 A/B converted on the GPU
 
 `--impl reference` times the reference's own CPU path for this workload on
 the host cores (the reference planner from oracle/_ref planning a CPU-only
@@ -498,70 +500,88 @@ def main():
         cublas_ms = statistics.median(t_lib)
         del C_lib
 
-    # ---- e2e through the C ABI with host buffers (fp32 over PCIe)
+    # ---- e2e through the C ABI with host buffers over PCIe. Headline: the
+    # tensor unit's link carries 16-bit A/B (the reference's XPU link model,
+    # elem_size 2; the workload's operand precision, as in the resident run);
+    # alongside: fp32 host A/B converted on the GPU. CPU-side units (host
+    # cores, the CUDA-core unit's fp32 operands) read the fp32 host copies.
     e2e = None
     if not args.no_e2e:
-        units_e2e = units_res.replace("elem=2:link=hbm", "elem=4:link=pcie").replace(
-            "elem=4:link=hbm", "elem=4:link=pcie")
-        if not args.no_e2e_cpu:
-            # With host-resident operands the host cores are a unit too: they
-            # compute rows in place while the GPU units' copies hold the link.
-            units_e2e += f";cpu{rank}=cpu:threads={max(1, (os.cpu_count() or 2) - 2)}"
-        prof_e2e = poas.profile_machine(units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048",
-                                        bus=True)
-        sched_e2e = poas.plan_policy(prof_e2e, m, n, k, args.policy)
-        ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
-        se = json.loads(sched_e2e)
-        if save and rank == 0:
-            (save / "profile_e2e.txt").write_text(prof_e2e)
-            (save / "schedule_e2e.json").write_text(sched_e2e)
         hA = torch.empty(m, k, dtype=torch.float32, pin_memory=True)
         hB = torch.empty(k, n, dtype=torch.float32, pin_memory=True)
         hC = torch.empty(m, n, dtype=torch.float32, pin_memory=True)
         poas.fill_uniform_host(hA.data_ptr(), k, m, k, row0, 0, k, sa)
         poas.fill_uniform_host(hB.data_ptr(), n, k, n, 0, 0, n, sb)
-        ex_e2e = poas.Executor(units_e2e)
-        io_h = poas.GemmIO(m=m, n=n, k=k, a_host=hA.data_ptr(), lda_host=k, b_host=hB.data_ptr(),
-                           ldb_host=n, c_host=hC.data_ptr(), ldc_host=n, resident=0)
-        # dynamic scheduling warm-up (as for the resident run): the host
-        # unit's probes (sides <= 2048, cache-resident B) cannot see the
-        # 1 GiB B stream of the real share; measured runs re-fit it.
-        dyn_e2e = ex_e2e.run_dynamic(prof_e2e, m, n, k, io_h, iterations=max(args.warmup, 6),
-                                     policy=args.policy, alpha=args.alpha,
-                                     replan_threshold_pct=args.replan_threshold)
-        sched_e2e = poas.schedule_roundtrip(json.dumps(dyn_e2e["schedule"]))
-        se = json.loads(sched_e2e)
-        if save and rank == 0:
-            (save / "dynamic_e2e.json").write_text(json.dumps(dyn_e2e, indent=1))
-        ex_e2e.execute(sched_e2e, io_h, 1)
-        if world > 1:
-            dist.barrier()
-        steps_e2e = max(3, min(args.steps, 10))
-        t0 = time.perf_counter()
-        r_e2e = ex_e2e.execute(sched_e2e, io_h, steps_e2e)
-        wall = time.perf_counter() - t0
-        tw = torch.tensor([wall], device=dev)
-        if world > 1:
-            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-        wall = float(tw.item())
-        linked = [d for d in se["devices"] if d["rows"] > 0 and not d["id"].startswith("cpu")]
-        h2d = sum(4 * (d["rows"] * k + k * n) for d in linked)  # A rows + all of B, fp32
-        d2h = sum(4 * d["rows"] * n for d in linked)            # C rows, fp32
-        e2e = {"value": round(2.0 * m * world * n * k / (wall / steps_e2e) / 1e12, 3), "unit": "TFLOP/s",
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "ms_per_step": round(wall / steps_e2e * 1e3, 3),
-               "plan_rows": {d["id"]: d["rows"] for d in se["devices"]},
-               "reference_policy_plan_rows": {d["id"]: d["rows"] for d in ref_e2e["devices"]},
-               "reference_policy_predicted_ms": round(ref_e2e["makespan"] * 1e3, 4),
-               "predicted_makespan_ms": round(r_e2e["predicted_makespan"] * 1e3, 4),
-               "measured_makespan_ms": round(r_e2e["measured_makespan"] * 1e3, 4),
-               "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
-               "static_plan": _static_summary(dyn_e2e),
-               "dynamic_replans": dyn_e2e["replans"],
-               "units": units_e2e,
-               "path": "poas_b200_execute (C ABI), pinned host fp32 A/B/C, H2D+compute+D2H in step"}
-        if save and rank == 0:
-            (save / "report_e2e.json").write_text(json.dumps(r_e2e, indent=1))
+        hA16 = hA.bfloat16().pin_memory()  # RNE, bit-identical to the device conversion
+        hB16 = hB.bfloat16().pin_memory()
+
+        def run_e2e(tc_elem):
+            units_e2e = units_res.replace("elem=2:link=hbm", f"elem={tc_elem}:link=pcie").replace(
+                "elem=4:link=hbm", "elem=4:link=pcie")
+            if not args.no_e2e_cpu:
+                # With host-resident operands the host cores are a unit too:
+                # they compute rows in place while the GPU units' copies hold
+                # the link.
+                units_e2e += f";cpu{rank}=cpu:threads={max(1, (os.cpu_count() or 2) - 2)}"
+            prof_e2e = poas.profile_machine(units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048",
+                                            bus=True)
+            ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
+            ex_e2e = poas.Executor(units_e2e)
+            io_h = poas.GemmIO(m=m, n=n, k=k, a_host=hA.data_ptr(), lda_host=k, b_host=hB.data_ptr(),
+                               ldb_host=n, c_host=hC.data_ptr(), ldc_host=n, resident=0)
+            if tc_elem == 2:
+                io_h.a16_host, io_h.lda16_host = hA16.data_ptr(), k
+                io_h.b16_host, io_h.ldb16_host = hB16.data_ptr(), n
+            # dynamic scheduling warm-up (as for the resident run): the host
+            # unit's probes (sides <= 2048, cache-resident B) cannot see the
+            # 1 GiB B stream of the real share; measured runs re-fit it.
+            dyn_e2e = ex_e2e.run_dynamic(prof_e2e, m, n, k, io_h, iterations=max(args.warmup, 6),
+                                         policy=args.policy, alpha=args.alpha,
+                                         replan_threshold_pct=args.replan_threshold)
+            sched_e2e = poas.schedule_roundtrip(json.dumps(dyn_e2e["schedule"]))
+            se = json.loads(sched_e2e)
+            ex_e2e.execute(sched_e2e, io_h, 1)
+            if world > 1:
+                dist.barrier()
+            steps_e2e = max(3, min(args.steps, 10))
+            t0 = time.perf_counter()
+            r_e2e = ex_e2e.execute(sched_e2e, io_h, steps_e2e)
+            wall = time.perf_counter() - t0
+            tw = torch.tensor([wall], device=dev)
+            if world > 1:
+                dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+            wall = float(tw.item())
+            linked = [d for d in se["devices"] if d["rows"] > 0 and not d["id"].startswith("cpu")]
+            # bytes crossing the link per step: each GPU unit's A rows and all
+            # of B in its link element size, its C rows in fp32
+            esz = {d["id"]: (tc_elem if d["id"] == tc_id else 4) for d in linked}
+            h2d = sum(esz[d["id"]] * (d["rows"] * k + k * n) for d in linked)
+            d2h = sum(4 * d["rows"] * n for d in linked)
+            out = {"value": round(2.0 * m * world * n * k / (wall / steps_e2e) / 1e12, 3), "unit": "TFLOP/s",
+                   "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                   "ms_per_step": round(wall / steps_e2e * 1e3, 3),
+                   "plan_rows": {d["id"]: d["rows"] for d in se["devices"]},
+                   "reference_policy_plan_rows": {d["id"]: d["rows"] for d in ref_e2e["devices"]},
+                   "reference_policy_predicted_ms": round(ref_e2e["makespan"] * 1e3, 4),
+                   "predicted_makespan_ms": round(r_e2e["predicted_makespan"] * 1e3, 4),
+                   "measured_makespan_ms": round(r_e2e["measured_makespan"] * 1e3, 4),
+                   "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
+                   "static_plan": _static_summary(dyn_e2e),
+                   "dynamic_replans": dyn_e2e["replans"],
+                   "units": units_e2e,
+                   "path": "poas_b200_execute (C ABI), pinned host "
+                           + ("bf16 A/B for the tensor unit (fp32 for the others)" if tc_elem == 2
+                              else "fp32 A/B converted on the GPU")
+                           + ", fp32 C; H2D + compute + D2H in every step"}
+            if save and rank == 0:
+                tag = "e2e" if tc_elem == 2 else "e2e_fp32"
+                (save / f"profile_{tag}.txt").write_text(prof_e2e)
+                (save / f"dynamic_{tag}.json").write_text(json.dumps(dyn_e2e, indent=1))
+                (save / f"report_{tag}.json").write_text(json.dumps(r_e2e, indent=1))
+            return out
+
+        e2e = run_e2e(2)
+        e2e["fp32_host"] = run_e2e(4)
 
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu_baseline = None

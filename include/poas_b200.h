@@ -189,6 +189,15 @@ typedef struct {
    * b_ready is given, every GPU unit waits on b_ready[0] before computing. */
   int b_panels;
   void* const* b_ready;
+  /* Optional (resident == 0): host copies of A and B in the tensor units'
+   * 16-bit type. A tensor unit whose link element size is 2 (elem=2) then
+   * copies these -- half the bytes of fp32, the reference's XPU link model
+   * (elem_size 2) -- instead of copying fp32 and converting on the GPU.
+   * Row pitches are in elements. */
+  const void* a16_host;
+  int64_t lda16_host;
+  const void* b16_host;
+  int64_t ldb16_host;
 } poas_gemm_io;
 
 /* One executor per process per machine description (same unit specs as

@@ -73,6 +73,11 @@ struct GemmOperands {
   // Panel-major B with per-panel readiness events (see poas_gemm_io).
   int b_panels = 0;
   void* const* b_ready = nullptr;
+  // 16-bit host operands for elem=2 tensor units (see poas_gemm_io).
+  const void* a16_host = nullptr;
+  std::int64_t lda16_host = 0;
+  const void* b16_host = nullptr;
+  std::int64_t ldb16_host = 0;
 };
 
 double rel_err_pct(double measured, double predicted);

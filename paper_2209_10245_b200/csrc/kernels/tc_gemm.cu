@@ -53,22 +53,9 @@ struct TcArgs {
   int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
   int raster_n;        // 1: groups run along N instead of M (experiments)
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
-  unsigned* start_sync;  // optional zeroed counter: all producers start K in step
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
   int wave_sync;         // 1: static order + per-wave barrier on tile_counter[0]
-  int epi_backoff_ns;    // epilogue warps sleep between accumulator polls (0: spin)
 };
-
-// The epilogue warps wait a whole mainloop (~100 us) for each accumulator;
-// sleeping between polls keeps them from issuing millions of try_wait
-// instructions (power under the cap). The accumulator is double buffered, so
-// a late wake-up delays nothing on the tensor pipe.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, int ns) {
-  const uint32_t a = smem_addr(bar);
-  while (!mbar_try_wait(a, parity)) {
-    if (ns) __nanosleep(static_cast<unsigned>(ns));
-  }
-}
 
 // ---------------------------------------------------------- tile scheduler
 // The producer thread (of the CTA, or of the pair's leader) owns the tile
@@ -119,18 +106,6 @@ __device__ __forceinline__ bool wave_barrier(const TcArgs& a, int i, int workers
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - start > 200000ull) return false;  // 200 us: a worker is not resident
   }
-}
-
-// One-time start barrier of the producers (persistent grid, all CTAs
-// co-resident): CTAs that share A/B panels through L2 then sweep K in step
-// instead of inheriting the launch stagger of cluster scheduling.
-__device__ __forceinline__ void start_barrier(unsigned* counter, unsigned expected) {
-  if (!counter) return;
-  atomicAdd(counter, 1u);
-  unsigned seen = 0;
-  do {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
-  } while (seen < expected);
 }
 
 // Grouped raster: consecutive tile ids walk `group` M-tiles down a column of
@@ -205,7 +180,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      start_barrier(args.start_sync, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
       int next_static = blockIdx.x;
@@ -312,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t < 0) break;
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
-      mbar_wait_backoff(&acc_full[acc], acc_phase, args.epi_backoff_ns);
+      mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * kBM + quad * 32 + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
@@ -437,7 +411,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      start_barrier(args.start_sync, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
       int next_static = first;
@@ -552,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (t < 0) break;
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
-      mbar_wait_backoff(&acc_full[acc], acc_phase, args.epi_backoff_ns);
+      mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + quad * 32 + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
@@ -659,26 +632,6 @@ int device_sm_count() {
 }
 
 namespace {
-// Per-device ring of start-barrier counters: concurrent launches (other
-// streams) get distinct counters; each is zeroed on the launch's stream.
-unsigned* next_sync_counter() {
-  constexpr int kRing = 256;
-  static std::mutex mu;
-  static unsigned* ring[64] = {};
-  static int next[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!ring[dev] && cudaMalloc(&ring[dev], kRing * 32 * sizeof(unsigned)) != cudaSuccess) {
-    ring[dev] = nullptr;
-    return nullptr;
-  }
-  unsigned* c = ring[dev] + (next[dev] % kRing) * 32;  // 128 B apart
-  ++next[dev];
-  return c;
-}
-
 // Per-device ring of tile-scheduler counters {next, done}. Zeroed once at
 // allocation; every launch leaves its counter zero again (release_counter),
 // so no per-launch memset. Launches in flight at the same time (other
@@ -771,7 +724,6 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.C = C;
   args.ldc = ldc;
   args.accumulate = accumulate ? 1 : 0;
-  args.start_sync = nullptr;
   auto hint = [](const char* name) {
     const char* v = std::getenv(name);
     if (v && std::string(v) == "first") return kEvictFirst;
@@ -782,24 +734,12 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.hint_b = hint("POAS_TC_HINT_B");
   const char* raster_env = std::getenv("POAS_TC_RASTER");
   args.raster_n = raster_env && std::string(raster_env) == "n";
-  // Optional start barrier (POAS_TC_SYNC=1; off by default: measured no DRAM
-  // or time benefit, and it needs every CTA co-resident, which concurrent
-  // kernels -- e.g. NCCL's during an overlapped broadcast -- can break).
-  const char* sync_env = std::getenv("POAS_TC_SYNC");
-  if (sync_env && sync_env[0] == '1' && budget <= sms) {
-    args.start_sync = next_sync_counter();
-    if (!args.start_sync) return cudaErrorMemoryAllocation;
-    const cudaError_t e = cudaMemsetAsync(args.start_sync, 0, sizeof(unsigned), stream);
-    if (e != cudaSuccess) return e;
-  }
   // Tile scheduler: dynamic claiming below 2^44 MACs; wave-synchronised
   // static order from there on (a tile lasts long enough that the claim
   // order's stagger spreads A-panel sharers over more than an L2 lifetime:
   // 206 -> 69 GB DRAM and +25% sustained at 32768^3). POAS_TC_SCHED=
   // dynamic|wave|static overrides.
   const std::string sched = tc_gemm_scheduler_name(M, N, K);
-  const char* backoff_env = std::getenv("POAS_TC_BACKOFF");
-  args.epi_backoff_ns = backoff_env ? std::atoi(backoff_env) : 0;
   args.tile_counter = nullptr;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
@@ -826,25 +766,6 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
-  // Experiment knob (POAS_TC_CLUSTER1=1): launch the single-SM kernel as
-  // clusters of 2 -- same work, cluster scheduling -- to separate placement
-  // effects from the pair MMA in the DRAM-traffic comparison.
-  const char* cl_env = std::getenv("POAS_TC_CLUSTER1");
-  if (cl_env && cl_env[0] == '1' && grid % 2 == 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel, ma, mb, args);
-  }
   tc_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
   return cudaGetLastError();
 }

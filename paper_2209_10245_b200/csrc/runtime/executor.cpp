@@ -174,8 +174,18 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     if (schedule.devices[i].rows == 0) continue;
     if (!unit[i]->on_gpu()) any_cpu = true;
   }
-  if ((any_cpu || !io.resident) && (!io.a_host || !io.b_host || !io.c_host))
-    fail(errc::invalid_argument, "host operands (a_host, b_host, c_host) are required");
+  // A tensor unit with a 2-byte link reads 16-bit host operands when given.
+  const auto host16_link = [&](const Unit* u) {
+    return u->spec().kind == DeviceKind::xpu && u->spec().elem == 2 && io.a16_host && io.b16_host;
+  };
+  if ((any_cpu || !io.resident) && !io.c_host)
+    fail(errc::invalid_argument, "host operand c_host is required");
+  for (std::size_t i = 0; i < nd; ++i) {
+    if (schedule.devices[i].rows == 0) continue;
+    const bool needs_f32_host = !unit[i]->on_gpu() || (!io.resident && !host16_link(unit[i]));
+    if (needs_f32_host && (!io.a_host || !io.b_host))
+      fail(errc::invalid_argument, "host operands (a_host, b_host, c_host) are required");
+  }
   const int panels = io.b_panels > 1 ? io.b_panels : 1;
   if (panels > 1) {
     if (!io.resident) fail(errc::invalid_argument, "B panels need resident operands");
@@ -345,18 +355,34 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       float* c = nullptr;
       std::int64_t ldc = 0;
 
+      const bool link16 = !io.resident && tensor && host16_link(u);
       if (!io.resident) {
         if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(s, evr[prev_in].ci1, 0), "wait");
         cuda_check(cudaEventRecord(evr[i].ci0, s), "cudaEventRecord");
-        float* da = static_cast<float*>(u->scratch(0).ensure(static_cast<std::size_t>(r * d.k) * 4));
-        float* db = static_cast<float*>(u->scratch(1).ensure(static_cast<std::size_t>(d.k * d.n) * 4));
-        copy2d(da, d.k, io.a_host + r0 * io.lda_host, io.lda_host, r, d.k, 4,
-               cudaMemcpyHostToDevice, s);
-        copy2d(db, d.n, io.b_host, io.ldb_host, d.k, d.n, 4, cudaMemcpyHostToDevice, s);
-        a = da;
-        b = db;
-        lda = d.k;
-        ldb = d.n;
+        if (link16) {
+          // 16-bit operands cross the link and land in the kernel's layout
+          // (row pitch a multiple of 8 elements): no conversion pass.
+          const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
+          void* a16 = u->scratch(2).ensure(static_cast<std::size_t>(r * lda16) * 2);
+          void* b16 = u->scratch(3).ensure(static_cast<std::size_t>(d.k * ldb16) * 2);
+          copy2d(a16, lda16, static_cast<const char*>(io.a16_host) + r0 * io.lda16_host * 2,
+                 io.lda16_host, r, d.k, 2, cudaMemcpyHostToDevice, s);
+          copy2d(b16, ldb16, io.b16_host, io.ldb16_host, d.k, d.n, 2, cudaMemcpyHostToDevice, s);
+          a = a16;
+          b = b16;
+          lda = lda16;
+          ldb = ldb16;
+        } else {
+          float* da = static_cast<float*>(u->scratch(0).ensure(static_cast<std::size_t>(r * d.k) * 4));
+          float* db = static_cast<float*>(u->scratch(1).ensure(static_cast<std::size_t>(d.k * d.n) * 4));
+          copy2d(da, d.k, io.a_host + r0 * io.lda_host, io.lda_host, r, d.k, 4,
+                 cudaMemcpyHostToDevice, s);
+          copy2d(db, d.n, io.b_host, io.ldb_host, d.k, d.n, 4, cudaMemcpyHostToDevice, s);
+          a = da;
+          b = db;
+          lda = d.k;
+          ldb = d.n;
+        }
         c = static_cast<float*>(u->scratch(4).ensure(static_cast<std::size_t>(r * d.n) * 4));
         ldc = d.n;
         prev_in = i;
@@ -378,7 +404,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       if (!io.resident) cuda_check(cudaEventRecord(evr[i].ci1, s), "cudaEventRecord");
 
       cuda_check(cudaEventRecord(evr[i].cp0, s), "cudaEventRecord");
-      const bool need_convert = tensor && !(io.resident && io.a16_dev && io.b16_dev);
+      const bool need_convert = tensor && !(io.resident && io.a16_dev && io.b16_dev) && !link16;
       if (need_convert) {
         const AbType t = u->spec().dtype;
         const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);

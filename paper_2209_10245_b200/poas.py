@@ -180,6 +180,8 @@ class GemmIO(C.Structure):
         ("c_dev", C.c_void_p), ("ldc_dev", C.c_int64),
         ("resident", C.c_int),
         ("b_panels", C.c_int), ("b_ready", C.POINTER(C.c_void_p)),
+        ("a16_host", C.c_void_p), ("lda16_host", C.c_int64),
+        ("b16_host", C.c_void_p), ("ldb16_host", C.c_int64),
     ]
 
 

@@ -300,3 +300,35 @@ def test_sm_lending_idle_units(torch_cuda, poas):
         ex.execute(sched_text, d["io_res"], 1)
         torch.cuda.synchronize()
         assert oracle.rel_frobenius(result_c(torch, sched, d, True), exp) <= TOL
+
+
+def test_execute_host_bf16_operands_elem2(torch_cuda, poas):
+    """A tensor unit with a 2-byte link copies 16-bit host operands
+    (a16_host/b16_host) -- half the PCIe bytes, no conversion pass -- and
+    needs no fp32 host A/B when it is the only busy unit."""
+    import oracle
+
+    torch = torch_cuda
+    units = "gpu0.tc=xpu:dev=0:sms=16:dtype=bf16:elem=2:link=pcie:probe=512-2048"
+    m, n, k = 1500, 1000, 516  # k % 8 != 0: staging pads A rows to 8 elements
+    profile = poas.profile_machine(units, PROF, True)
+    sched_text = poas.plan(profile, m, n, k)
+    sched = json.loads(sched_text)
+    d = operands(torch, poas, m, n, k)
+    hA16 = d["A16"][:, :k].cpu().contiguous().pin_memory()
+    hB16 = d["B16"][:, :n].cpu().contiguous().pin_memory()
+    hC = torch.full((m, n), float("nan")).pin_memory()
+    io = poas.GemmIO(m=m, n=n, k=k, c_host=hC.data_ptr(), ldc_host=n, resident=0,
+                     a16_host=hA16.data_ptr(), lda16_host=k, b16_host=hB16.data_ptr(), ldb16_host=n)
+    ex = poas.Executor(units)
+    rep = ex.execute(sched_text, io, 2)
+    exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2})
+    assert oracle.rel_frobenius(hC.numpy(), exp) <= TOL
+    tc = [x for x in rep["devices"] if x["id"] == "gpu0.tc"][0]
+    assert tc["copy_in"]["measured"] > 0 and tc["copy_out"]["measured"] > 0
+    # without 16-bit host operands the unit needs fp32 host A/B
+    from paper_2209_10245_b200 import PoasError
+
+    bad = poas.GemmIO(m=m, n=n, k=k, c_host=hC.data_ptr(), ldc_host=n, resident=0)
+    with pytest.raises(PoasError):
+        ex.execute(sched_text, bad, 1)

@@ -28,13 +28,13 @@ try:
 except Exception:  # pragma: no cover
     NV = None
 
-ENV_KEYS = ("POAS_TC_KERNEL", "POAS_TC_GROUP", "POAS_TC_SCHED", "POAS_TC_RASTER", "POAS_TC_BACKOFF")
+ENV_KEYS = ("POAS_TC_KERNEL", "POAS_TC_GROUP", "POAS_TC_SCHED", "POAS_TC_RASTER")
 DEFAULT_VARIANTS = {
-    "2cta:g8": {"POAS_TC_KERNEL": "2cta", "POAS_TC_GROUP": "8"},
-    "2cta:g8:backoff500": {"POAS_TC_KERNEL": "2cta", "POAS_TC_GROUP": "8", "POAS_TC_BACKOFF": "500"},
-    "2cta:g4": {"POAS_TC_KERNEL": "2cta", "POAS_TC_GROUP": "4"},
-    "1cta:g16": {"POAS_TC_KERNEL": "1cta", "POAS_TC_GROUP": "16"},
-    "1cta:g16:backoff500": {"POAS_TC_KERNEL": "1cta", "POAS_TC_GROUP": "16", "POAS_TC_BACKOFF": "500"},
+    "default": {},  # tc_gemm's own choice of kernel / scheduler for the size
+    "2cta:dynamic": {"POAS_TC_KERNEL": "2cta", "POAS_TC_SCHED": "dynamic"},
+    "2cta:wave": {"POAS_TC_KERNEL": "2cta", "POAS_TC_SCHED": "wave"},
+    "1cta:dynamic": {"POAS_TC_KERNEL": "1cta", "POAS_TC_SCHED": "dynamic"},
+    "1cta:wave": {"POAS_TC_KERNEL": "1cta", "POAS_TC_SCHED": "wave"},
     "cublas": None,
 }
 
