@@ -268,6 +268,8 @@ def main():
                     help="reuse a poas-profile v1 file for the resident units instead of probing "
                          "('{rank}' is replaced by the rank); probes timed under a profiler are "
                          "meaningless")
+    ap.add_argument("--no-adapt", action="store_true",
+                    help="warm-up runs the static plan (no model re-fit / re-plan)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=None)
     ap.add_argument("--save", default=None, help="directory for profile/schedule/report artefacts")
@@ -385,9 +387,14 @@ def main():
     step()  # lands B on every rank (N > 1) before the loop
     # at least ~0.3 s of work, so the power-capped clock has settled before
     # the timed region (the adapted model then predicts it)
+    # (--no-adapt: W plain executions of the static plan -- e.g. under a
+    # profiler, whose serialised launches make measured phases meaningless)
     warm_iters = min(200, max(args.warmup, int(0.3 / max(sched["makespan"], 1e-6)) + 1))
+    if args.no_adapt:
+        warm_iters = args.warmup
     dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
-                         alpha=args.alpha, replan_threshold_pct=args.replan_threshold)
+                         alpha=args.alpha,
+                         replan_threshold_pct=1e9 if args.no_adapt else args.replan_threshold)
     schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
     sched = json.loads(schedule)
     rows = {d["id"]: d["rows"] for d in sched["devices"]}

@@ -22,6 +22,6 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt
 timeout 300 ncu --set full --clock-control none -k regex:simt_skinny -s 1 -c 1 \
   -o "$OUT/prof_simt_skinny" python tools/ncu_target.py simt 8 16384 2 > "$OUT/ncu_simt_skinny.log" 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
-  python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --profile "$OUT/bench/profile_resident.txt" \
+  python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-adapt --profile "$OUT/bench/profile_resident.txt" \
   > "$OUT/ncu_launch.log" 2>&1
 echo done
