@@ -389,11 +389,14 @@ def main():
     # the timed region (the adapted model then predicts it)
     # (--no-adapt: W plain executions of the static plan -- e.g. under a
     # profiler, whose serialised launches make measured phases meaningless)
-    warm_iters = min(200, max(args.warmup, int(0.3 / max(sched["makespan"], 1e-6)) + 1))
+    # Each round runs `warm_reps` steps back to back, the timed region's duty
+    # cycle (single steps with host gaps run measurably cooler and faster).
+    warm_reps = 5
+    warm_iters = min(100, max(args.warmup, int(0.3 / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
     if args.no_adapt:
-        warm_iters = args.warmup
+        warm_iters, warm_reps = args.warmup, 1
     dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
-                         alpha=args.alpha,
+                         alpha=args.alpha, repeats=warm_reps,
                          replan_threshold_pct=1e9 if args.no_adapt else args.replan_threshold)
     schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
     sched = json.loads(schedule)
@@ -630,6 +633,7 @@ def main():
                 "static_plan": _static_summary(dyn),
                 "dynamic_replans": dyn["replans"],
                 "dynamic_warmup_iterations": len(dyn["iterations"]),
+                "dynamic_warmup_steps_per_iteration": warm_reps,
                 "speedup_vs_best_single_unit": round(speedup, 4) if speedup else None,
                 "best_single_unit": {"id": tc_id, "measured_makespan_ms": round(best_single * 1e3, 4),
                                      "coexec_paired_makespan_ms": round(co_median * 1e3, 4),

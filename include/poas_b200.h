@@ -228,15 +228,18 @@ int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_
  * phases. alpha in (0, 1]. Identity (and machine hash) unchanged. */
 int poas_b200_refit_profile(const char* profile_text, const char* report_json, double alpha,
                             char** out_profile);
-/* `iterations` executions of an m x n x k GEMM with re-planning: plan from
- * the profile with `policy` (NULL = "reference"), execute once, re-fit,
- * re-plan when |makespan error| > replan_threshold_pct, repeat. out_json:
+/* `iterations` rounds of an m x n x k GEMM with re-planning: plan from the
+ * profile with `policy` (NULL = "reference"), execute `repeats` times
+ * back to back (the mean is the observation; use the duty cycle of the real
+ * workload, since power-capped clocks depend on it), re-fit, re-plan when
+ * |makespan error| > replan_threshold_pct, repeat. out_json:
  * {"iterations": [{iteration, replanned, rows{id: n}, predicted_makespan,
  * measured_makespan, makespan_error_pct}], "replans", "profile" (final,
  * poas-profile v1 text), "schedule" (final)}. */
 int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t m, int64_t n,
                           int64_t k, const char* policy, const poas_gemm_io* io, int iterations,
-                          double alpha, double replan_threshold_pct, char** out_json);
+                          int repeats, double alpha, double replan_threshold_pct,
+                          char** out_json);
 
 /* ------------------------------------------------------------------------
  * Raw unit kernels (device pointers, caller's cudaStream_t or NULL).

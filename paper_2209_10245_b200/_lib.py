@@ -50,7 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "poas_b200_tc_kernel_name": (cp, [i64, i64, i64]),
     "poas_b200_tc_scheduler_name": (cp, [i64, i64, i64]),
     "poas_b200_refit_profile": (C.c_int, [cp, cp, C.c_double, C.POINTER(vp)]),
-    "poas_b200_run_dynamic": (C.c_int, [vp, cp, i64, i64, i64, cp, vp, C.c_int, C.c_double,
+    "poas_b200_run_dynamic": (C.c_int, [vp, cp, i64, i64, i64, cp, vp, C.c_int, C.c_int, C.c_double,
                                         C.c_double, C.POINTER(vp)]),
     "poas_b200_tc_gemm": (C.c_int, [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int,
                                     C.c_int, vp]),

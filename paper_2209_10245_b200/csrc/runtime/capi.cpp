@@ -424,12 +424,14 @@ int poas_b200_refit_profile(const char* profile_text, const char* report_json, d
 
 int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t m, int64_t n,
                           int64_t k, const char* policy, const poas_gemm_io* io, int iterations,
-                          double alpha, double replan_threshold_pct, char** out_json) {
+                          int repeats, double alpha, double replan_threshold_pct,
+                          char** out_json) {
   return guard([&] {
     need_ptr(ex, "executor");
     need_ptr(io, "io");
     need_ptr(out_json, "out_json");
     if (iterations < 1) raise(POAS_E_INVALID_ARGUMENT, "iterations must be >= 1");
+    if (repeats < 1) raise(POAS_E_INVALID_ARGUMENT, "repeats must be >= 1");
     poas::DynamicOptions opt;
     opt.refit.alpha = alpha;
     opt.replan_threshold_pct = replan_threshold_pct;
@@ -440,7 +442,7 @@ int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t 
     std::string o = "{\n  \"iterations\": [\n";
     bool replanned = false;
     for (int it = 0; it < iterations; ++it) {
-      const poas::SimulationResult r = ex->ex->run(dyn.schedule(), op, 1);
+      const poas::SimulationResult r = ex->ex->run(dyn.schedule(), op, repeats);
       o += "    {\"iteration\": " + std::to_string(it) +
            ", \"replanned\": " + (replanned ? "true" : "false") + ", \"rows\": {";
       for (std::size_t i = 0; i < r.devices.size(); ++i)

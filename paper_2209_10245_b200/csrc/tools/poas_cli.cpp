@@ -463,8 +463,8 @@ int cmd_evaluate(const Args& a) {
       o.policy = policy;
       o.refit.alpha = std::atof(a.get("alpha", "0.5").c_str());
       poas::DynamicScheduler dyn(live, in.dims, o);
-      for (int it = 0; it < adapt; ++it) {
-        const poas::SimulationResult w = ex.run(dyn.schedule(), ops->io, 1);
+      for (int it = 0; it < adapt; ++it) {  // same duty cycle as the measured run
+        const poas::SimulationResult w = ex.run(dyn.schedule(), ops->io, repeats);
         if (it == 0) static_err = w.makespan_error_pct;
         dyn.observe(w);
       }

@@ -207,14 +207,14 @@ class Executor:
 
     def run_dynamic(self, profile: str, m: int, n: int, k: int, io: GemmIO, iterations: int,
                     policy: str = "reference", alpha: float = 0.5,
-                    replan_threshold_pct: float = 2.0) -> dict:
-        """Dynamic scheduling loop (poas_b200_run_dynamic): plan, execute,
-        re-fit, re-plan when |makespan error| > threshold; per-iteration log,
-        the final profile and schedule."""
+                    replan_threshold_pct: float = 2.0, repeats: int = 1) -> dict:
+        """Dynamic scheduling loop (poas_b200_run_dynamic): plan, execute
+        `repeats` times back to back, re-fit, re-plan when |makespan error| >
+        threshold; per-iteration log, the final profile and schedule."""
         out = C.c_void_p()
         check(lib.poas_b200_run_dynamic(self._h, _b(profile), m, n, k, _b(policy), C.byref(io),
-                                        iterations, float(alpha), float(replan_threshold_pct),
-                                        C.byref(out)))
+                                        iterations, repeats, float(alpha),
+                                        float(replan_threshold_pct), C.byref(out)))
         from ._lib import take_string
         return json.loads(take_string(out))
 
