@@ -512,9 +512,13 @@ def main():
 
     # ---- e2e through the C ABI with host buffers over PCIe. Headline: the
     # tensor unit's link carries 16-bit A/B (the reference's XPU link model,
-    # elem_size 2; the workload's operand precision, as in the resident run);
-    # alongside: fp32 host A/B converted on the GPU. CPU-side units (host
-    # cores, the CUDA-core unit's fp32 operands) read the fp32 host copies.
+    # elem_size 2; the workload's operand precision, as in the resident run)
+    # with overlapped copies (planner policy "overlap" + executor
+    # "overlap=1": B, then A row parts host->device while earlier parts
+    # compute and their C goes device->host). Alongside:
+    # fp32 host A/B converted on the GPU, and the paper's synchronous copies
+    # (copy-in, compute, copy-out per unit). CPU-side units (host cores, the
+    # CUDA-core unit's fp32 operands) read the fp32 host copies.
     e2e = None
     if not args.no_e2e:
         hA = torch.empty(m, k, dtype=torch.float32, pin_memory=True)
@@ -524,19 +528,25 @@ def main():
         poas.fill_uniform_host(hB.data_ptr(), n, k, n, 0, 0, n, sb)
         hA16 = hA.bfloat16().pin_memory()  # RNE, bit-identical to the device conversion
         hB16 = hB.bfloat16().pin_memory()
+        local_world = env_int("LOCAL_WORLD_SIZE", world)
+        e2e_profiles = {}
 
-        def run_e2e(tc_elem):
+        def run_e2e(tc_elem, overlap):
             units_e2e = units_res.replace("elem=2:link=hbm", f"elem={tc_elem}:link=pcie").replace(
                 "elem=4:link=hbm", "elem=4:link=pcie")
             if not args.no_e2e_cpu:
                 # With host-resident operands the host cores are a unit too:
                 # they compute rows in place while the GPU units' copies hold
-                # the link.
-                units_e2e += f";cpu{rank}=cpu:threads={max(1, (os.cpu_count() or 2) - 2)}"
-            prof_e2e = poas.profile_machine(units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048",
-                                            bus=True)
+                # the link (the box's cores shared by the ranks on this node).
+                threads = max(1, ((os.cpu_count() or 2) - 2) // max(1, local_world))
+                units_e2e += f";cpu{rank}=cpu:threads={threads}"
+            policy = "overlap" if overlap else args.policy
+            if tc_elem not in e2e_profiles:  # same units either way: probe once
+                e2e_profiles[tc_elem] = poas.profile_machine(
+                    units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048", bus=True)
+            prof_e2e = e2e_profiles[tc_elem]
             ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
-            ex_e2e = poas.Executor(units_e2e)
+            ex_e2e = poas.Executor(units_e2e + (";overlap=1" if overlap else ""))
             io_h = poas.GemmIO(m=m, n=n, k=k, a_host=hA.data_ptr(), lda_host=k, b_host=hB.data_ptr(),
                                ldb_host=n, c_host=hC.data_ptr(), ldc_host=n, resident=0)
             if tc_elem == 2:
@@ -546,7 +556,7 @@ def main():
             # unit's probes (sides <= 2048, cache-resident B) cannot see the
             # 1 GiB B stream of the real share; measured runs re-fit it.
             dyn_e2e = ex_e2e.run_dynamic(prof_e2e, m, n, k, io_h, iterations=max(args.warmup, 6),
-                                         policy=args.policy, alpha=args.alpha,
+                                         policy=policy, alpha=args.alpha,
                                          replan_threshold_pct=args.replan_threshold)
             sched_e2e = poas.schedule_roundtrip(json.dumps(dyn_e2e["schedule"]))
             se = json.loads(sched_e2e)
@@ -567,10 +577,16 @@ def main():
             esz = {d["id"]: (tc_elem if d["id"] == tc_id else 4) for d in linked}
             h2d = sum(esz[d["id"]] * (d["rows"] * k + k * n) for d in linked)
             d2h = sum(4 * d["rows"] * n for d in linked)
-            out = {"value": round(2.0 * m * world * n * k / (wall / steps_e2e) / 1e12, 3), "unit": "TFLOP/s",
+            ms = wall / steps_e2e * 1e3
+            out = {"value": round(2.0 * m * world * n * k / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-                   "ms_per_step": round(wall / steps_e2e * 1e3, 3),
+                   "ms_per_step": round(ms, 3),
+                   # link roofline: the busiest direction's bytes at the
+                   # profiled link bandwidth (full duplex when overlapped)
+                   "link_bound_ms": None,
                    "plan_rows": {d["id"]: d["rows"] for d in se["devices"]},
+                   "row_parts": {d["id"]: len(d["tiles"]) for d in linked} if overlap else None,
+                   "policy": policy,
                    "reference_policy_plan_rows": {d["id"]: d["rows"] for d in ref_e2e["devices"]},
                    "reference_policy_predicted_ms": round(ref_e2e["makespan"] * 1e3, 4),
                    "predicted_makespan_ms": round(r_e2e["predicted_makespan"] * 1e3, 4),
@@ -578,20 +594,31 @@ def main():
                    "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
                    "static_plan": _static_summary(dyn_e2e),
                    "dynamic_replans": dyn_e2e["replans"],
-                   "units": units_e2e,
+                   "units": units_e2e + (";overlap=1" if overlap else ""),
                    "path": "poas_b200_execute (C ABI), pinned host "
                            + ("bf16 A/B for the tensor unit (fp32 for the others)" if tc_elem == 2
                               else "fp32 A/B converted on the GPU")
-                           + ", fp32 C; H2D + compute + D2H in every step"}
+                           + ", fp32 C; H2D + compute + D2H in every step"
+                           + ("; copies overlapped with compute (row parts)" if overlap
+                              else "; synchronous copies (the paper's scheme)")}
+            bw = [float(ln.split()[1]) for ln in prof_e2e.splitlines() if ln.startswith("bandwidth ")]
+            bw = max(bw) if bw else 0.0
+            if bw > 0:
+                per_rank_h2d, per_rank_d2h = h2d, d2h
+                link_s = max(per_rank_h2d, per_rank_d2h) / bw if overlap else (per_rank_h2d + per_rank_d2h) / bw
+                out["link_bound_ms"] = round(link_s * 1e3, 3)
+                out["link_bandwidth_gbs"] = round(bw / 1e9, 2)
             if save and rank == 0:
-                tag = "e2e" if tc_elem == 2 else "e2e_fp32"
+                tag = ("e2e" if tc_elem == 2 else "e2e_fp32") + ("" if overlap else "_sync")
                 (save / f"profile_{tag}.txt").write_text(prof_e2e)
                 (save / f"dynamic_{tag}.json").write_text(json.dumps(dyn_e2e, indent=1))
                 (save / f"report_{tag}.json").write_text(json.dumps(r_e2e, indent=1))
+                (save / f"schedule_{tag}.json").write_text(sched_e2e)
             return out
 
-        e2e = run_e2e(2)
-        e2e["fp32_host"] = run_e2e(4)
+        e2e = run_e2e(2, overlap=True)
+        e2e["fp32_host"] = run_e2e(4, overlap=True)
+        e2e["synchronous"] = run_e2e(2, overlap=False)
 
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu_baseline = None

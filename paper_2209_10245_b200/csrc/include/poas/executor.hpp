@@ -94,6 +94,7 @@ class Executor {
   // flag; a schedule planned for this box carries the same hash.
   const std::string& machine_hash() const { return hash_; }
   bool bus() const { return bus_; }
+  bool overlap() const { return overlap_; }
   poas_b200::Unit* find(const std::string& id) const;
   const std::vector<std::unique_ptr<poas_b200::Unit>>& units() const { return units_; }
 
@@ -102,7 +103,11 @@ class Executor {
  private:
   std::vector<std::unique_ptr<poas_b200::Unit>> units_;
   bool bus_ = true;
-  bool lend_ = true;  // idle units' SMs go to the one busy unit on their GPU
+  bool lend_ = true;      // idle units' SMs go to the one busy unit on their GPU
+  bool overlap_ = false;  // host runs: pipeline link units' row parts (poas/overlap.hpp)
+  // Per unit (units_ order; null for cpu units): the host->device and
+  // device->host copy streams of overlapped runs.
+  std::vector<void*> h2d_, d2h_;
 
  public:
   // Start-gate flags (mapped pinned ints, one per repeat; grown on demand,

@@ -19,6 +19,7 @@
 #include "poas/adapter.hpp"
 #include "poas/error.hpp"
 #include "poas/optimizer.hpp"
+#include "poas/overlap.hpp"
 #include "poas/policy.hpp"
 #include "poas/scheduler.hpp"
 
@@ -29,11 +30,11 @@ Schedule plan_schedule(const MachineProfile& machine, const MatrixDims& dims) {
   return build_schedule(build_tile_plan(machine, dims, split), machine);
 }
 
-Schedule plan_best_subset(const MachineProfile& machine, const MatrixDims& dims) {
+std::vector<TilePlan> subset_tile_plans(const MachineProfile& machine, const MatrixDims& dims) {
   validate_machine(machine);
   validate_dims(dims);
   const std::size_t nd = machine.devices.size();
-  if (nd > 12) fail(errc::too_many_devices, "best-subset policy supports at most 12 units");
+  if (nd > 12) fail(errc::too_many_devices, "subset policies support at most 12 units");
 
   // Masks in decreasing popcount order (full machine first), then ascending.
   std::vector<unsigned> masks;
@@ -42,8 +43,7 @@ Schedule plan_best_subset(const MachineProfile& machine, const MatrixDims& dims)
     return __builtin_popcount(a) > __builtin_popcount(b);
   });
 
-  Schedule best;
-  double best_makespan = std::numeric_limits<double>::infinity();
+  std::vector<TilePlan> out;
   for (const unsigned mask : masks) {
     MachineProfile sub;
     sub.bus = machine.bus;
@@ -71,14 +71,22 @@ Schedule plan_best_subset(const MachineProfile& machine, const MatrixDims& dims)
       full.devices.push_back(pd);
     }
     for (std::size_t j = 0; j < index.size(); ++j) full.devices[index[j]] = sub_plan.devices[j];
+    out.push_back(std::move(full));
+  }
+  if (out.empty()) fail(errc::no_feasible_tiling, "no subset of units can hold the workload");
+  return out;
+}
+
+Schedule plan_best_subset(const MachineProfile& machine, const MatrixDims& dims) {
+  Schedule best;
+  double best_makespan = std::numeric_limits<double>::infinity();
+  for (const TilePlan& full : subset_tile_plans(machine, dims)) {
     Schedule s = build_schedule(full, machine);
     if (s.makespan < best_makespan) {
       best_makespan = s.makespan;
       best = std::move(s);
     }
   }
-  if (!std::isfinite(best_makespan))
-    fail(errc::no_feasible_tiling, "no subset of units can hold the workload");
   return best;
 }
 
@@ -86,6 +94,7 @@ Schedule plan_with_policy(const MachineProfile& machine, const MatrixDims& dims,
                           const std::string& policy) {
   if (policy.empty() || policy == "reference") return plan_schedule(machine, dims);
   if (policy == "best-subset") return plan_best_subset(machine, dims);
+  if (policy == "overlap") return plan_overlap(machine, dims);
   fail(errc::invalid_argument, "unknown planner policy '" + policy + "'");
 }
 

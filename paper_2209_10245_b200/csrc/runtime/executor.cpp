@@ -19,6 +19,11 @@
 //   copy-out    schedule order; the first waits for the last copy-in, each
 //               later one for the previous copy-out (shared bus)
 // Resident runs (operands already in HBM) skip both copy phases.
+// Overlapped host runs ("overlap=1", poas/overlap.hpp): each link unit has
+// its own host->device and device->host streams; B and then the A rows of
+// every row part go host->device back to back, part p computes once its A
+// part landed, its C rows go device->host while part p+1 computes. On a
+// shared bus each direction is served in schedule order.
 // Rows are contiguous in schedule order (poas::row_offsets).
 #include "poas/executor.hpp"
 
@@ -33,6 +38,7 @@
 
 #include "capi_util.hpp"
 #include "poas/error.hpp"
+#include "poas/overlap.hpp"
 #include "units.hpp"
 
 namespace poas {
@@ -86,6 +92,30 @@ void copy2d(void* dst, std::int64_t ld_dst, const void* src, std::int64_t ld_src
                "cudaMemcpy2DAsync");
 }
 
+// Untimed events of one run(), destroyed with it.
+class EventPool {
+ public:
+  EventPool() = default;
+  ~EventPool() {
+    for (auto& [dev, e] : events_) {
+      DeviceGuard g(dev);
+      cudaEventDestroy(e);
+    }
+  }
+  EventPool(const EventPool&) = delete;
+  EventPool& operator=(const EventPool&) = delete;
+  cudaEvent_t make(int dev) {
+    DeviceGuard g(dev);
+    cudaEvent_t e = nullptr;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    events_.emplace_back(dev, e);
+    return e;
+  }
+
+ private:
+  std::vector<std::pair<int, cudaEvent_t>> events_;
+};
+
 // The start gates of one run() (see gate_wait): flag r opens repeat r.
 // Every flag is opened on destruction, so an exception between a gate's
 // launch and its opening cannot leave a kernel waiting.
@@ -126,7 +156,8 @@ class StartGates {
 }  // namespace
 
 Executor::Executor(const std::string& spec) {
-  const std::vector<poas_b200::UnitSpec> specs = poas_b200::parse_unit_list(spec, &bus_, &lend_);
+  const std::vector<poas_b200::UnitSpec> specs =
+      poas_b200::parse_unit_list(spec, &bus_, &lend_, &overlap_);
   std::vector<DeviceIdentity> ids;
   for (const auto& s : specs) {
     if (find(s.id)) fail(errc::invalid_argument, "duplicate unit id '" + s.id + "'");
@@ -134,9 +165,27 @@ Executor::Executor(const std::string& spec) {
     ids.push_back({s.id, s.kind, s.elem});
   }
   hash_ = machine_identity_hash(ids, bus_);
+  h2d_.assign(units_.size(), nullptr);
+  d2h_.assign(units_.size(), nullptr);
+  if (overlap_)
+    for (std::size_t i = 0; i < units_.size(); ++i) {
+      if (!units_[i]->on_gpu()) continue;
+      DeviceGuard g(units_[i]->spec().device);
+      cudaStream_t a = nullptr, b = nullptr;
+      cuda_check(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "cudaStreamCreate");
+      h2d_[i] = a;
+      cuda_check(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking), "cudaStreamCreate");
+      d2h_[i] = b;
+    }
 }
 
 Executor::~Executor() {
+  for (std::size_t i = 0; i < units_.size(); ++i)
+    for (void* s : {h2d_[i], d2h_[i]})
+      if (s) {
+        DeviceGuard g(units_[i]->spec().device);
+        cudaStreamDestroy(static_cast<cudaStream_t>(s));
+      }
   if (gates_.host) cudaFreeHost(gates_.host);
   for (int* p : gates_.retired) cudaFreeHost(p);
 }
@@ -159,11 +208,17 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
 
   const std::size_t nd = schedule.devices.size();
   std::vector<Unit*> unit(nd);
+  std::vector<cudaStream_t> h2d(nd, nullptr), d2h(nd, nullptr);  // overlapped runs
   std::int64_t covered = 0;
   for (std::size_t i = 0; i < nd; ++i) {
     unit[i] = find(schedule.devices[i].id);
     if (!unit[i]) fail(errc::missing_device, "no unit '" + schedule.devices[i].id + "'");
     covered += schedule.devices[i].rows;
+    for (std::size_t j = 0; j < units_.size(); ++j)
+      if (units_[j].get() == unit[i]) {
+        h2d[i] = static_cast<cudaStream_t>(h2d_[j]);
+        d2h[i] = static_cast<cudaStream_t>(d2h_[j]);
+      }
   }
   if (covered != d.m) fail(errc::invalid_argument, "schedule rows do not cover m");
   const std::vector<std::int64_t> row0 = row_offsets(schedule);
@@ -207,6 +262,9 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         fail(errc::invalid_argument, "resident CUDA-core unit needs a_dev/b_dev");
     }
   }
+
+  // Overlapped host runs: every busy link unit pipelines its row parts.
+  const bool overlapped = overlap_ && !io.resident;
 
   // SM lending: when exactly one unit of a GPU has rows in this schedule,
   // the SM budgets of its idle siblings are added to its launch (the plan
@@ -282,6 +340,114 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     DeviceGuard g(unit[i]->spec().device);
     for (auto& per_rep : ev) per_rep[i].create();
   }
+  // Overlapped runs: each busy link unit's row parts (the schedule's tiles,
+  // poas::schedule_row_parts) and per-part readiness events, reused by every
+  // repeat (repeats are serialised on the device).
+  EventPool pool;
+  std::vector<std::vector<std::int64_t>> parts(nd);
+  std::vector<std::vector<cudaEvent_t>> in_ev(nd), cp_ev(nd);
+  if (overlapped)
+    for (std::size_t i = 0; i < nd; ++i) {
+      if (!unit[i]->on_gpu() || schedule.devices[i].rows == 0) continue;
+      if (!h2d[i] || !d2h[i]) fail(errc::invalid_argument, "overlap: unit has no copy streams");
+      parts[i] = schedule_row_parts(schedule.devices[i], d);
+      for (std::size_t p = 0; p < parts[i].size(); ++p) {
+        in_ev[i].push_back(pool.make(unit[i]->spec().device));
+        cp_ev[i].push_back(pool.make(unit[i]->spec().device));
+      }
+    }
+  // One repeat of an overlapped link unit: host->device (B, then A part by
+  // part), per-part compute, per-part device->host; `prev_in`/`prev_out` are
+  // the previous busy link unit in schedule order (shared-bus order).
+  const auto enqueue_overlapped = [&](std::size_t i, std::size_t rr, std::size_t prev_in,
+                                      std::size_t prev_out) {
+    const ScheduledDevice& sd = schedule.devices[i];
+    Unit* u = unit[i];
+    PhaseEvents& e = ev[rr][i];
+    cudaStream_t cs = u->stream(), hs = h2d[i], ds = d2h[i];
+    const bool tensor = u->spec().kind == DeviceKind::xpu;
+    const bool link16 = tensor && host16_link(u);
+    const bool convert = tensor && !link16;
+    const std::int64_t r = sd.rows, r0 = row0[i];
+    const std::size_t esz = link16 ? 2 : 4;
+    const std::int64_t lda_l = link16 ? round_up(d.k, 8) : d.k;
+    const std::int64_t ldb_l = link16 ? round_up(d.n, 8) : d.n;
+    char* a_l = static_cast<char*>(u->scratch(link16 ? 2 : 0).ensure(static_cast<std::size_t>(r * lda_l) * esz));
+    char* b_l = static_cast<char*>(u->scratch(link16 ? 3 : 1).ensure(static_cast<std::size_t>(d.k * ldb_l) * esz));
+    float* c = static_cast<float*>(u->scratch(4).ensure(static_cast<std::size_t>(r * d.n) * 4));
+
+    // host -> device
+    cuda_check(cudaStreamWaitEvent(hs, t0[u->spec().device][rr], 0), "wait t0");
+    if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(hs, ev[rr][prev_in].ci1, 0), "wait");
+    cuda_check(cudaEventRecord(e.ci0, hs), "cudaEventRecord");
+    if (link16)
+      copy2d(b_l, ldb_l, io.b16_host, io.ldb16_host, d.k, d.n, 2, cudaMemcpyHostToDevice, hs);
+    else
+      copy2d(b_l, ldb_l, io.b_host, io.ldb_host, d.k, d.n, 4, cudaMemcpyHostToDevice, hs);
+    std::int64_t off = 0;
+    for (std::size_t p = 0; p < parts[i].size(); ++p) {
+      const std::int64_t rp = parts[i][p];
+      if (link16)
+        copy2d(a_l + off * lda_l * 2, lda_l,
+               static_cast<const char*>(io.a16_host) + (r0 + off) * io.lda16_host * 2, io.lda16_host,
+               rp, d.k, 2, cudaMemcpyHostToDevice, hs);
+      else
+        copy2d(a_l + off * lda_l * 4, lda_l, io.a_host + (r0 + off) * io.lda_host, io.lda_host, rp,
+               d.k, 4, cudaMemcpyHostToDevice, hs);
+      cuda_check(cudaEventRecord(in_ev[i][p], hs), "cudaEventRecord");
+      off += rp;
+    }
+    cuda_check(cudaEventRecord(e.ci1, hs), "cudaEventRecord");
+
+    // compute, part by part as the A parts land
+    const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
+    char* a16 = convert ? static_cast<char*>(u->scratch(2).ensure(static_cast<std::size_t>(r * lda16) * 2)) : nullptr;
+    const void* bk = b_l;
+    std::int64_t ldbk = ldb_l;
+    off = 0;
+    for (std::size_t p = 0; p < parts[i].size(); ++p) {
+      const std::int64_t rp = parts[i][p];
+      cuda_check(cudaStreamWaitEvent(cs, in_ev[i][p], 0), "wait A part");
+      if (p == 0) {
+        cuda_check(cudaEventRecord(e.cp0, cs), "cudaEventRecord");
+        if (convert) {  // fp32 B crossed the link: one conversion, after it landed
+          void* b16 = u->scratch(3).ensure(static_cast<std::size_t>(d.k * ldb16) * 2);
+          cuda_check(poas_b200::convert_f32(u->spec().dtype, reinterpret_cast<const float*>(b_l), ldb_l,
+                                            b16, ldb16, d.k, d.n, cs),
+                     "convert B");
+          bk = b16;
+          ldbk = ldb16;
+        }
+      }
+      const void* ap = a_l + off * lda_l * static_cast<std::int64_t>(esz);
+      std::int64_t ldak = lda_l;
+      if (convert) {
+        cuda_check(poas_b200::convert_f32(u->spec().dtype, reinterpret_cast<const float*>(ap), lda_l,
+                                          a16 + off * lda16 * 2, lda16, rp, d.k, cs),
+                   "convert A");
+        ap = a16 + off * lda16 * 2;
+        ldak = lda16;
+      }
+      u->gemm(rp, d.n, d.k, ap, ldak, bk, ldbk, c + off * d.n, d.n, false, extra_sms[i]);
+      cuda_check(cudaEventRecord(cp_ev[i][p], cs), "cudaEventRecord");
+      off += rp;
+    }
+    cuda_check(cudaEventRecord(e.cp1, cs), "cudaEventRecord");
+
+    // device -> host, part by part as they are computed
+    if (bus_ && prev_out != nd) cuda_check(cudaStreamWaitEvent(ds, ev[rr][prev_out].co1, 0), "wait");
+    off = 0;
+    for (std::size_t p = 0; p < parts[i].size(); ++p) {
+      const std::int64_t rp = parts[i][p];
+      cuda_check(cudaStreamWaitEvent(ds, cp_ev[i][p], 0), "wait part");
+      if (p == 0) cuda_check(cudaEventRecord(e.co0, ds), "cudaEventRecord");
+      copy2d(io.c_host + (r0 + off) * io.ldc_host, io.ldc_host, c + off * d.n, d.n, rp, d.n, 4,
+             cudaMemcpyDeviceToHost, ds);
+      off += rp;
+    }
+    cuda_check(cudaEventRecord(e.co1, ds), "cudaEventRecord");
+  };
+
   // Resident runs have no copy phases: only compute is bracketed by events.
   const auto last_event = [&](std::size_t rep, std::size_t i) {
     return io.resident ? ev[rep][i].cp1 : ev[rep][i].co1;
@@ -306,6 +472,8 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       if (unit[i]->on_gpu()) {
         DeviceGuard g(unit[i]->spec().device);
         cuda_check(cudaStreamSynchronize(unit[i]->stream()), "cudaStreamSynchronize");
+        for (cudaStream_t x : {h2d[i], d2h[i]})
+          if (x) cuda_check(cudaStreamSynchronize(x), "cudaStreamSynchronize");
       }
   };
   std::chrono::steady_clock::time_point first_open;
@@ -327,7 +495,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       cudaStream_t hs = unit[h]->stream();
       if (rep > 0 && !host_sync_repeats)  // chain after the other units' previous repeat
         for (std::size_t j = 0; j < nd; ++j)
-          if (j != h && unit[j]->on_gpu() && schedule.devices[j].rows > 0 &&
+          if ((j != h || overlapped) && unit[j]->on_gpu() && schedule.devices[j].rows > 0 &&
               unit[j]->spec().device == dev)
             cuda_check(cudaStreamWaitEvent(hs, last_event(rr - 1, j), 0), "cudaStreamWaitEvent");
       cuda_check(poas_b200::gate_wait(gates.device_flag(rep), hs), "gate_wait");
@@ -345,6 +513,11 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       Unit* u = unit[i];
       if (!u->on_gpu() || sd.rows == 0) continue;
       DeviceGuard g(u->spec().device);
+      if (overlapped) {  // copy-in, compute and copy-out of this unit
+        enqueue_overlapped(i, rr, prev_in, prev_in);
+        prev_in = i;
+        continue;
+      }
       cudaStream_t s = u->stream();
       const bool tensor = u->spec().kind == DeviceKind::xpu;
       const std::int64_t r = sd.rows, r0 = row0[i];
@@ -450,7 +623,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       if (!u->on_gpu() || sd.rows == 0) continue;
       DeviceGuard g(u->spec().device);
       cudaStream_t s = u->stream();
-      if (!io.resident) {
+      if (!io.resident && !overlapped) {
         if (bus_) {
           if (prev_out == nd) {
             if (last_in != nd && last_in != i)

@@ -88,10 +88,12 @@ UnitSpec parse_unit_spec(const std::string& text) {
   return u;
 }
 
-std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus, bool* lend) {
+std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus, bool* lend,
+                                      bool* overlap) {
   std::vector<UnitSpec> out;
   if (bus) *bus = true;
   if (lend) *lend = true;
+  if (overlap) *overlap = false;
   for (const std::string& item : split(text, ';')) {
     if (item.rfind("bus=", 0) == 0) {
       if (bus) *bus = item.substr(4) != "0" && item.substr(4) != "false";
@@ -99,6 +101,10 @@ std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus, bool* 
     }
     if (item.rfind("lend=", 0) == 0) {
       if (lend) *lend = item.substr(5) != "0" && item.substr(5) != "false";
+      continue;
+    }
+    if (item.rfind("overlap=", 0) == 0) {
+      if (overlap) *overlap = item.substr(8) != "0" && item.substr(8) != "false";
       continue;
     }
     out.push_back(parse_unit_spec(item));

@@ -47,12 +47,13 @@ struct UnitSpec {
 
 // "<id>=<kind>[:key=value]*"
 UnitSpec parse_unit_spec(const std::string& text);
-// ';'-separated unit specs, optionally with a "bus=0|1" token.
 // ';'-separated unit specs plus optional machine tokens: "bus=0|1" (shared
-// link, default 1) and "lend=0|1" (idle units lend their SMs to the one busy
-// unit on the same GPU during execute, default 1).
+// link, default 1), "lend=0|1" (idle units lend their SMs to the one busy
+// unit on the same GPU during execute, default 1) and "overlap=0|1" (host
+// operand runs pipeline each link unit's row parts: copies overlap compute,
+// see poas/overlap.hpp; default 0 = the paper's synchronous copies).
 std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus = nullptr,
-                                      bool* lend = nullptr);
+                                      bool* lend = nullptr, bool* overlap = nullptr);
 
 // Device scratch that grows on demand and is reused across calls.
 class DeviceBuffer {

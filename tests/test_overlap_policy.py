@@ -1,0 +1,208 @@
+"""The "overlap" planner policy (B200 extension; paper PAPER.md:486-489:
+"could be improved using CUDA streams and overlapping the computation with
+memory copies ... the performance predictor can be adapted to predict the
+memory copies with or without overlap").
+
+The C++ planner's overlapped timeline is checked against an independent
+restatement here (`overlap_timeline`), on hand-computed and random machines;
+the row parts, the subset/part choice, the schedule interchange format and
+the untouched reference policy are checked too.
+"""
+import json
+import random
+
+import pytest
+
+from conftest import GOLDEN
+from test_planner_parity import random_dims, random_profile
+
+REL = 1e-9
+
+
+def parse_profile(text):
+    devs, cur, bus = [], None, True
+    for line in text.splitlines():
+        p = line.split()
+        if len(p) != 2:
+            continue
+        if p[0] == "bus":
+            bus = p[1] == "true"
+        elif p[0] == "device":
+            cur = {"id": p[1]}
+            devs.append(cur)
+        elif cur is not None:
+            cur[p[0]] = p[1]
+    for d in devs:
+        for key in ("slope", "intercept", "bandwidth"):
+            d[key] = float(d[key])
+        d["elem_size"] = int(d["elem_size"])
+        d["priority"] = int(d["priority"])
+    return devs, bus
+
+
+def row_parts(rows, parts):
+    """poas::overlap_row_parts: 128-row blocks spread evenly, tail last."""
+    if rows <= 0:
+        return []
+    blocks = rows // 128
+    if blocks == 0:
+        return [rows]
+    q = max(1, min(parts, blocks))
+    out = [(blocks // q + (1 if p < blocks % q else 0)) * 128 for p in range(q)]
+    out[-1] += rows % 128
+    return out
+
+
+def overlap_timeline(devs, bus, rows_parts, m, n, k):
+    """Restatement of poas::evaluate_overlap_timeline over a schedule's row
+    parts: B then the A parts on the host->device queue, part p computes
+    after its A part and part p-1, its C (fp32) leaves after that and after
+    the previous copy-out on the device->host queue; queues shared in
+    priority order when `bus`. Returns ({id: (copy_in, compute, copy_out)}, makespan)."""
+    h2d = d2h = 0.0
+    out, makespan = {}, 0.0
+    for d in sorted(devs, key=lambda x: x["priority"]):
+        parts = rows_parts[d["id"]]
+        slope, icpt = d["slope"], d["intercept"]
+        if d["kind"] == "cpu":
+            c = sum(slope * r * n * k + icpt for r in parts)
+            out[d["id"]] = ((0.0, 0.0), (0.0, c), (c, c))
+            makespan = max(makespan, c)
+            continue
+        if not parts:
+            at = h2d if bus else 0.0
+            out[d["id"]] = ((at, at), (at, at), (at, at))
+            continue
+        bw, e = d["bandwidth"], d["elem_size"]
+        t_in = h2d if bus else 0.0
+        free_out = d2h if bus else 0.0
+        start_in = t_in
+        t_in += e * k * n / bw
+        c_end = t_in
+        c_start = o_start = None
+        for r in parts:
+            t_in += e * r * k / bw
+            cs = max(t_in, c_end)
+            c_end = cs + slope * r * n * k + icpt
+            os_ = max(c_end, free_out)
+            free_out = os_ + 4.0 * r * n / bw
+            if c_start is None:
+                c_start, o_start = cs, os_
+        out[d["id"]] = ((start_in, t_in), (c_start, c_end), (o_start, free_out))
+        if bus:
+            h2d, d2h = t_in, free_out
+        makespan = max(makespan, free_out)
+    return out, makespan
+
+
+def check_against_restatement(poas, prof, m, n, k):
+    s = json.loads(poas.plan_policy(prof, m, n, k, "overlap"))
+    devs, bus = parse_profile(prof)
+    parts = {}
+    for d in s["devices"]:
+        dev = next(x for x in devs if x["id"] == d["id"])
+        if dev["kind"] == "cpu":
+            parts[d["id"]] = [d["rows"]] if d["rows"] else []
+        else:
+            # link units: full-K row parts as produced by overlap_row_parts
+            assert all(t["k"] == k and t["n"] == n for t in d["tiles"])
+            rp = [t["m"] for t in d["tiles"]]
+            assert sum(rp) == d["rows"]
+            assert rp == row_parts(d["rows"], len(rp)) or (d["rows"] == 0 and rp == [])
+            parts[d["id"]] = rp
+    tl, makespan = overlap_timeline(devs, bus, parts, m, n, k)
+    assert s["makespan"] == pytest.approx(makespan, rel=REL, abs=2e-9)
+    for d in s["devices"]:
+        want = tl[d["id"]]
+        for key, iv in zip(("copy_in", "compute", "copy_out"), want):
+            # schedule times are %.9f (reference proj/src/scheduler.cpp:96-100)
+            assert d[key][0] == pytest.approx(iv[0], abs=1e-9), (d["id"], key)
+            assert d[key][1] == pytest.approx(iv[1], abs=1e-9), (d["id"], key)
+    return s
+
+
+def test_row_parts():
+    assert row_parts(16384, 64) == [256] * 64
+    assert row_parts(1000, 4) == [256, 256, 256, 232]
+    assert row_parts(100, 8) == [100]
+    assert row_parts(300, 8) == [128, 172]
+
+
+def test_overlap_b200_e2e_profile(poas):
+    """The e2e machine of the r1i box (bf16 link for the tensor unit): the
+    overlapped plan keeps the tensor unit alone, cuts it into row parts and
+    predicts B + the C stream instead of copy-in + compute + copy-out."""
+    prof = (GOLDEN / "profiles" / "b200_e2e_r1i.profile").read_text()
+    m = n = k = 16384
+    seq = json.loads(poas.plan_policy(prof, m, n, k, "best-subset"))
+    s = check_against_restatement(poas, prof, m, n, k)
+    rows = {d["id"]: d["rows"] for d in s["devices"]}
+    assert rows == {"gpu0.tc": 16384, "cpu0": 0, "gpu0.simt": 0}
+    tc = next(d for d in s["devices"] if d["id"] == "gpu0.tc")
+    assert len(tc["tiles"]) >= 16
+    # copies overlap compute: C leaves while A is still arriving
+    assert tc["copy_out"][0] < tc["copy_in"][1]
+    # lower bound: B in, then all of C out (fp32) at the link bandwidth
+    devs, _ = parse_profile(prof)
+    bw = next(d for d in devs if d["id"] == "gpu0.tc")["bandwidth"]
+    floor = (2 * k * n + 4 * m * n) / bw
+    assert floor < s["makespan"] < 1.05 * floor
+    # the synchronous plan charges the 2-byte unit's C at 2 bytes (reference
+    # transfer_bytes), yet overlap still predicts less
+    assert s["makespan"] < seq["makespan"]
+    assert poas.schedule_roundtrip(json.dumps(s)) == poas.plan_policy(prof, m, n, k, "overlap")
+
+
+def test_overlap_hand_computed(poas):
+    """One link unit, exact numbers: bw 1e9 B/s, e=4, slope 1e-12, no
+    intercept; 1024x512x256 -> B 0.524288 ms, each 256-row A part 0.262144 ms,
+    compute 33.554 us, C part 0.524288 ms."""
+    prof = "\n".join([
+        "poas-profile v1", "", "bus true", "",
+        "device g", "kind gpu", "slope 1e-12", "intercept 0", "bandwidth 1000000000",
+        "elem_size 4", "priority 0", "ops_min 1", "ops_max 1000000000000", ""])
+    m, n, k = 1024, 512, 256
+    s = check_against_restatement(poas, prof, m, n, k)
+    g = s["devices"][0]
+    parts = [t["m"] for t in g["tiles"]]
+    b = 4 * k * n / 1e9
+    a = [4 * r * k / 1e9 for r in parts]
+    c = [1e-12 * r * n * k for r in parts]
+    o = [4 * r * n / 1e9 for r in parts]
+    # hand-rolled pipeline recurrence, independent of both implementations
+    t_in, c_end, o_end = b, b, 0.0
+    for ai, ci, oi in zip(a, c, o):
+        t_in += ai
+        c_end = max(t_in, c_end) + ci
+        o_end = max(c_end, o_end) + oi
+    assert s["makespan"] == pytest.approx(o_end, abs=2e-9)
+    # sequential model for comparison: everything back to back
+    seq = b + sum(a) + sum(c) + 4 * m * n / 1e9
+    assert s["makespan"] < seq
+
+
+def test_overlap_random_machines(poas):
+    rng = random.Random(7)
+    checked = 0
+    for _ in range(120):
+        nd = rng.randint(1, 4)
+        prof = random_profile(rng, nd, with_cpu=rng.random() < 0.5, bus=rng.random() < 0.7)
+        m, n, k = random_dims(rng)
+        try:
+            ref = json.loads(poas.plan_policy(prof, m, n, k, "best-subset"))
+        except Exception:
+            continue
+        s = check_against_restatement(poas, prof, m, n, k)
+        assert sum(d["rows"] for d in s["devices"]) == m
+        assert s["machine_hash"] == ref["machine_hash"]
+        checked += 1
+    assert checked > 60
+
+
+def test_reference_policy_unchanged_by_overlap(poas, ref):
+    prof = (GOLDEN / "profiles" / "b200_like.profile").read_text()
+    assert poas.plan_policy(prof, 16384, 16384, 16384, "reference") == ref.plan(prof, 16384, 16384, 16384)
+    from paper_2209_10245_b200 import PoasError
+
+    with pytest.raises(PoasError):
+        poas.plan_policy(prof, 16384, 16384, 16384, "no-such-policy")
