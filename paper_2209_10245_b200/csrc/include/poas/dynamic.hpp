@@ -10,7 +10,9 @@
 // linear model (slope and intercept) by g = 1 + alpha (r - 1): clock and
 // power-cap drift stretch every probe by the same factor, so the fitted shape
 // is kept and only its scale follows the evidence (EWMA with weight alpha).
-// Link bandwidth is divided by the same update of the copy-phase ratio. A
+// Link bandwidth is divided by the same update of the copy-phase ratio
+// (overlapped runs, poas/overlap.hpp: by the finish ratio of a link-bound
+// unit, see refit_profile). A
 // bus unit whose copy phases were predicted but measured as zero ran on
 // resident operands: its kernel streams them while computing, so its
 // measured compute stands for all three phases and only the compute model

@@ -34,6 +34,7 @@ struct DeviceOutcome {
   PhaseError copy_in, compute, copy_out;
   PhaseError copy;
   PhaseError finish;
+  bool overlapped = false;  // its copies ran pipelined with compute (overlap=1)
 };
 
 struct SimulationResult {

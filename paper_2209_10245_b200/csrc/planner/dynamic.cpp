@@ -68,6 +68,11 @@ SimulationResult parse_execution_report(const std::string& report_json) {
     o.copy_in = phase(d, "copy_in");
     o.compute = phase(d, "compute");
     o.copy_out = phase(d, "copy_out");
+    if (d.get("finish")) o.finish = phase(d, "finish");
+    if (const json::Value* ov = d.get("overlapped")) {
+      if (ov->type != json::Value::Type::boolean) bad_report("\"overlapped\" is not a boolean");
+      o.overlapped = ov->b;
+    }
     r.devices.push_back(std::move(o));
   }
   return r;
@@ -90,6 +95,24 @@ MachineProfile refit_profile(const MachineProfile& prior, const std::vector<Devi
     const bool fused = d->uses_bus() && pred_link > 0.0 && o.copy_in.measured == 0.0 &&
                        o.copy_out.measured == 0.0;
     double g = 1.0;
+    if (o.overlapped && d->uses_bus() && d->bandwidth > 0.0) {
+      // Overlapped copies (poas/overlap.hpp): the phases are overlapping
+      // spans, each paced by the others, and the link's two directions
+      // contend while both are busy (measured: PCIe H2D 55 GB/s alone, ~45
+      // GB/s beside a D2H stream). One factor moves the bound the plan
+      // predicted: a link-bound unit's finish is B plus its busiest copy
+      // stream, so its finish ratio rescales the link bandwidth; a
+      // compute-bound unit's compute span is its back-to-back part GEMMs.
+      const bool link_bound =
+          std::max(o.copy_in.predicted, o.copy_out.predicted) >= o.compute.predicted;
+      if (link_bound) {
+        if (update_factor(o.finish, options, &g)) d->bandwidth /= g;
+      } else if (update_factor(o.compute, options, &g)) {
+        d->compute.slope *= g;
+        d->compute.intercept *= g;
+      }
+      continue;
+    }
     if (fused) {
       // Operands resident where the unit computes: the modelled link phases
       // happen inside the kernel (it streams its operands while computing),

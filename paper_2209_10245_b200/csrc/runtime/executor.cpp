@@ -742,6 +742,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     o.copy = {(sum_in[i] + sum_out[i]) * inv,
               sd.timeline.copy_in.duration() + sd.timeline.copy_out.duration(), 0.0};
     o.finish = {sum_fin[i] * inv, link ? sd.timeline.copy_out.end : sd.timeline.compute.end, 0.0};
+    o.overlapped = overlapped && link && sd.rows > 0;
     for (PhaseError* p : {&o.copy_in, &o.compute, &o.copy_out, &o.copy, &o.finish})
       p->error_pct = rel_err_pct(p->measured, p->predicted);
     if (sd.rows > 0) {
@@ -797,7 +798,7 @@ std::string format_execution_report(const Schedule& s, const SimulationResult& r
          ",\n     \"copy_in\": " + phase_json(d.copy_in) + ",\n     \"compute\": " +
          phase_json(d.compute) + ",\n     \"copy_out\": " + phase_json(d.copy_out) +
          ",\n     \"copy\": " + phase_json(d.copy) + ",\n     \"finish\": " +
-         phase_json(d.finish) + "}";
+         phase_json(d.finish) + (d.overlapped ? ",\n     \"overlapped\": true" : "") + "}";
     o += i + 1 < r.devices.size() ? ",\n" : "\n";
   }
   o += "  ],\n";

@@ -334,15 +334,16 @@ def test_execute_host_bf16_operands_elem2(torch_cuda, poas):
         ex.execute(sched_text, bad, 1)
 
 
-def _plant(profile, unit, factor):
-    """Scale one unit's compute model (a hand-made machine for the planner)."""
-    lines, cur = [], None
+def _set_models(profile, slope):
+    """Every unit gets the same compute model (a hand-made machine for the
+    planner: compute-bound and symmetric, so it splits the rows)."""
+    lines = []
     for line in profile.splitlines():
         parts = line.split()
-        if len(parts) == 2 and parts[0] == "device":
-            cur = parts[1]
-        if cur == unit and len(parts) == 2 and parts[0] in ("slope", "intercept"):
-            line = f"{parts[0]} {float(parts[1]) * factor!r}"
+        if len(parts) == 2 and parts[0] == "slope":
+            line = f"slope {slope!r}"
+        elif len(parts) == 2 and parts[0] == "intercept":
+            line = "intercept 0"
         lines.append(line)
     return "\n".join(lines) + "\n"
 
@@ -359,12 +360,13 @@ def test_overlapped_host_execution(torch_cuda, poas):
     units = UNITS.replace("elem=2:link=hbm", "elem=4:link=pcie").replace("elem=4:link=hbm", "elem=4:link=pcie")
     m, n, k = 3000, 2048, 1024
     profile = poas.profile_machine(units, PROF, True)
-    # make the CUDA-core unit look fast enough to keep rows, so both paths run
-    planted = _plant(profile, "gpu0.simt", 0.02)
+    # a machine on which both units keep rows, so both paths run
+    planted = _set_models(profile, 2e-13)
     sched_text = poas.plan_policy(planted, m, n, k, "overlap")
     sched = json.loads(sched_text)
     rows = {d["id"]: d["rows"] for d in sched["devices"]}
     assert rows["gpu0.tc"] > 0 and rows["gpu0.simt"] > 0, rows
+    assert all(len(x["tiles"]) > 1 for x in sched["devices"]), sched["devices"]
     d = operands(torch, poas, m, n, k)
     ex = poas.Executor(units + ";overlap=1")
     rep = ex.execute(sched_text, d["io_host"], 3)

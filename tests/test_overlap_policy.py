@@ -206,3 +206,46 @@ def test_reference_policy_unchanged_by_overlap(poas, ref):
 
     with pytest.raises(PoasError):
         poas.plan_policy(prof, 16384, 16384, 16384, "no-such-policy")
+
+
+def _overlap_report(s, finish_scale, compute_scale=1.0):
+    devs = []
+    for d in s["devices"]:
+        ci = d["copy_in"][1] - d["copy_in"][0]
+        cc = d["compute"][1] - d["compute"][0]
+        co = d["copy_out"][1] - d["copy_out"][0]
+        fin = d["copy_out"][1]
+
+        def ph(pred, f):
+            return {"measured": pred * f, "predicted": pred, "error_pct": 0.0}
+
+        devs.append({"id": d["id"], "rows": d["rows"], "copy_in": ph(ci, 1.0), "compute": ph(cc, compute_scale),
+                     "copy_out": ph(co, 1.0), "finish": ph(fin, finish_scale), "overlapped": d["rows"] > 0})
+    return {"measured_makespan": s["makespan"] * finish_scale, "predicted_makespan": s["makespan"],
+            "makespan_error_pct": 0.0, "devices": devs}
+
+
+def test_refit_of_overlapped_runs(poas):
+    """Dynamic re-fit of an overlapped run (csrc/planner/dynamic.cpp): a
+    link-bound unit's finish ratio rescales its link bandwidth (the copy
+    spans overlap and the directions contend, so their sum is no measure);
+    its compute model is left alone. Re-planned, the prediction follows."""
+    prof = (GOLDEN / "profiles" / "b200_e2e_r1i.profile").read_text()
+    m = n = k = 16384
+    s = json.loads(poas.plan_policy(prof, m, n, k, "overlap"))
+    rep = _overlap_report(s, finish_scale=1.08, compute_scale=1.3)
+    out = poas.refit_profile(prof, rep, 1.0)
+    before, _ = parse_profile(prof)
+    after, _ = parse_profile(out)
+    b = {d["id"]: d for d in before}
+    a = {d["id"]: d for d in after}
+    assert a["gpu0.tc"]["bandwidth"] == pytest.approx(b["gpu0.tc"]["bandwidth"] / 1.08, rel=1e-12)
+    assert a["gpu0.tc"]["slope"] == b["gpu0.tc"]["slope"]
+    s2 = json.loads(poas.plan_policy(out, m, n, k, "overlap"))
+    assert s2["makespan"] == pytest.approx(s["makespan"] * 1.08, rel=0.01)
+    # without the flag the same numbers are a synchronous run: compute moves
+    for d in rep["devices"]:
+        d.pop("overlapped")
+    out2 = poas.refit_profile(prof, rep, 1.0)
+    a2 = {d["id"]: d for d in parse_profile(out2)[0]}
+    assert a2["gpu0.tc"]["slope"] == pytest.approx(b["gpu0.tc"]["slope"] * 1.3, rel=1e-12)
