@@ -287,10 +287,17 @@ def main():
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
-    local = env_int("LOCAL_RANK", 0)
+    # One process per GPU. POAS_DIST_BACKEND=gloo (with ranks sharing GPUs,
+    # LOCAL_RANK modulo the visible devices) exercises the multi-rank path on
+    # a one-GPU box; the measured configuration is NCCL, one GPU per rank.
+    backend = os.environ.get("POAS_DIST_BACKEND", "nccl")
+    local = env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     n = k = args.n
     m = args.n  # rows per rank (weak scaling)
@@ -432,6 +439,35 @@ def main():
     flops_step_total = 2.0 * m * world * n * k
     value = flops_step_total / (ms_step * 1e-3) / 1e12
     clocks = clk.summary()
+
+    # ---- check C (every rank, full size): the size-independent property
+    # C.x = A_u.(B_u.x) in fp64, with A_u/B_u the operands each unit consumed
+    # (bf16 for the tensor unit's rows, fp32 for the CUDA-core unit's); B is
+    # panel-major [P][K][N/P]. Outside the timed region.
+    def verify_c():
+        x = torch.randn(n, dtype=torch.float64, device=dev, generator=torch.Generator(dev).manual_seed(7))
+        xs = x.view(P, np_)
+        y = C.double() @ x
+        y_ref = torch.empty_like(y)
+        r0 = 0
+        for d_ in sched["devices"]:
+            r = d_["rows"]
+            if r == 0:
+                continue
+            Bu, Au = (B16, A16) if d_["id"] == tc_id else (B32, A32)
+            bx = sum(Bu[p].double() @ xs[p] for p in range(P))
+            y_ref[r0:r0 + r] = Au[r0:r0 + r].double() @ bx
+            r0 += r
+        err = float((y - y_ref).norm() / y_ref.norm())
+        t = torch.tensor([err], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    c_check = verify_c()
+    C_TOL = 2e-5  # the relative Frobenius bound of the parity tests
+    if not c_check <= C_TOL:
+        raise SystemExit(f"C check failed: rel err {c_check:.3e} > {C_TOL}")
 
     # per-unit measured vs predicted (mean over the timed reports)
     def unit_mean(key, field="measured"):
@@ -671,6 +707,9 @@ def main():
                 "cublas_bf16_fp32out_tflops": round(2.0 * m * n * k / (cublas_ms * 1e-3) / 1e12, 2)
                 if cublas_ms else None,
                 "sm_count": sms_all, "profile_seconds": round(t_prof, 2),
+                "c_check": {"property": "C.x = A.(B.x), fp64, each unit's own operand precision, every rank",
+                            "max_rel_err": float(f"{c_check:.3e}"), "tol": C_TOL},
+                "dist_backend": backend if world > 1 else None,
             },
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst,
                          "unit": "TFLOP/s", "frac": round(achieved / peak_burst, 4),
