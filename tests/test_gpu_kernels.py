@@ -169,10 +169,15 @@ def test_full_size_tc_property(torch_cuda, poas):
     poas.tc_gemm(2, n, n, n, a.data_ptr(), n, b.data_ptr(), n, c.data_ptr(), n)
     torch.cuda.synchronize()
     x = torch.randn(n, 4, device="cuda", dtype=torch.float64)
-    lhs = c.double() @ x
     rhs = a.double() @ (b.double() @ x)
-    rel = ((lhs - rhs).norm() / rhs.norm()).item()
-    assert rel <= TOL, rel
+    rel = ((c.double() @ x - rhs).norm() / rhs.norm()).item()
+    # fp32 accumulation over K = 16384 on the tensor pipe: the stated bound
+    # grows with K; cuBLAS on the same inputs for scale
+    tol = max(TOL, n * 2.0 ** -28)
+    assert rel <= tol, rel
+    ref = torch.mm(a, b, out_dtype=torch.float32)
+    rel_cublas = ((ref.double() @ x - rhs).norm() / rhs.norm()).item()
+    assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])

@@ -23,7 +23,7 @@ def test_two_ranks_one_gpu_bench(tmp_path):
     env = dict(os.environ, POAS_DIST_BACKEND="gloo", OMP_NUM_THREADS="2")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29531", str(ROOT / "bench.py"), "--gpus", "2",
-           "--n", "2048", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e-cpu",
+           "--size=2048", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e-cpu",
            "--save", str(tmp_path / "out")]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-4000:]
