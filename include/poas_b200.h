@@ -65,10 +65,14 @@ const char* poas_b200_version(void);
 int poas_b200_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
                    char** schedule_json);
 
-/* poas_b200_plan with a planner policy: "reference" (== poas_b200_plan) or
+/* poas_b200_plan with a planner policy: "reference" (== poas_b200_plan),
  * "best-subset" -- an opt-in B200 extension that also plans every subset of
  * units and keeps the smallest predicted makespan (the reference LP charges
- * every unit the full B transfer; proj/src/optimizer.cpp:21-32,257-275). */
+ * every unit the full B transfer; proj/src/optimizer.cpp:21-32,257-275) --
+ * or "overlap": best-subset with each link unit's rows cut into row parts
+ * whose copies overlap compute (full-duplex link), predicted by the
+ * pipelined timeline of poas/overlap.hpp; run it with an "overlap=1"
+ * executor (the paper's "memory copies with overlap"). */
 int poas_b200_plan_policy(const char* profile_text, int64_t m, int64_t n, int64_t k,
                           const char* policy, char** schedule_json);
 
@@ -203,7 +207,10 @@ typedef struct {
 /* One executor per process per machine description (same unit specs as
  * the profile that produced the schedule; "bus=0|1" token for the link
  * topology, default shared; "lend=0|1": when a schedule leaves all but one
- * unit of a GPU idle, the busy unit runs on their SMs too, default 1). */
+ * unit of a GPU idle, the busy unit runs on their SMs too, default 1;
+ * "overlap=0|1": host-operand runs pipeline every link unit's row parts --
+ * the schedule's tiles -- on separate H2D / compute / D2H streams, default 0
+ * = the paper's synchronous copy-in, compute, copy-out). */
 int poas_b200_executor_create(const char* units, poas_executor_t* out);
 void poas_b200_executor_destroy(poas_executor_t ex);
 /* machine_identity_hash over the executor's units (device_model.hpp:130). */
