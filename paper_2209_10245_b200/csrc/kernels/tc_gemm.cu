@@ -55,6 +55,7 @@ struct TcArgs {
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
   int wave_sync;         // 1: static order + per-wave barrier on tile_counter[0]
+  int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
 };
 
 // ---------------------------------------------------------- tile scheduler
@@ -62,7 +63,9 @@ struct TcArgs {
 // sequence and hands each tile id to the other roles through a small smem
 // ring (tile_full / tile_empty mbarriers; -1 ends the sequence).
 //
-// Dynamic mode: tiles are claimed with one global atomicAdd per tile, so the
+// Dynamic mode: a worker's first tile is its own index (no claim on the
+// critical path of the first loads); later tiles are claimed with one global
+// atomicAdd per tile (counter + number of workers), so the
 // tiles in flight are always a contiguous window of the raster order however
 // far individual CTAs drift (launch stagger, far-die L2 latency, co-running
 // kernels taking SMs). With a static round-robin a lagging CTA works on a
@@ -71,7 +74,7 @@ struct TcArgs {
 constexpr int kTileSlots = 4;
 
 __device__ __forceinline__ int claim_tile(const TcArgs& a, int& next_static, int step) {
-  if (a.tile_counter && !a.wave_sync) return atomicAdd(a.tile_counter, 1);
+  if (a.tile_counter && !a.wave_sync) return atomicAdd(a.tile_counter, 1) + step;
   const int t = next_static;
   next_static += step;
   return t;
@@ -187,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t tphase = 0;
       int wave = 0, wave_target = 0;
       bool wave_on = args.wave_sync != 0;
-      int t = claim_tile(args, next_static, gridDim.x);
+      // first tile = blockIdx.x without a claim; claims continue after the grid
+      int t = next_static;
+      next_static += gridDim.x;
       while (true) {
         const int tt = t < total ? t : -1;
         mbar_wait(&tile_empty[slot], tphase ^ 1);
@@ -356,18 +361,23 @@ constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
 constexpr int k2StageBytes = k2ABytes + k2BBytes;
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
-constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + 256;
+// Epilogue staging (TMA-store path): per epilogue warp one 32 x 32 fp32 box,
+// 128-byte swizzled rows (4 KB, 1024-aligned).
+constexpr int k2StagingBytes = 4 * 32 * 32 * 4;
+constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + k2StagingBytes + 256;
 
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* s_a = smem;
   uint8_t* s_b = smem + k2Stages * k2ABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * k2StageBytes);
+  uint8_t* s_c = smem + k2Stages * k2StageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_c + k2StagingBytes);
   uint64_t* empty = full + k2Stages;
   uint64_t* acc_full = empty + k2Stages;
   uint64_t* acc_empty = acc_full + 2;
@@ -384,6 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    if (args.tma_store) tma_prefetch_desc(&map_c);
     for (int s = 0; s < k2Stages; ++s) {
       mbar_init(&full[s], 1);   // leader: its expect_tx arrive + both CTAs' bytes
       mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both
@@ -420,7 +431,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // peer's producer follows its own ring.
       int wave = 0, wave_target = 0;
       bool wave_on = args.wave_sync != 0;
-      int t = leader ? claim_tile(args, next_static, step) : 0;
+      // The first tile of every worker is its cluster id (no claim on the
+      // critical path of the first loads); dynamic claims start after them.
+      int t = 0;
+      if (leader) {
+        t = first;
+        next_static = first + step;
+      }
       while (true) {
         if (leader) {
           t = t < total ? t : -1;
@@ -527,7 +544,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * 256 + static_cast<int>(rank) * 128 + quad * 32 + lane;
+      const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
+      if (args.tma_store) {
+        // TMEM -> registers -> this warp's 32 x 32 staging box (128-byte
+        // swizzled rows: conflict-free, the TMA's layout) -> one TMA store
+        // (or f32 add-reduction) per box: full-line writes, and the threads
+        // never wait on global memory. The accumulator is released as soon
+        // as its last columns are in registers.
+        uint8_t* box = s_c + quad * 4096;
+        uint8_t* my_row = box + lane * 128;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                 static_cast<uint32_t>(acc * kBN + c * 32),
+                             v);
+          tmem_wait_ld();
+          if (c == kBN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
+          }
+          if (lane == 0) bulk_wait_read<0>();  // the previous box has left smem
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int col0 = nb * kBN + c * 32;
+            if (args.accumulate)
+              tma_reduce_add_2d(&map_c, box, col0, row_base);
+            else
+              tma_store_2d(&map_c, box, col0, row_base);
+            bulk_commit();
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
+      const int row = row_base + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
 #pragma unroll 1
       for (int c = 0; c < kBN / 32; ++c) {
@@ -573,6 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (args.tma_store && lane == 0) bulk_wait_all();  // C written before the CTA retires
   }
 
   tc_fence_before();
@@ -620,6 +680,20 @@ bool make_map(CUtensorMap* map, AbType t, const void* base, int64_t rows, int64_
          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// 2-D map over a row-major fp32 [rows x cols] C with leading dim `ld`
+// (elements): 32 x 32 boxes, 128-byte swizzle (the epilogue staging layout).
+bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -741,6 +815,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   // dynamic|wave|static overrides.
   const std::string sched = tc_gemm_scheduler_name(M, N, K);
   args.tile_counter = nullptr;
+  args.tma_store = 0;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
     args.tile_counter = next_tile_counter();
@@ -749,6 +824,15 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
 
   if (!force_1cta && budget >= 2) {
     // CTA pairs: 256 x 256 tiles, grid = even SM budget (one pair per TPC).
+    // Epilogue through TMA stores when C allows a tensor map (16-byte
+    // aligned base and row pitch); POAS_TC_EPILOGUE=direct forces the
+    // register -> global path.
+    CUtensorMap mc;
+    const char* epi = std::getenv("POAS_TC_EPILOGUE");
+    const bool direct = epi && std::string(epi) == "direct";
+    args.tma_store = !direct && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 &&
+                     make_map_c(&mc, C, M, N, ldc);
+    if (!args.tma_store) mc = ma;  // unused
     args.tiles_m = static_cast<int>((M + 255) / 256);
     args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
     args.idesc = idesc_f16(t == AbType::bf16, 256, kBN, false, true);
@@ -756,7 +840,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
     const int tiles = args.tiles_m * args.tiles_n;
     int pairs = budget / 2;
     if (pairs > tiles) pairs = tiles;
-    tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, args);
+    tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, mc, args);
     return cudaGetLastError();
   }
   args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);

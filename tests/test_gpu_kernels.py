@@ -180,18 +180,24 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
+@pytest.mark.parametrize("epilogue", ["tma", "direct"])
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
 @pytest.mark.parametrize("variant", ["1cta", "2cta"])
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
-def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched):
+def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched, epilogue):
     """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) under
-    both tile schedulers agree with the oracle, including partial pair tiles
-    and odd SM budgets."""
+    every tile scheduler and both pair-kernel epilogues (TMA store; direct
+    register stores) agree with the oracle, including partial pair tiles,
+    odd SM budgets and a C pitch TMA cannot map (n = 777)."""
     import oracle
 
+    if variant == "1cta" and epilogue == "direct":
+        pytest.skip("the single-SM kernel has one epilogue")
     torch = torch_cuda
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
     monkeypatch.setenv("POAS_TC_SCHED", sched)
+    if epilogue == "direct":
+        monkeypatch.setenv("POAS_TC_EPILOGUE", "direct")
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 31), oracle.fill_uniform(k, n, 32)
     ldb = (n + 7) // 8 * 8
@@ -204,6 +210,37 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
         poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), ldb, c.data_ptr(), n, num_ctas=ctas)
         torch.cuda.synchronize()
         assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, (variant, ctas)
+
+
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_tc_epilogue_pitch_and_alignment(torch_cuda, poas, accumulate):
+    """C inside a wider buffer: a padded pitch (TMA-store epilogue, tails
+    clipped: the padding is never written) and a 4-byte-offset base (no
+    tensor map: direct stores); both plain and accumulating (TMA f32 add
+    reduction)."""
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = 700, 600, 320
+    A, B = oracle.fill_uniform(m, k, 41), oracle.fill_uniform(k, n, 42)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    for pad, off in ((8, 0), (5, 1)):
+        big = torch.full((m, n + pad), float("nan") if not accumulate else 0.0, device="cuda")
+        if accumulate:
+            big[:, off:off + n] = 1.0
+        c = big[:, off:off + n]
+        poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n + pad,
+                     accumulate=accumulate)
+        torch.cuda.synchronize()
+        got = c.cpu().numpy() - (1.0 if accumulate else 0.0)
+        assert oracle.rel_frobenius(got, ref) <= TOL, (pad, off)
+        rest = torch.cat([big[:, :off], big[:, off + n:]], dim=1).cpu().numpy()
+        if accumulate:
+            assert (rest == 0.0).all()
+        else:
+            assert np.isnan(rest).all()
 
 
 def test_tc_tile_counter_reuse_and_concurrency(torch_cuda, poas):
