@@ -16,10 +16,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.hpp"
 #include "sm100_ptx.cuh"
@@ -56,7 +58,19 @@ struct TcArgs {
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
   int wave_sync;         // 1: static order + per-wave barrier on tile_counter[0]
   int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
+  unsigned long long* trace;  // dev: per-CTA %globaltimer stamps (POAS_TC_TRACE), or null
 };
+
+// Dev instrumentation (POAS_TC_TRACE=1): per CTA, 8 %globaltimer stamps.
+//   0 entry  1 prologue done  2 first TMA issued  3 first stage full (MMA)
+//   4 last MMA commit  5 epilogue sees its first accumulator  6 last box
+//   issued  7 exit
+__device__ __forceinline__ void trace_stamp(const TcArgs& a, int idx) {
+  if (!a.trace) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (a.trace[blockIdx.x * 8 + idx] == 0) a.trace[blockIdx.x * 8 + idx] = t;
+}
 
 // ---------------------------------------------------------- tile scheduler
 // The producer thread (of the CTA, or of the pair's leader) owns the tile
@@ -390,6 +404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  if (threadIdx.x == 0) trace_stamp(args, 0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -414,6 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace_stamp(args, 1);
 
   const int total = args.tiles_m * args.tiles_n;
   const int k_blocks = (args.K + kBK - 1) / kBK;
@@ -472,6 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                            args.hint_b);
           tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
                            col0 + 64, kb * kBK, args.hint_b);
+          trace_stamp(args, 2);
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
@@ -504,6 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          trace_stamp(args, 3);
           const uint32_t a0 = smem_addr(s_a + stage * k2ABytes);
           const uint32_t b0 = smem_addr(s_b + stage * k2BBytes);
 #pragma unroll
@@ -519,6 +537,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit_pair(&acc_full[acc], 0x3);
+        if (args.trace) {  // the last commit of this worker overwrites
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          args.trace[blockIdx.x * 8 + 4] = tt;
+        }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -544,6 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
+      if (quad == 0 && lane == 0) trace_stamp(args, 5);
       const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
       if (args.tma_store) {
         // TMEM -> registers -> this warp's 32 x 32 staging box (128-byte
@@ -581,6 +605,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_store_2d(&map_c, box, col0, row_base);
             bulk_commit();
           }
+        }
+        if (args.trace && quad == 0 && lane == 0) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          args.trace[blockIdx.x * 8 + 6] = tt;
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -642,6 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, kTmemCols);
   }
+  if (threadIdx.x == 0) trace_stamp(args, 7);
 }
 
 // ------------------------------------------------------------------ host side
@@ -694,6 +724,32 @@ bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// POAS_TC_TRACE: synchronise, read the stamps back, print per-event
+// percentiles (us after the earliest entry) to stderr.
+void print_trace(unsigned long long* dev, int ctas, cudaStream_t stream, int64_t M, int64_t N,
+                 int64_t K) {
+  std::vector<unsigned long long> h(static_cast<size_t>(ctas) * 8);
+  cudaStreamSynchronize(stream);
+  cudaMemcpy(h.data(), dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < ctas; ++c)
+    if (h[c * 8]) t0 = std::min(t0, h[c * 8]);
+  static const char* names[8] = {"entry", "prologue", "first_tma", "first_full",
+                                 "last_commit", "epi_acc", "epi_issued", "exit"};
+  std::fprintf(stderr, "tc_trace M=%lld N=%lld K=%lld ctas=%d:", static_cast<long long>(M),
+               static_cast<long long>(N), static_cast<long long>(K), ctas);
+  for (int e = 0; e < 8; ++e) {
+    std::vector<double> v;
+    for (int c = 0; c < ctas; ++c)
+      if (h[c * 8 + e]) v.push_back((h[c * 8 + e] - t0) * 1e-3);
+    std::sort(v.begin(), v.end());
+    if (v.empty()) continue;
+    std::fprintf(stderr, " %s[min %.2f med %.2f max %.2f n %zu]", names[e], v.front(),
+                 v[v.size() / 2], v.back(), v.size());
+  }
+  std::fprintf(stderr, "\n");
 }
 
 }  // namespace
@@ -816,6 +872,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   const std::string sched = tc_gemm_scheduler_name(M, N, K);
   args.tile_counter = nullptr;
   args.tma_store = 0;
+  args.trace = nullptr;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
     args.tile_counter = next_tile_counter();
@@ -840,7 +897,16 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
     const int tiles = args.tiles_m * args.tiles_n;
     int pairs = budget / 2;
     if (pairs > tiles) pairs = tiles;
+    static unsigned long long* trace_buf = nullptr;
+    const bool trace = std::getenv("POAS_TC_TRACE") != nullptr;
+    if (trace) {
+      if (!trace_buf && cudaMalloc(&trace_buf, 4096 * 8 * sizeof(unsigned long long)) != cudaSuccess)
+        return cudaErrorMemoryAllocation;
+      cudaMemsetAsync(trace_buf, 0, 2 * pairs * 8 * sizeof(unsigned long long), stream);
+      args.trace = trace_buf;
+    }
     tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, mc, args);
+    if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return cudaGetLastError();
   }
   args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
