@@ -65,11 +65,13 @@ struct TcArgs {
 //   0 entry  1 prologue done  2 first TMA issued  3 first stage full (MMA)
 //   4 last MMA commit  5 epilogue sees its first accumulator  6 last box
 //   issued  7 exit
+// Write-only (no global read on the traced thread's path); callers stamp
+// each event once.
 __device__ __forceinline__ void trace_stamp(const TcArgs& a, int idx) {
   if (!a.trace) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  if (a.trace[blockIdx.x * 8 + idx] == 0) a.trace[blockIdx.x * 8 + idx] = t;
+  a.trace[blockIdx.x * 8 + idx] = t;
 }
 
 // ---------------------------------------------------------- tile scheduler
@@ -375,8 +377,8 @@ constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
 constexpr int k2StageBytes = k2ABytes + k2BBytes;
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
-// Epilogue staging (TMA-store path): per epilogue warp one 32 x 32 fp32 box,
-// 128-byte swizzled rows (4 KB, 1024-aligned).
+// Epilogue staging (TMA-store path): per epilogue warp two 32-row x 16-column
+// fp32 boxes, 64-byte swizzled rows (2 x 2 KB).
 constexpr int k2StagingBytes = 4 * 32 * 32 * 4;
 constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + k2StagingBytes + 256;
 
@@ -474,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (t < 0) break;
         if (leader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
         ++wave;
-        const int t_next = leader ? claim_tile(args, next_static, step) : 0;
+        int t_next = 0;  // claimed once this tile's first loads are out
         int mb, nb;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
@@ -488,7 +490,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                            args.hint_b);
           tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
                            col0 + 64, kb * kBK, args.hint_b);
-          trace_stamp(args, 2);
+          if (wave == 1 && kb == 0) trace_stamp(args, 2);
+          if (kb == 0 && leader) t_next = claim_tile(args, next_static, step);  // behind the first loads
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
@@ -506,6 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       int slot = 0;
       uint32_t tphase = 0;
+      bool traced = false;
       while (true) {
         mbar_wait_cluster(&tile_full[slot], tphase);
         const int t = tile_ring[slot];
@@ -521,7 +525,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          trace_stamp(args, 3);
+          if (!traced) {
+            trace_stamp(args, 3);
+            traced = true;
+          }
           const uint32_t a0 = smem_addr(s_a + stage * k2ABytes);
           const uint32_t b0 = smem_addr(s_b + stage * k2BBytes);
 #pragma unroll
@@ -553,6 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     int slot = 0;
     uint32_t tphase = 0;
+    bool epi_traced = false;
     while (true) {
       mbar_wait_cluster(&tile_full[slot], tphase);
       const int t = tile_ring[slot];
@@ -567,38 +575,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      if (quad == 0 && lane == 0) trace_stamp(args, 5);
+      if (quad == 0 && lane == 0 && !epi_traced) {
+        trace_stamp(args, 5);
+        epi_traced = true;
+      }
       const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
       if (args.tma_store) {
-        // TMEM -> registers -> this warp's 32 x 32 staging box (128-byte
-        // swizzled rows: conflict-free, the TMA's layout) -> one TMA store
-        // (or f32 add-reduction) per box: full-line writes, and the threads
-        // never wait on global memory. The accumulator is released as soon
-        // as its last columns are in registers.
-        uint8_t* box = s_c + quad * 4096;
-        uint8_t* my_row = box + lane * 128;
+        // TMEM -> registers -> a 32-row x 16-column staging box of this
+        // warp (64-byte swizzled rows: conflict-free, the TMA's layout) ->
+        // one TMA store (or f32 add-reduction) per box: full-line writes,
+        // the threads never wait on global memory. Two boxes per warp, so a
+        // box's store drains while the next one fills. The accumulator is
+        // released as soon as its last columns are in registers.
+        uint8_t* boxes = s_c + quad * 4096;
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                                 static_cast<uint32_t>(acc * kBN + c * 32),
+        for (int c = 0; c < kBN / 16; ++c) {
+          uint32_t v[16];
+          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                 static_cast<uint32_t>(acc * kBN + c * 16),
                              v);
           tmem_wait_ld();
-          if (c == kBN / 32 - 1) {
+          if (c == kBN / 16 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
           }
-          if (lane == 0) bulk_wait_read<0>();  // the previous box has left smem
+          uint8_t* box = boxes + (c & 1) * 2048;
+          if (lane == 0) bulk_wait_read<1>();  // the store two boxes back has left smem
           __syncwarp();
+          uint8_t* my_row = box + lane * 64;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(my_row + ((j ^ ((lane >> 1) & 3)) << 4)) =
                 make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int col0 = nb * kBN + c * 32;
+            const int col0 = nb * kBN + c * 16;
             if (args.accumulate)
               tma_reduce_add_2d(&map_c, box, col0, row_base);
             else
@@ -713,16 +726,17 @@ bool make_map(CUtensorMap* map, AbType t, const void* base, int64_t rows, int64_
 }
 
 // 2-D map over a row-major fp32 [rows x cols] C with leading dim `ld`
-// (elements): 32 x 32 boxes, 128-byte swizzle (the epilogue staging layout).
+// (elements): 16-column x 32-row boxes, 64-byte swizzle (the epilogue
+// staging layout).
 bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t box[2] = {16, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
