@@ -61,17 +61,18 @@ struct TcArgs {
   unsigned long long* trace;  // dev: per-CTA %globaltimer stamps (POAS_TC_TRACE), or null
 };
 
-// Dev instrumentation (POAS_TC_TRACE=1): per CTA, 8 %globaltimer stamps.
+// Dev instrumentation (POAS_TC_TRACE=1): per CTA, 16 %globaltimer slots.
 //   0 entry  1 prologue done  2 first TMA issued  3 first stage full (MMA)
 //   4 last MMA commit  5 epilogue sees its first accumulator  6 last box
-//   issued  7 exit
+//   issued  7 exit  8 producer: first tile published  9 producer: first
+//   empty-slot wait passed
 // Write-only (no global read on the traced thread's path); callers stamp
 // each event once.
 __device__ __forceinline__ void trace_stamp(const TcArgs& a, int idx) {
   if (!a.trace) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  a.trace[blockIdx.x * 8 + idx] = t;
+  a.trace[blockIdx.x * 16 + idx] = t;
 }
 
 // ---------------------------------------------------------- tile scheduler
@@ -469,6 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           t = tile_ring[slot];
           mbar_arrive_cluster(&tile_empty[slot], 0);
         }
+        if (wave == 0) trace_stamp(args, 8);
         if (++slot == kTileSlots) {
           slot = 0;
           tphase ^= 1;
@@ -483,6 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int col0 = nb * 256 + static_cast<int>(rank) * 128;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (wave == 1 && kb == 0) trace_stamp(args, 9);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
           tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kb * kBK, row0,
                            args.hint_a);
@@ -547,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (args.trace) {  // the last commit of this worker overwrites
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-          args.trace[blockIdx.x * 8 + 4] = tt;
+          args.trace[blockIdx.x * 16 + 4] = tt;
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -585,21 +588,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // warp (64-byte swizzled rows: conflict-free, the TMA's layout) ->
         // one TMA store (or f32 add-reduction) per box: full-line writes,
         // the threads never wait on global memory. Two boxes per warp, so a
-        // box's store drains while the next one fills. The accumulator is
+        // box's store drains while the next one fills; the TMEM load of the
+        // next 32 columns is in flight while the current ones are written
+        // (TMEM reads at 64 B/clk/SM are the floor). The accumulator is
         // released as soon as its last columns are in registers.
         uint8_t* boxes = s_c + quad * 4096;
-#pragma unroll 1
-        for (int c = 0; c < kBN / 16; ++c) {
-          uint32_t v[16];
-          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                                 static_cast<uint32_t>(acc * kBN + c * 16),
-                             v);
-          tmem_wait_ld();
-          if (c == kBN / 16 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
-          }
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                               static_cast<uint32_t>(acc * kBN);
+        auto put_box = [&](const uint32_t* w, int c) {  // 16 columns, box (c & 1)
           uint8_t* box = boxes + (c & 1) * 2048;
           if (lane == 0) bulk_wait_read<1>();  // the store two boxes back has left smem
           __syncwarp();
@@ -607,7 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(my_row + ((j ^ ((lane >> 1) & 3)) << 4)) =
-                make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -618,11 +614,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_store_2d(&map_c, box, col0, row_base);
             bulk_commit();
           }
+        };
+        uint32_t va[32], vb[32];
+        tmem_ld_32x32b_x32(taddr, va);
+        tmem_wait_ld();
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; c += 2) {
+          tmem_ld_32x32b_x32(taddr + (c + 1) * 32, vb);
+          put_box(va, 2 * c);
+          put_box(va + 16, 2 * c + 1);
+          tmem_wait_ld();
+          if (c + 2 < kBN / 32) {
+            tmem_ld_32x32b_x32(taddr + (c + 2) * 32, va);
+          } else {  // all 256 columns are in registers: free the accumulator
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
+          }
+          put_box(vb, 2 * c + 2);
+          put_box(vb + 16, 2 * c + 3);
+          tmem_wait_ld();
         }
         if (args.trace && quad == 0 && lane == 0) {
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-          args.trace[blockIdx.x * 8 + 6] = tt;
+          args.trace[blockIdx.x * 16 + 6] = tt;
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -744,20 +760,20 @@ bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64
 // percentiles (us after the earliest entry) to stderr.
 void print_trace(unsigned long long* dev, int ctas, cudaStream_t stream, int64_t M, int64_t N,
                  int64_t K) {
-  std::vector<unsigned long long> h(static_cast<size_t>(ctas) * 8);
+  std::vector<unsigned long long> h(static_cast<size_t>(ctas) * 16);
   cudaStreamSynchronize(stream);
   cudaMemcpy(h.data(), dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull;
   for (int c = 0; c < ctas; ++c)
-    if (h[c * 8]) t0 = std::min(t0, h[c * 8]);
-  static const char* names[8] = {"entry", "prologue", "first_tma", "first_full",
-                                 "last_commit", "epi_acc", "epi_issued", "exit"};
+    if (h[c * 16]) t0 = std::min(t0, h[c * 16]);
+  static const char* names[10] = {"entry", "prologue", "first_tma", "first_full", "last_commit",
+                                  "epi_acc", "epi_issued", "exit", "published", "empty_ok"};
   std::fprintf(stderr, "tc_trace M=%lld N=%lld K=%lld ctas=%d:", static_cast<long long>(M),
                static_cast<long long>(N), static_cast<long long>(K), ctas);
-  for (int e = 0; e < 8; ++e) {
+  for (int e = 0; e < 10; ++e) {
     std::vector<double> v;
     for (int c = 0; c < ctas; ++c)
-      if (h[c * 8 + e]) v.push_back((h[c * 8 + e] - t0) * 1e-3);
+      if (h[c * 16 + e]) v.push_back((h[c * 16 + e] - t0) * 1e-3);
     std::sort(v.begin(), v.end());
     if (v.empty()) continue;
     std::fprintf(stderr, " %s[min %.2f med %.2f max %.2f n %zu]", names[e], v.front(),
@@ -914,9 +930,9 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
     static unsigned long long* trace_buf = nullptr;
     const bool trace = std::getenv("POAS_TC_TRACE") != nullptr;
     if (trace) {
-      if (!trace_buf && cudaMalloc(&trace_buf, 4096 * 8 * sizeof(unsigned long long)) != cudaSuccess)
+      if (!trace_buf && cudaMalloc(&trace_buf, 4096 * 16 * sizeof(unsigned long long)) != cudaSuccess)
         return cudaErrorMemoryAllocation;
-      cudaMemsetAsync(trace_buf, 0, 2 * pairs * 8 * sizeof(unsigned long long), stream);
+      cudaMemsetAsync(trace_buf, 0, 2 * pairs * 16 * sizeof(unsigned long long), stream);
       args.trace = trace_buf;
     }
     tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, mc, args);
