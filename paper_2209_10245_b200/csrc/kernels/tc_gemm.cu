@@ -59,6 +59,7 @@ struct TcArgs {
   int wave_sync;         // 1: static order + per-wave barrier on tile_counter[0]
   int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
   unsigned long long* trace;  // dev: per-CTA %globaltimer stamps (POAS_TC_TRACE), or null
+  int epi_skip;               // dev (POAS_TC_EPI_SKIP): TMA-store epilogue stages boxes, stores nothing
 };
 
 // Dev instrumentation (POAS_TC_TRACE=1): per CTA, 16 %globaltimer slots.
@@ -450,32 +451,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // peer's producer follows its own ring.
       int wave = 0, wave_target = 0;
       bool wave_on = args.wave_sync != 0;
-      // The first tile of every worker is its cluster id (no claim on the
-      // critical path of the first loads); dynamic claims start after them.
-      int t = 0;
-      if (leader) {
-        t = first;
-        next_static = first + step;
-      }
-      while (true) {
-        if (leader) {
-          t = t < total ? t : -1;
-          mbar_wait_cluster(&tile_empty[slot], tphase ^ 1);
-          tile_ring[slot] = t;
-          st_shared_cluster(&tile_ring[slot], 1, t);
-          mbar_arrive(&tile_full[slot]);
-          mbar_arrive_cluster(&tile_full[slot], 1);
-        } else {
-          mbar_wait_cluster(&tile_full[slot], tphase);
-          t = tile_ring[slot];
-          mbar_arrive_cluster(&tile_empty[slot], 0);
-        }
-        if (wave == 0) trace_stamp(args, 8);
-        if (++slot == kTileSlots) {
-          slot = 0;
-          tphase ^= 1;
-        }
-        if (t < 0) break;
+      // The first tile of every worker is its cluster id: every role starts
+      // on it without a claim or a ring round trip. The ring carries the
+      // later tiles; dynamic claims continue after the first wave.
+      int t = first < total ? first : -1;
+      next_static = first + step;
+      while (t >= 0) {
         if (leader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
         ++wave;
         int t_next = 0;  // claimed once this tile's first loads are out
@@ -500,7 +481,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        t = t_next;
+        // hand the next tile to both CTAs' roles (the leader publishes)
+        if (leader) {
+          t = t_next < total ? t_next : -1;
+          mbar_wait_cluster(&tile_empty[slot], tphase ^ 1);
+          tile_ring[slot] = t;
+          st_shared_cluster(&tile_ring[slot], 1, t);
+          mbar_arrive(&tile_full[slot]);
+          mbar_arrive_cluster(&tile_full[slot], 1);
+        } else {
+          mbar_wait_cluster(&tile_full[slot], tphase);
+          t = tile_ring[slot];
+          mbar_arrive_cluster(&tile_empty[slot], 0);
+        }
+        if (wave == 1) trace_stamp(args, 8);
+        if (++slot == kTileSlots) {
+          slot = 0;
+          tphase ^= 1;
+        }
       }
       if (leader) release_counter(args, step);
     }
@@ -513,15 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int slot = 0;
       uint32_t tphase = 0;
       bool traced = false;
-      while (true) {
-        mbar_wait_cluster(&tile_full[slot], tphase);
-        const int t = tile_ring[slot];
-        mbar_arrive(&tile_empty[slot]);
-        if (++slot == kTileSlots) {
-          slot = 0;
-          tphase ^= 1;
-        }
-        if (t < 0) break;
+      for (int t = first < total ? first : -1; t >= 0;) {
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
@@ -554,6 +544,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
+        mbar_wait_cluster(&tile_full[slot], tphase);  // the next tile
+        t = tile_ring[slot];
+        mbar_arrive(&tile_empty[slot]);
+        if (++slot == kTileSlots) {
+          slot = 0;
+          tphase ^= 1;
+        }
       }
     }
   } else {
@@ -564,16 +561,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int slot = 0;
     uint32_t tphase = 0;
     bool epi_traced = false;
-    while (true) {
+    auto next_tile = [&]() {
       mbar_wait_cluster(&tile_full[slot], tphase);
-      const int t = tile_ring[slot];
+      const int tn = tile_ring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tile_empty[slot], 0);  // the leader's barrier
       if (++slot == kTileSlots) {
         slot = 0;
         tphase ^= 1;
       }
-      if (t < 0) break;
+      return tn;
+    };
+    for (int t = first < total ? first : -1; t >= 0; t = next_tile()) {
       int mb, nb;
       tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
       mbar_wait(&acc_full[acc], acc_phase);
@@ -606,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !args.epi_skip) {
             const int col0 = nb * kBN + c * 16;
             if (args.accumulate)
               tma_reduce_add_2d(&map_c, box, col0, row_base);
@@ -642,7 +641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-        continue;
+        continue;  // (the for-increment fetches the next tile)
       }
       const int row = row_base + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
@@ -903,6 +902,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.tile_counter = nullptr;
   args.tma_store = 0;
   args.trace = nullptr;
+  args.epi_skip = std::getenv("POAS_TC_EPI_SKIP") != nullptr;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
     args.tile_counter = next_tile_counter();
