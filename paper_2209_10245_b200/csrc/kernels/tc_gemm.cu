@@ -379,8 +379,8 @@ constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
 constexpr int k2StageBytes = k2ABytes + k2BBytes;
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
-// Epilogue staging (TMA-store path): per epilogue warp one 32 x 32 fp32 box,
-// 128-byte swizzled rows (4 KB, 1024-aligned).
+// Epilogue staging (TMA-store path): per epilogue warp two 32-row x 16-column
+// fp32 boxes, 64-byte swizzled rows (2 x 2 KB).
 constexpr int k2StagingBytes = 4 * 32 * 32 * 4;
 constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + k2StagingBytes + 256;
 
@@ -583,29 +583,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
       if (args.tma_store) {
-        // TMEM -> registers -> this warp's 32 x 32 fp32 staging box
-        // (128-byte swizzled rows: conflict-free, the TMA's layout) -> one
-        // TMA store (or f32 add-reduction) per box: full-line writes, the
-        // threads never wait on global memory. The TMEM load of the next 32
-        // columns is in flight while the current box is written and its
-        // store drains (TMEM reads at 64 B/clk/SM are the floor; one proxy
-        // fence per 32 columns). The accumulator is released as soon as its
-        // last columns are in registers.
-        uint8_t* box = s_c + quad * 4096;
-        uint8_t* my_row = box + lane * 128;
+        // TMEM -> registers -> a 32-row x 16-column staging box of this
+        // warp (64-byte swizzled rows: conflict-free, the TMA's layout) ->
+        // one TMA store (or f32 add-reduction) per box: full-line writes,
+        // the threads never wait on global memory. Two boxes per warp, so a
+        // box's store drains while the next one fills; the TMEM load of the
+        // next 32 columns is in flight while the current ones are written
+        // (TMEM reads at 64 B/clk/SM are the floor). The accumulator is
+        // released as soon as its last columns are in registers.
+        uint8_t* boxes = s_c + quad * 4096;
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                static_cast<uint32_t>(acc * kBN);
-        auto put_box = [&](const uint32_t* w, int c) {  // columns c*32 .. c*32+31
-          if (lane == 0) bulk_wait_read<0>();  // the previous box has left smem
+        auto put_box = [&](const uint32_t* w, int c) {  // 16 columns, box (c & 1)
+          uint8_t* box = boxes + (c & 1) * 2048;
+          if (lane == 0) bulk_wait_read<1>();  // the store two boxes back has left smem
           __syncwarp();
+          uint8_t* my_row = box + lane * 64;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(my_row + ((j ^ ((lane >> 1) & 3)) << 4)) =
                 make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && !args.epi_skip) {
-            const int col0 = nb * kBN + c * 32;
+            const int col0 = nb * kBN + c * 16;
             if (args.accumulate)
               tma_reduce_add_2d(&map_c, box, col0, row_base);
             else
@@ -619,7 +620,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int c = 0; c < kBN / 32; c += 2) {
           tmem_ld_32x32b_x32(taddr + (c + 1) * 32, vb);
-          put_box(va, c);
+          put_box(va, 2 * c);
+          put_box(va + 16, 2 * c + 1);
           tmem_wait_ld();
           if (c + 2 < kBN / 32) {
             tmem_ld_32x32b_x32(taddr + (c + 2) * 32, va);
@@ -628,7 +630,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
           }
-          put_box(vb, c + 1);
+          put_box(vb, 2 * c + 2);
+          put_box(vb + 16, 2 * c + 3);
           tmem_wait_ld();
         }
         if (args.trace && quad == 0 && lane == 0) {
@@ -738,16 +741,17 @@ bool make_map(CUtensorMap* map, AbType t, const void* base, int64_t rows, int64_
 }
 
 // 2-D map over a row-major fp32 [rows x cols] C with leading dim `ld`
-// (elements): 32 x 32 boxes, 128-byte swizzle (the epilogue staging layout).
+// (elements): 16-column x 32-row boxes, 64-byte swizzle (the epilogue
+// staging layout).
 bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t box[2] = {16, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
