@@ -12,8 +12,10 @@ Per rank (one process per GPU, torchrun for N > 1; weak scaling):
   optimize/adapt/schedule   the reference-identical planner -> schedule JSON
   step       one co-executed GEMM of this rank's M=16384 rows x N=K=16384:
              every unit's share concurrently through the executor (C ABI);
-             at N > 1 rank 0's B (bf16 + fp32) is broadcast with NCCL inside
-             the step
+             at N > 1 rank 0's B (bf16; fp32 too if the CUDA-core unit has
+             rows) is broadcast with NCCL inside the step, in column panels;
+             the tensor unit consumes them in ONE launch whose producers wait
+             per panel on a device flag written after that panel landed
   value      whole-job TFLOP/s = 2*M_total*N*K / max-over-ranks device time
   e2e        the same GEMM through poas_b200_execute with HOST pinned buffers
              (bf16 A/B for the tensor unit, fp32 for the others, fp32 C):
@@ -43,6 +45,7 @@ sys.path.insert(0, str(ROOT))
 SEED = 20261017
 N_DEFAULT = 16384
 TC_SMS = 146
+TC_SMS_MULTI = 140  # N > 1: 6 SMs stay free for NCCL's broadcast kernels during the GEMM
 SIMT_SMS = 2
 PROFILING = "probes=9,repetitions=3,bandwidth_payload=268435456"
 
@@ -252,11 +255,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     # (--size: "--n" is ambiguous on a torchrun command line)
     ap.add_argument("--n", "--size", dest="n", type=int, default=N_DEFAULT)
-    ap.add_argument("--tc-sms", type=int, default=TC_SMS)
+    ap.add_argument("--tc-sms", type=int, default=None,
+                    help=f"tensor unit SM budget (default {TC_SMS}; {TC_SMS_MULTI} at N > 1)")
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-cpu", action="store_true", help="e2e without the host-CPU unit")
-    ap.add_argument("--b-panels", type=int, default=4,
+    ap.add_argument("--b-panels", type=int, default=8,
                     help="N > 1: B column panels broadcast separately (overlap with compute)")
     ap.add_argument("--policy", default="best-subset", choices=["reference", "best-subset"],
                     help="planner policy: the reference algorithm (byte-identical plans) or the "
@@ -300,6 +304,8 @@ def main():
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    if args.tc_sms is None:
+        args.tc_sms = TC_SMS if world == 1 else TC_SMS_MULTI
     n = k = args.n
     m = args.n  # rows per rank (weak scaling)
     save = Path(args.save) if args.save else None
@@ -361,9 +367,15 @@ def main():
     simt_busy = rows.get(simt_id, 0) > 0
     ready = [torch.cuda.Event() for _ in range(P)]
     comm_side = torch.cuda.Stream()
+    flags = torch.zeros(P, dtype=torch.int32, device=dev)  # per-panel readiness (tensor unit)
+    epoch = [0]
     if world > 1 and rank != 0:
         handles = (ctypes.c_void_p * P)()
         io.b_ready = ctypes.cast(handles, ctypes.POINTER(ctypes.c_void_p))
+        io.b_flags = flags.data_ptr()
+    elif world > 1:  # the root's B is local: every panel ready, still one launch
+        flags.fill_(1)
+        io.b_flags, io.b_epoch = flags.data_ptr(), 1
     # Level-1 (per-GPU) split of the whole job by the same planner: equal
     # shards of `m` rows for identical GPUs (weak scaling).
     l1_rows = shard.shard_rows(world, m * world, n, k, profile) if world > 1 else [m]
@@ -378,10 +390,14 @@ def main():
                 works.append([dist.broadcast(B16[p], src=0, async_op=True)] +
                              ([dist.broadcast(B32[p], src=0, async_op=True)] if simt_busy else []))
             if rank != 0:
+                epoch[0] += 1
+                io.b_epoch = epoch[0]
                 with torch.cuda.stream(comm_side):
                     for p in range(P):
                         for w in works[p]:
                             w.wait()
+                        # panel p landed: the tensor unit's kernel starts on it
+                        poas.signal_flag(flags[p:p + 1].data_ptr(), epoch[0], comm_side.cuda_stream)
                         ready[p].record(comm_side)
                 for p in range(P):
                     handles[p] = ready[p].cuda_event
@@ -675,9 +691,10 @@ def main():
             cpu_baseline = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                             "sample": f"unavailable: {exc}"}
 
-    # per step: one GEMM launch per busy unit and B panel, plus the
-    # executor's start-gate kernel on this GPU
-    launches_per_step = sum(P for d in sched["devices"] if d["rows"] > 0) + 1
+    # per step: one GEMM launch per busy unit (the tensor unit consumes all
+    # B panels in one launch; a CUDA-core unit launches once per panel),
+    # plus the executor's start-gate kernel on this GPU
+    launches_per_step = sum((1 if d["id"] == tc_id else P) for d in sched["devices"] if d["rows"] > 0) + 1
     if save and rank == 0:
         (save / "report_resident.json").write_text(json.dumps(rep_last, indent=1))
     if rank == 0:
@@ -719,6 +736,7 @@ def main():
                             "max_rel_err": float(f"{c_check:.3e}"), "tol": C_TOL,
                             "cublas_rel_err": float(f"{cublas_rel:.3e}") if cublas_rel is not None else None},
                 "dist_backend": backend if world > 1 else None,
+                "b_panels": P,
             },
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst,
                          "unit": "TFLOP/s", "frac": round(achieved / peak_burst, 4),

@@ -202,6 +202,15 @@ typedef struct {
   int64_t lda16_host;
   const void* b16_host;
   int64_t ldb16_host;
+  /* Optional (resident == 1, b_panels > 1): device readiness flags, one int
+   * per panel. A tensor unit then computes every panel in ONE launch whose
+   * producers start on panel p once b_flags[p] >= b_epoch (the deliverer
+   * writes the flags in panel order, e.g. poas_b200_signal_flag on its
+   * stream after each panel's broadcast) instead of one launch per panel
+   * behind b_ready[p]. n/b_panels must be a multiple of 256. Units without
+   * this path (CUDA cores) still wait on b_ready. */
+  const int* b_flags;
+  int b_epoch;
 } poas_gemm_io;
 
 /* One executor per process per machine description (same unit specs as
@@ -254,6 +263,15 @@ int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t 
 int poas_b200_tc_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
                       const void* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
                       int num_ctas, void* stream);
+/* poas_b200_tc_gemm over panel-major B (`panels` column panels, panel p a
+ * row-major [k x n/panels] block with row pitch ldb at b + p*k*ldb), one
+ * launch; with `flags`, tiles of panel p start once flags[p] >= epoch
+ * (10 s timeout, then the launch traps). n/panels % 256 == 0. */
+int poas_b200_tc_gemm_panels(int dtype, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                             const void* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
+                             int num_ctas, int panels, const int* flags, int epoch, void* stream);
+/* *flag = value on `stream`, in stream order (cuStreamWriteValue32). */
+int poas_b200_signal_flag(int* flag, int value, void* stream);
 /* Name of the kernel poas_b200_tc_gemm launches for this shape
  * ("tc_gemm_2cta_kernel" or "tc_gemm_kernel"; static string). */
 const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k);

@@ -74,6 +74,8 @@ struct GemmOperands {
   // Panel-major B with per-panel readiness events (see poas_gemm_io).
   int b_panels = 0;
   void* const* b_ready = nullptr;
+  const int* b_flags = nullptr;  // per-panel device flags: one fused tensor launch
+  int b_epoch = 0;
   // 16-bit host operands for elem=2 tensor units (see poas_gemm_io).
   const void* a16_host = nullptr;
   std::int64_t lda16_host = 0;

@@ -17,6 +17,26 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
                     const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                     int num_ctas, cudaStream_t stream);
 
+// Panel-major B for tc_gemm_panels: `panels` column panels, panel p =
+// B[:, p*N/P : (p+1)*N/P] stored as its own row-major [K x N/P] block (row
+// pitch ldb, panel stride K*ldb) -- the layout a per-panel broadcast lands.
+// N/P must be a multiple of 256 (the pair tile). With `flags`, the kernel's
+// producers start on panel p once flags[p] >= epoch: whoever delivers B
+// writes the flags in panel order (signal_flag after each panel's copy or
+// broadcast), so one launch consumes B as it arrives. A flag never written
+// traps the kernel after 10 s.
+struct TcPanels {
+  int panels = 1;
+  const int* flags = nullptr;
+  int epoch = 0;
+};
+cudaError_t tc_gemm_panels(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                           const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                           int num_ctas, const TcPanels& panels, cudaStream_t stream);
+
+// *flag = value in stream order (cuStreamWriteValue32).
+cudaError_t signal_flag(int* flag, int value, cudaStream_t stream);
+
 // The kernel tc_gemm launches: "tc_gemm_2cta_kernel" (CTA pairs,
 // cta_group::2); POAS_TC_KERNEL=1cta selects "tc_gemm_kernel" (single SM).
 const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t K);

@@ -60,7 +60,32 @@ struct TcArgs {
   int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
   unsigned long long* trace;  // dev: per-CTA %globaltimer stamps (POAS_TC_TRACE), or null
   int epi_skip;               // dev (POAS_TC_EPI_SKIP): TMA-store epilogue stages boxes, stores nothing
+  // Panel-major B (pair kernel): `panels` column panels of tiles_n_panel
+  // N-tiles each, B loaded through a 3-D map {column, k, panel}; tiles are
+  // ordered panel by panel. With panel_flags, a producer starts on panel p
+  // once panel_flags[p] >= panel_epoch (set in panel order by whoever
+  // delivers B, e.g. after each panel's broadcast).
+  int panels;
+  int tiles_n_panel;
+  const int* panel_flags;
+  int panel_epoch;
 };
+
+// Spin (acquire, with backoff) until *flag >= epoch; traps after 10 s so a
+// missing signal fails the launch instead of hanging the GPU.
+__device__ __forceinline__ void wait_panel_flag(const int* flag, int epoch) {
+  unsigned long long start, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  while (true) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= epoch) break;
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start > 10000000000ull) __trap();
+  }
+  fence_proxy_async_global();  // B's bytes (another kernel's writes) before our TMA reads
+}
 
 // Dev instrumentation (POAS_TC_TRACE=1): per CTA, 16 %globaltimer slots.
 //   0 entry  1 prologue done  2 first TMA issued  3 first stage full (MMA)
@@ -151,6 +176,22 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   const int r = t - g * per_group;
   mb = first_m + r % gm;
   nb = r / gm;
+}
+
+// Tile t of a (possibly panel-major) problem: M-tile mb, global N-tile nb,
+// its panel p and N-tile inside the panel nbl (grouped raster per panel).
+__device__ __forceinline__ void tile_coords_panel(const TcArgs& a, int t, int& mb, int& nb, int& p,
+                                                  int& nbl) {
+  if (a.panels > 1) {
+    const int per = a.tiles_m * a.tiles_n_panel;
+    p = t / per;
+    tile_coords(t - p * per, a.tiles_m, a.tiles_n_panel, a.group, mb, nbl, a.raster_n);
+    nb = p * a.tiles_n_panel + nbl;
+    return;
+  }
+  p = 0;
+  tile_coords(t, a.tiles_m, a.tiles_n, a.group, mb, nb, a.raster_n);
+  nbl = nb;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -456,24 +497,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // later tiles; dynamic claims continue after the first wave.
       int t = first < total ? first : -1;
       next_static = first + step;
+      int confirmed = -1;  // highest B panel seen ready
       while (t >= 0) {
         if (leader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
         ++wave;
         int t_next = 0;  // claimed once this tile's first loads are out
-        int mb, nb;
-        tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
+        int mb, nb, pnl, nbl;
+        tile_coords_panel(args, t, mb, nb, pnl, nbl);
+        if (args.panel_flags && pnl > confirmed) {  // flags are set in panel order
+          wait_panel_flag(args.panel_flags + pnl, args.panel_epoch);
+          confirmed = pnl;
+        }
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
-        const int col0 = nb * 256 + static_cast<int>(rank) * 128;
+        const int col0 = nbl * 256 + static_cast<int>(rank) * 128;  // inside the panel
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (wave == 1 && kb == 0) trace_stamp(args, 9);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
           tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kb * kBK, row0,
                            args.hint_a);
-          tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK,
-                           args.hint_b);
-          tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
-                           col0 + 64, kb * kBK, args.hint_b);
+          if (args.panels > 1) {
+            tma_load_3d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK, pnl,
+                             args.hint_b);
+            tma_load_3d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
+                             col0 + 64, kb * kBK, pnl, args.hint_b);
+          } else {
+            tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK,
+                             args.hint_b);
+            tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
+                             col0 + 64, kb * kBK, args.hint_b);
+          }
           if (wave == 1 && kb == 0) trace_stamp(args, 2);
           if (kb == 0 && leader) t_next = claim_tile(args, next_static, step);  // behind the first loads
           if (++stage == k2Stages) {
@@ -574,7 +627,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     };
     for (int t = first < total ? first : -1; t >= 0; t = next_tile()) {
       int mb, nb;
-      tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
+      int pnl_unused, nbl_unused;
+      tile_coords_panel(args, t, mb, nb, pnl_unused, nbl_unused);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (quad == 0 && lane == 0 && !epi_traced) {
@@ -740,6 +794,24 @@ bool make_map(CUtensorMap* map, AbType t, const void* base, int64_t rows, int64_
   return r == CUDA_SUCCESS;
 }
 
+// 3-D map over panel-major 16-bit B: P panels of [K x np] (row pitch ld
+// elements, panel stride K * ld), boxes of 64 columns x 64 k x 1 panel.
+bool make_map_panels(CUtensorMap* map, AbType t, const void* base, int64_t K, int64_t np,
+                     int64_t ld, int P) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(np), static_cast<cuuint64_t>(K),
+                              static_cast<cuuint64_t>(P)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2,
+                                 static_cast<cuuint64_t>(K) * static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kBK), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, t == AbType::bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+            3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2-D map over a row-major fp32 [rows x cols] C with leading dim `ld`
 // (elements): 16-column x 32-row boxes, 64-byte swizzle (the epilogue
 // staging layout).
@@ -835,25 +907,52 @@ const char* tc_gemm_scheduler_name(int64_t M, int64_t N, int64_t K) {
   return macs >= 17592186044416.0 ? "wave" : "dynamic";
 }
 
+namespace {
+cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                         const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                         int num_ctas, const TcPanels* ps, cudaStream_t stream);
+}
+
 cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                     int num_ctas, cudaStream_t stream) {
+  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, accumulate, num_ctas, nullptr, stream);
+}
+
+cudaError_t tc_gemm_panels(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                           const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                           int num_ctas, const TcPanels& panels, cudaStream_t stream) {
+  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, accumulate, num_ctas, &panels, stream);
+}
+
+namespace {
+cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                         const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
+                         int num_ctas, const TcPanels* ps, cudaStream_t stream) {
   if (t != AbType::bf16 && t != AbType::f16) return cudaErrorInvalidValue;
   if (M <= 0 || N <= 0) return cudaSuccess;
+  const int P = ps ? ps->panels : 1;
+  if (P < 1 || N % P != 0) return cudaErrorInvalidValue;
+  const int64_t np = N / P;  // columns per panel
+  if (P > 1 && np % 256 != 0) return cudaErrorInvalidValue;  // a pair tile never straddles panels
   if (K <= 0) {
     if (accumulate) return cudaSuccess;
     return cudaMemset2DAsync(C, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(N) * 4,
                              static_cast<size_t>(M), stream);
   }
-  // TMA: 16-byte aligned base and row pitch.
+  // TMA: 16-byte aligned base and row pitch (ldb: a panel's row pitch).
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
-      (lda * 2) % 16 || (ldb * 2) % 16 || lda < K || ldb < N || ldc < N)
+      (lda * 2) % 16 || (ldb * 2) % 16 || lda < K || ldb < np || ldc < N)
     return cudaErrorInvalidValue;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return cudaErrorInvalidValue;
 
   CUtensorMap ma, mb;
   if (!make_map(&ma, t, A, M, K, lda, kBK, kBM)) return cudaErrorInvalidValue;
-  if (!make_map(&mb, t, B, K, N, ldb, 64, kBK)) return cudaErrorInvalidValue;
+  if (P > 1) {
+    if (!make_map_panels(&mb, t, B, K, np, ldb, P)) return cudaErrorInvalidValue;
+  } else if (!make_map(&mb, t, B, K, N, ldb, 64, kBK)) {
+    return cudaErrorInvalidValue;
+  }
 
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -871,6 +970,7 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   // once its scheduler fits the size, profiles/r01_tile_scheduler).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const bool force_1cta = std::string(tc_gemm_kernel_name(M, N, K)) == "tc_gemm_kernel";
+  if (P > 1 && force_1cta) return cudaErrorNotSupported;  // panels: pair kernel only
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -902,6 +1002,10 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   args.tile_counter = nullptr;
   args.tma_store = 0;
   args.trace = nullptr;
+  args.panels = P;
+  args.tiles_n_panel = static_cast<int>(np / 256);
+  args.panel_flags = ps ? ps->flags : nullptr;
+  args.panel_epoch = ps ? ps->epoch : 0;
   args.epi_skip = std::getenv("POAS_TC_EPI_SKIP") != nullptr;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
@@ -948,6 +1052,27 @@ cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, in
   if (grid > tiles) grid = tiles;
   tc_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
   return cudaGetLastError();
+}
+}  // namespace
+
+// Writes `value` to a device int in `stream` order (cuStreamWriteValue32:
+// no kernel, no SM).
+cudaError_t signal_flag(int* flag, int value, cudaStream_t stream) {
+  using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WriteFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteFn>(p);
+  });
+  if (!fn) return cudaErrorNotSupported;
+  return fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag),
+            static_cast<cuuint32_t>(value), 0) == CUDA_SUCCESS
+             ? cudaSuccess
+             : cudaErrorUnknown;
 }
 
 }  // namespace poas_b200

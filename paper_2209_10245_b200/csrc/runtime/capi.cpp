@@ -135,6 +135,8 @@ poas::GemmOperands operands_of(const poas_gemm_io& io) {
   op.resident = io.resident != 0;
   op.b_panels = io.b_panels;
   op.b_ready = io.b_ready;
+  op.b_flags = io.b_flags;
+  op.b_epoch = io.b_epoch;
   op.a16_host = io.a16_host;
   op.lda16_host = io.lda16_host;
   op.b16_host = io.b16_host;

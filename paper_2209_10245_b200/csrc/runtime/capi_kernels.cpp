@@ -38,6 +38,33 @@ int poas_b200_tc_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
   });
 }
 
+int poas_b200_tc_gemm_panels(int dtype, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                             const void* b, int64_t ldb, float* c, int64_t ldc, int accumulate,
+                             int num_ctas, int panels, const int* flags, int epoch, void* stream) {
+  return poas_b200::capi::guard([&] {
+    if (dtype != POAS_DTYPE_F16 && dtype != POAS_DTYPE_BF16)
+      poas_b200::capi::raise(POAS_E_INVALID_ARGUMENT, "tc_gemm_panels: dtype must be f16 or bf16");
+    if (panels < 1 || n % panels != 0 || (panels > 1 && (n / panels) % 256 != 0))
+      poas_b200::capi::raise(POAS_E_INVALID_ARGUMENT,
+                             "tc_gemm_panels: n must split into panels of a multiple of 256 columns");
+    poas_b200::TcPanels ps;
+    ps.panels = panels;
+    ps.flags = flags;
+    ps.epoch = epoch;
+    poas_b200::capi::cuda_check(
+        poas_b200::tc_gemm_panels(ab_type(dtype), m, n, k, a, lda, b, ldb, c, ldc, accumulate != 0,
+                                  num_ctas, ps, static_cast<cudaStream_t>(stream)),
+        "tc_gemm_panels launch");
+  });
+}
+
+int poas_b200_signal_flag(int* flag, int value, void* stream) {
+  return poas_b200::capi::guard([&] {
+    poas_b200::capi::cuda_check(
+        poas_b200::signal_flag(flag, value, static_cast<cudaStream_t>(stream)), "signal_flag");
+  });
+}
+
 const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k) {
   return poas_b200::tc_gemm_kernel_name(m, n, k);
 }

@@ -272,7 +272,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
   // Not while B arrives through readiness events: the idle SMs are where
   // the collective's kernels run concurrently with the GEMM.
   std::vector<int> extra_sms(nd, 0);
-  if (lend_ && !io.b_ready) {
+  if (lend_ && !io.b_ready && !io.b_flags) {
     std::map<int, std::vector<std::size_t>> by_dev;
     for (std::size_t i = 0; i < nd; ++i)
       if (unit[i]->on_gpu()) by_dev[unit[i]->spec().device].push_back(i);
@@ -592,7 +592,15 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         lda = lda16;
         ldb = ldb16;
       }
-      if (panels > 1) {
+      if (panels > 1 && io.b_flags && tensor && !need_convert && (d.n / panels) % 256 == 0) {
+        // Panel-major B arriving panel by panel, consumed by ONE launch:
+        // the kernel's producers start on panel p once b_flags[p] reaches
+        // b_epoch (written in panel order by the deliverer), so compute on
+        // early panels overlaps the transfer of later ones without per-panel
+        // launches (no wave-quantisation tail per panel).
+        u->gemm_panels(r, d.n, d.k, a, lda, b, d.n / panels, c, ldc, panels, io.b_flags,
+                       io.b_epoch, extra_sms[i]);
+      } else if (panels > 1) {
         // Panel-major B arriving panel by panel: compute each column panel
         // as soon as it has landed (overlaps e.g. a chunked broadcast).
         const std::int64_t np = d.n / panels;

@@ -189,6 +189,20 @@ void Unit::gemm(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, s
   }
 }
 
+void Unit::gemm_panels(std::int64_t m, std::int64_t n, std::int64_t k, const void* a,
+                       std::int64_t lda, const void* b, std::int64_t ldb, float* c, std::int64_t ldc,
+                       int panels, const int* flags, int epoch, int extra_sms) {
+  if (spec_.kind != poas::DeviceKind::xpu)
+    poas::fail(poas::errc::invalid_argument, "gemm_panels: tensor units only");
+  const int sms = spec_.sms > 0 ? spec_.sms + extra_sms : 0;
+  TcPanels ps;
+  ps.panels = panels;
+  ps.flags = flags;
+  ps.epoch = epoch;
+  cuda_check(tc_gemm_panels(spec_.dtype, m, n, k, a, lda, b, ldb, c, ldc, false, sms, ps, stream_),
+             "tc_gemm_panels");
+}
+
 double Unit::time_gemm(std::int64_t side) {
   if (side < 1) poas::fail(poas::errc::invalid_argument, "time_gemm: side must be positive");
   if (!on_gpu()) {

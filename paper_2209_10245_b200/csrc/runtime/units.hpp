@@ -105,6 +105,12 @@ class Unit : public poas::DeviceBackend {
             const void* b, std::int64_t ldb, float* c, std::int64_t ldc, bool accumulate,
             int extra_sms = 0);
 
+  // xpu only: all `panels` column panels of panel-major B in one launch,
+  // panel p gated on flags[p] >= epoch (kernels.hpp TcPanels).
+  void gemm_panels(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, std::int64_t lda,
+                   const void* b, std::int64_t ldb, float* c, std::int64_t ldc, int panels,
+                   const int* flags, int epoch, int extra_sms = 0);
+
   // Scratch owned by the unit (staging for link copies in execute()).
   DeviceBuffer& scratch(int slot) { return scratch_[slot]; }
 

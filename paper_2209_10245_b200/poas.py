@@ -182,6 +182,7 @@ class GemmIO(C.Structure):
         ("b_panels", C.c_int), ("b_ready", C.POINTER(C.c_void_p)),
         ("a16_host", C.c_void_p), ("lda16_host", C.c_int64),
         ("b16_host", C.c_void_p), ("ldb16_host", C.c_int64),
+        ("b_flags", C.c_void_p), ("b_epoch", C.c_int),
     ]
 
 
@@ -230,6 +231,18 @@ class Executor:
 def tc_gemm(dtype: int, m, n, k, a, lda, b, ldb, c, ldc, accumulate=False, num_ctas=0, stream=None):
     check(lib.poas_b200_tc_gemm(dtype, m, n, k, a, lda, b, ldb, c, ldc, int(accumulate), num_ctas,
                                 stream))
+
+
+def tc_gemm_panels(dtype: int, m, n, k, a, lda, b, ldb, c, ldc, panels, flags=None, epoch=0,
+                   accumulate=False, num_ctas=0, stream=None):
+    """One launch over panel-major B; panel p gated on flags[p] >= epoch."""
+    check(lib.poas_b200_tc_gemm_panels(dtype, m, n, k, a, lda, b, ldb, c, ldc, int(accumulate),
+                                       num_ctas, panels, flags, epoch, stream))
+
+
+def signal_flag(flag_ptr: int, value: int, stream=None):
+    """*flag = value in `stream` order (cuStreamWriteValue32)."""
+    check(lib.poas_b200_signal_flag(flag_ptr, value, stream))
 
 
 def tc_kernel_name(m: int, n: int, k: int) -> str:

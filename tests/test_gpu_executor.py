@@ -412,3 +412,38 @@ def test_overlapped_parts_and_bf16_link(torch_cuda, poas):
     assert rep["measured_makespan"] < (tc["copy_in"]["measured"] + tc["compute"]["measured"]
                                        + tc["copy_out"]["measured"])
     assert abs(rep["makespan_error_pct"]) < 60.0, rep["makespan_error_pct"]
+
+
+def test_b_panels_with_flags_one_launch(torch_cuda, poas):
+    """Resident run with panel-major B and device readiness flags: the
+    tensor unit consumes all panels in one launch gated per panel; flags
+    delivered late on another stream; C exact."""
+    import oracle
+
+    torch = torch_cuda
+    units = "gpu0.tc=xpu:dev=0:sms=16:dtype=bf16:elem=2:link=hbm:probe=512-2048"
+    m, n, k, P = 1500, 1024, 384, 4
+    profile = poas.profile_machine(units, PROF, True)
+    sched_text = poas.plan(profile, m, n, k)
+    sched = json.loads(sched_text)
+    d = operands(torch, poas, m, n, k)
+    np_ = n // P
+    good = torch.stack([d["B16"][:, p * np_:(p + 1) * np_] for p in range(P)]).contiguous()
+    b16 = torch.full_like(good, float("nan"))
+    flags = torch.zeros(P, dtype=torch.int32, device="cuda")
+    C = torch.full((m, n), float("nan"), device="cuda")
+    io = poas.GemmIO(m=m, n=n, k=k, a16_dev=d["A16"].data_ptr(), lda16_dev=d["A16"].shape[1],
+                     b16_dev=b16.data_ptr(), ldb16_dev=np_, c_dev=C.data_ptr(), ldc_dev=n,
+                     resident=1, b_panels=P, b_flags=flags.data_ptr(), b_epoch=3)
+    ex = poas.Executor(units)
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(1_000_000)
+        for p in range(P):
+            b16[p].copy_(good[p])
+            poas.signal_flag(flags[p:p + 1].data_ptr(), 3, s.cuda_stream)
+    ex.execute(sched_text, io, 1)
+    torch.cuda.synchronize()
+    exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2})
+    assert oracle.rel_frobenius(C.cpu().numpy(), exp) <= TOL

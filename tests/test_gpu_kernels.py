@@ -290,3 +290,72 @@ def test_tc_wave_scheduler_survives_non_resident_workers(torch_cuda, poas, monke
         torch.cuda.synchronize()
         assert time.perf_counter() - t0 < 5.0
         assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, ctas
+
+
+def _panel_major(torch, B16, panels):
+    k, n = B16.shape
+    np_ = n // panels
+    return torch.stack([B16[:, p * np_:(p + 1) * np_] for p in range(panels)]).contiguous()
+
+
+@pytest.mark.parametrize("panels", [2, 4])
+@pytest.mark.parametrize("shape", [(1000, 1024, 320), (300, 2048, 136)])
+def test_tc_gemm_panels(torch_cuda, poas, shape, panels):
+    """One launch over panel-major B (the layout a per-panel broadcast
+    lands): tiles are ordered panel by panel and B is read through a 3-D
+    tensor map; with readiness flags already set and without flags."""
+    import oracle
+
+    torch = torch_cuda
+    m, n, k = shape
+    A, B = oracle.fill_uniform(m, k, 51), oracle.fill_uniform(k, n, 52)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    bp = _panel_major(torch, torch.from_numpy(B).cuda().bfloat16(), panels)
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    flags = torch.ones(panels, dtype=torch.int32, device="cuda")
+    for fl in (None, flags.data_ptr()):
+        for ctas in (0, 10):
+            c = torch.full((m, n), float("nan"), device="cuda")
+            poas.tc_gemm_panels(2, m, n, k, a.data_ptr(), k, bp.data_ptr(), n // panels, c.data_ptr(), n,
+                                panels, flags=fl, epoch=1, num_ctas=ctas)
+            torch.cuda.synchronize()
+            assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, (fl, ctas)
+    from paper_2209_10245_b200 import PoasError
+
+    with pytest.raises(PoasError):  # a panel narrower than a pair tile
+        poas.tc_gemm_panels(2, m, 768, k, a.data_ptr(), k, bp.data_ptr(), 256, c.data_ptr(), n, 3)
+
+
+def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
+    """The fused consumer: the GEMM is queued first with every flag clear;
+    another stream delivers the panels later (a ~spin, then one flag per
+    panel in order, each after the panel's bytes were written). The kernel
+    must not read a panel before its flag: B is garbage until delivered."""
+    import oracle
+
+    torch = torch_cuda
+    m, n, k, panels = 2048, 2048, 512, 4
+    A, B = oracle.fill_uniform(m, k, 61), oracle.fill_uniform(k, n, 62)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    good = _panel_major(torch, torch.from_numpy(B).cuda().bfloat16(), panels)
+    bp = torch.full_like(good, float("nan"))
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    flags = torch.zeros(panels, dtype=torch.int32, device="cuda")
+    c = torch.full((m, n), float("nan"), device="cuda")
+    s_gemm, s_deliver = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s_gemm):
+        e0.record()
+        poas.tc_gemm_panels(2, m, n, k, a.data_ptr(), k, bp.data_ptr(), n // panels, c.data_ptr(), n,
+                            panels, flags=flags.data_ptr(), epoch=7, num_ctas=64,
+                            stream=s_gemm.cuda_stream)
+        e1.record()
+    with torch.cuda.stream(s_deliver):
+        for p in range(panels):
+            torch.cuda._sleep(2_000_000)  # ~1 ms
+            bp[p].copy_(good[p])
+            poas.signal_flag(flags[p:p + 1].data_ptr(), 7, s_deliver.cuda_stream)
+    torch.cuda.synchronize()
+    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+    assert e0.elapsed_time(e1) > 2.0  # it waited for the deliveries
