@@ -323,7 +323,7 @@ def test_tc_gemm_panels(torch_cuda, poas, shape, panels):
     from paper_2209_10245_b200 import PoasError
 
     with pytest.raises(PoasError):  # a panel narrower than a pair tile
-        poas.tc_gemm_panels(2, m, 768, k, a.data_ptr(), k, bp.data_ptr(), 256, c.data_ptr(), n, 3)
+        poas.tc_gemm_panels(2, m, 768, k, a.data_ptr(), k, bp.data_ptr(), 384, c.data_ptr(), n, 2)
 
 
 def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
