@@ -343,6 +343,15 @@ def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
     flags = torch.zeros(panels, dtype=torch.int32, device="cuda")
     c = torch.full((m, n), float("nan"), device="cuda")
     s_gemm, s_deliver = torch.cuda.Stream(), torch.cuda.Stream()
+    # warm the delivery side first: a kernel's first launch may load its
+    # module lazily, which waits for the device -- and the device would be
+    # waiting (spinning) for this delivery
+    scratch = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(s_deliver):
+        torch.cuda._sleep(1)
+        bp[0].copy_(good[0])
+        bp[0].fill_(float("nan"))
+        poas.signal_flag(scratch.data_ptr(), 1, s_deliver.cuda_stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s_gemm):
