@@ -24,4 +24,9 @@ timeout 300 ncu --set full --clock-control none -k regex:simt_skinny -s 1 -c 1 \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-adapt --profile "$OUT/bench/profile_resident.txt" \
   > "$OUT/ncu_launch.log" 2>&1
+# the tensor kernel at the bench size, full set (roofline traffic, pipe utilisation)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_gemm_2cta -s 2 -c 1 \
+  -o "$OUT/prof_tc_16384" python tools/ncu_target.py tc 16384 > "$OUT/ncu_tc_16384.log" 2>&1
+# C5 / C2 sweep
+timeout 1200 python tools/sweep.py > "$OUT/sweep.json" 2> "$OUT/sweep.err"
 echo done
