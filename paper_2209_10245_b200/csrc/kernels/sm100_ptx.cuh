@@ -74,6 +74,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       "r"(smem_addr(src)), "r"(c0), "r"(c1)
       : "memory");
 }
+// With an L2 cache-policy hint (e.g. evict_first for write-once output).
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int32_t c0,
+                                                  int32_t c1, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_addr(src)), "r"(c0), "r"(c1), "l"(cache_hint)
+      : "memory");
+}
 // Same, adding into global (f32 add reduction): C += tile.
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src,
                                                   int32_t c0, int32_t c1) {

@@ -55,6 +55,7 @@ struct TcArgs {
   int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
   int raster_n;        // 1: groups run along N instead of M (experiments)
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
+  uint64_t hint_c;          // TMA-store epilogue: L2 policy of the C writes
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
   int wave_sync;         // 1: static order + per-wave barrier on tile_counter[0]
   int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
@@ -663,6 +664,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int col0 = nb * kBN + c * 16;
             if (args.accumulate)
               tma_reduce_add_2d(&map_c, box, col0, row_base);
+            else if (args.hint_c != kEvictNormal)
+              tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
             else
               tma_store_2d(&map_c, box, col0, row_base);
             bulk_commit();
@@ -991,6 +994,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   };
   args.hint_a = hint("POAS_TC_HINT_A");  // experiment knobs; default evict_normal
   args.hint_b = hint("POAS_TC_HINT_B");
+  args.hint_c = hint("POAS_TC_HINT_C");
   const char* raster_env = std::getenv("POAS_TC_RASTER");
   args.raster_n = raster_env && std::string(raster_env) == "n";
   // Tile scheduler: dynamic claiming below 2^44 MACs; wave-synchronised
