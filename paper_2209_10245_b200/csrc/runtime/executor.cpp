@@ -20,10 +20,10 @@
 //               later one for the previous copy-out (shared bus)
 // Resident runs (operands already in HBM) skip both copy phases.
 // Overlapped host runs ("overlap=1", poas/overlap.hpp): each link unit has
-// its own host->device and device->host streams; B and then the A rows of
-// every row part go host->device back to back, part p computes once its A
-// part landed, its C rows go device->host while part p+1 computes. On a
-// shared bus each direction is served in schedule order.
+// its own host->device and device->host streams; its A row parts and B
+// column panels go host->device interleaved, each block (part x panel) is
+// computed once both landed, and its C goes device->host while later blocks
+// compute. On a shared bus each direction is served in schedule order.
 // Rows are contiguous in schedule order (poas::row_offsets).
 #include "poas/executor.hpp"
 
@@ -340,25 +340,33 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     DeviceGuard g(unit[i]->spec().device);
     for (auto& per_rep : ev) per_rep[i].create();
   }
-  // Overlapped runs: each busy link unit's row parts (the schedule's tiles,
-  // poas::schedule_row_parts) and per-part readiness events, reused by every
-  // repeat (repeats are serialised on the device).
+  // Overlapped runs: each busy link unit's grid of row parts x column panels
+  // (the schedule's tiles, poas::schedule_grid), its link order and block
+  // order (poas/overlap.hpp), and readiness events per link item and per
+  // block, reused by every repeat (repeats are serialised on the device).
   EventPool pool;
-  std::vector<std::vector<std::int64_t>> parts(nd);
+  std::vector<RowColGrid> grid(nd);
+  std::vector<std::vector<OverlapItem>> link_order(nd);
+  std::vector<std::vector<OverlapBlock>> block_order(nd);
   std::vector<std::vector<cudaEvent_t>> in_ev(nd), cp_ev(nd);
   if (overlapped)
     for (std::size_t i = 0; i < nd; ++i) {
       if (!unit[i]->on_gpu() || schedule.devices[i].rows == 0) continue;
       if (!h2d[i] || !d2h[i]) fail(errc::invalid_argument, "overlap: unit has no copy streams");
-      parts[i] = schedule_row_parts(schedule.devices[i], d);
-      for (std::size_t p = 0; p < parts[i].size(); ++p) {
+      grid[i] = schedule_grid(schedule.devices[i], d);
+      const int R = static_cast<int>(grid[i].parts.size()), Q = static_cast<int>(grid[i].panels.size());
+      link_order[i] = overlap_link_order(R, Q);
+      block_order[i] = overlap_block_order(R, Q);
+      for (std::size_t k = 0; k < link_order[i].size(); ++k)
         in_ev[i].push_back(pool.make(unit[i]->spec().device));
+      for (std::size_t b = 0; b < block_order[i].size(); ++b)
         cp_ev[i].push_back(pool.make(unit[i]->spec().device));
-      }
     }
-  // One repeat of an overlapped link unit: host->device (B, then A part by
-  // part), per-part compute, per-part device->host; `prev_in`/`prev_out` are
-  // the previous busy link unit in schedule order (shared-bus order).
+  // One repeat of an overlapped link unit: host->device (A parts and B
+  // panels interleaved in link order), one GEMM per block as soon as its A
+  // part and B panel landed, each block's C device->host as soon as it is
+  // computed; `prev_in`/`prev_out` are the previous busy link unit in
+  // schedule order (shared-bus order).
   const auto enqueue_overlapped = [&](std::size_t i, std::size_t rr, std::size_t prev_in,
                                       std::size_t prev_out) {
     const ScheduledDevice& sd = schedule.devices[i];
@@ -375,75 +383,86 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     char* a_l = static_cast<char*>(u->scratch(link16 ? 2 : 0).ensure(static_cast<std::size_t>(r * lda_l) * esz));
     char* b_l = static_cast<char*>(u->scratch(link16 ? 3 : 1).ensure(static_cast<std::size_t>(d.k * ldb_l) * esz));
     float* c = static_cast<float*>(u->scratch(4).ensure(static_cast<std::size_t>(r * d.n) * 4));
+    const std::vector<std::int64_t>& rp = grid[i].parts;
+    const std::vector<std::int64_t>& cp = grid[i].panels;
+    std::vector<std::int64_t> roff(rp.size(), 0), coff(cp.size(), 0);
+    for (std::size_t p = 1; p < rp.size(); ++p) roff[p] = roff[p - 1] + rp[p - 1];
+    for (std::size_t q = 1; q < cp.size(); ++q) coff[q] = coff[q - 1] + cp[q - 1];
 
     // host -> device
     cuda_check(cudaStreamWaitEvent(hs, t0[u->spec().device][rr], 0), "wait t0");
     if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(hs, ev[rr][prev_in].ci1, 0), "wait");
     cuda_check(cudaEventRecord(e.ci0, hs), "cudaEventRecord");
-    if (link16)
-      copy2d(b_l, ldb_l, io.b16_host, io.ldb16_host, d.k, d.n, 2, cudaMemcpyHostToDevice, hs);
-    else
-      copy2d(b_l, ldb_l, io.b_host, io.ldb_host, d.k, d.n, 4, cudaMemcpyHostToDevice, hs);
-    std::int64_t off = 0;
-    for (std::size_t p = 0; p < parts[i].size(); ++p) {
-      const std::int64_t rp = parts[i][p];
-      if (link16)
-        copy2d(a_l + off * lda_l * 2, lda_l,
-               static_cast<const char*>(io.a16_host) + (r0 + off) * io.lda16_host * 2, io.lda16_host,
-               rp, d.k, 2, cudaMemcpyHostToDevice, hs);
-      else
-        copy2d(a_l + off * lda_l * 4, lda_l, io.a_host + (r0 + off) * io.lda_host, io.lda_host, rp,
-               d.k, 4, cudaMemcpyHostToDevice, hs);
-      cuda_check(cudaEventRecord(in_ev[i][p], hs), "cudaEventRecord");
-      off += rp;
+    for (std::size_t k = 0; k < link_order[i].size(); ++k) {
+      const OverlapItem& it = link_order[i][k];
+      const std::size_t x = static_cast<std::size_t>(it.index);
+      if (it.a) {
+        if (link16)
+          copy2d(a_l + roff[x] * lda_l * 2, lda_l,
+                 static_cast<const char*>(io.a16_host) + (r0 + roff[x]) * io.lda16_host * 2,
+                 io.lda16_host, rp[x], d.k, 2, cudaMemcpyHostToDevice, hs);
+        else
+          copy2d(a_l + roff[x] * lda_l * 4, lda_l, io.a_host + (r0 + roff[x]) * io.lda_host,
+                 io.lda_host, rp[x], d.k, 4, cudaMemcpyHostToDevice, hs);
+      } else {
+        if (link16)
+          copy2d(b_l + coff[x] * 2, ldb_l, static_cast<const char*>(io.b16_host) + coff[x] * 2,
+                 io.ldb16_host, d.k, cp[x], 2, cudaMemcpyHostToDevice, hs);
+        else
+          copy2d(b_l + coff[x] * 4, ldb_l, io.b_host + coff[x], io.ldb_host, d.k, cp[x], 4,
+                 cudaMemcpyHostToDevice, hs);
+      }
+      cuda_check(cudaEventRecord(in_ev[i][k], hs), "cudaEventRecord");
     }
     cuda_check(cudaEventRecord(e.ci1, hs), "cudaEventRecord");
 
-    // compute, part by part as the A parts land
+    // compute, block by block as their operands land
     const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
     char* a16 = convert ? static_cast<char*>(u->scratch(2).ensure(static_cast<std::size_t>(r * lda16) * 2)) : nullptr;
-    const void* bk = b_l;
-    std::int64_t ldbk = ldb_l;
-    off = 0;
-    for (std::size_t p = 0; p < parts[i].size(); ++p) {
-      const std::int64_t rp = parts[i][p];
-      cuda_check(cudaStreamWaitEvent(cs, in_ev[i][p], 0), "wait A part");
-      if (p == 0) {
-        cuda_check(cudaEventRecord(e.cp0, cs), "cudaEventRecord");
-        if (convert) {  // fp32 B crossed the link: one conversion, after it landed
-          void* b16 = u->scratch(3).ensure(static_cast<std::size_t>(d.k * ldb16) * 2);
-          cuda_check(poas_b200::convert_f32(u->spec().dtype, reinterpret_cast<const float*>(b_l), ldb_l,
-                                            b16, ldb16, d.k, d.n, cs),
-                     "convert B");
-          bk = b16;
-          ldbk = ldb16;
+    char* b16 = convert ? static_cast<char*>(u->scratch(3).ensure(static_cast<std::size_t>(d.k * ldb16) * 2)) : nullptr;
+    std::vector<char> a_done(rp.size(), 0), b_done(cp.size(), 0);  // converted (fp32 link)
+    for (std::size_t bi = 0; bi < block_order[i].size(); ++bi) {
+      const OverlapBlock& blk = block_order[i][bi];
+      const std::size_t p = static_cast<std::size_t>(blk.part), q = static_cast<std::size_t>(blk.panel);
+      cuda_check(cudaStreamWaitEvent(cs, in_ev[i][static_cast<std::size_t>(blk.ready_item)], 0),
+                 "wait operands");
+      if (bi == 0) cuda_check(cudaEventRecord(e.cp0, cs), "cudaEventRecord");
+      const void* ap = a_l + roff[p] * lda_l * static_cast<std::int64_t>(esz);
+      const void* bp = b_l + coff[q] * static_cast<std::int64_t>(esz);
+      std::int64_t ldak = lda_l, ldbk = ldb_l;
+      if (convert) {  // fp32 crossed the link: each part / panel converted once
+        if (!a_done[p]) {
+          cuda_check(poas_b200::convert_f32(u->spec().dtype, reinterpret_cast<const float*>(ap), lda_l,
+                                            a16 + roff[p] * lda16 * 2, lda16, rp[p], d.k, cs),
+                     "convert A");
+          a_done[p] = 1;
         }
-      }
-      const void* ap = a_l + off * lda_l * static_cast<std::int64_t>(esz);
-      std::int64_t ldak = lda_l;
-      if (convert) {
-        cuda_check(poas_b200::convert_f32(u->spec().dtype, reinterpret_cast<const float*>(ap), lda_l,
-                                          a16 + off * lda16 * 2, lda16, rp, d.k, cs),
-                   "convert A");
-        ap = a16 + off * lda16 * 2;
+        if (!b_done[q]) {
+          cuda_check(poas_b200::convert_f32(u->spec().dtype, reinterpret_cast<const float*>(bp), ldb_l,
+                                            b16 + coff[q] * 2, ldb16, d.k, cp[q], cs),
+                     "convert B");
+          b_done[q] = 1;
+        }
+        ap = a16 + roff[p] * lda16 * 2;
+        bp = b16 + coff[q] * 2;
         ldak = lda16;
+        ldbk = ldb16;
       }
-      u->gemm(rp, d.n, d.k, ap, ldak, bk, ldbk, c + off * d.n, d.n, false, extra_sms[i]);
-      cuda_check(cudaEventRecord(cp_ev[i][p], cs), "cudaEventRecord");
-      off += rp;
+      u->gemm(rp[p], cp[q], d.k, ap, ldak, bp, ldbk, c + roff[p] * d.n + coff[q], d.n, false,
+              extra_sms[i]);
+      cuda_check(cudaEventRecord(cp_ev[i][bi], cs), "cudaEventRecord");
     }
     cuda_check(cudaEventRecord(e.cp1, cs), "cudaEventRecord");
 
-    // device -> host, part by part as they are computed
+    // device -> host, block by block as they are computed
     if (bus_ && prev_out != nd) cuda_check(cudaStreamWaitEvent(ds, ev[rr][prev_out].co1, 0), "wait");
-    off = 0;
-    for (std::size_t p = 0; p < parts[i].size(); ++p) {
-      const std::int64_t rp = parts[i][p];
-      cuda_check(cudaStreamWaitEvent(ds, cp_ev[i][p], 0), "wait part");
-      if (p == 0) cuda_check(cudaEventRecord(e.co0, ds), "cudaEventRecord");
-      copy2d(io.c_host + (r0 + off) * io.ldc_host, io.ldc_host, c + off * d.n, d.n, rp, d.n, 4,
-             cudaMemcpyDeviceToHost, ds);
-      off += rp;
+    for (std::size_t bi = 0; bi < block_order[i].size(); ++bi) {
+      const OverlapBlock& blk = block_order[i][bi];
+      const std::size_t p = static_cast<std::size_t>(blk.part), q = static_cast<std::size_t>(blk.panel);
+      cuda_check(cudaStreamWaitEvent(ds, cp_ev[i][bi], 0), "wait block");
+      if (bi == 0) cuda_check(cudaEventRecord(e.co0, ds), "cudaEventRecord");
+      copy2d(io.c_host + (r0 + roff[p]) * io.ldc_host + coff[q], io.ldc_host,
+             c + roff[p] * d.n + coff[q], d.n, rp[p], cp[q], 4, cudaMemcpyDeviceToHost, ds);
     }
     cuda_check(cudaEventRecord(e.co1, ds), "cudaEventRecord");
   };

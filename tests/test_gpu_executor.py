@@ -447,3 +447,37 @@ def test_b_panels_with_flags_one_launch(torch_cuda, poas):
     torch.cuda.synchronize()
     exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2})
     assert oracle.rel_frobenius(C.cpu().numpy(), exp) <= TOL
+
+
+@pytest.mark.parametrize("link", ["bf16", "fp32"])
+def test_overlapped_grid_ragged(torch_cuda, poas, link):
+    """Overlapped execution of a hand-made 3 x 3 grid of blocks (ragged row
+    parts and column panels, the tiles of an "overlap" schedule): A parts
+    and B panels interleaved host->device, one GEMM per block, each block's
+    C back -- every element of C exact, over a 16-bit and an fp32 link."""
+    import oracle
+
+    torch = torch_cuda
+    elem = 2 if link == "bf16" else 4
+    units = f"gpu0.tc=xpu:dev=0:sms=16:dtype=bf16:elem={elem}:link=pcie:probe=512-2048"
+    m, n, k = 1000, 1000, 520
+    profile = poas.profile_machine(units, PROF, True)
+    sched = json.loads(poas.plan_policy(profile, m, n, k, "overlap"))
+    parts, panels = [384, 384, 232], [256, 256, 488]
+    sched["devices"][0]["tiles"] = [{"m": r, "k": k, "n": w} for r in parts for w in panels]
+    sched_text = poas.schedule_roundtrip(json.dumps(sched))
+    d = operands(torch, poas, m, n, k)
+    hC = torch.full((m, n), float("nan")).pin_memory()
+    io = poas.GemmIO(m=m, n=n, k=k, a_host=d["hA"].data_ptr(), lda_host=k, b_host=d["hB"].data_ptr(),
+                     ldb_host=n, c_host=hC.data_ptr(), ldc_host=n, resident=0)
+    if link == "bf16":
+        hA16 = d["A16"][:, :k].cpu().contiguous().pin_memory()
+        hB16 = d["B16"][:, :n].cpu().contiguous().pin_memory()
+        io.a16_host, io.lda16_host, io.b16_host, io.ldb16_host = hA16.data_ptr(), k, hB16.data_ptr(), n
+    ex = poas.Executor(units + ";overlap=1")
+    rep = ex.execute(sched_text, io, 2)
+    exp = oracle.expected_c(sched, d["A"], d["B"], {"gpu0.tc": 2})
+    got = hC.numpy()
+    assert not np.isnan(got).any()
+    assert oracle.rel_frobenius(got, exp) <= TOL
+    assert rep["devices"][0].get("overlapped") is True

@@ -40,52 +40,84 @@ def parse_profile(text):
     return devs, bus
 
 
-def row_parts(rows, parts):
-    """poas::overlap_row_parts: 128-row blocks spread evenly, tail last."""
-    if rows <= 0:
+def split(extent, parts, block):
+    """poas::overlap_split: whole blocks spread evenly, tail on the last."""
+    if extent <= 0:
         return []
-    blocks = rows // 128
+    blocks = extent // block
     if blocks == 0:
-        return [rows]
+        return [extent]
     q = max(1, min(parts, blocks))
-    out = [(blocks // q + (1 if p < blocks % q else 0)) * 128 for p in range(q)]
-    out[-1] += rows % 128
+    out = [(blocks // q + (1 if p < blocks % q else 0)) * block for p in range(q)]
+    out[-1] += extent % block
     return out
 
 
-def overlap_timeline(devs, bus, rows_parts, m, n, k):
-    """Restatement of poas::evaluate_overlap_timeline over a schedule's row
-    parts: B then the A parts on the host->device queue, part p computes
-    after its A part and part p-1, its C (fp32) leaves after that and after
-    the previous copy-out on the device->host queue; queues shared in
-    priority order when `bus`. Returns ({id: (copy_in, compute, copy_out)}, makespan)."""
+def row_parts(rows, parts):
+    return split(rows, parts, 128)
+
+
+def link_order(R, Q):
+    """poas::overlap_link_order: A while proportionally behind."""
+    out, a, b = [], 0, 0
+    while a < R or b < Q:
+        if b >= Q or (a < R and a * Q <= b * R):
+            out.append(("A", a))
+            a += 1
+        else:
+            out.append(("B", b))
+            b += 1
+    return out
+
+
+def block_order(R, Q):
+    """poas::overlap_block_order: (part, panel, ready item) as items land."""
+    out, a, b = [], 0, 0
+    for k, (kind, _) in enumerate(link_order(R, Q)):
+        if kind == "A":
+            out += [(a, j, k) for j in range(b)]
+            a += 1
+        else:
+            out += [(i, b, k) for i in range(a)]
+            b += 1
+    return out
+
+
+def overlap_timeline(devs, bus, grids, m, n, k):
+    """Restatement of poas::evaluate_overlap_timeline over each unit's grid
+    of row parts x column panels: link items (A parts, B panels) back to
+    back on the host->device queue in link order; block b computes after its
+    ready item and block b-1; its C (fp32) leaves after that and after the
+    previous copy-out on the device->host queue; queues shared in priority
+    order when `bus`. Returns ({id: (copy_in, compute, copy_out)}, makespan)."""
     h2d = d2h = 0.0
     out, makespan = {}, 0.0
     for d in sorted(devs, key=lambda x: x["priority"]):
-        parts = rows_parts[d["id"]]
+        rp, cp = grids[d["id"]]
         slope, icpt = d["slope"], d["intercept"]
         if d["kind"] == "cpu":
-            c = sum(slope * r * n * k + icpt for r in parts)
+            c = sum(slope * r * n * k + icpt for r in rp)
             out[d["id"]] = ((0.0, 0.0), (0.0, c), (c, c))
             makespan = max(makespan, c)
             continue
-        if not parts:
+        if not rp:
             at = h2d if bus else 0.0
             out[d["id"]] = ((at, at), (at, at), (at, at))
             continue
         bw, e = d["bandwidth"], d["elem_size"]
         t_in = h2d if bus else 0.0
-        free_out = d2h if bus else 0.0
         start_in = t_in
-        t_in += e * k * n / bw
-        c_end = t_in
-        c_start = o_start = None
-        for r in parts:
-            t_in += e * r * k / bw
-            cs = max(t_in, c_end)
-            c_end = cs + slope * r * n * k + icpt
+        landed = []
+        for kind, x in link_order(len(rp), len(cp)):
+            t_in += e * k * (rp[x] if kind == "A" else cp[x]) / bw
+            landed.append(t_in)
+        free_out = d2h if bus else 0.0
+        c_end, c_start, o_start = 0.0, None, None
+        for i, j, ready in block_order(len(rp), len(cp)):
+            cs = max(landed[ready], c_end)
+            c_end = cs + slope * rp[i] * cp[j] * k + icpt
             os_ = max(c_end, free_out)
-            free_out = os_ + 4.0 * r * n / bw
+            free_out = os_ + 4.0 * rp[i] * cp[j] / bw
             if c_start is None:
                 c_start, o_start = cs, os_
         out[d["id"]] = ((start_in, t_in), (c_start, c_end), (o_start, free_out))
@@ -95,22 +127,41 @@ def overlap_timeline(devs, bus, rows_parts, m, n, k):
     return out, makespan
 
 
+def grid_of(tiles, n):
+    """Row parts and column panels of an overlap schedule's part-major tiles."""
+    cp, covered = [], 0
+    for t in tiles:
+        if covered >= n:
+            break
+        cp.append(t["n"])
+        covered += t["n"]
+    q = len(cp)
+    rp = [tiles[p * q]["m"] for p in range(len(tiles) // q)] if q else []
+    return rp, cp
+
+
 def check_against_restatement(poas, prof, m, n, k):
     s = json.loads(poas.plan_policy(prof, m, n, k, "overlap"))
     devs, bus = parse_profile(prof)
-    parts = {}
+    grids = {}
     for d in s["devices"]:
         dev = next(x for x in devs if x["id"] == d["id"])
         if dev["kind"] == "cpu":
-            parts[d["id"]] = [d["rows"]] if d["rows"] else []
+            grids[d["id"]] = ([d["rows"]] if d["rows"] else [], [n])
+        elif d["rows"] == 0:
+            assert d["tiles"] == []
+            grids[d["id"]] = ([], [])
         else:
-            # link units: full-K row parts as produced by overlap_row_parts
-            assert all(t["k"] == k and t["n"] == n for t in d["tiles"])
-            rp = [t["m"] for t in d["tiles"]]
-            assert sum(rp) == d["rows"]
-            assert rp == row_parts(d["rows"], len(rp)) or (d["rows"] == 0 and rp == [])
-            parts[d["id"]] = rp
-    tl, makespan = overlap_timeline(devs, bus, parts, m, n, k)
+            # link units: an R x Q grid of full-K blocks, part-major
+            assert all(t["k"] == k for t in d["tiles"])
+            rp, cp = grid_of(d["tiles"], n)
+            assert len(rp) * len(cp) == len(d["tiles"])
+            assert [t["m"] for t in d["tiles"]] == [r for r in rp for _ in cp]
+            assert [t["n"] for t in d["tiles"]] == cp * len(rp)
+            assert sum(rp) == d["rows"] and sum(cp) == n
+            assert rp == row_parts(d["rows"], len(rp)) and cp == split(n, len(cp), 256)
+            grids[d["id"]] = (rp, cp)
+    tl, makespan = overlap_timeline(devs, bus, grids, m, n, k)
     assert s["makespan"] == pytest.approx(makespan, rel=REL, abs=2e-9)
     for d in s["devices"]:
         want = tl[d["id"]]
@@ -119,6 +170,16 @@ def check_against_restatement(poas, prof, m, n, k):
             assert d[key][0] == pytest.approx(iv[0], abs=1e-9), (d["id"], key)
             assert d[key][1] == pytest.approx(iv[1], abs=1e-9), (d["id"], key)
     return s
+
+
+def test_link_and_block_order():
+    assert link_order(3, 1) == [("A", 0), ("B", 0), ("A", 1), ("A", 2)]
+    assert link_order(2, 2) == [("A", 0), ("B", 0), ("A", 1), ("B", 1)]
+    assert link_order(1, 3) == [("A", 0), ("B", 0), ("B", 1), ("B", 2)]
+    assert block_order(2, 2) == [(0, 0, 1), (1, 0, 2), (0, 1, 3), (1, 1, 3)]
+    for R, Q in ((1, 1), (4, 2), (3, 5), (8, 8)):
+        blocks = block_order(R, Q)
+        assert sorted((i, j) for i, j, _ in blocks) == [(i, j) for i in range(R) for j in range(Q)]
 
 
 def test_row_parts():
@@ -139,14 +200,18 @@ def test_overlap_b200_e2e_profile(poas):
     rows = {d["id"]: d["rows"] for d in s["devices"]}
     assert rows == {"gpu0.tc": 16384, "cpu0": 0, "gpu0.simt": 0}
     tc = next(d for d in s["devices"] if d["id"] == "gpu0.tc")
-    assert len(tc["tiles"]) >= 16
-    # copies overlap compute: C leaves while A is still arriving
+    rp, cp = grid_of(tc["tiles"], n)
+    assert len(rp) >= 4 and len(cp) >= 2, (len(rp), len(cp))  # a 2-D grid wins here
+    # copies overlap compute: C leaves while A and B are still arriving
     assert tc["copy_out"][0] < tc["copy_in"][1]
-    # lower bound: B in, then all of C out (fp32) at the link bandwidth
+    # floor: the busier link direction (host->device: A and B, 2 bytes; C
+    # back is 4 bytes, as much) -- the 1-D scheme (B, then A parts) pays
+    # all of B before any C can leave
     devs, _ = parse_profile(prof)
     bw = next(d for d in devs if d["id"] == "gpu0.tc")["bandwidth"]
-    floor = (2 * k * n + 4 * m * n) / bw
-    assert floor < s["makespan"] < 1.05 * floor
+    floor = max(2 * (m * k + k * n), 4 * m * n) / bw
+    one_d = (2 * k * n + 4 * m * n) / bw
+    assert floor < s["makespan"] < 0.9 * one_d
     # the synchronous plan charges the 2-byte unit's C at 2 bytes (reference
     # transfer_bytes), yet overlap still predicts less
     assert s["makespan"] < seq["makespan"]
@@ -155,29 +220,27 @@ def test_overlap_b200_e2e_profile(poas):
 
 def test_overlap_hand_computed(poas):
     """One link unit, exact numbers: bw 1e9 B/s, e=4, slope 1e-12, no
-    intercept; 1024x512x256 -> B 0.524288 ms, each 256-row A part 0.262144 ms,
-    compute 33.554 us, C part 0.524288 ms."""
+    intercept, 1024x512x256. Whatever grid the policy picks, its makespan
+    is the pipeline recurrence over that grid written out by hand here, and
+    beats the synchronous copy-in, compute, copy-out."""
     prof = "\n".join([
         "poas-profile v1", "", "bus true", "",
         "device g", "kind gpu", "slope 1e-12", "intercept 0", "bandwidth 1000000000",
         "elem_size 4", "priority 0", "ops_min 1", "ops_max 1000000000000", ""])
     m, n, k = 1024, 512, 256
     s = check_against_restatement(poas, prof, m, n, k)
-    g = s["devices"][0]
-    parts = [t["m"] for t in g["tiles"]]
-    b = 4 * k * n / 1e9
-    a = [4 * r * k / 1e9 for r in parts]
-    c = [1e-12 * r * n * k for r in parts]
-    o = [4 * r * n / 1e9 for r in parts]
-    # hand-rolled pipeline recurrence, independent of both implementations
-    t_in, c_end, o_end = b, b, 0.0
-    for ai, ci, oi in zip(a, c, o):
-        t_in += ai
-        c_end = max(t_in, c_end) + ci
-        o_end = max(c_end, o_end) + oi
+    rp, cp = grid_of(s["devices"][0]["tiles"], n)
+    # hand-rolled: items in link order, blocks as they become computable
+    landed, t = {}, 0.0
+    for kind, x in link_order(len(rp), len(cp)):
+        t += 4 * k * (rp[x] if kind == "A" else cp[x]) / 1e9
+        landed[(kind, x)] = t
+    c_end = o_end = 0.0
+    for i, j, _ in block_order(len(rp), len(cp)):
+        c_end = max(landed[("A", i)], landed[("B", j)], c_end) + 1e-12 * rp[i] * cp[j] * k
+        o_end = max(c_end, o_end) + 4 * rp[i] * cp[j] / 1e9
     assert s["makespan"] == pytest.approx(o_end, abs=2e-9)
-    # sequential model for comparison: everything back to back
-    seq = b + sum(a) + sum(c) + 4 * m * n / 1e9
+    seq = 4 * (m * k + k * n) / 1e9 + 1e-12 * m * n * k + 4 * m * n / 1e9
     assert s["makespan"] < seq
 
 
