@@ -75,7 +75,8 @@ double evaluate_overlap_timeline(const std::vector<OverlapEntry>& entries, bool 
 // spread evenly (earlier pieces one block larger), the extent % block tail
 // on the last piece; fewer pieces when there are fewer blocks.
 std::vector<std::int64_t> overlap_split(std::int64_t extent, int parts, std::int64_t block);
-// Row parts: 128-row blocks (the tensor kernel's tile height).
+// Row parts: 256-row blocks (the pair kernel's tile height: a streamed
+// launch never lets a tile straddle two parts).
 std::vector<std::int64_t> overlap_row_parts(std::int64_t rows, int parts);
 // Column panels: 256-column blocks (the pair kernel's tile width).
 std::vector<std::int64_t> overlap_col_panels(std::int64_t n, int panels);

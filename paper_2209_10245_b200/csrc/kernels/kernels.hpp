@@ -34,8 +34,32 @@ cudaError_t tc_gemm_panels(AbType t, int64_t M, int64_t N, int64_t K, const void
                            const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                            int num_ctas, const TcPanels& panels, cudaStream_t stream);
 
+// Streamed operands: one launch over an R x Q grid of output blocks whose A
+// row parts and B column panels arrive over time (overlapped copies). Block
+// b: `blocks[4*b .. 4*b+3]` = {first M-tile | M-tiles << 16, first N-tile |
+// N-tiles << 16, first tile id, A item | B item << 16} in 256-element tile
+// units (device memory; blocks in compute order, first tile ids ascending,
+// together covering every tile of C once). Producers start a block's tiles
+// once item_flags of both its items are >= epoch; when every tile of block
+// b is in global memory the kernel sets block_flags[b] = epoch
+// (block_count[b] counts 8 per tile and must be epoch-1 times that at
+// launch: zero it with the flags and count epochs from 1).
+struct TcStream {
+  const int* blocks = nullptr;
+  int nblocks = 0;
+  const int* item_flags = nullptr;
+  int* block_count = nullptr;
+  int* block_flags = nullptr;
+  int epoch = 0;
+};
+cudaError_t tc_gemm_stream(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                           const void* B, int64_t ldb, float* C, int64_t ldc, int num_ctas,
+                           const TcStream& s, cudaStream_t stream);
+
 // *flag = value in stream order (cuStreamWriteValue32).
 cudaError_t signal_flag(int* flag, int value, cudaStream_t stream);
+// The stream waits until *flag >= value (cuStreamWaitValue32, GEQ).
+cudaError_t wait_flag(const int* flag, int value, cudaStream_t stream);
 
 // The kernel tc_gemm launches: "tc_gemm_2cta_kernel" (CTA pairs,
 // cta_group::2); POAS_TC_KERNEL=1cta selects "tc_gemm_kernel" (single SM).

@@ -70,6 +70,18 @@ struct TcArgs {
   int tiles_n_panel;
   const int* panel_flags;
   int panel_epoch;
+  // Streamed operands (pair kernel; see tc_gemm_stream): tiles ordered by a
+  // block table {mb0 | tiles_m << 16, nb0 | tiles_n << 16, first tile,
+  // item_a | item_b << 16}; a producer starts a tile once both link items
+  // of its block are flagged (item_flags[i] >= stream_epoch); the epilogue
+  // counts finished tiles per block (8 warps per pair tile) and raises the
+  // block's flag once its C is in global memory.
+  const int4* sblocks;
+  int nsblocks;
+  const int* item_flags;
+  int* block_count;
+  int* block_flags;
+  int stream_epoch;
 };
 
 // Spin (acquire, with backoff) until *flag >= epoch; traps after 10 s so a
@@ -177,6 +189,24 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   const int r = t - g * per_group;
   mb = first_m + r % gm;
   nb = r / gm;
+}
+
+// Tile t of a streamed problem: its block (binary search over first tiles)
+// and the grouped raster inside the block.
+__device__ __forceinline__ int4 tile_coords_stream(const TcArgs& a, int t, int& mb, int& nb,
+                                                   int& blk) {
+  int lo = 0, hi = a.nsblocks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.sblocks[mid].z <= t) lo = mid; else hi = mid - 1;
+  }
+  const int4 d = a.sblocks[lo];
+  blk = lo;
+  int lm, ln;
+  tile_coords(t - d.z, d.x >> 16, d.y >> 16, a.group, lm, ln);
+  mb = (d.x & 0xffff) + lm;
+  nb = (d.y & 0xffff) + ln;
+  return d;
 }
 
 // Tile t of a (possibly panel-major) problem: M-tile mb, global N-tile nb,
@@ -499,12 +529,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int t = first < total ? first : -1;
       next_static = first + step;
       int confirmed = -1;  // highest B panel seen ready
+      uint64_t seen_lo = 0, seen_hi = 0;  // streamed link items seen ready
       while (t >= 0) {
         if (leader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
         ++wave;
         int t_next = 0;  // claimed once this tile's first loads are out
         int mb, nb, pnl, nbl;
-        tile_coords_panel(args, t, mb, nb, pnl, nbl);
+        if (args.sblocks) {
+          int blk;
+          const int4 d = tile_coords_stream(args, t, mb, nb, blk);
+          pnl = 0;
+          nbl = nb;
+          for (int h = 0; h < 2; ++h) {  // the block's A part, then its B panel
+            const int item = h ? (d.w >> 16) : (d.w & 0xffff);
+            uint64_t& mask = item < 64 ? seen_lo : seen_hi;
+            const uint64_t bit = 1ull << (item & 63);
+            if (!(mask & bit)) {
+              wait_panel_flag(args.item_flags + item, args.stream_epoch);
+              mask |= bit;
+            }
+          }
+        } else {
+          tile_coords_panel(args, t, mb, nb, pnl, nbl);
+        }
         if (args.panel_flags && pnl > confirmed) {  // flags are set in panel order
           wait_panel_flag(args.panel_flags + pnl, args.panel_epoch);
           confirmed = pnl;
@@ -628,8 +675,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     };
     for (int t = first < total ? first : -1; t >= 0; t = next_tile()) {
       int mb, nb;
-      int pnl_unused, nbl_unused;
-      tile_coords_panel(args, t, mb, nb, pnl_unused, nbl_unused);
+      int pnl_unused, nbl_unused, blk = 0, blk_tiles = 0;
+      if (args.sblocks) {
+        const int4 d = tile_coords_stream(args, t, mb, nb, blk);
+        blk_tiles = (d.x >> 16) * (d.y >> 16);
+      } else {
+        tile_coords_panel(args, t, mb, nb, pnl_unused, nbl_unused);
+      }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (quad == 0 && lane == 0 && !epi_traced) {
@@ -695,6 +747,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           args.trace[blockIdx.x * 16 + 6] = tt;
+        }
+        if (args.sblocks && lane == 0) {
+          // this warp's boxes of the tile are in global memory: count it;
+          // the block's last warp raises the block flag (its copy-out waits
+          // on it, cuStreamWaitValue32)
+          bulk_wait_all();
+          fence_proxy_async_global();
+          __threadfence();
+          const int target = args.stream_epoch * blk_tiles * 8;
+          if (atomicAdd(args.block_count + blk, 1) + 1 == target) {
+            __threadfence();
+            atomicExch(args.block_flags + blk, args.stream_epoch);
+          }
         }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -913,25 +978,33 @@ const char* tc_gemm_scheduler_name(int64_t M, int64_t N, int64_t K) {
 namespace {
 cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                          const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
-                         int num_ctas, const TcPanels* ps, cudaStream_t stream);
+                         int num_ctas, const TcPanels* ps, const TcStream* ss, cudaStream_t stream);
 }
 
 cudaError_t tc_gemm(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                     int num_ctas, cudaStream_t stream) {
-  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, accumulate, num_ctas, nullptr, stream);
+  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, accumulate, num_ctas, nullptr, nullptr,
+                      stream);
+}
+
+cudaError_t tc_gemm_stream(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                           const void* B, int64_t ldb, float* C, int64_t ldc, int num_ctas,
+                           const TcStream& s, cudaStream_t stream) {
+  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, false, num_ctas, nullptr, &s, stream);
 }
 
 cudaError_t tc_gemm_panels(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                            const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                            int num_ctas, const TcPanels& panels, cudaStream_t stream) {
-  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, accumulate, num_ctas, &panels, stream);
+  return tc_gemm_impl(t, M, N, K, A, lda, B, ldb, C, ldc, accumulate, num_ctas, &panels, nullptr,
+                      stream);
 }
 
 namespace {
 cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                          const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
-                         int num_ctas, const TcPanels* ps, cudaStream_t stream) {
+                         int num_ctas, const TcPanels* ps, const TcStream* ss, cudaStream_t stream) {
   if (t != AbType::bf16 && t != AbType::f16) return cudaErrorInvalidValue;
   if (M <= 0 || N <= 0) return cudaSuccess;
   const int P = ps ? ps->panels : 1;
@@ -973,7 +1046,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   // once its scheduler fits the size, profiles/r01_tile_scheduler).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const bool force_1cta = std::string(tc_gemm_kernel_name(M, N, K)) == "tc_gemm_kernel";
-  if (P > 1 && force_1cta) return cudaErrorNotSupported;  // panels: pair kernel only
+  if ((P > 1 || ss) && force_1cta) return cudaErrorNotSupported;  // pair kernel only
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -1013,6 +1086,20 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.tiles_n_panel = static_cast<int>(np / 256);
   args.panel_flags = ps ? ps->flags : nullptr;
   args.panel_epoch = ps ? ps->epoch : 0;
+  args.sblocks = nullptr;
+  args.nsblocks = 0;
+  args.item_flags = nullptr;
+  args.block_count = nullptr;
+  args.block_flags = nullptr;
+  args.stream_epoch = 0;
+  if (ss) {
+    args.sblocks = reinterpret_cast<const int4*>(ss->blocks);
+    args.nsblocks = ss->nblocks;
+    args.item_flags = ss->item_flags;
+    args.block_count = ss->block_count;
+    args.block_flags = ss->block_flags;
+    args.stream_epoch = ss->epoch;
+  }
   args.epi_skip = std::getenv("POAS_TC_EPI_SKIP") != nullptr;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
@@ -1061,6 +1148,25 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   return cudaGetLastError();
 }
 }  // namespace
+
+cudaError_t wait_flag(const int* flag, int value, cudaStream_t stream) {
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WaitFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitFn>(p);
+  });
+  if (!fn) return cudaErrorNotSupported;
+  return fn(reinterpret_cast<CUstream>(stream),
+            reinterpret_cast<CUdeviceptr>(const_cast<int*>(flag)), static_cast<cuuint32_t>(value),
+            CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
 
 // Writes `value` to a device int in `stream` order (cuStreamWriteValue32:
 // no kernel, no SM).

@@ -126,7 +126,7 @@ std::vector<std::int64_t> overlap_split(std::int64_t extent, int parts, std::int
 }
 
 std::vector<std::int64_t> overlap_row_parts(std::int64_t rows, int parts) {
-  return overlap_split(rows, parts, 128);
+  return overlap_split(rows, parts, 256);
 }
 
 std::vector<std::int64_t> overlap_col_panels(std::int64_t n, int panels) {

@@ -362,6 +362,75 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       for (std::size_t b = 0; b < block_order[i].size(); ++b)
         cp_ev[i].push_back(pool.make(unit[i]->spec().device));
     }
+  // A tensor unit with a 16-bit link streams its grid through ONE launch
+  // (tc_gemm_stream): the H2D stream flags each link item as it lands, the
+  // persistent kernel's producers wait for their block's two items, the
+  // epilogue flags each finished block and the D2H stream waits on those
+  // flags (cuStreamWaitValue32) -- no per-block launches, every SM busy on
+  // whatever blocks are ready. Needs the pair kernel and 256-aligned parts
+  // and panels (a tile never straddles two link items).
+  struct StreamState {
+    int* item_flags = nullptr;
+    int* block_count = nullptr;
+    int* block_flags = nullptr;
+    int* blocks = nullptr;
+    cudaEvent_t ready = nullptr;
+  };
+  std::vector<StreamState> sstate(nd);
+  const auto aligned256 = [](const std::vector<std::int64_t>& v) {
+    for (std::size_t x = 0; x + 1 < v.size(); ++x)
+      if (v[x] % 256) return false;
+    return true;
+  };
+  if (overlapped)
+    for (std::size_t i = 0; i < nd; ++i) {
+      Unit* u = unit[i];
+      if (!u->on_gpu() || schedule.devices[i].rows == 0) continue;
+      if (u->spec().kind != DeviceKind::xpu || !host16_link(u)) continue;
+      if (std::string(poas_b200::tc_gemm_kernel_name(schedule.devices[i].rows, d.n, d.k)) !=
+          "tc_gemm_2cta_kernel")
+        continue;
+      if (!aligned256(grid[i].parts) || !aligned256(grid[i].panels)) continue;
+      if (link_order[i].size() > 128 || block_order[i].size() > 4096) continue;
+      DeviceGuard g(u->spec().device);
+      const std::size_t ni = link_order[i].size(), nb = block_order[i].size();
+      std::vector<int> item_a(grid[i].parts.size()), item_b(grid[i].panels.size());
+      for (std::size_t k = 0; k < ni; ++k)
+        (link_order[i][k].a ? item_a : item_b)[static_cast<std::size_t>(link_order[i][k].index)] =
+            static_cast<int>(k);
+      std::vector<std::int64_t> roff(grid[i].parts.size(), 0), coff(grid[i].panels.size(), 0);
+      for (std::size_t x = 1; x < roff.size(); ++x) roff[x] = roff[x - 1] + grid[i].parts[x - 1];
+      for (std::size_t x = 1; x < coff.size(); ++x) coff[x] = coff[x - 1] + grid[i].panels[x - 1];
+      std::vector<int> table(4 * nb);
+      int first = 0;
+      for (std::size_t b = 0; b < nb; ++b) {
+        const std::size_t pp = static_cast<std::size_t>(block_order[i][b].part);
+        const std::size_t qq = static_cast<std::size_t>(block_order[i][b].panel);
+        const int tm = static_cast<int>((grid[i].parts[pp] + 255) / 256);
+        const int tn = static_cast<int>((grid[i].panels[qq] + 255) / 256);
+        table[4 * b] = static_cast<int>(roff[pp] / 256) | (tm << 16);
+        table[4 * b + 1] = static_cast<int>(coff[qq] / 256) | (tn << 16);
+        table[4 * b + 2] = first;
+        table[4 * b + 3] = item_a[pp] | (item_b[qq] << 16);
+        first += tm * tn;
+      }
+      const std::size_t ints = ni + 2 * nb + 4 * nb;
+      int* base = static_cast<int*>(u->scratch(5).ensure((ints + 4) * sizeof(int)));
+      StreamState& st = sstate[i];
+      st.item_flags = base;
+      st.block_count = base + ni;
+      st.block_flags = base + ni + nb;
+      st.blocks = base + ni + 2 * nb;
+      cudaStream_t cs = u->stream();
+      cuda_check(cudaMemsetAsync(base, 0, (ni + 2 * nb) * sizeof(int), cs), "cudaMemsetAsync");
+      cuda_check(cudaMemcpyAsync(st.blocks, table.data(), table.size() * sizeof(int),
+                                 cudaMemcpyHostToDevice, cs),
+                 "cudaMemcpyAsync");
+      st.ready = pool.make(u->spec().device);
+      cuda_check(cudaEventRecord(st.ready, cs), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(h2d[i], st.ready, 0), "wait stream setup");
+      cuda_check(cudaStreamWaitEvent(d2h[i], st.ready, 0), "wait stream setup");
+    }
   // One repeat of an overlapped link unit: host->device (A parts and B
   // panels interleaved in link order), one GEMM per block as soon as its A
   // part and B panel landed, each block's C device->host as soon as it is
@@ -413,8 +482,37 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
                  cudaMemcpyHostToDevice, hs);
       }
       cuda_check(cudaEventRecord(in_ev[i][k], hs), "cudaEventRecord");
+      if (sstate[i].item_flags)
+        cuda_check(poas_b200::signal_flag(sstate[i].item_flags + k, static_cast<int>(rr) + 1, hs),
+                   "signal item");
     }
     cuda_check(cudaEventRecord(e.ci1, hs), "cudaEventRecord");
+
+    if (sstate[i].item_flags) {  // one streamed launch; copy-out on block flags
+      const StreamState& st = sstate[i];
+      const int epoch = static_cast<int>(rr) + 1;
+      cuda_check(cudaEventRecord(e.cp0, cs), "cudaEventRecord");
+      poas_b200::TcStream ts;
+      ts.blocks = st.blocks;
+      ts.nblocks = static_cast<int>(block_order[i].size());
+      ts.item_flags = st.item_flags;
+      ts.block_count = st.block_count;
+      ts.block_flags = st.block_flags;
+      ts.epoch = epoch;
+      u->gemm_stream(r, d.n, d.k, a_l, lda_l, b_l, ldb_l, c, d.n, ts, extra_sms[i]);
+      cuda_check(cudaEventRecord(e.cp1, cs), "cudaEventRecord");
+      if (bus_ && prev_out != nd) cuda_check(cudaStreamWaitEvent(ds, ev[rr][prev_out].co1, 0), "wait");
+      for (std::size_t bi = 0; bi < block_order[i].size(); ++bi) {
+        const OverlapBlock& blk = block_order[i][bi];
+        const std::size_t p = static_cast<std::size_t>(blk.part), q = static_cast<std::size_t>(blk.panel);
+        cuda_check(poas_b200::wait_flag(st.block_flags + bi, epoch, ds), "wait block flag");
+        if (bi == 0) cuda_check(cudaEventRecord(e.co0, ds), "cudaEventRecord");
+        copy2d(io.c_host + (r0 + roff[p]) * io.ldc_host + coff[q], io.ldc_host,
+               c + roff[p] * d.n + coff[q], d.n, rp[p], cp[q], 4, cudaMemcpyDeviceToHost, ds);
+      }
+      cuda_check(cudaEventRecord(e.co1, ds), "cudaEventRecord");
+      return;
+    }
 
     // compute, block by block as their operands land
     const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);

@@ -203,6 +203,16 @@ void Unit::gemm_panels(std::int64_t m, std::int64_t n, std::int64_t k, const voi
              "tc_gemm_panels");
 }
 
+void Unit::gemm_stream(std::int64_t m, std::int64_t n, std::int64_t k, const void* a,
+                       std::int64_t lda, const void* b, std::int64_t ldb, float* c, std::int64_t ldc,
+                       const TcStream& s, int extra_sms) {
+  if (spec_.kind != poas::DeviceKind::xpu)
+    poas::fail(poas::errc::invalid_argument, "gemm_stream: tensor units only");
+  const int sms = spec_.sms > 0 ? spec_.sms + extra_sms : 0;
+  cuda_check(tc_gemm_stream(spec_.dtype, m, n, k, a, lda, b, ldb, c, ldc, sms, s, stream_),
+             "tc_gemm_stream");
+}
+
 double Unit::time_gemm(std::int64_t side) {
   if (side < 1) poas::fail(poas::errc::invalid_argument, "time_gemm: side must be positive");
   if (!on_gpu()) {

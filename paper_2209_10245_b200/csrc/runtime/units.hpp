@@ -111,6 +111,12 @@ class Unit : public poas::DeviceBackend {
                    const void* b, std::int64_t ldb, float* c, std::int64_t ldc, int panels,
                    const int* flags, int epoch, int extra_sms = 0);
 
+  // xpu only: the streamed launch of an overlapped grid (kernels.hpp
+  // TcStream), on stream().
+  void gemm_stream(std::int64_t m, std::int64_t n, std::int64_t k, const void* a, std::int64_t lda,
+                   const void* b, std::int64_t ldb, float* c, std::int64_t ldc, const TcStream& s,
+                   int extra_sms = 0);
+
   // Scratch owned by the unit (staging for link copies in execute()).
   DeviceBuffer& scratch(int slot) { return scratch_[slot]; }
 
@@ -122,7 +128,7 @@ class Unit : public poas::DeviceBackend {
   PinnedBuffer xfer_host_;
   std::vector<float> host_a_, host_b_, host_c_;
   std::int64_t probe_side_ = 0;
-  DeviceBuffer scratch_[6];
+  DeviceBuffer scratch_[6];  // 0-4 staging, 5 streamed-launch state
 };
 
 // RAII device selection.

@@ -395,7 +395,9 @@ def test_overlapped_parts_and_bf16_link(torch_cuda, poas):
     sched_text = poas.plan_policy(profile, m, n, k, "overlap")
     sched = json.loads(sched_text)
     tiles = sched["devices"][0]["tiles"]
-    assert len(tiles) > 1 and sum(t["m"] for t in tiles) == m
+    panels = [t["n"] for t in tiles[:next(i for i in range(1, len(tiles) + 1)
+                                          if sum(x["n"] for x in tiles[:i]) >= n)]]
+    assert len(tiles) > 1 and sum(t["m"] for t in tiles) == m * len(panels)
     d = operands(torch, poas, m, n, k)
     hA16 = d["A16"][:, :k].cpu().contiguous().pin_memory()
     hB16 = d["B16"][:, :n].cpu().contiguous().pin_memory()
@@ -449,12 +451,15 @@ def test_b_panels_with_flags_one_launch(torch_cuda, poas):
     assert oracle.rel_frobenius(C.cpu().numpy(), exp) <= TOL
 
 
+@pytest.mark.parametrize("grid", ["aligned", "ragged"])
 @pytest.mark.parametrize("link", ["bf16", "fp32"])
-def test_overlapped_grid_ragged(torch_cuda, poas, link):
+def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
     """Overlapped execution of a hand-made 3 x 3 grid of blocks (ragged row
     parts and column panels, the tiles of an "overlap" schedule): A parts
-    and B panels interleaved host->device, one GEMM per block, each block's
-    C back -- every element of C exact, over a 16-bit and an fp32 link."""
+    and B panels interleaved host->device, each block's C back as soon as it
+    is computed -- every element of C exact. 16-bit link + 256-aligned grid:
+    ONE streamed tensor launch (producers wait on per-item flags, the
+    copy-out on per-block flags); otherwise one GEMM per block."""
     import oracle
 
     torch = torch_cuda
@@ -463,7 +468,8 @@ def test_overlapped_grid_ragged(torch_cuda, poas, link):
     m, n, k = 1000, 1000, 520
     profile = poas.profile_machine(units, PROF, True)
     sched = json.loads(poas.plan_policy(profile, m, n, k, "overlap"))
-    parts, panels = [384, 384, 232], [256, 256, 488]
+    parts, panels = ([512, 256, 232], [256, 512, 232]) if grid == "aligned" else ([384, 384, 232],
+                                                                                   [256, 256, 488])
     sched["devices"][0]["tiles"] = [{"m": r, "k": k, "n": w} for r in parts for w in panels]
     sched_text = poas.schedule_roundtrip(json.dumps(sched))
     d = operands(torch, poas, m, n, k)

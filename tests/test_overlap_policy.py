@@ -54,7 +54,7 @@ def split(extent, parts, block):
 
 
 def row_parts(rows, parts):
-    return split(rows, parts, 128)
+    return split(rows, parts, 256)
 
 
 def link_order(R, Q):
@@ -184,9 +184,9 @@ def test_link_and_block_order():
 
 def test_row_parts():
     assert row_parts(16384, 64) == [256] * 64
-    assert row_parts(1000, 4) == [256, 256, 256, 232]
+    assert row_parts(1000, 4) == [256, 256, 488]
     assert row_parts(100, 8) == [100]
-    assert row_parts(300, 8) == [128, 172]
+    assert row_parts(600, 8) == [256, 344]
 
 
 def test_overlap_b200_e2e_profile(poas):
