@@ -272,6 +272,8 @@ int poas_b200_tc_gemm_panels(int dtype, int64_t m, int64_t n, int64_t k, const v
                              int num_ctas, int panels, const int* flags, int epoch, void* stream);
 /* *flag = value on `stream`, in stream order (cuStreamWriteValue32). */
 int poas_b200_signal_flag(int* flag, int value, void* stream);
+/* `stream` waits until *flag >= value (cuStreamWaitValue32, GEQ). */
+int poas_b200_wait_flag(const int* flag, int value, void* stream);
 /* Name of the kernel poas_b200_tc_gemm launches for this shape
  * ("tc_gemm_2cta_kernel" or "tc_gemm_kernel"; static string). */
 const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k);

@@ -57,6 +57,7 @@ SIGNATURES: dict[str, tuple] = {
     "poas_b200_tc_gemm_panels": (C.c_int, [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int,
                                            C.c_int, C.c_int, vp, C.c_int, vp]),
     "poas_b200_signal_flag": (C.c_int, [vp, C.c_int, vp]),
+    "poas_b200_wait_flag": (C.c_int, [vp, C.c_int, vp]),
     "poas_b200_simt_gemm": (C.c_int, [i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int, C.c_int,
                                       C.c_int, vp]),
     "poas_b200_host_gemm": (C.c_int, [i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int, C.c_int]),

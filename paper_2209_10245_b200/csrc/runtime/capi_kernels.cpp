@@ -65,6 +65,13 @@ int poas_b200_signal_flag(int* flag, int value, void* stream) {
   });
 }
 
+int poas_b200_wait_flag(const int* flag, int value, void* stream) {
+  return poas_b200::capi::guard([&] {
+    poas_b200::capi::cuda_check(
+        poas_b200::wait_flag(flag, value, static_cast<cudaStream_t>(stream)), "wait_flag");
+  });
+}
+
 const char* poas_b200_tc_kernel_name(int64_t m, int64_t n, int64_t k) {
   return poas_b200::tc_gemm_kernel_name(m, n, k);
 }

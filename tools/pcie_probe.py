@@ -60,5 +60,55 @@ def main():
     print(json.dumps(out, indent=1))
 
 
+
+
+def calls():
+    """Many smaller 2-D D2H copies (the overlapped executor's C blocks),
+    with and without a stream-wait-value before each, alone and beside a
+    stream of H2D copies. GB/s of the D2H stream."""
+    import sys
+    sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+    from paper_2209_10245_b200 import poas  # noqa: F401  (flag helpers)
+    import paper_2209_10245_b200._lib as L
+    lib = L.lib
+    total = 1 << 30
+    pitch = 16384 * 4
+    h = torch.empty(total, dtype=torch.uint8).pin_memory()
+    d = torch.empty(total, dtype=torch.uint8, device="cuda")
+    h2 = torch.empty(total, dtype=torch.uint8).pin_memory()
+    d2 = torch.empty(total, dtype=torch.uint8, device="cuda")
+    flag = torch.ones(1, dtype=torch.int32, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = {}
+    for rows, width in ((1024, 4096), (2048, 8192), (4096, 16384), (2048, 65536), (16384, 65536)):
+        nblk = total // (rows * width)
+        for waits in (False, True):
+            for busy in (False, True):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+                e0.record(s1)
+                if busy:
+                    s2.wait_event(e0)
+                    rc = rt.cudaMemcpy2DAsync(d2.data_ptr(), pitch, h2.data_ptr(), pitch, pitch,
+                                              total // pitch, H2D, s2.cuda_stream)
+                    assert rc == 0
+                for b in range(nblk):
+                    if waits:
+                        assert lib.poas_b200_wait_flag(flag.data_ptr(), 1, s1.cuda_stream) == 0
+                    # blocks tile a 16384-column fp32 matrix: row pitch 64 KB
+                    off = (b % (pitch // width)) * width + (b // (pitch // width)) * rows * pitch
+                    rc = rt.cudaMemcpy2DAsync(h.data_ptr() + off, pitch, d.data_ptr() + off, pitch, width,
+                                              rows, D2H, s1.cuda_stream)
+                    assert rc == 0
+                e1.record(s1)
+                torch.cuda.synchronize()
+                out[f"{rows}x{width}B{' wait' if waits else ''}{' +h2d' if busy else ''}"] = round(
+                    total / (e0.elapsed_time(e1) * 1e-3) / 1e9, 2)
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "calls":
+        calls()
+    else:
+        main()
