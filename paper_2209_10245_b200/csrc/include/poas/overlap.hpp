@@ -105,9 +105,10 @@ Schedule build_overlap_schedule(const TilePlan& plan, const MachineProfile& mach
 
 // The policy: every non-empty subset of units planned with the reference
 // pipeline (as "best-subset"), each laid out with 1, 2, 4, ... 64 row parts
-// and 1, 2, 4, 8, 16 column panels; the smallest predicted makespan wins; a
-// later candidate (a smaller subset, more parts or panels) must beat the
-// best so far by more than 0.1%.
+// and 1, 2, 4, 8, 16 column panels of at least 4096 columns (narrower C
+// blocks make slow device->host DMA segments); the smallest predicted
+// makespan wins; a later candidate (a smaller subset, more parts or panels)
+// must beat the best so far by more than 0.1%.
 Schedule plan_overlap(const MachineProfile& machine, const MatrixDims& dims);
 
 }  // namespace poas

@@ -12,6 +12,10 @@
 
 namespace poas {
 
+namespace {
+constexpr std::int64_t kMinPanelCols = 4096;
+}  // namespace
+
 std::vector<OverlapItem> overlap_link_order(int parts, int panels) {
   std::vector<OverlapItem> out;
   int a = 0, b = 0;
@@ -251,6 +255,12 @@ Schedule plan_overlap(const MachineProfile& machine, const MatrixDims& dims) {
   double best_makespan = std::numeric_limits<double>::infinity();
   for (const TilePlan& full : subset_tile_plans(machine, dims)) {
     for (int panels = 1; panels <= 16; panels *= 2) {
+      // Column panels no narrower than kMinPanelCols: a C block's rows are
+      // separate DMA segments, and device->host copies of 4 KB segments run
+      // at ~38 GB/s beside host->device traffic against ~48 GB/s for 16 KB
+      // and ~50 GB/s contiguous (profiles/r01_overlap/pcie_calls.json) --
+      // a per-segment cost the bandwidth model does not carry.
+      if (panels > 1 && dims.n / panels < kMinPanelCols) break;
       for (int parts = 1; parts <= 64; parts *= 2) {
         // A candidate must gain > 0.1%: per-block launch/copy latencies are
         // not modelled, so more blocks (or fewer units) win only on a margin.

@@ -211,7 +211,7 @@ def test_overlap_b200_e2e_profile(poas):
     bw = next(d for d in devs if d["id"] == "gpu0.tc")["bandwidth"]
     floor = max(2 * (m * k + k * n), 4 * m * n) / bw
     one_d = (2 * k * n + 4 * m * n) / bw
-    assert floor < s["makespan"] < 0.9 * one_d
+    assert floor < s["makespan"] < 0.95 * one_d
     # the synchronous plan charges the 2-byte unit's C at 2 bytes (reference
     # transfer_bytes), yet overlap still predicts less
     assert s["makespan"] < seq["makespan"]
