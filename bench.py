@@ -255,6 +255,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     # (--size: "--n" is ambiguous on a torchrun command line)
     ap.add_argument("--n", "--size", dest="n", type=int, default=N_DEFAULT)
+    ap.add_argument("--m-total", type=int, default=None,
+                    help="strong scaling (config C4: --m-total 65536 --size 8192): the job's M rows "
+                         "split over the ranks instead of --size rows per rank")
     ap.add_argument("--tc-sms", type=int, default=None,
                     help=f"tensor unit SM budget (default {TC_SMS}; {TC_SMS_MULTI} at N > 1)")
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
@@ -308,6 +311,10 @@ def main():
         args.tc_sms = TC_SMS if world == 1 else TC_SMS_MULTI
     n = k = args.n
     m = args.n  # rows per rank (weak scaling)
+    if args.m_total:
+        if args.m_total % world:
+            raise SystemExit(f"--m-total {args.m_total} does not split over {world} ranks")
+        m = args.m_total // world
     save = Path(args.save) if args.save else None
     if save and rank == 0:
         save.mkdir(parents=True, exist_ok=True)
@@ -702,9 +709,11 @@ def main():
             "metric": "co-executed GEMM TFLOP/s at N=16384 (1/2/4/8 B200); speedup vs best single unit",
             "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if args.m_total else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
             "config": {
-                "workload": f"C3: square GEMM N={args.n} per GPU (M={m}*{world}), bf16 tensor-core + fp32 "
+                "workload": (f"C4: M={m * world} x N=K={args.n} row-sharded over {world} GPU(s)" if args.m_total
+                             else f"C3: square GEMM N={args.n} per GPU (M={m}*{world})") + ", bf16 tensor-core + fp32 "
                             f"CUDA-core co-execution planned by POAS; B broadcast from rank 0 (NCCL) at N>1",
                 "m": m * world, "n": n, "k": k, "parallelism": f"POAS row split x {world} GPU(s)",
                 "level1_rows_per_gpu": l1_rows,
@@ -712,7 +721,9 @@ def main():
                           simt_id: f"fp32 SIMT on {args.simt_sms} SMs"},
                 "planner_policy": args.policy,
                 "reference_policy_predicted_ms": round(ref_policy_makespan * 1e3, 4),
-                "plan_rows": rows, "l2": "inputs larger than L2 (A,B bf16 512 MiB each; fp32 1 GiB each)",
+                "plan_rows": rows, "l2": (f"inputs larger than L2 (per rank: A {m * k * 2 / 2**20:.0f} MiB + B {k * n * 2 / 2**20:.0f} MiB bf16, "
+                       f"fp32 copies twice that; L2 126 MB)" if (m * k + k * n) * 2 > 126e6
+                       else "inputs fit in L2 (small size)"),
                 "predicted_makespan_ms": round(pred_make * 1e3, 4),
                 "measured_makespan_ms": round(meas_make * 1e3, 4),
                 "makespan_error_pct": round(100.0 * (meas_make - pred_make) / meas_make, 3),

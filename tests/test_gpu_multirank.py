@@ -38,3 +38,21 @@ def test_two_ranks_one_gpu_bench(tmp_path):
     e2e = line["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert e2e["synchronous"]["value"] > 0
+
+
+def test_two_ranks_strong_scaling_c4_shape(tmp_path):
+    """Config C4's shape (M_total rows split over the ranks, N = K), small."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ, POAS_DIST_BACKEND="gloo", OMP_NUM_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533", str(ROOT / "bench.py"), "--gpus", "2",
+           "--m-total=6144", "--size=2048", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+           "--no-e2e"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    cfg = line["config"]
+    assert line["scaling"] == "strong" and cfg["m"] == 6144 and cfg["level1_rows_per_gpu"] == [3072, 3072]
+    assert cfg["c_check"]["max_rel_err"] <= cfg["c_check"]["tol"]

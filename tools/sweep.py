@@ -136,8 +136,31 @@ def c2(n=8192):
             "devices": rep["devices"]}
 
 
+def simt_vs_cublas_fp32(n=8192):
+    """The CUDA-core unit's kernel on every SM beside cuBLAS SGEMM (fp32,
+    TF32 off) on the same operands: the reference point for the FP32 pipe."""
+    d = operands(n)
+    st = torch.cuda.current_stream().cuda_stream
+    ours = lambda: poas.simt_gemm(n, n, n, d["A32"].data_ptr(), n, d["B32"].data_ptr(), n,  # noqa: E731
+                                  d["C"].data_ptr(), n, num_ctas=0, exclusive=False, stream=st)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    c_lib = torch.empty(n, n, device="cuda")
+    lib = lambda: torch.mm(d["A32"], d["B32"], out=c_lib)  # noqa: E731
+    ours()
+    lib()
+    t_ours, t_lib = [], []
+    for _ in range(3):  # alternate: same power state
+        t_ours.append(ev_time(ours, 2))
+        t_lib.append(ev_time(lib, 2))
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    f = 2 * n ** 3
+    return {"n": n, "simt_all_sms_tflops": f / min(t_ours) / 1e12, "cublas_sgemm_tflops": f / min(t_lib) / 1e12}
+
+
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
     sizes = [1024, 2048, 4096, 8192, 16384] + ([] if quick else [32768])
-    res = {"gpu": torch.cuda.get_device_name(), "c5": c5(sizes), "c2": c2()}
+    res = {"gpu": torch.cuda.get_device_name(), "c5": c5(sizes), "c2": c2(),
+           "simt_vs_cublas_fp32": simt_vs_cublas_fp32()}
     print(json.dumps(res, indent=1))
