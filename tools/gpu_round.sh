@@ -12,6 +12,8 @@ nproc > "$OUT/host.txt"; lscpu | grep -E "Model name|^CPU\(s\)" >> "$OUT/host.tx
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -15 > "$OUT/pytest_gpu.txt"
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.txt" 2>&1
 timeout 900 python bench.py --steps "$STEPS" --warmup 3 --save "$OUT/bench" > "$OUT/bench.json" 2> "$OUT/bench.err"
+timeout 600 python bench.py --m-total 65536 --size 8192 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline \
+  > "$OUT/bench_c4.json" 2> "$OUT/bench_c4.err"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
 timeout 900 paper_2209_10245_b200/bin/poas evaluate \
   --units "gpu0.tc=xpu:dev=0:sms=146:dtype=bf16:elem=2:link=hbm:probe=4096-12288;gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048" \
