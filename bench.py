@@ -92,6 +92,8 @@ class ClockSampler:
         self.samples: list[tuple[int, int, int]] = []  # (sm_mhz, max_mhz, reason bits)
         self._stop = threading.Event()
         self._nv = None
+        self._max = None
+        self.error = None
 
     def __enter__(self):
         try:
@@ -99,10 +101,12 @@ class ClockSampler:
 
             pynvml.nvmlInit()
             self._nv = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu))
+            self._sample()  # one synchronous sample: fails here, not silently in the thread
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
             return self
-        except Exception:
+        except Exception as exc:
+            self.error = repr(exc)
             self._nv = None
         try:
             self.proc = subprocess.Popen(
@@ -115,14 +119,22 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def _poll(self):
+    def _sample(self):
         nv, h = self._nv
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        if self._max is None:
+            self._max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:  # older bindings: the pre-rename entry point
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), self._max, bits))
+
+    def _poll(self):
         while not self._stop.is_set():
             try:
-                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
-                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
-            except Exception:
+                self._sample()
+            except Exception as exc:  # keep the reason; the summary reports it
+                self.error = repr(exc)
                 break
             self._stop.wait(0.01)
 
@@ -131,6 +143,11 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self._nv is not None:
+            try:
+                self._sample()  # the region's last moment
+            except Exception as e:
+                self.error = repr(e)
         self._stop.set()
         if self.proc:
             self.proc.terminate()
@@ -161,7 +178,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "error": self.error}
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}

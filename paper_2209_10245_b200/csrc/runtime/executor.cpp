@@ -414,15 +414,16 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         table[4 * b + 3] = item_a[pp] | (item_b[qq] << 16);
         first += tm * tn;
       }
-      const std::size_t ints = ni + 2 * nb + 4 * nb;
-      int* base = static_cast<int*>(u->scratch(5).ensure((ints + 4) * sizeof(int)));
+      // block table first: the kernel reads it as int4 (16-byte aligned)
+      const std::size_t ints = 4 * nb + ni + 2 * nb;
+      int* base = static_cast<int*>(u->scratch(5).ensure(ints * sizeof(int)));
       StreamState& st = sstate[i];
-      st.item_flags = base;
-      st.block_count = base + ni;
-      st.block_flags = base + ni + nb;
-      st.blocks = base + ni + 2 * nb;
+      st.blocks = base;
+      st.item_flags = base + 4 * nb;
+      st.block_count = st.item_flags + ni;
+      st.block_flags = st.block_count + nb;
       cudaStream_t cs = u->stream();
-      cuda_check(cudaMemsetAsync(base, 0, (ni + 2 * nb) * sizeof(int), cs), "cudaMemsetAsync");
+      cuda_check(cudaMemsetAsync(st.item_flags, 0, (ni + 2 * nb) * sizeof(int), cs), "cudaMemsetAsync");
       cuda_check(cudaMemcpyAsync(st.blocks, table.data(), table.size() * sizeof(int),
                                  cudaMemcpyHostToDevice, cs),
                  "cudaMemcpyAsync");
