@@ -12,7 +12,9 @@
 // Persistent over tiles so the grid size is the unit's SM budget.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "kernels.hpp"
 
@@ -38,38 +40,44 @@ struct SimtArgs {
   int tiles_m, tiles_n;
 };
 
-template <bool kVec>
+// kWN = 2: 128 x 128 CTA tile, 8 x 8 per thread; kWN = 4: 128 x 256, 8 x 16
+// per thread (four 4-column quadrants 64 apart: fewer shared-memory reads
+// per FMA).
+template <bool kVec, int kWN>
 __global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p) {
+  constexpr int kTN = 64 * kWN;  // CTA tile width
+  constexpr int kCols = 4 * kWN;  // per-thread columns
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float* As = smem;                          // [2][kBK][kBM + kPad]  (A transposed)
-  float* Bs = smem + 2 * kBK * (kBM + kPad);  // [2][kBK][kBN]
+  float* Bs = smem + 2 * kBK * (kBM + kPad);  // [2][kBK][kTN]
 
   const int tid = threadIdx.x;
   const int tx = tid & 15;  // column group
   const int ty = tid >> 4;  // row group
 
   // Global-load assignment: A tile 128 x 16 -> two float4 per thread along K;
-  // B tile 16 x 128 -> two float4 per thread along N.
+  // B tile 16 x kTN -> kWN float4 per thread, 64 columns apart.
   const int a_row = tid >> 1;          // 0..127
   const int a_k = (tid & 1) * 8;       // 0 or 8 (two float4: +0, +4)
   const int b_k = tid >> 4;            // 0..15
-  const int b_col = (tid & 15) * 8;    // two float4: +0, +4
+  const int b_col = (tid & 15) * 4;    // + 64 h
 
-  const int total = p.tiles_m * p.tiles_n;
+  const int tiles_n = (p.N + kTN - 1) / kTN;
+  const int total = p.tiles_m * tiles_n;
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
-    const int mb = t / p.tiles_n;
-    const int nb = t % p.tiles_n;
+    const int mb = t / tiles_n;
+    const int nb = t % tiles_n;
     const int m0 = mb * kBM;
-    const int n0 = nb * kBN;
+    const int n0 = nb * kTN;
 
-    float acc[8][8];
+    float acc[8][kCols];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+      for (int j = 0; j < kCols; ++j) acc[i][j] = 0.f;
 
-    float ra[8], rb[8];
+    float ra[8], rb[4 * kWN];
     auto load_global = [&](int k0) {
       const int gr = m0 + a_row;
 #pragma unroll
@@ -86,8 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p
       }
       const int gk = k0 + b_k;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gc = n0 + b_col + h * 4;
+      for (int h = 0; h < kWN; ++h) {
+        const int gc = n0 + b_col + h * 64;
         if (kVec && gk < p.K && gc + 3 < p.N) {
           const float4 v = __ldg(reinterpret_cast<const float4*>(p.B + (long long)gk * p.ldb + gc));
           rb[4 * h] = v.x; rb[4 * h + 1] = v.y; rb[4 * h + 2] = v.z; rb[4 * h + 3] = v.w;
@@ -102,9 +110,11 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p
       float* as = As + buf * kBK * (kBM + kPad);
 #pragma unroll
       for (int e = 0; e < 8; ++e) as[(a_k + e) * (kBM + kPad) + a_row] = ra[e];
-      float* bs = Bs + buf * kBK * kBN + b_k * kBN + b_col;
-      reinterpret_cast<float4*>(bs)[0] = make_float4(rb[0], rb[1], rb[2], rb[3]);
-      reinterpret_cast<float4*>(bs)[1] = make_float4(rb[4], rb[5], rb[6], rb[7]);
+      float* bs = Bs + buf * kBK * kTN + b_k * kTN + b_col;
+#pragma unroll
+      for (int h = 0; h < kWN; ++h)
+        *reinterpret_cast<float4*>(bs + 64 * h) =
+            make_float4(rb[4 * h], rb[4 * h + 1], rb[4 * h + 2], rb[4 * h + 3]);
     };
 
     const int k_steps = (p.K + kBK - 1) / kBK;
@@ -117,19 +127,22 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p
       const int buf = ks & 1;
       if (ks + 1 < k_steps) load_global((ks + 1) * kBK);
       const float* as = As + buf * kBK * (kBM + kPad);
-      const float* bs = Bs + buf * kBK * kBN;
+      const float* bs = Bs + buf * kBK * kTN;
 #pragma unroll
       for (int k = 0; k < kBK; ++k) {
         const float4 a0 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + ty * 4);
         const float4 a1 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + 64 + ty * 4);
-        const float4 b0 = *reinterpret_cast<const float4*>(bs + k * kBN + tx * 4);
-        const float4 b1 = *reinterpret_cast<const float4*>(bs + k * kBN + 64 + tx * 4);
+        float b[kCols];
+#pragma unroll
+        for (int h = 0; h < kWN; ++h) {
+          const float4 v = *reinterpret_cast<const float4*>(bs + k * kTN + 64 * h + tx * 4);
+          b[4 * h] = v.x; b[4 * h + 1] = v.y; b[4 * h + 2] = v.z; b[4 * h + 3] = v.w;
+        }
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < kCols; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
       }
       if (ks + 1 < k_steps) store_shared(buf ^ 1);
       __syncthreads();
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p
       if (r >= p.M) continue;
       float* crow = p.C + (long long)r * p.ldc;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kWN; ++h) {
         const int c = n0 + h * 64 + tx * 4;
         if (kVec && c + 3 < p.N) {
           float4 o = make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2],
@@ -444,11 +457,12 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(simt_gemm_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(simt_gemm_kernel<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+    for (const void* f : {reinterpret_cast<const void*>(simt_gemm_kernel<true, 2>),
+                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 2>),
+                          reinterpret_cast<const void*>(simt_gemm_kernel<true, 4>),
+                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 4>)})
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
   });
   if (attr_err != cudaSuccess) return attr_err;
   int grid = num_ctas > 0 ? num_ctas : device_sm_count();
@@ -467,12 +481,24 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
     const size_t dyn = exclusive_sm ? 100 * 1024 : 0;
     return launch_skinny(vec, rg, grid, dyn, stream, p);
   }
-  const int tiles = p.tiles_m * p.tiles_n;
+  // Tile width: 256 columns (8 x 16 per thread) unless POAS_SIMT_TILE=128.
+  const char* tw = std::getenv("POAS_SIMT_TILE");
+  const bool wide = !(tw && std::string(tw) == "128");
+  const int tn = wide ? 256 : 128;
+  const int tiles = p.tiles_m * static_cast<int>((N + tn - 1) / tn);
   if (grid > tiles) grid = tiles;
-  if (vec)
-    simt_gemm_kernel<true><<<grid, kThreads, smem, stream>>>(p);
-  else
-    simt_gemm_kernel<false><<<grid, kThreads, smem, stream>>>(p);
+  const size_t smem_w =
+      exclusive_sm ? 120 * 1024 : (2 * kBK * (kBM + kPad) + 2 * kBK * tn) * sizeof(float);
+  if (wide) {
+    if (vec)
+      simt_gemm_kernel<true, 4><<<grid, kThreads, smem_w, stream>>>(p);
+    else
+      simt_gemm_kernel<false, 4><<<grid, kThreads, smem_w, stream>>>(p);
+  } else if (vec) {
+    simt_gemm_kernel<true, 2><<<grid, kThreads, smem_w, stream>>>(p);
+  } else {
+    simt_gemm_kernel<false, 2><<<grid, kThreads, smem_w, stream>>>(p);
+  }
   return cudaGetLastError();
 }
 

@@ -9,7 +9,7 @@ mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv > "$OUT/gpu.txt" 2>&1
 nproc > "$OUT/host.txt"; lscpu | grep -E "Model name|^CPU\(s\)" >> "$OUT/host.txt"
 
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -15 > "$OUT/pytest_gpu.txt"
+timeout 900 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.txt" 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.txt" 2>&1
 timeout 900 python bench.py --steps "$STEPS" --warmup 3 --save "$OUT/bench" > "$OUT/bench.json" 2> "$OUT/bench.err"
 timeout 600 python bench.py --m-total 65536 --size 8192 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline \
