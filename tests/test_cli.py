@@ -35,6 +35,14 @@ def test_plan_matches_reference(cli, ref, tmp_path):
             "16384x16384x16384", "--policy", "best-subset", "--out", str(out2))
     assert r.returncode == 0
     assert json.loads(out2.read_text())["makespan"] == pytest.approx(0.006448, abs=1e-6)
+    out3 = tmp_path / "s3.json"
+    prof_e2e = GOLDEN / "profiles" / "b200_e2e_r1i.profile"
+    r = run("plan", "--profile", str(prof_e2e), "--dims", "16384x16384x16384", "--policy", "overlap",
+            "--out", str(out3))
+    assert r.returncode == 0, r.stderr
+    from paper_2209_10245_b200 import poas
+
+    assert out3.read_text() == poas.plan_policy(prof_e2e.read_text(), 16384, 16384, 16384, "overlap")
 
 
 def test_profile_plan_run_cpu(cli, tmp_path):
