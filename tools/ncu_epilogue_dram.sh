@@ -1,4 +1,5 @@
 set -u
+# (dev) usage: bash tools/ncu_epilogue_dram.sh <tag>  -- writes gpurun_out/<tag>/
 OUT=gpurun_out/${1:-dram}; mkdir -p $OUT
 M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed
 for hc in normal first; do

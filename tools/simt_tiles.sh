@@ -1,4 +1,5 @@
 set -u
+# (dev) usage: bash tools/simt_tiles.sh <tag>  -- writes gpurun_out/<tag>/
 OUT=gpurun_out/${1:-simt}; mkdir -p $OUT
 timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "simt" > $OUT/pytest.txt 2>&1
 M=gpu__time_duration.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second,smsp__issue_active.avg.pct_of_peak_sustained_active
