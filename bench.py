@@ -45,7 +45,7 @@ sys.path.insert(0, str(ROOT))
 SEED = 20261017
 N_DEFAULT = 16384
 TC_SMS = 146
-TC_SMS_MULTI = 140  # N > 1: 6 SMs stay free for NCCL's broadcast kernels during the GEMM
+TC_SMS_MULTI = 144  # N > 1: 4 SMs (with the idle CUDA-core unit's 2) stay free for NCCL's broadcast kernels
 SIMT_SMS = 2
 PROFILING = "probes=9,repetitions=3,bandwidth_payload=268435456"
 
@@ -280,7 +280,7 @@ def main():
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-cpu", action="store_true", help="e2e without the host-CPU unit")
-    ap.add_argument("--b-panels", type=int, default=8,
+    ap.add_argument("--b-panels", type=int, default=16,
                     help="N > 1: B column panels broadcast separately (overlap with compute)")
     ap.add_argument("--policy", default="best-subset", choices=["reference", "best-subset"],
                     help="planner policy: the reference algorithm (byte-identical plans) or the "
