@@ -366,6 +366,8 @@ def main():
     # broadcast separately and the units start on panel p as soon as it
     # lands (executor b_ready events), overlapping the rest of the broadcast.
     P = args.b_panels if world > 1 else 1
+    while P > 1 and (n % P or (n // P) % 256):  # panels of whole pair tiles (one-launch path)
+        P //= 2
     np_ = n // P
     B32 = torch.empty(P, k, np_, device=dev, dtype=torch.float32)
     B16 = torch.empty(P, k, np_, device=dev, dtype=torch.bfloat16)
