@@ -748,7 +748,13 @@ def main():
                 "makespan_error_pct": round(100.0 * (meas_make - pred_make) / meas_make, 3),
                 "prediction": "adapted: warm-up runs re-fit the profile (dynamic scheduling); "
                               "static_plan = the profile-only plan's first run",
-                "static_plan": _static_summary(dyn),
+                "static_plan": dict(_static_summary(dyn), **(
+                    {"error_vs_timed_pct": round(100.0 * (meas_make - dyn["iterations"][0]["predicted_makespan"])
+                                                 / meas_make, 3),
+                     "error_vs_timed_note": "the profile-only prediction against the timed steps' mean "
+                                            "(same rows as the adapted plan; the first run alone is at a "
+                                            "cooler clock)"}
+                    if dyn["iterations"][0]["rows"] == rows else {})),
                 "dynamic_replans": dyn["replans"],
                 "dynamic_warmup_iterations": len(dyn["iterations"]),
                 "dynamic_warmup_steps_per_iteration": warm_reps,
