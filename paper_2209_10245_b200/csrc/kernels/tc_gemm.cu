@@ -451,19 +451,13 @@ constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
 constexpr int k2StageBytes = k2ABytes + k2BBytes;
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
-// Epilogue staging (TMA-store path): per epilogue warp (8) one 32-row x
-// 16-column fp32 box, 64-byte swizzled rows (2 KB).
+// Epilogue staging (TMA-store path): per epilogue warp two 32-row x 16-column
+// fp32 boxes, 64-byte swizzled rows (2 x 2 KB).
 constexpr int k2StagingBytes = 4 * 32 * 32 * 4;
-// Pair kernel: warp 0 TMA, warp 1 MMA, warps 2..9 epilogue -- two warps per
-// TMEM lane quadrant (warp w reads lanes 32 (w % 4) ..), each draining half
-// of the 256 accumulator columns, so a tile's epilogue takes half as long
-// (it is the whole tail of a small GEMM).
-constexpr int k2Threads = 320;
-constexpr int k2EpiWarps = 8;
 constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + k2StagingBytes + 256;
 
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
@@ -498,11 +492,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 2 * k2EpiWarps);  // leader: every epilogue warp of both CTAs
+      mbar_init(&acc_empty[b], 8);  // leader: 4 epilogue warps x 2 CTAs
     }
     for (int s = 0; s < kTileSlots; ++s) {
       mbar_init(&tile_full[s], 1);    // the leader's producer (local or remote arrive)
-      mbar_init(&tile_empty[s], 2 + 2 * k2EpiWarps);  // leader: its MMA thread + peer producer + epilogue warps
+      mbar_init(&tile_empty[s], 10);  // leader: its MMA thread + peer producer + 2 x 4 epilogue warps
     }
     fence_mbar_init();
   }
@@ -662,8 +656,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     }
   } else {
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;  // which 128 accumulator columns
-    const int col_base = half * (kBN / 2);
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
@@ -692,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
       }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      if (warp == 2 && lane == 0 && !epi_traced) {
+      if (quad == 0 && lane == 0 && !epi_traced) {
         trace_stamp(args, 5);
         epi_traced = true;
       }
@@ -706,11 +698,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
         // next 32 columns is in flight while the current ones are written
         // (TMEM reads at 64 B/clk/SM are the floor). The accumulator is
         // released as soon as its last columns are in registers.
-        uint8_t* box = s_c + (warp - 2) * 2048;  // this warp's 32 x 16 staging box
+        uint8_t* boxes = s_c + quad * 4096;
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(acc * kBN + col_base);
-        auto put_box = [&](const uint32_t* w, int c) {  // columns col_base + 16 c ..
-          if (lane == 0) bulk_wait_read<0>();  // the previous box has left smem
+                               static_cast<uint32_t>(acc * kBN);
+        auto put_box = [&](const uint32_t* w, int c) {  // 16 columns, box (c & 1)
+          uint8_t* box = boxes + (c & 1) * 2048;
+          if (lane == 0) bulk_wait_read<1>();  // the store two boxes back has left smem
           __syncwarp();
           uint8_t* my_row = box + lane * 64;
 #pragma unroll
@@ -720,7 +713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && !args.epi_skip) {
-            const int col0 = nb * kBN + col_base + c * 16;
+            const int col0 = nb * kBN + c * 16;
             if (args.accumulate)
               tma_reduce_add_2d(&map_c, box, col0, row_base);
             else if (args.hint_c != kEvictNormal)
@@ -733,14 +726,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
         uint32_t va[32], vb[32];
         tmem_ld_32x32b_x32(taddr, va);
         tmem_wait_ld();
-        constexpr int kChunks = kBN / 2 / 32;  // 32-column loads per warp
 #pragma unroll 1
-        for (int c = 0; c < kChunks; c += 2) {
+        for (int c = 0; c < kBN / 32; c += 2) {
           tmem_ld_32x32b_x32(taddr + (c + 1) * 32, vb);
           put_box(va, 2 * c);
           put_box(va + 16, 2 * c + 1);
           tmem_wait_ld();
-          if (c + 2 < kChunks) {
+          if (c + 2 < kBN / 32) {
             tmem_ld_32x32b_x32(taddr + (c + 2) * 32, va);
           } else {  // all 256 columns are in registers: free the accumulator
             tc_fence_before();
@@ -751,7 +743,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
           put_box(vb + 16, 2 * c + 3);
           tmem_wait_ld();
         }
-        if (args.trace && warp == 2 && lane == 0) {
+        if (args.trace && quad == 0 && lane == 0) {
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           args.trace[blockIdx.x * 16 + 6] = tt;
@@ -763,7 +755,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
           bulk_wait_all();
           fence_proxy_async_global();
           __threadfence();
-          const int target = args.stream_epoch * blk_tiles * 2 * k2EpiWarps;
+          const int target = args.stream_epoch * blk_tiles * 8;
           if (atomicAdd(args.block_count + blk, 1) + 1 == target) {
             __threadfence();
             atomicExch(args.block_flags + blk, args.stream_epoch);
@@ -776,14 +768,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
       const int row = row_base + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
 #pragma unroll 1
-      for (int c = 0; c < kBN / 2 / 32; ++c) {  // this warp's half of the columns
+      for (int c = 0; c < kBN / 32; ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(acc * kBN + col_base + c * 32),
+                               static_cast<uint32_t>(acc * kBN + c * 32),
                            v);
         tmem_wait_ld();
         if (row < args.M) {
-          const int col0 = nb * kBN + col_base + c * 32;
+          const int col0 = nb * kBN + c * 32;
           if (vec && col0 + 32 <= args.N) {
             float4* dst = reinterpret_cast<float4*>(crow + col0);
 #pragma unroll
@@ -1141,7 +1133,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       cudaMemsetAsync(trace_buf, 0, 2 * pairs * 16 * sizeof(unsigned long long), stream);
       args.trace = trace_buf;
     }
-    tc_gemm_2cta_kernel<<<2 * pairs, k2Threads, k2SmemBytes, stream>>>(ma, mb, mc, args);
+    tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return cudaGetLastError();
   }
