@@ -14,6 +14,10 @@ namespace poas {
 
 namespace {
 constexpr std::int64_t kMinPanelCols = 4096;
+// Fixed cost of one block's copy-out beyond its bytes (one stream wait + one
+// 2-D copy): ~20 us measured past ~128 blocks (profiles/r01_overlap/
+// grid_sweep.json: 64 x 8 blocks 37.5 ms vs 32 x 4 at 30.1 ms).
+constexpr double kBlockCopyLatency = 20e-6;
 }  // namespace
 
 std::vector<OverlapItem> overlap_link_order(int parts, int panels) {
@@ -220,7 +224,7 @@ Schedule build_overlap_schedule(const TilePlan& plan, const MachineProfile& mach
           dev, static_cast<OpsCount>(rp[static_cast<std::size_t>(b.part)]) *
                    static_cast<OpsCount>(cp[static_cast<std::size_t>(b.panel)]) *
                    static_cast<OpsCount>(dims.k)));
-      e.c_out.push_back(4.0 * m * w / bw);
+      e.c_out.push_back(4.0 * m * w / bw + (rp.size() * cp.size() > 1 ? kBlockCopyLatency : 0.0));
     }
     tiles[i].clear();  // the R x Q grid, part-major
     for (const std::int64_t m : rp)

@@ -117,7 +117,7 @@ def overlap_timeline(devs, bus, grids, m, n, k):
             cs = max(landed[ready], c_end)
             c_end = cs + slope * rp[i] * cp[j] * k + icpt
             os_ = max(c_end, free_out)
-            free_out = os_ + 4.0 * rp[i] * cp[j] / bw
+            free_out = os_ + 4.0 * rp[i] * cp[j] / bw + (20e-6 if len(rp) * len(cp) > 1 else 0.0)
             if c_start is None:
                 c_start, o_start = cs, os_
         out[d["id"]] = ((start_in, t_in), (c_start, c_end), (o_start, free_out))
@@ -238,7 +238,7 @@ def test_overlap_hand_computed(poas):
     c_end = o_end = 0.0
     for i, j, _ in block_order(len(rp), len(cp)):
         c_end = max(landed[("A", i)], landed[("B", j)], c_end) + 1e-12 * rp[i] * cp[j] * k
-        o_end = max(c_end, o_end) + 4 * rp[i] * cp[j] / 1e9
+        o_end = max(c_end, o_end) + 4 * rp[i] * cp[j] / 1e9 + (20e-6 if len(rp) * len(cp) > 1 else 0.0)
     assert s["makespan"] == pytest.approx(o_end, abs=2e-9)
     seq = 4 * (m * k + k * n) / 1e9 + 1e-12 * m * n * k + 4 * m * n / 1e9
     assert s["makespan"] < seq

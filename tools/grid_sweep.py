@@ -27,7 +27,7 @@ io = poas.GemmIO(m=m, n=n, k=k, c_host=hC.data_ptr(), ldc_host=n, resident=0,
                  a16_host=hA16.data_ptr(), lda16_host=k, b16_host=hB16.data_ptr(), ldb16_host=n)
 ex = poas.Executor(units + ";overlap=1")
 out = {}
-grids = [(64, 1), (32, 2), (32, 4), (16, 8), (32, 8), (64, 8), (16, 16), (32, 16)]
+grids = [(int(g.split("x")[0]), int(g.split("x")[1])) for g in sys.argv[1].split(",")] if len(sys.argv) > 1 else [(64, 1), (32, 2), (32, 4), (16, 8), (32, 8), (64, 8), (16, 16), (32, 16)]
 for R, Q in grids:
     s = dict(base)
     dev = dict(s["devices"][0])
