@@ -339,6 +339,11 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":
+            # The broadcast's kernels must all fit on the SMs the persistent
+            # GEMM leaves free (TC_SMS_MULTI): the GEMM spins on per-panel
+            # flags that only the broadcast can release.
+            for var in ("NCCL_MAX_NCHANNELS", "NCCL_MAX_CTAS"):
+                os.environ.setdefault(var, str(148 - TC_SMS_MULTI))
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
