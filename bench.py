@@ -440,6 +440,10 @@ def main():
         if world > 1:
             # B lives on rank 0: NCCL broadcast over NVLink inside the step,
             # one async broadcast per panel; panel p's event fires when it lands.
+            # The one-launch flag path only while the CUDA-core unit is idle:
+            # with its SMs busy the broadcast's CTAs might not all fit beside
+            # a spinning GEMM, so per-panel launches behind events are used.
+            io.b_flags = flags.data_ptr() if not simt_busy else None
             works = []
             for p in range(P):
                 works.append([dist.broadcast(B16[p], src=0, async_op=True)] +
