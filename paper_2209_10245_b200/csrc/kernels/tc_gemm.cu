@@ -32,18 +32,14 @@ namespace {
 using namespace ptx;
 
 constexpr int kBM = 128;
-constexpr int kBN = 256;
+constexpr int kBN = 256;  // pair tile width; the single-SM kernel's is a template argument
 constexpr int kBK = 64;  // one 128-byte swizzle row of 16-bit elements
-constexpr int kStages = 4;
 constexpr int kUmmaK = 16;
 constexpr int kABytes = kBM * kBK * 2;       // 16 KiB
-constexpr int kBBytes = kBN * kBK * 2;       // 32 KiB
 constexpr int kBChunkBytes = 64 * kBK * 2;   // one 64-column N chunk: 8 KiB
-constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 192;
-constexpr int kTmemCols = 512;  // two 256-column fp32 accumulators
+constexpr int kTmemCols = 512;  // pair kernel: two 256-column fp32 accumulators
 constexpr int kGroupM = 16;     // tile raster: 16 M-tiles per group for L2 reuse
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
 
 struct TcArgs {
   int M, N, K;
@@ -225,9 +221,27 @@ __device__ __forceinline__ void tile_coords_panel(const TcArgs& a, int t, int& m
   nbl = nb;
 }
 
+// Single-SM kernel, templated on its tile width: 128 x 256 (4 stages; the
+// POAS_TC_KERNEL=1cta variant) and 128 x 128 (6 stages; small GEMMs whose
+// 256 x 256 pair tiles cannot fill the SMs).
+template <int BN, int STAGES>
+struct Tile1 {
+  static constexpr int kB = BN * kBK * 2;       // B bytes per stage
+  static constexpr int kStage = kABytes + kB;
+  static constexpr int kTmem = 2 * BN;          // two accumulators
+  static constexpr size_t kSmem = 1024 + STAGES * kStage + 256;
+};
+
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, const TcArgs args) {
+  using T1 = Tile1<BN, STAGES>;
+  constexpr int kBN = BN;
+  constexpr int kStages = STAGES;
+  constexpr int kBBytes = T1::kB;
+  constexpr int kStageBytes = T1::kStage;
+  constexpr uint32_t kTmemCols = T1::kTmem;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -960,9 +974,38 @@ int* next_tile_counter() {
 }
 }  // namespace
 
-const char* tc_gemm_kernel_name(int64_t, int64_t, int64_t) {
-  const char* v = std::getenv("POAS_TC_KERNEL");
-  return v && std::string(v) == "1cta" ? "tc_gemm_kernel" : "tc_gemm_2cta_kernel";
+namespace {
+// Kernel variants: the CTA-pair kernel (256 x 256 tiles; 1/3 fewer operand
+// bytes into shared memory per MAC than a single SM's 128 x 256) wherever
+// its tiles fill the SM budget; when they cannot (fewer pair tiles than
+// pairs, e.g. 1024^3 has 16 for 74 pairs) the single-SM kernel with 128 x
+// 128 tiles spreads the work over 4x as many CTAs. POAS_TC_KERNEL = 2cta |
+// 1cta (128 x 256) | 1cta128 overrides.
+enum class TcVariant { pair, single256, single128 };
+
+TcVariant choose_variant(int64_t M, int64_t N, int budget) {
+  if (const char* v = std::getenv("POAS_TC_KERNEL")) {
+    const std::string s(v);
+    if (s == "1cta") return TcVariant::single256;
+    if (s == "1cta128") return TcVariant::single128;
+    if (s == "2cta") return TcVariant::pair;
+  }
+  const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  return pair_tiles < budget / 2 ? TcVariant::single128 : TcVariant::pair;
+}
+
+const char* variant_name(TcVariant v) {
+  switch (v) {
+    case TcVariant::single256: return "tc_gemm_kernel";
+    case TcVariant::single128: return "tc_gemm_kernel_n128";
+    case TcVariant::pair: break;
+  }
+  return "tc_gemm_2cta_kernel";
+}
+}  // namespace
+
+const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t) {
+  return variant_name(choose_variant(M, N, device_sm_count()));
 }
 
 const char* tc_gemm_scheduler_name(int64_t M, int64_t N, int64_t K) {
@@ -1033,8 +1076,12 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSmemBytes));
+    attr_err = cudaFuncSetAttribute(tc_gemm_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(Tile1<256, 4>::kSmem));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_kernel<128, 6>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Tile1<128, 6>::kSmem));
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1045,8 +1092,14 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   // memory per MAC than the single-SM kernel; faster at every size measured
   // once its scheduler fits the size, profiles/r01_tile_scheduler).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
-  const bool force_1cta = std::string(tc_gemm_kernel_name(M, N, K)) == "tc_gemm_kernel";
-  if ((P > 1 || ss) && force_1cta) return cudaErrorNotSupported;  // pair kernel only
+  const int budget_all = num_ctas > 0 ? num_ctas : device_sm_count();
+  TcVariant variant = choose_variant(M, N, budget_all);
+  if (P > 1 || ss) {  // panels / streamed operands: the pair kernel only
+    const char* v = std::getenv("POAS_TC_KERNEL");
+    if (v && std::string(v) != "2cta") return cudaErrorNotSupported;
+    variant = TcVariant::pair;
+  }
+  const bool force_1cta = variant != TcVariant::pair;
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -1137,14 +1190,18 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return cudaGetLastError();
   }
+  const int bn = variant == TcVariant::single128 ? 128 : 256;
   args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
-  args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
-  args.idesc = idesc_f16(t == AbType::bf16, kBM, kBN, false, true);
+  args.tiles_n = static_cast<int>((N + bn - 1) / bn);
+  args.idesc = idesc_f16(t == AbType::bf16, kBM, bn, false, true);
   args.group = group_override > 0 ? group_override : kGroupM;
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
-  tc_gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
+  if (bn == 128)
+    tc_gemm_kernel<128, 6><<<grid, kThreads, Tile1<128, 6>::kSmem, stream>>>(ma, mb, args);
+  else
+    tc_gemm_kernel<256, 4><<<grid, kThreads, Tile1<256, 4>::kSmem, stream>>>(ma, mb, args);
   return cudaGetLastError();
 }
 }  // namespace

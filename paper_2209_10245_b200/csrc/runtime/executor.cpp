@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <thread>
@@ -387,9 +388,8 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       Unit* u = unit[i];
       if (!u->on_gpu() || schedule.devices[i].rows == 0) continue;
       if (u->spec().kind != DeviceKind::xpu || !host16_link(u)) continue;
-      if (std::string(poas_b200::tc_gemm_kernel_name(schedule.devices[i].rows, d.n, d.k)) !=
-          "tc_gemm_2cta_kernel")
-        continue;
+      if (const char* kv = std::getenv("POAS_TC_KERNEL"))  // a forced single-SM variant
+        if (std::string(kv) != "2cta") continue;
       if (!aligned256(grid[i].parts) || !aligned256(grid[i].panels)) continue;
       if (link_order[i].size() > 128 || block_order[i].size() > 4096) continue;
       DeviceGuard g(u->spec().device);

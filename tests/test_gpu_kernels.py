@@ -182,7 +182,7 @@ def test_full_size_tc_property(torch_cuda, poas):
 
 @pytest.mark.parametrize("epilogue", ["tma", "direct"])
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
-@pytest.mark.parametrize("variant", ["1cta", "2cta"])
+@pytest.mark.parametrize("variant", ["1cta", "1cta128", "2cta"])
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
 def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched, epilogue):
     """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) under
@@ -191,8 +191,8 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
     odd SM budgets and a C pitch TMA cannot map (n = 777)."""
     import oracle
 
-    if variant == "1cta" and epilogue == "direct":
-        pytest.skip("the single-SM kernel has one epilogue")
+    if variant != "2cta" and epilogue == "direct":
+        pytest.skip("the single-SM kernels have one epilogue")
     torch = torch_cuda
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
     monkeypatch.setenv("POAS_TC_SCHED", sched)
@@ -368,3 +368,15 @@ def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
     torch.cuda.synchronize()
     assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
     assert e0.elapsed_time(e1) > 2.0  # it waited for the deliveries
+
+
+def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
+    """Pair tiles where they fill the SMs, 128 x 128 single-SM tiles where
+    they cannot; the env override wins."""
+    monkeypatch.delenv("POAS_TC_KERNEL", raising=False)
+    assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel"
+    assert poas.tc_kernel_name(4096, 4096, 4096) == "tc_gemm_2cta_kernel"
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_kernel_n128"
+    assert poas.tc_kernel_name(256, 16384, 16384) == "tc_gemm_kernel_n128"
+    monkeypatch.setenv("POAS_TC_KERNEL", "2cta")
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel"
