@@ -977,9 +977,10 @@ int* next_tile_counter() {
 namespace {
 // Kernel variants: the CTA-pair kernel (256 x 256 tiles; 1/3 fewer operand
 // bytes into shared memory per MAC than a single SM's 128 x 256) wherever
-// its tiles fill the SM budget; when they cannot (fewer pair tiles than
-// pairs, e.g. 1024^3 has 16 for 74 pairs) the single-SM kernel with 128 x
-// 128 tiles spreads the work over 4x as many CTAs. POAS_TC_KERNEL = 2cta |
+// its tiles keep the SM budget reasonably busy; when at most a quarter of
+// the pairs would have a tile (e.g. 1024^3: 16 tiles for 74 pairs) the
+// single-SM kernel with 128 x 128 tiles spreads the work over 4x as many
+// CTAs. POAS_TC_KERNEL = 2cta |
 // 1cta (128 x 256) | 1cta128 overrides.
 enum class TcVariant { pair, single256, single128 };
 
@@ -990,8 +991,11 @@ TcVariant choose_variant(int64_t M, int64_t N, int budget) {
     if (s == "1cta128") return TcVariant::single128;
     if (s == "2cta") return TcVariant::pair;
   }
+  // Single-SM 128 x 128 tiles only when the pairs would be mostly idle (at
+  // most a quarter busy): measured (profiles/r01_small_variants) 1024^3
+  // 16.1 -> 12.4 us, but 2048^3 22.3 -> 29.6 us (64 pair tiles for 74 pairs).
   const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  return pair_tiles < budget / 2 ? TcVariant::single128 : TcVariant::pair;
+  return 4 * pair_tiles <= budget / 2 ? TcVariant::single128 : TcVariant::pair;
 }
 
 const char* variant_name(TcVariant v) {

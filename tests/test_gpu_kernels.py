@@ -371,12 +371,13 @@ def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
 
 
 def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
-    """Pair tiles where they fill the SMs, 128 x 128 single-SM tiles where
-    they cannot; the env override wins."""
+    """Pair tiles unless at most a quarter of the pairs would be busy, then
+    128 x 128 single-SM tiles; the env override wins."""
     monkeypatch.delenv("POAS_TC_KERNEL", raising=False)
     assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel"
     assert poas.tc_kernel_name(4096, 4096, 4096) == "tc_gemm_2cta_kernel"
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_kernel_n128"
-    assert poas.tc_kernel_name(256, 16384, 16384) == "tc_gemm_kernel_n128"
+    assert poas.tc_kernel_name(2048, 2048, 2048) == "tc_gemm_2cta_kernel"
+    assert poas.tc_kernel_name(256, 4096, 16384) == "tc_gemm_kernel_n128"
     monkeypatch.setenv("POAS_TC_KERNEL", "2cta")
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel"
