@@ -218,3 +218,22 @@ def test_refit_resident_unit_folds_link_phases_into_compute(poas, b200_like):
         assert float(after["gpu0.tc"][key]) == pytest.approx(float(before["gpu0.tc"][key]) * g,
                                                              rel=1e-12)
     assert after["gpu0.tc"]["bandwidth"] == before["gpu0.tc"]["bandwidth"]
+
+
+def test_refit_resident_unit_by_finish(poas, b200_like):
+    """Resident operands with the unit's finish measured: the compute model
+    moves by the finish's miss (launch latency between t0 and the kernel is
+    part of it), so the re-planned finish matches the measurement."""
+    s = json.loads(poas.plan(b200_like, 16384, 16384, 16384))
+    rep = _fake_report(s)
+    tc = [d for d in rep["devices"] if d["id"] == "gpu0.tc"][0]
+    sd = [d for d in s["devices"] if d["id"] == "gpu0.tc"][0]
+    for ph in ("copy_in", "copy_out"):
+        tc[ph]["measured"] = 0.0
+    fin_pred = sd["copy_out"][1]
+    tc["finish"] = {"measured": fin_pred + 0.0004, "predicted": fin_pred, "error_pct": 0.0}
+    out = poas.refit_profile(b200_like, rep, 1.0)
+    before, after = _profile_fields(b200_like), _profile_fields(out)
+    g = (tc["compute"]["predicted"] + 0.0004) / tc["compute"]["predicted"]
+    for key in ("slope", "intercept"):
+        assert float(after["gpu0.tc"][key]) == pytest.approx(float(before["gpu0.tc"][key]) * g, rel=1e-9)
