@@ -650,7 +650,7 @@ def main():
         local_world = env_int("LOCAL_WORLD_SIZE", world)
         e2e_profiles = {}
 
-        def run_e2e(tc_elem, overlap):
+        def run_e2e(tc_elem, overlap, pipeline=False):
             units_e2e = units_res.replace("elem=2:link=hbm", f"elem={tc_elem}:link=pcie").replace(
                 "elem=4:link=hbm", "elem=4:link=pcie")
             if not args.no_e2e_cpu:
@@ -665,7 +665,8 @@ def main():
                     units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048", bus=True)
             prof_e2e = e2e_profiles[tc_elem]
             ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
-            ex_e2e = poas.Executor(units_e2e + (";overlap=1" if overlap else ""))
+            ex_e2e = poas.Executor(units_e2e + (";overlap=1" if overlap else "")
+                                   + (";pipeline=1" if pipeline else ""))
             io_h = poas.GemmIO(m=m, n=n, k=k, a_host=hA.data_ptr(), lda_host=k, b_host=hB.data_ptr(),
                                ldb_host=n, c_host=hC.data_ptr(), ldc_host=n, resident=0)
             if tc_elem == 2:
@@ -713,13 +714,16 @@ def main():
                    "makespan_error_pct": round(r_e2e["makespan_error_pct"], 3),
                    "static_plan": _static_summary(dyn_e2e),
                    "dynamic_replans": dyn_e2e["replans"],
-                   "units": units_e2e + (";overlap=1" if overlap else ""),
+                   "units": units_e2e + (";overlap=1" if overlap else "") + (";pipeline=1" if pipeline else ""),
+                   "gemm_latency_ms": round(r_e2e["measured_makespan"] * 1e3, 3),
                    "path": "poas_b200_execute (C ABI), pinned host "
                            + ("bf16 A/B for the tensor unit (fp32 for the others)" if tc_elem == 2
                               else "fp32 A/B converted on the GPU")
                            + ", fp32 C; H2D + compute + D2H in every step"
-                           + ("; copies overlapped with compute (row parts)" if overlap
-                              else "; synchronous copies (the paper's scheme)")}
+                           + ("; copies overlapped with compute (row parts x column panels)" if overlap
+                              else "; synchronous copies (the paper's scheme)")
+                           + ("; consecutive steps pipelined (step i+1's copies start beside step i's "
+                              "copy-out tail)" if pipeline else "")}
             bw = [float(ln.split()[1]) for ln in prof_e2e.splitlines() if ln.startswith("bandwidth ")]
             bw = max(bw) if bw else 0.0
             if bw > 0:
@@ -728,7 +732,8 @@ def main():
                 out["link_bound_ms"] = round(link_s * 1e3, 3)
                 out["link_bandwidth_gbs"] = round(bw / 1e9, 2)
             if save and rank == 0:
-                tag = ("e2e" if tc_elem == 2 else "e2e_fp32") + ("" if overlap else "_sync")
+                tag = ("e2e" if tc_elem == 2 else "e2e_fp32") + ("" if overlap else "_sync") + (
+                    "_pipelined" if pipeline else "")
                 (save / f"profile_{tag}.txt").write_text(prof_e2e)
                 (save / f"dynamic_{tag}.json").write_text(json.dumps(dyn_e2e, indent=1))
                 (save / f"report_{tag}.json").write_text(json.dumps(r_e2e, indent=1))
@@ -738,6 +743,7 @@ def main():
         e2e = run_e2e(2, overlap=True)
         e2e["fp32_host"] = run_e2e(4, overlap=True)
         e2e["synchronous"] = run_e2e(2, overlap=False)
+        e2e["pipelined"] = run_e2e(2, overlap=True, pipeline=True)
 
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu_baseline = None

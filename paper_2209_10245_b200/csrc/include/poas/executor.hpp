@@ -108,6 +108,7 @@ class Executor {
   bool bus_ = true;
   bool lend_ = true;      // idle units' SMs go to the one busy unit on their GPU
   bool overlap_ = false;  // host runs: pipeline link units' row parts (poas/overlap.hpp)
+  bool pipeline_ = false;  // overlapped host runs: consecutive repeats overlap (units.hpp)
   // Per unit (units_ order; null for cpu units): the host->device and
   // device->host copy streams of overlapped runs.
   std::vector<void*> h2d_, d2h_;

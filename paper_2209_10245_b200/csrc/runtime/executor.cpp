@@ -158,7 +158,7 @@ class StartGates {
 
 Executor::Executor(const std::string& spec) {
   const std::vector<poas_b200::UnitSpec> specs =
-      poas_b200::parse_unit_list(spec, &bus_, &lend_, &overlap_);
+      poas_b200::parse_unit_list(spec, &bus_, &lend_, &overlap_, &pipeline_);
   std::vector<DeviceIdentity> ids;
   for (const auto& s : specs) {
     if (find(s.id)) fail(errc::invalid_argument, "duplicate unit id '" + s.id + "'");
@@ -432,6 +432,22 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       cuda_check(cudaStreamWaitEvent(h2d[i], st.ready, 0), "wait stream setup");
       cuda_check(cudaStreamWaitEvent(d2h[i], st.ready, 0), "wait stream setup");
     }
+  // Pipelined repeats (units token "pipeline=1"): one busy GPU unit on the
+  // streamed path, no host-CPU unit. Repeat r+1 is queued behind repeat r's
+  // GEMM only (its gate sits on the compute stream after that launch), not
+  // behind r's copy-out: its host->device copies run beside r's
+  // device->host tail. A and B staging are free again once r's GEMM is
+  // done; C is double-buffered (r+1 writes one buffer while r's copy-out
+  // reads the other; r+2 waits for r's copy-out).
+  std::size_t busy_gpu_units = 0, busy_unit = nd;
+  for (std::size_t i = 0; i < nd; ++i)
+    if (unit[i]->on_gpu() && schedule.devices[i].rows > 0) {
+      ++busy_gpu_units;
+      busy_unit = i;
+    }
+  const bool pipelined = overlapped && pipeline_ && !any_cpu && busy_gpu_units == 1 &&
+                         sstate[busy_unit].item_flags != nullptr;
+
   // One repeat of an overlapped link unit: host->device (A parts and B
   // panels interleaved in link order), one GEMM per block as soon as its A
   // part and B panel landed, each block's C device->host as soon as it is
@@ -492,6 +508,11 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     if (sstate[i].item_flags) {  // one streamed launch; copy-out on block flags
       const StreamState& st = sstate[i];
       const int epoch = static_cast<int>(rr) + 1;
+      float* cb = c;  // pipelined: odd repeats write the second C buffer
+      if (pipelined && (rr & 1))
+        cb = static_cast<float*>(u->scratch(6).ensure(static_cast<std::size_t>(r * d.n) * 4));
+      if (pipelined && rr >= 2)  // that buffer's previous copy-out is done
+        cuda_check(cudaStreamWaitEvent(cs, ev[rr - 2][i].co1, 0), "wait C buffer");
       cuda_check(cudaEventRecord(e.cp0, cs), "cudaEventRecord");
       poas_b200::TcStream ts;
       ts.blocks = st.blocks;
@@ -500,7 +521,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       ts.block_count = st.block_count;
       ts.block_flags = st.block_flags;
       ts.epoch = epoch;
-      u->gemm_stream(r, d.n, d.k, a_l, lda_l, b_l, ldb_l, c, d.n, ts, extra_sms[i]);
+      u->gemm_stream(r, d.n, d.k, a_l, lda_l, b_l, ldb_l, cb, d.n, ts, extra_sms[i]);
       cuda_check(cudaEventRecord(e.cp1, cs), "cudaEventRecord");
       if (bus_ && prev_out != nd) cuda_check(cudaStreamWaitEvent(ds, ev[rr][prev_out].co1, 0), "wait");
       for (std::size_t bi = 0; bi < block_order[i].size(); ++bi) {
@@ -509,7 +530,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         cuda_check(poas_b200::wait_flag(st.block_flags + bi, epoch, ds), "wait block flag");
         if (bi == 0) cuda_check(cudaEventRecord(e.co0, ds), "cudaEventRecord");
         copy2d(io.c_host + (r0 + roff[p]) * io.ldc_host + coff[q], io.ldc_host,
-               c + roff[p] * d.n + coff[q], d.n, rp[p], cp[q], 4, cudaMemcpyDeviceToHost, ds);
+               cb + roff[p] * d.n + coff[q], d.n, rp[p], cp[q], 4, cudaMemcpyDeviceToHost, ds);
       }
       cuda_check(cudaEventRecord(e.co1, ds), "cudaEventRecord");
       return;
@@ -611,7 +632,7 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     for (const auto& [dev, h] : host_unit) {
       DeviceGuard g(dev);
       cudaStream_t hs = unit[h]->stream();
-      if (rep > 0 && !host_sync_repeats)  // chain after the other units' previous repeat
+      if (rep > 0 && !host_sync_repeats && !pipelined)  // chain after the previous repeat
         for (std::size_t j = 0; j < nd; ++j)
           if ((j != h || overlapped) && unit[j]->on_gpu() && schedule.devices[j].rows > 0 &&
               unit[j]->spec().device == dev)

@@ -89,11 +89,12 @@ UnitSpec parse_unit_spec(const std::string& text) {
 }
 
 std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus, bool* lend,
-                                      bool* overlap) {
+                                      bool* overlap, bool* pipeline) {
   std::vector<UnitSpec> out;
   if (bus) *bus = true;
   if (lend) *lend = true;
   if (overlap) *overlap = false;
+  if (pipeline) *pipeline = false;
   for (const std::string& item : split(text, ';')) {
     if (item.rfind("bus=", 0) == 0) {
       if (bus) *bus = item.substr(4) != "0" && item.substr(4) != "false";
@@ -105,6 +106,10 @@ std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus, bool* 
     }
     if (item.rfind("overlap=", 0) == 0) {
       if (overlap) *overlap = item.substr(8) != "0" && item.substr(8) != "false";
+      continue;
+    }
+    if (item.rfind("pipeline=", 0) == 0) {
+      if (pipeline) *pipeline = item.substr(9) != "0" && item.substr(9) != "false";
       continue;
     }
     out.push_back(parse_unit_spec(item));

@@ -51,9 +51,13 @@ UnitSpec parse_unit_spec(const std::string& text);
 // link, default 1), "lend=0|1" (idle units lend their SMs to the one busy
 // unit on the same GPU during execute, default 1) and "overlap=0|1" (host
 // operand runs pipeline each link unit's row parts: copies overlap compute,
-// see poas/overlap.hpp; default 0 = the paper's synchronous copies).
+// see poas/overlap.hpp; default 0 = the paper's synchronous copies) and
+// "pipeline=0|1" (overlapped host runs of one streamed tensor unit: repeat
+// r+1's host->device copies start once repeat r's GEMM is done, beside
+// repeat r's device->host tail; C double-buffered; default 0).
 std::vector<UnitSpec> parse_unit_list(const std::string& text, bool* bus = nullptr,
-                                      bool* lend = nullptr, bool* overlap = nullptr);
+                                      bool* lend = nullptr, bool* overlap = nullptr,
+                                      bool* pipeline = nullptr);
 
 // Device scratch that grows on demand and is reused across calls.
 class DeviceBuffer {
@@ -128,7 +132,7 @@ class Unit : public poas::DeviceBackend {
   PinnedBuffer xfer_host_;
   std::vector<float> host_a_, host_b_, host_c_;
   std::int64_t probe_side_ = 0;
-  DeviceBuffer scratch_[6];  // 0-4 staging, 5 streamed-launch state
+  DeviceBuffer scratch_[7];  // 0-4 staging, 5 streamed-launch state, 6 second C (pipelined)
 };
 
 // RAII device selection.

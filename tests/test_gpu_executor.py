@@ -487,3 +487,14 @@ def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
     assert not np.isnan(got).any()
     assert oracle.rel_frobenius(got, exp) <= TOL
     assert rep["devices"][0].get("overlapped") is True
+    if link == "bf16" and grid == "aligned":
+        # pipelined repeats (one streamed unit): repeat r+1's copies start
+        # beside r's copy-out tail, C double-buffered -- every repeat exact
+        exp_host = hC.clone()
+        ex_p = poas.Executor(units + ";overlap=1;pipeline=1")
+        for reps in (1, 2, 5):
+            hC.fill_(float("nan"))
+            rep = ex_p.execute(sched_text, io, reps)
+            assert oracle.rel_frobenius(hC.numpy(), exp) <= TOL, reps
+            assert torch.equal(hC, exp_host), reps
+            assert rep["repeats"] == reps and rep["measured_makespan"] > 0
