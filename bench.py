@@ -633,11 +633,13 @@ def main():
     # tensor unit's link carries 16-bit A/B (the reference's XPU link model,
     # elem_size 2; the workload's operand precision, as in the resident run)
     # with overlapped copies (planner policy "overlap" + executor
-    # "overlap=1": B, then A row parts host->device while earlier parts
-    # compute and their C goes device->host). Alongside:
-    # fp32 host A/B converted on the GPU, and the paper's synchronous copies
-    # (copy-in, compute, copy-out per unit). CPU-side units (host cores, the
-    # CUDA-core unit's fp32 operands) read the fp32 host copies.
+    # "overlap=1": A row parts and B column panels host->device while
+    # earlier blocks compute and their C goes device->host)
+    # and consecutive steps pipelined ("pipeline=1"). Alongside: every step
+    # isolated, fp32 host A/B converted on the GPU, and the paper's
+    # synchronous copies (copy-in, compute, copy-out per unit). CPU-side
+    # units (host cores, the CUDA-core unit's fp32 operands) read the fp32
+    # host copies.
     e2e = None
     if not args.no_e2e:
         hA = torch.empty(m, k, dtype=torch.float32, pin_memory=True)
@@ -740,10 +742,14 @@ def main():
                 (save / f"schedule_{tag}.json").write_text(sched_e2e)
             return out
 
-        e2e = run_e2e(2, overlap=True)
+        # headline: a stream of GEMMs, each step's copies and GEMM overlapped
+        # and consecutive steps pipelined; beside it the same with every step
+        # isolated (its latency is the per-GEMM makespan), fp32 host operands,
+        # and the paper's synchronous copies
+        e2e = run_e2e(2, overlap=True, pipeline=True)
+        e2e["single_step"] = run_e2e(2, overlap=True)
         e2e["fp32_host"] = run_e2e(4, overlap=True)
         e2e["synchronous"] = run_e2e(2, overlap=False)
-        e2e["pipelined"] = run_e2e(2, overlap=True, pipeline=True)
 
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu_baseline = None
