@@ -153,6 +153,13 @@ def test_cpu_only_executor_run(poas, ref):
     d = rep["devices"][0]
     assert d["rows"] == m and d["compute"]["measured"] > 0 and d["copy_in"]["measured"] == 0
     assert rep["measured_makespan"] == pytest.approx(d["finish"]["measured"])
+    # machine tokens (shared link, lending, overlapped / pipelined copies)
+    # leave a host-only run and the machine identity unchanged
+    ex2 = poas.Executor(units + ";bus=1;lend=0;overlap=1;pipeline=1")
+    assert ex2.machine_hash == ex.machine_hash
+    C[:] = np.nan
+    ex2.execute(sched, io, 1)
+    assert oracle.rel_frobenius(C, oracle.gemm_rows_f64(A, B, 0)) <= 2e-5
 
 
 def test_unit_spec_parsing(poas):
