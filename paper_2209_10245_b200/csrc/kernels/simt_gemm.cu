@@ -43,8 +43,8 @@ struct SimtArgs {
 // kWN = 2: 128 x 128 CTA tile, 8 x 8 per thread; kWN = 4: 128 x 256, 8 x 16
 // per thread (four 4-column quadrants 64 apart: fewer shared-memory reads
 // per FMA).
-template <bool kVec, int kWN>
-__global__ void __launch_bounds__(kThreads, 1) simt_gemm_kernel(const SimtArgs p) {
+template <bool kVec, int kWN, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) simt_gemm_kernel(const SimtArgs p) {
   constexpr int kTN = 64 * kWN;  // CTA tile width
   constexpr int kCols = 4 * kWN;  // per-thread columns
   extern __shared__ float4 smem4[];
@@ -460,7 +460,9 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
     for (const void* f : {reinterpret_cast<const void*>(simt_gemm_kernel<true, 2>),
                           reinterpret_cast<const void*>(simt_gemm_kernel<false, 2>),
                           reinterpret_cast<const void*>(simt_gemm_kernel<true, 4>),
-                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 4>)})
+                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 4>),
+                          reinterpret_cast<const void*>(simt_gemm_kernel<true, 2, 2>),
+                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 2, 2>)})
       if (attr_err == cudaSuccess)
         attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
   });
@@ -481,19 +483,32 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
     const size_t dyn = exclusive_sm ? 100 * 1024 : 0;
     return launch_skinny(vec, rg, grid, dyn, stream, p);
   }
-  // Tile width: 256 columns (8 x 16 per thread) unless POAS_SIMT_TILE=128.
+  // Tile: 128 x 256 (8 x 16 per thread, one CTA per SM) by default;
+  // POAS_SIMT_TILE=128: 128 x 128 (8 x 8), one CTA per SM; =128x2: 128 x 128
+  // with registers capped so two CTAs share an SM (16 warps to hide
+  // shared-memory latency). Exclusive units pad shared memory so that no
+  // tensor-core CTA (210 KB) fits beside them.
   const char* tw = std::getenv("POAS_SIMT_TILE");
-  const bool wide = !(tw && std::string(tw) == "128");
+  const std::string tile = tw ? tw : "256";
+  const bool wide = tile != "128" && tile != "128x2";
+  const bool two = tile == "128x2";
   const int tn = wide ? 256 : 128;
+  const int per_sm = two ? 2 : 1;
   const int tiles = p.tiles_m * static_cast<int>((N + tn - 1) / tn);
+  grid *= per_sm;
   if (grid > tiles) grid = tiles;
-  const size_t smem_w =
-      exclusive_sm ? 120 * 1024 : (2 * kBK * (kBM + kPad) + 2 * kBK * tn) * sizeof(float);
+  const size_t smem_w = exclusive_sm ? (two ? 100 * 1024 : 120 * 1024)
+                                     : (2 * kBK * (kBM + kPad) + 2 * kBK * tn) * sizeof(float);
   if (wide) {
     if (vec)
       simt_gemm_kernel<true, 4><<<grid, kThreads, smem_w, stream>>>(p);
     else
       simt_gemm_kernel<false, 4><<<grid, kThreads, smem_w, stream>>>(p);
+  } else if (two) {
+    if (vec)
+      simt_gemm_kernel<true, 2, 2><<<grid, kThreads, smem_w, stream>>>(p);
+    else
+      simt_gemm_kernel<false, 2, 2><<<grid, kThreads, smem_w, stream>>>(p);
   } else if (vec) {
     simt_gemm_kernel<true, 2><<<grid, kThreads, smem_w, stream>>>(p);
   } else {

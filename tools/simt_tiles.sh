@@ -3,7 +3,7 @@ set -u
 OUT=gpurun_out/${1:-simt}; mkdir -p $OUT
 timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "simt" > $OUT/pytest.txt 2>&1
 M=gpu__time_duration.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second,smsp__issue_active.avg.pct_of_peak_sustained_active
-for tw in 256 128; do
+for tw in 256 128 128x2; do
   POAS_SIMT_TILE=$tw timeout 300 python -c "
 import sys; sys.path.insert(0,'tools'); sys.argv=['x']
 import ncu_target as t
