@@ -185,44 +185,62 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- reference
-def reference_cpu_path(n: int, sample_rows: int | None = None, reps: int = 1):
+class ReferenceCPUPath:
     """The reference's CPU path for an N^3 GEMM on this host: the reference
     planner (oracle/_ref/libpoasref.so, compiled from /root/reference) plans
     a CPU-only machine; the oracle port executes a bounded sample of that
-    plan's tiles (the first m-part of every k'-strip, split-K). Returns
-    (TFLOP/s, seconds per rep, sample description, cores)."""
-    import numpy as np
-    import oracle
+    plan's work (the first `rows` rows of A against every k'-strip of B,
+    split-K, as the plan's tiles do) on all host cores. B and the largest A
+    sample are generated once."""
 
-    cores = os.cpu_count() or 1
-    # CPU-only machine, reference ProfilingConfig defaults (cpu sides 1000-2000).
-    cfg = ("poas-machine v1\n\nbus true\n\ndevice cpu0\nkind cpu\ntrue_slope 2e-12\n"
-           "true_intercept 0.0005\nelem_size 4\nnoise 0\ndrift 0\ncache_bytes 33554432\n")
-    profile = oracle.ref.exact_profile(cfg)
-    t0 = time.perf_counter()
-    sched = json.loads(oracle.ref.plan(profile, n, n, n))
-    plan_s = time.perf_counter() - t0
-    dev = sched["devices"][0]
-    tiles = dev["tiles"]
-    kp = tiles[0]["k"]
-    strips = n // kp
-    parts = len(tiles) // strips
-    rows = tiles[0]["m"] if sample_rows is None else sample_rows
-    tile_m = [rows] * strips  # one m-part per strip: rows x k, split-K over strips
-    A = oracle.fill_uniform(rows, n, oracle.stream_seed(SEED, "A"), total_cols=n)
-    B = oracle.fill_uniform(n, n, oracle.stream_seed(SEED, "B"))
-    oracle.exec_tiles_f32(A[:8], B, [8] * strips, kp)  # warm-up (page-in, thread spin-up)
-    times = []
-    for _ in range(reps):
+    def __init__(self, n: int, max_rows: int):
+        import oracle
+
+        self.oracle, self.n = oracle, n
+        self.cores = os.cpu_count() or 1
+        # CPU-only machine, reference ProfilingConfig defaults (cpu sides 1000-2000).
+        cfg = ("poas-machine v1\n\nbus true\n\ndevice cpu0\nkind cpu\ntrue_slope 2e-12\n"
+               "true_intercept 0.0005\nelem_size 4\nnoise 0\ndrift 0\ncache_bytes 33554432\n")
+        profile = oracle.ref.exact_profile(cfg)
         t0 = time.perf_counter()
-        oracle.exec_tiles_f32(A, B, tile_m, kp)
-        times.append(time.perf_counter() - t0)
-    sec = sum(times) / len(times)
-    tflops = 2.0 * rows * n * n / sec / 1e12
-    sample = (f"reference CPU-only plan of {n}^3 ({len(tiles)} tiles {parts}x{strips}, k'={kp}) "
-              f"planned by oracle/_ref in {plan_s * 1e6:.0f} us; timed: {rows} rows x full K "
-              f"({strips} split-K tiles of {rows}x{kp}x{n}) by the oracle port, fp32, {cores} threads")
-    return tflops, sec, sample, cores
+        sched = json.loads(oracle.ref.plan(profile, n, n, n))
+        self.plan_s = time.perf_counter() - t0
+        tiles = sched["devices"][0]["tiles"]
+        self.kp = tiles[0]["k"]
+        self.strips = n // self.kp
+        self.parts = len(tiles) // self.strips
+        self.ntiles = len(tiles)
+        self.A = oracle.fill_uniform(min(max_rows, n), n, oracle.stream_seed(SEED, "A"), total_cols=n)
+        self.B = oracle.fill_uniform(n, n, oracle.stream_seed(SEED, "B"))
+        oracle.exec_tiles_f32(self.A[:8], self.B, [8] * self.strips, self.kp)  # page-in, thread spin-up
+
+    def run(self, rows: int) -> float:
+        """Seconds for `rows` rows x full K (split-K over the plan's strips)."""
+        t0 = time.perf_counter()
+        self.oracle.exec_tiles_f32(self.A[:rows], self.B, [rows] * self.strips, self.kp)
+        return time.perf_counter() - t0
+
+    def rows_for(self, seconds: float) -> int:
+        """Rows whose sample takes about `seconds` (multiples of 64)."""
+        t = self.run(64)
+        rows = int(64 * seconds / max(t, 1e-6)) // 64 * 64
+        return max(64, min(rows, self.A.shape[0]))
+
+    def sample(self, rows: int) -> str:
+        return (f"reference CPU-only plan of {self.n}^3 ({self.ntiles} tiles {self.parts}x{self.strips}, "
+                f"k'={self.kp}) planned by oracle/_ref in {self.plan_s * 1e6:.0f} us; timed: {rows} rows x "
+                f"full K ({self.strips} split-K tiles of {rows}x{self.kp}x{self.n}) by the oracle port, "
+                f"fp32, {self.cores} threads")
+
+
+def reference_cpu_path(n: int, sample_rows: int | None = None, reps: int = 1, seconds: float = 10.0):
+    """(TFLOP/s, seconds per rep, sample description, cores) of the
+    reference CPU path on a bounded sample: `sample_rows` rows, or as many
+    as take about `seconds`."""
+    ref = ReferenceCPUPath(n, sample_rows or 8192)
+    rows = sample_rows or ref.rows_for(seconds)
+    sec = sum(ref.run(rows) for _ in range(reps)) / reps
+    return 2.0 * rows * n * n / sec / 1e12, sec, ref.sample(rows), ref.cores
 
 
 def run_reference(args):
@@ -231,12 +249,14 @@ def run_reference(args):
     if rank != 0:
         return 0
     n = args.n
-    rows = args.ref_rows
-    reps_w, reps_k = args.warmup, args.steps
-    # warm-up steps
-    for _ in range(max(0, reps_w)):
-        reference_cpu_path(n, sample_rows=rows, reps=1)
-    tfl, sec, sample, cores = reference_cpu_path(n, sample_rows=rows, reps=max(1, reps_k))
+    reps_w, reps_k = max(0, args.warmup), max(1, args.steps)
+    # each step a bounded sample: ~10 s, and the whole run under ~3 minutes
+    ref = ReferenceCPUPath(n, args.ref_rows or 8192)
+    rows = args.ref_rows or ref.rows_for(min(10.0, 150.0 / (reps_w + reps_k)))
+    for _ in range(reps_w):
+        ref.run(rows)
+    sec = sum(ref.run(rows) for _ in range(reps_k)) / reps_k
+    tfl, sample, cores = 2.0 * rows * n * n / sec / 1e12, ref.sample(rows), ref.cores
     line = {
         "metric": "co-executed GEMM TFLOP/s at N=16384 (1/2/4/8 B200); speedup vs best single unit",
         "value": round(tfl, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": reps_k,
