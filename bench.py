@@ -492,12 +492,13 @@ def main():
     # the timed region (the adapted model then predicts it)
     # (--no-adapt: W plain executions of the static plan -- e.g. under a
     # profiler, whose serialised launches make measured phases meaningless)
-    # Each round runs as many steps back to back as the timed region (its
-    # duty cycle: shorter bursts with host gaps run measurably cooler and
-    # faster), for >= 0.6 s in all, so the last re-fit -- the prediction of
-    # the timed steps -- saw the power-capped state they run in.
-    warm_reps = max(5, args.steps)
-    warm_iters = min(50, max(args.warmup, int(0.6 / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
+    # Each round runs 5 steps back to back (the timed region's duty cycle:
+    # single steps with host gaps run measurably cooler and faster), for
+    # >= 0.3 s in all. (Rounds as long as the timed region were tried:
+    # adapted errors -6..-11% against -6..+4% with 5-step rounds,
+    # profiles/r01_warmup.)
+    warm_reps = 5
+    warm_iters = min(100, max(args.warmup, int(0.3 / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
     if args.no_adapt:
         warm_iters, warm_reps = args.warmup, 1
     dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
