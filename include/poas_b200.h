@@ -217,9 +217,11 @@ typedef struct {
  * the profile that produced the schedule; "bus=0|1" token for the link
  * topology, default shared; "lend=0|1": when a schedule leaves all but one
  * unit of a GPU idle, the busy unit runs on their SMs too, default 1;
- * "overlap=0|1": host-operand runs pipeline every link unit's row parts --
- * the schedule's tiles -- on separate H2D / compute / D2H streams, default 0
- * = the paper's synchronous copy-in, compute, copy-out). */
+ * "overlap=0|1": host-operand runs overlap every link unit's copies with its
+ * GEMMs over the schedule's grid of row parts x column panels (its tiles) on
+ * separate H2D / compute / D2H streams, default 0 = the paper's synchronous
+ * copy-in, compute, copy-out; "pipeline=0|1": with overlap and one busy
+ * streamed tensor unit, consecutive repeats overlap too, default 0). */
 int poas_b200_executor_create(const char* units, poas_executor_t* out);
 void poas_b200_executor_destroy(poas_executor_t ex);
 /* machine_identity_hash over the executor's units (device_model.hpp:130). */
