@@ -330,6 +330,8 @@ def main():
                     help="reuse a poas-profile v1 file for the resident units instead of probing "
                          "('{rank}' is replaced by the rank); probes timed under a profiler are "
                          "meaningless")
+    ap.add_argument("--warmup-seconds", type=float, default=1.5,
+                    help="minimum length of the dynamic warm-up (steady power-capped state)")
     ap.add_argument("--probe-warmup", type=float, default=0.5,
                     help="seconds of tensor-core GEMMs before profiling (0: probe a cool GPU)")
     ap.add_argument("--no-adapt", action="store_true",
@@ -492,13 +494,14 @@ def main():
     # the timed region (the adapted model then predicts it)
     # (--no-adapt: W plain executions of the static plan -- e.g. under a
     # profiler, whose serialised launches make measured phases meaningless)
-    # Each round runs 5 steps back to back (the timed region's duty cycle:
-    # single steps with host gaps run measurably cooler and faster), for
-    # >= 0.3 s in all. (Rounds as long as the timed region were tried:
-    # adapted errors -6..-11% against -6..+4% with 5-step rounds,
-    # profiles/r01_warmup.)
+    # Each round runs 5 steps back to back (single steps with host gaps run
+    # cooler and faster), for >= --warmup-seconds in all: long enough for the
+    # power cap to settle, so the timed steps run in the steady state the
+    # last re-fit saw (0.3 s left the controller mid-transient: a short
+    # timed region then ran at up to 1900 MHz against a model fit at ~1400,
+    # -13% adapted error; profiles/r01_warmup).
     warm_reps = 5
-    warm_iters = min(100, max(args.warmup, int(0.3 / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
+    warm_iters = min(400, max(args.warmup, int(args.warmup_seconds / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
     if args.no_adapt:
         warm_iters, warm_reps = args.warmup, 1
     dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
