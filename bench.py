@@ -330,7 +330,9 @@ def main():
                     help="reuse a poas-profile v1 file for the resident units instead of probing "
                          "('{rank}' is replaced by the rank); probes timed under a profiler are "
                          "meaningless")
-    ap.add_argument("--warmup-seconds", type=float, default=0.3,
+    ap.add_argument("--alpha-resident", type=float, default=0.2,
+                    help="dynamic scheduling of the resident run: EWMA weight of the newest round")
+    ap.add_argument("--warmup-seconds", type=float, default=1.0,
                     help="minimum length of the dynamic warm-up (steady power-capped state)")
     ap.add_argument("--probe-warmup", type=float, default=0.5,
                     help="seconds of tensor-core GEMMs before profiling (0: probe a cool GPU)")
@@ -495,14 +497,16 @@ def main():
     # (--no-adapt: W plain executions of the static plan -- e.g. under a
     # profiler, whose serialised launches make measured phases meaningless)
     # Each round runs 5 steps back to back (single steps with host gaps run
-    # cooler and faster), for >= --warmup-seconds in all; a rehearsal of the
-    # timed sequence follows (below).
+    # cooler and faster), for >= --warmup-seconds in all. Under the power
+    # cap the step time wanders +-8% from one 60 ms block to the next
+    # (profiles/r01_warmup/power_dynamics_*.json), so the re-fit is an EWMA
+    # (alpha 0.2: ~25 steps) of the steady state rather than the last block.
     warm_reps = 5
     warm_iters = min(400, max(args.warmup, int(args.warmup_seconds / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
     if args.no_adapt:
         warm_iters, warm_reps = args.warmup, 1
     dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
-                         alpha=args.alpha, repeats=warm_reps,
+                         alpha=args.alpha_resident, repeats=warm_reps,
                          replan_threshold_pct=1e9 if args.no_adapt else args.replan_threshold)
     schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
     sched = json.loads(schedule)
@@ -534,18 +538,6 @@ def main():
             dist.barrier()
         return e0.elapsed_time(e1), reps, clk
 
-    # Rehearsal: the exact timed sequence once more, untimed for the line;
-    # its measurement is the last re-fit (the power cap's clock depends on
-    # the recent duty cycle -- a model fit inside the warm-up rounds missed
-    # a short timed region by up to 19%, profiles/r01_warmup). Then the
-    # timed steps, predicted by that re-fit.
-    if not args.no_adapt:
-        _, reh, _ = timed_steps()
-        prof_reh = poas.refit_profile(dyn["profile"], reh[-1], 1.0)
-        schedule = poas.plan_policy(prof_reh, m, n, k, args.policy)
-        sched = json.loads(schedule)
-        rows = {d["id"]: d["rows"] for d in sched["devices"]}
-        simt_busy = rows.get(simt_id, 0) > 0
     ms_total, reports, clk = timed_steps()
     t = torch.tensor([ms_total], device=dev)
     if world > 1:
