@@ -119,16 +119,17 @@ MachineProfile refit_profile(const MachineProfile& prior, const std::vector<Devi
       // so the measured compute phase stands for copy-in + compute +
       // copy-out. Move the compute model so the three predicted phases sum
       // to the measurement; the link model is left as profiled.
-      // With the unit's finish measured (from its repeat's t0), the target
-      // is its predicted finish: that also absorbs the launch latency
-      // between t0 and the kernel's start, which dominates small GEMMs.
-      if (o.finish.measured > 0.0 && o.finish.predicted > 0.0 && o.compute.predicted > 0.0 &&
-          std::isfinite(o.finish.measured)) {
-        const double target =
-            o.compute.predicted + options.alpha * (o.finish.measured - o.finish.predicted);
-        g = std::clamp(target / o.compute.predicted, 1.0 / options.max_step, options.max_step);
+      // With the unit's finish measured (from its repeat's t0), its whole
+      // predicted timeline -- compute and the modelled streaming of its
+      // operands -- scales by the finish ratio: that also absorbs the
+      // launch latency between t0 and the kernel's start (small GEMMs), and
+      // converges for a unit whose time is mostly the operand stream (a
+      // one-row CUDA-core share reads all of B; scaling compute alone would
+      // need thousands of clamped steps).
+      if (update_factor(o.finish, options, &g)) {
         d->compute.slope *= g;
         d->compute.intercept *= g;
+        if (d->bandwidth > 0.0) d->bandwidth /= g;
         continue;
       }
       PhaseError whole;

@@ -221,9 +221,10 @@ def test_refit_resident_unit_folds_link_phases_into_compute(poas, b200_like):
 
 
 def test_refit_resident_unit_by_finish(poas, b200_like):
-    """Resident operands with the unit's finish measured: the compute model
-    moves by the finish's miss (launch latency between t0 and the kernel is
-    part of it), so the re-planned finish matches the measurement."""
+    """Resident operands with the unit's finish measured: its whole timeline
+    (compute and the modelled operand stream) scales by the finish ratio
+    (launch latency between t0 and the kernel is part of it), so the
+    re-planned finish matches the measurement."""
     s = json.loads(poas.plan(b200_like, 16384, 16384, 16384))
     rep = _fake_report(s)
     tc = [d for d in rep["devices"] if d["id"] == "gpu0.tc"][0]
@@ -234,6 +235,13 @@ def test_refit_resident_unit_by_finish(poas, b200_like):
     tc["finish"] = {"measured": fin_pred + 0.0004, "predicted": fin_pred, "error_pct": 0.0}
     out = poas.refit_profile(b200_like, rep, 1.0)
     before, after = _profile_fields(b200_like), _profile_fields(out)
-    g = (tc["compute"]["predicted"] + 0.0004) / tc["compute"]["predicted"]
+    g = (fin_pred + 0.0004) / fin_pred  # the whole timeline scales by the finish ratio
     for key in ("slope", "intercept"):
         assert float(after["gpu0.tc"][key]) == pytest.approx(float(before["gpu0.tc"][key]) * g, rel=1e-9)
+    assert float(after["gpu0.tc"]["bandwidth"]) == pytest.approx(float(before["gpu0.tc"]["bandwidth"]) / g,
+                                                                 rel=1e-9)
+    # re-planned with the same rows, the unit's predicted finish is the measurement
+    s2 = json.loads(poas.plan(out, 16384, 16384, 16384))
+    sd2 = [d for d in s2["devices"] if d["id"] == "gpu0.tc"][0]
+    if sd2["rows"] == sd["rows"]:
+        assert sd2["copy_out"][1] == pytest.approx(fin_pred + 0.0004, rel=1e-6)
