@@ -95,12 +95,29 @@ class ClockSampler:
         self._max = None
         self.error = None
 
-    def __enter__(self):
+    _nvml = {}  # gpu -> (pynvml, handle): initialised once (nvmlInit can take
+    # ~100 ms; right before a timed region that idle gap lets the power cap
+    # recover and the region run at boost clocks)
+
+    @classmethod
+    def prepare(cls, gpu: int) -> None:
+        """NVML up front, outside any timed region."""
+        if gpu in cls._nvml:
+            return
         try:
             import pynvml
 
             pynvml.nvmlInit()
-            self._nv = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu))
+            cls._nvml[gpu] = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(gpu))
+        except Exception:
+            cls._nvml[gpu] = None
+
+    def __enter__(self):
+        try:
+            self.prepare(self.gpu)
+            if self._nvml[self.gpu] is None:
+                raise RuntimeError("NVML unavailable")
+            self._nv = self._nvml[self.gpu]
             self._sample()  # one synchronous sample: fails here, not silently in the thread
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
@@ -374,6 +391,7 @@ def main():
     dev = torch.device("cuda", local)
     if args.tc_sms is None:
         args.tc_sms = TC_SMS if world == 1 else TC_SMS_MULTI
+    ClockSampler.prepare(local)
     n = k = args.n
     m = args.n  # rows per rank (weak scaling)
     if args.m_total:
