@@ -447,6 +447,11 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     }
   const bool pipelined = overlapped && pipeline_ && !any_cpu && busy_gpu_units == 1 &&
                          sstate[busy_unit].item_flags != nullptr;
+  if (pipelined && repeats > 1) {  // the second C buffer, before any repeat is queued
+    DeviceGuard g(unit[busy_unit]->spec().device);
+    unit[busy_unit]->scratch(6).ensure(
+        static_cast<std::size_t>(schedule.devices[busy_unit].rows * d.n) * 4);
+  }
 
   // One repeat of an overlapped link unit: host->device (A parts and B
   // panels interleaved in link order), one GEMM per block as soon as its A
