@@ -743,7 +743,7 @@ def main():
                                          replan_threshold_pct=args.replan_threshold)
             sched_e2e = poas.schedule_roundtrip(json.dumps(dyn_e2e["schedule"]))
             se = json.loads(sched_e2e)
-            ex_e2e.execute(sched_e2e, io_h, 1)
+            ex_e2e.execute(sched_e2e, io_h, 3)  # a multi-step run's one-time costs, untimed
             # probe (before, and apart from, the timed steps): 3 steps back to
             # back -- decides between pipelined and isolated steps below
             t_probe = time.perf_counter()
