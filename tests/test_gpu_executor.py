@@ -147,7 +147,7 @@ def test_cpu_unit_coexecution_config_c2(torch_cuda, poas, ref):
     units = ("cpu0=cpu:threads=4;gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=128-512;"
              "gpu0.tc=xpu:dev=0:sms=4:dtype=f16:elem=2:link=hbm:probe=256-1024")
     m, n, k = 1024, 512, 512
-    profile = poas.profile_machine(units, "probes=3,repetitions=1,cpu_min_side=64,cpu_max_side=256,"
+    profile = poas.profile_machine(units, "probes=4,repetitions=2,cpu_min_side=128,cpu_max_side=320,"
                                           "bandwidth_payload=4194304", True)
     sched = json.loads(poas.plan(profile, m, n, k))
     assert json.dumps(sched) == json.dumps(json.loads(ref.plan(profile, m, n, k)))
