@@ -180,9 +180,12 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
-@pytest.mark.parametrize("epilogue", ["tma", "direct"])
+# (variant, epilogue): the single-SM kernels have one epilogue
+_TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct")]
+
+
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
-@pytest.mark.parametrize("variant", ["1cta", "1cta128", "2cta"])
+@pytest.mark.parametrize("variant,epilogue", _TC_VARIANTS)
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
 def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched, epilogue):
     """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) under
@@ -191,8 +194,6 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
     odd SM budgets and a C pitch TMA cannot map (n = 777)."""
     import oracle
 
-    if variant != "2cta" and epilogue == "direct":
-        pytest.skip("the single-SM kernels have one epilogue")
     torch = torch_cuda
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
     monkeypatch.setenv("POAS_TC_SCHED", sched)
