@@ -50,6 +50,7 @@ struct TcArgs {
   uint32_t idesc;
   int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
   int raster_n;        // 1: groups run along N instead of M (experiments)
+  int kserp;           // 1: tiles of odd waves (t / workers) sweep K last-to-first
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   uint64_t hint_c;          // TMA-store epilogue: L2 policy of the C writes
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
@@ -312,15 +313,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int t_next = claim_tile(args, next_static, gridDim.x);  // latency hidden by the loads
         int mb, nb;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group, mb, nb, args.raster_n);
+        const bool rev = args.kserp && ((t / static_cast<int>(gridDim.x)) & 1);
         for (int kb = 0; kb < k_blocks; ++kb) {
+          const int kc = (rev ? k_blocks - 1 - kb : kb) * kBK;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
-          tma_load_2d(s_a + stage * kABytes, &map_a, &full[stage], kb * kBK, mb * kBM,
-                      args.hint_a);
+          tma_load_2d(s_a + stage * kABytes, &map_a, &full[stage], kc, mb * kBM, args.hint_a);
 #pragma unroll
           for (int j = 0; j < kBN / 64; ++j)
             tma_load_2d(s_b + stage * kBBytes + j * kBChunkBytes, &map_b, &full[stage],
-                        nb * kBN + j * 64, kb * kBK, args.hint_b);
+                        nb * kBN + j * 64, kc, args.hint_b);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -572,22 +574,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
         const int col0 = nbl * 256 + static_cast<int>(rank) * 128;  // inside the panel
+        // K serpentine: the tiles of a wave that follows one sweeping K
+        // forwards start where it ended, on the K-slices still in L2
+        const bool rev = args.kserp && ((t / step) & 1);
         for (int kb = 0; kb < k_blocks; ++kb) {
+          const int kc = (rev ? k_blocks - 1 - kb : kb) * kBK;
           mbar_wait(&empty[stage], phase ^ 1);
           if (wave == 1 && kb == 0) trace_stamp(args, 9);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
-          tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kb * kBK, row0,
+          tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kc, row0,
                            args.hint_a);
           if (args.panels > 1) {
-            tma_load_3d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK, pnl,
+            tma_load_3d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kc, pnl,
                              args.hint_b);
             tma_load_3d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
-                             col0 + 64, kb * kBK, pnl, args.hint_b);
+                             col0 + 64, kc, pnl, args.hint_b);
           } else {
-            tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kb * kBK,
+            tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kc,
                              args.hint_b);
             tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
-                             col0 + 64, kb * kBK, args.hint_b);
+                             col0 + 64, kc, args.hint_b);
           }
           if (wave == 1 && kb == 0) trace_stamp(args, 2);
           if (kb == 0 && leader) t_next = claim_tile(args, next_static, step);  // behind the first loads
@@ -1130,6 +1136,8 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.hint_c = hc && std::string(hc) == "normal" ? kEvictNormal : kEvictFirst;
   const char* raster_env = std::getenv("POAS_TC_RASTER");
   args.raster_n = raster_env && std::string(raster_env) == "n";
+  const char* kserp_env = std::getenv("POAS_TC_KSERP");
+  args.kserp = kserp_env && std::string(kserp_env) == "1";
   // Tile scheduler: dynamic claiming below 2^44 MACs; wave-synchronised
   // static order from there on (a tile lasts long enough that the claim
   // order's stagger spreads A-panel sharers over more than an L2 lifetime:

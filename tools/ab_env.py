@@ -14,7 +14,8 @@ import torch  # noqa: E402
 
 from paper_2209_10245_b200 import poas  # noqa: E402
 
-KEYS = ("POAS_TC_HINT_A", "POAS_TC_HINT_B", "POAS_TC_HINT_C", "POAS_TC_GROUP", "POAS_TC_SCHED", "POAS_TC_KERNEL")
+KEYS = ("POAS_TC_HINT_A", "POAS_TC_HINT_B", "POAS_TC_HINT_C", "POAS_TC_GROUP", "POAS_TC_SCHED", "POAS_TC_KERNEL",
+        "POAS_TC_KSERP")
 
 
 def env_of(spec):
