@@ -50,7 +50,7 @@ struct TcArgs {
   uint32_t idesc;
   int group;  // raster: M-tiles per group (a wave covers group x (grid/group) tiles)
   int raster_n;        // 1: groups run along N instead of M (experiments)
-  int kserp;           // 1: tiles of odd waves (t / workers) sweep K last-to-first
+  int kserp;           // 1: tiles of odd waves (t / workers) sweep K last-to-first (L2 tail reuse)
   uint64_t hint_a, hint_b;  // TMA L2 cache-policy hints per operand
   uint64_t hint_c;          // TMA-store epilogue: L2 policy of the C writes
   int* tile_counter;     // {next, done}, zero at launch: dynamic tile scheduler (or null)
@@ -1136,8 +1136,11 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.hint_c = hc && std::string(hc) == "normal" ? kEvictNormal : kEvictFirst;
   const char* raster_env = std::getenv("POAS_TC_RASTER");
   args.raster_n = raster_env && std::string(raster_env) == "n";
+  // K serpentine (default on; POAS_TC_KSERP=0 = every tile sweeps K
+  // forwards): DRAM reads per launch -7.5% at 8192^3 and 16384^3, -5.7% at
+  // 32768^3, time neutral to +0.25% (profiles/r01_kserp)
   const char* kserp_env = std::getenv("POAS_TC_KSERP");
-  args.kserp = kserp_env && std::string(kserp_env) == "1";
+  args.kserp = !(kserp_env && std::string(kserp_env) == "0");
   // Tile scheduler: dynamic claiming below 2^44 MACs; wave-synchronised
   // static order from there on (a tile lasts long enough that the claim
   // order's stagger spreads A-panel sharers over more than an L2 lifetime:

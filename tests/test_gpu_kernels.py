@@ -180,6 +180,31 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
+@pytest.mark.parametrize("variant", ["1cta", "2cta"])
+def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
+    """POAS_TC_KSERP=0: every tile sweeps K forwards (the default alternates
+    the direction per wave of tiles); both orders agree with the oracle and
+    with each other to fp32 accumulation-order rounding."""
+    import oracle
+
+    torch = torch_cuda
+    monkeypatch.setenv("POAS_TC_KERNEL", variant)
+    m, n, k = 1500, 1300, 1000
+    A, B = oracle.fill_uniform(m, k, 41), oracle.fill_uniform(k, n, 42)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    out = []
+    for ks in ("0", "1"):
+        monkeypatch.setenv("POAS_TC_KSERP", ks)
+        c = torch.full((m, n), float("nan"), device="cuda")
+        poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n, num_ctas=8)
+        torch.cuda.synchronize()
+        assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, ks
+        out.append(c)
+    assert ((out[0] - out[1]).abs().max() / out[0].abs().max()).item() < 1e-5
+
+
 # (variant, epilogue): the single-SM kernels have one epilogue
 _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct")]
 

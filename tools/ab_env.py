@@ -25,7 +25,7 @@ def env_of(spec):
 def main():
     a_spec, b_spec = sys.argv[1], sys.argv[2]
     rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 6
-    n = 16384
+    n = int(os.environ.get("AB_N", "16384"))
     A = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
     B = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
     C = torch.empty(n, n, device="cuda")
