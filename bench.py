@@ -523,9 +523,12 @@ def main():
     warm_iters = min(400, max(args.warmup, int(args.warmup_seconds / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
     if args.no_adapt:
         warm_iters, warm_reps = args.warmup, 1
-    dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
-                         alpha=args.alpha_resident, repeats=warm_reps,
-                         replan_threshold_pct=1e9 if args.no_adapt else args.replan_threshold)
+    with ClockSampler(g) as warm_clk:  # the clocks the re-fit saw (last half of the warm-up)
+        dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
+                             alpha=args.alpha_resident, repeats=warm_reps,
+                             replan_threshold_pct=1e9 if args.no_adapt else args.replan_threshold)
+    warm_mhz = [x[0] for x in warm_clk.samples[len(warm_clk.samples) // 2:]]
+    warm_sm_mhz = float(statistics.median(warm_mhz)) if warm_mhz else None
     schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
     sched = json.loads(schedule)
     rows = {d["id"]: d["rows"] for d in sched["devices"]}
@@ -877,6 +880,7 @@ def main():
                                "adapted (the profile-only plan differed from the plan that ran)"),
                 "adapted": {"predicted_makespan_ms": round(pred_make * 1e3, 4),
                             "makespan_error_pct": round(100.0 * (meas_make - pred_make) / meas_make, 3),
+                            "warmup_sm_mhz": warm_sm_mhz,
                             "note": "dynamic scheduling: warm-up runs re-fit the profile (EWMA); under "
                                     "the power cap a short timed region can run in a boost phase the "
                                     "re-fit did not see (profiles/r01_warmup)"},
