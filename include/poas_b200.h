@@ -151,6 +151,34 @@ int poas_b200_has_transfers(poas_unit_t unit);
 int poas_b200_profile_machine(const char* units, const char* profiling, int bus,
                               char** profile_text);
 
+/* The same Predict pipeline over caller-supplied backends: the C form of
+ * the reference plugin `class DeviceBackend` (proj/include/poas/backend.hpp:
+ * 11-24), for a caller whose timing source is its own -- e.g. the
+ * reference's SyntheticBackend (proj/src/simulator.cpp:25-45) or recorded
+ * measurements. Per backend, exactly what profile_machine
+ * (proj/src/simulator.cpp:53-74) does per device: run_compute_probes over
+ * the kind's side range (or probe_min/max_side when both > 0),
+ * run_bandwidth_probe when time_transfer is non-NULL, align for xpu,
+ * cache_bytes for cpu; then fit_machine and format_profile. A callback
+ * returning <= 0 or a non-finite time fails with POAS_E_NON_POSITIVE_TIME
+ * (profiler.cpp:47-50,67-69). Priorities: all >= 0 (fixed) or all -1
+ * (ranked by modelled throughput), else POAS_E_INVALID_ARGUMENT. */
+enum { POAS_KIND_CPU = 0, POAS_KIND_GPU = 1, POAS_KIND_XPU = 2 };
+typedef struct {
+  const char* id;
+  int kind;               /* POAS_KIND_* */
+  uint32_t elem_size;
+  int64_t align;          /* used for xpu */
+  uint64_t cache_bytes;   /* used for cpu */
+  int priority;           /* >= 0 fixed; -1 ranked */
+  int64_t probe_min_side, probe_max_side;
+  double (*time_gemm)(void* ctx, int64_t side);
+  double (*time_transfer)(void* ctx, uint64_t bytes);  /* NULL: has_transfers() false */
+  void* ctx;
+} poas_probe_backend;
+int poas_b200_profile_backends(const poas_probe_backend* backends, size_t count,
+                               const char* profiling, int bus, char** profile_text);
+
 /* ------------------------------------------------------------------------
  * Execute: the real replacement of simulate() (simulator.hpp:68-69).
  * --------------------------------------------------------------------- */
@@ -158,7 +186,10 @@ typedef struct poas_executor_s* poas_executor_t;
 
 typedef struct {
   int64_t m, n, k;
-  /* Host fp32 operands (pinned memory recommended). Required when
+  /* Host fp32 operands. Pinned memory (cudaHostAlloc / cudaHostRegister)
+   * is the fast path; pageable ranges a GPU unit copies are page-locked
+   * (cudaHostRegister) for the duration of execute() and released after
+   * it, which costs time on every call. Required when
    * resident == 0 -- every GPU unit then copies its A rows and all of B over
    * its link, computes, and copies its C rows back, inside execute() -- and
    * whenever a CPU unit has rows (it computes in place on these). */

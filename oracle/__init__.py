@@ -65,6 +65,7 @@ def ref_lib() -> C.CDLL:
                                       C.POINTER(C.c_long)]),
             "ref_profile_synthetic": (C.c_int, [cp, u64, C.POINTER(vp)]),
             "ref_exact_profile": (C.c_int, [cp, C.POINTER(vp)]),
+            "ref_probe_trace": (C.c_int, [cp, u64, C.POINTER(vp)]),
             "ref_machine_config_roundtrip": (C.c_int, [cp, C.POINTER(vp)]),
             "ref_rng_draw": (u64, [u64, cp, C.c_int, dp]),
             "ref_time_plan": (C.c_int, [cp, i64, i64, i64, C.c_int, dp]),
@@ -190,6 +191,12 @@ class ref:
     @staticmethod
     def profile_synthetic(machine_cfg, seed):
         return _rcall(ref_lib().ref_profile_synthetic, machine_cfg.encode(), seed)
+
+    @staticmethod
+    def probe_trace(machine_cfg, seed):
+        """Every synthetic-backend measurement the reference profile_machine
+        takes, in call order (oracle/ref_shim.cpp ref_probe_trace)."""
+        return json.loads(_rcall(ref_lib().ref_probe_trace, machine_cfg.encode(), seed))
 
     @staticmethod
     def exact_profile(machine_cfg):

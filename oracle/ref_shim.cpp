@@ -216,6 +216,63 @@ int ref_profile_synthetic(const char* machine_cfg, uint64_t seed, char** out) {
   });
 }
 
+// Every measurement the reference's profile_machine (proj/src/simulator.cpp:
+// 53-74) draws from its synthetic backends, in call order: the reference's
+// own run_compute_probes / run_bandwidth_probe drive a recording wrapper
+// around make_synthetic_backend(dev, seed). JSON: {"bus", "profiling":
+// {...}, "devices": [{"id", "kind", "elem_size", "align", "cache_bytes",
+// "priority" (-1 = none), "gemm": [[side, seconds], ...], "transfer":
+// [[bytes, seconds], ...]}]}. Replaying it through another profiler must
+// give ref_profile_synthetic's bytes.
+int ref_probe_trace(const char* machine_cfg, uint64_t seed, char** out) {
+  class Recording final : public poas::DeviceBackend {
+   public:
+    explicit Recording(poas::BackendPtr inner) : inner_(std::move(inner)) {}
+    double time_gemm(std::int64_t side) override {
+      const double t = inner_->time_gemm(side);
+      gemm += (gemm.empty() ? "" : ", ") + ("[" + std::to_string(side) + ", " + g17(t) + "]");
+      return t;
+    }
+    double time_transfer(std::uint64_t bytes) override {
+      const double t = inner_->time_transfer(bytes);
+      transfer += (transfer.empty() ? "" : ", ") + ("[" + std::to_string(bytes) + ", " + g17(t) + "]");
+      return t;
+    }
+    bool has_transfers() const override { return inner_->has_transfers(); }
+    std::string gemm, transfer;
+
+   private:
+    poas::BackendPtr inner_;
+  };
+  return guarded([&] {
+    const poas::MachineConfig cfg = poas::parse_machine_config(machine_cfg);
+    const poas::ProfilingConfig& pc = cfg.profiling;
+    std::string js = std::string("{\"bus\": ") + (cfg.bus ? "true" : "false") +
+                     ", \"profiling\": {\"probes\": " + std::to_string(pc.probes) +
+                     ", \"repetitions\": " + std::to_string(pc.repetitions) +
+                     ", \"cpu_min_side\": " + std::to_string(pc.cpu_range.min_side) +
+                     ", \"cpu_max_side\": " + std::to_string(pc.cpu_range.max_side) +
+                     ", \"accel_min_side\": " + std::to_string(pc.accel_range.min_side) +
+                     ", \"accel_max_side\": " + std::to_string(pc.accel_range.max_side) +
+                     ", \"bandwidth_payload\": " + std::to_string(pc.bandwidth_payload) +
+                     "}, \"devices\": [";
+    bool first = true;
+    for (const poas::SyntheticDevice& dev : cfg.devices) {
+      Recording rec(poas::make_synthetic_backend(dev, seed));
+      poas::run_compute_probes(rec, pc.range_for(dev.kind), pc.probes, pc.repetitions);
+      if (rec.has_transfers()) poas::run_bandwidth_probe(rec, pc.bandwidth_payload, pc.repetitions);
+      js += std::string(first ? "" : ", ") + "{\"id\": \"" + dev.id + "\", \"kind\": \"" +
+            poas::kind_name(dev.kind) + "\", \"elem_size\": " + std::to_string(dev.elem_size) +
+            ", \"align\": " + std::to_string(dev.align) +
+            ", \"cache_bytes\": " + std::to_string(dev.cache_bytes) +
+            ", \"priority\": " + std::to_string(dev.priority ? *dev.priority : -1) +
+            ", \"gemm\": [" + rec.gemm + "], \"transfer\": [" + rec.transfer + "]}";
+      first = false;
+    }
+    *out = dup(js + "]}");
+  });
+}
+
 // The reference test fixture's exact (noise-free) profile of a machine config.
 int ref_exact_profile(const char* machine_cfg, char** out) {
   return guarded([&] {

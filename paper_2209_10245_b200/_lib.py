@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "poas_b200_time_transfer": (C.c_int, [vp, u64, dp]),
     "poas_b200_has_transfers": (C.c_int, [vp]),
     "poas_b200_profile_machine": (C.c_int, [cp, cp, C.c_int, C.POINTER(vp)]),
+    "poas_b200_profile_backends": (C.c_int, [vp, C.c_size_t, cp, C.c_int, C.POINTER(vp)]),
     "poas_b200_executor_create": (C.c_int, [cp, C.POINTER(vp)]),
     "poas_b200_executor_destroy": (None, [vp]),
     "poas_b200_execute": (C.c_int, [vp, cp, vp, C.c_int, C.POINTER(vp)]),

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -828,6 +829,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
+      if (args.sblocks) {
+        // direct stores (C pitch TMA cannot map): the same per-block count
+        // as the TMA-store path, after this warp's st.global are visible
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          const int target = args.stream_epoch * blk_tiles * 8;
+          if (atomicAdd(args.block_count + blk, 1) + 1 == target) {
+            __threadfence();
+            atomicExch(args.block_flags + blk, args.stream_epoch);
+          }
+        }
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -951,31 +965,38 @@ int device_sm_count() {
 }
 
 namespace {
-// Per-device ring of tile-scheduler counters {next, done}. Zeroed once at
-// allocation; every launch leaves its counter zero again (release_counter),
-// so no per-launch memset. Launches in flight at the same time (other
-// streams) take distinct slots.
-int* next_tile_counter() {
-  constexpr int kRing = 256;
+// Tile-scheduler counters {next, done}, one per (device, stream). Zeroed
+// once at allocation; every launch leaves its counter zero again
+// (release_counter), so no per-launch memset. Launches on one stream run
+// one after another, so they can share a counter; launches on different
+// streams may run at the same time and never do (a shared
+// per-device ring could hand two concurrent launches the same slot once one
+// stream had queued more launches than the ring had slots).
+int* next_tile_counter(cudaStream_t stream) {
+  constexpr int kBlock = 64;  // counters per allocation, 128 B apart
   static std::mutex mu;
-  static int* ring[64] = {};
-  static int next[64] = {};
+  static std::map<std::pair<int, cudaStream_t>, int*> by_stream;
+  static int* block[64] = {};
+  static int used[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  if (!ring[dev]) {
+  const auto key = std::make_pair(dev, stream);
+  if (auto it = by_stream.find(key); it != by_stream.end()) return it->second;
+  if (!block[dev] || used[dev] == kBlock) {
     int* p = nullptr;
-    const size_t bytes = kRing * 32 * sizeof(int);
+    const size_t bytes = kBlock * 32 * sizeof(int);
     if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
     if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
       cudaFree(p);
       return nullptr;
     }
-    ring[dev] = p;
+    block[dev] = p;  // earlier blocks stay allocated: their counters are in use
+    used[dev] = 0;
   }
-  int* c = ring[dev] + (next[dev] % kRing) * 32;  // 128 B apart
-  ++next[dev];
+  int* c = block[dev] + used[dev]++ * 32;
+  by_stream.emplace(key, c);
   return c;
 }
 }  // namespace
@@ -1115,6 +1136,10 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
 
   const int sms = device_sm_count();
   const int budget = num_ctas > 0 ? num_ctas : sms;
+  // panel flags / block tables / block flags exist only in the pair kernel:
+  // a one-SM budget would run the single-SM kernel, which ignores them
+  // (and a copy-out waiting on a block flag would never be released)
+  if ((P > 1 || ss) && budget < 2) return cudaErrorNotSupported;
   TcArgs args;
   args.M = static_cast<int>(M);
   args.N = static_cast<int>(N);
@@ -1171,7 +1196,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.epi_skip = std::getenv("POAS_TC_EPI_SKIP") != nullptr;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
-    args.tile_counter = next_tile_counter();
+    args.tile_counter = next_tile_counter(stream);
     if (!args.tile_counter) return cudaErrorMemoryAllocation;
   }
 

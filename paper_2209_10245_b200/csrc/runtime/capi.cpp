@@ -389,6 +389,52 @@ int poas_b200_profile_machine(const char* units, const char* profiling, int bus,
   });
 }
 
+int poas_b200_profile_backends(const poas_probe_backend* backends, size_t count,
+                               const char* profiling, int bus, char** profile_text) {
+  // A DeviceBackend over the caller's callbacks (reference backend.hpp:11-24).
+  class CallbackBackend final : public poas::DeviceBackend {
+   public:
+    explicit CallbackBackend(const poas_probe_backend& b) : b_(b) {}
+    double time_gemm(std::int64_t side) override { return b_.time_gemm(b_.ctx, side); }
+    double time_transfer(std::uint64_t bytes) override { return b_.time_transfer(b_.ctx, bytes); }
+    bool has_transfers() const override { return b_.time_transfer != nullptr; }
+
+   private:
+    const poas_probe_backend& b_;
+  };
+  return guard([&] {
+    need_ptr(profile_text, "profile_text");
+    if (count == 0) raise(POAS_E_INVALID_ARGUMENT, "no backends");
+    need_ptr(backends, "backends");
+    const poas::ProfilingConfig cfg = parse_profiling(profiling);
+    std::vector<poas::DeviceProbeData> probes;
+    std::vector<poas::SideRange> ranges;
+    for (size_t i = 0; i < count; ++i) {
+      const poas_probe_backend& b = backends[i];
+      if (!b.time_gemm) raise(POAS_E_INVALID_ARGUMENT, "backend without time_gemm");
+      if (b.kind < POAS_KIND_CPU || b.kind > POAS_KIND_XPU) raise(POAS_E_INVALID_ARGUMENT, "bad kind");
+      poas::DeviceProbeData p;
+      p.id = need_str(b.id, "id");
+      p.kind = b.kind == POAS_KIND_CPU   ? poas::DeviceKind::cpu
+               : b.kind == POAS_KIND_GPU ? poas::DeviceKind::gpu
+                                         : poas::DeviceKind::xpu;
+      p.elem_size = b.elem_size;
+      poas::SideRange range = cfg.range_for(p.kind);
+      if (b.probe_min_side > 0 && b.probe_max_side > 0) range = {b.probe_min_side, b.probe_max_side};
+      ranges.push_back(range);
+      CallbackBackend be(b);
+      p.samples = poas::run_compute_probes(be, range, cfg.probes, cfg.repetitions);
+      if (be.has_transfers())
+        p.bandwidth = poas::run_bandwidth_probe(be, cfg.bandwidth_payload, cfg.repetitions);
+      if (p.kind == poas::DeviceKind::xpu) p.align = b.align;
+      if (p.kind == poas::DeviceKind::cpu) p.cache_bytes = b.cache_bytes;
+      if (b.priority >= 0) p.fixed_priority = b.priority;
+      probes.push_back(std::move(p));
+    }
+    *profile_text = dup_string(poas::format_profile(poas::fit_machine_ranges(probes, bus != 0, cfg, ranges)));
+  });
+}
+
 int poas_b200_executor_create(const char* units, poas_executor_t* out) {
   return guard([&] {
     need_ptr(out, "out");

@@ -154,6 +154,45 @@ class StartGates {
   const int* dev_ = nullptr;
 };
 
+// Page-locks pageable host operand ranges for the duration of one run()
+// (pinned memory -- cudaHostAlloc or registered -- is left alone). Without
+// it an async copy to or from pageable memory would block the enqueueing
+// thread until the copy ran, i.e. until a start gate it is queued behind
+// opened -- which only that thread can do.
+class HostPins {
+ public:
+  HostPins() = default;
+  ~HostPins() {
+    if (regs_.empty()) return;
+    cudaDeviceSynchronize();  // nothing in flight may still read them
+    for (void* p : regs_) cudaHostUnregister(p);
+  }
+  HostPins(const HostPins&) = delete;
+  HostPins& operator=(const HostPins&) = delete;
+  void ensure(const void* p, std::size_t bytes) {
+    if (!p || bytes == 0) return;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      at.type = cudaMemoryTypeUnregistered;
+    }
+    if (at.type != cudaMemoryTypeUnregistered) return;
+    void* q = const_cast<void*>(p);
+    for (void* r : regs_)
+      if (r == q) return;
+    const cudaError_t e = cudaHostRegister(q, bytes, cudaHostRegisterPortable);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {  // shares pages with one registered above
+      cudaGetLastError();
+      return;
+    }
+    cuda_check(e, "cudaHostRegister (pageable host operand)");
+    regs_.push_back(q);
+  }
+
+ private:
+  std::vector<void*> regs_;
+};
+
 }  // namespace
 
 Executor::Executor(const std::string& spec) {
@@ -391,6 +430,9 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       if (const char* kv = std::getenv("POAS_TC_KERNEL"))  // a forced single-SM variant
         if (std::string(kv) != "2cta") continue;
       if (!aligned256(grid[i].parts) || !aligned256(grid[i].panels)) continue;
+      // the pair kernel needs >= 2 SMs (one CTA pair); a 1-SM budget runs
+      // the single-SM kernel, which has no block flags
+      if (u->spec().sms == 1 && extra_sms[i] == 0) continue;
       if (link_order[i].size() > 128 || block_order[i].size() > 4096) continue;
       DeviceGuard g(u->spec().device);
       const std::size_t ni = link_order[i].size(), nb = block_order[i].size();
@@ -596,6 +638,59 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
   const auto last_event = [&](std::size_t rep, std::size_t i) {
     return io.resident ? ev[rep][i].cp1 : ev[rep][i].co1;
   };
+
+  // Nothing inside the enqueue loop below may block on the device while a
+  // gate kernel spins on a flag the host has not opened yet:
+  // (1) every scratch buffer gets its final size here -- growing one later
+  //     calls cudaFree, which synchronizes the device;
+  // (2) pageable host operands are page-locked for this run -- a
+  //     cudaMemcpyAsync to or from pageable memory returns only after the
+  //     copy, i.e. after the gate it is queued behind.
+  for (std::size_t i = 0; i < nd; ++i) {
+    Unit* u = unit[i];
+    const std::int64_t r = schedule.devices[i].rows;
+    if (!u->on_gpu() || r == 0) continue;
+    DeviceGuard g(u->spec().device);
+    const bool tensor = u->spec().kind == DeviceKind::xpu;
+    const bool link16 = !io.resident && tensor && host16_link(u);
+    const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
+    const auto sz = [](std::int64_t a, std::int64_t b, std::size_t e) {
+      return static_cast<std::size_t>(a) * static_cast<std::size_t>(b) * e;
+    };
+    if (!io.resident) {
+      if (link16) {
+        u->scratch(2).ensure(sz(r, lda16, 2));
+        u->scratch(3).ensure(sz(d.k, ldb16, 2));
+      } else {
+        u->scratch(0).ensure(sz(r, d.k, 4));
+        u->scratch(1).ensure(sz(d.k, d.n, 4));
+      }
+      u->scratch(4).ensure(sz(r, d.n, 4));
+    }
+    if (tensor && !(io.resident && io.a16_dev && io.b16_dev) && !link16) {
+      u->scratch(2).ensure(sz(r, lda16, 2));
+      u->scratch(3).ensure(sz(d.k, ldb16, 2));
+    }
+    if (pipelined && repeats > 1 && i == busy_unit) u->scratch(6).ensure(sz(r, d.n, 4));
+  }
+  HostPins pins;
+  if (!io.resident) {
+    bool gpu_copies = false;
+    for (std::size_t i = 0; i < nd; ++i)
+      gpu_copies = gpu_copies || (unit[i]->on_gpu() && schedule.devices[i].rows > 0);
+    if (gpu_copies) {
+      const auto span = [](std::int64_t rows, std::int64_t ld, std::int64_t cols, std::size_t e) {
+        return rows <= 0 ? std::size_t{0}
+                         : (static_cast<std::size_t>(rows - 1) * static_cast<std::size_t>(ld) +
+                            static_cast<std::size_t>(cols)) * e;
+      };
+      pins.ensure(io.a_host, span(d.m, io.lda_host, d.k, 4));
+      pins.ensure(io.b_host, span(d.k, io.ldb_host, d.n, 4));
+      pins.ensure(io.c_host, span(d.m, io.ldc_host, d.n, 4));
+      pins.ensure(io.a16_host, span(d.m, io.lda16_host, d.k, 2));
+      pins.ensure(io.b16_host, span(d.k, io.ldb16_host, d.n, 2));
+    }
+  }
 
   // Start gates: each repeat's GPU work is enqueued behind a tiny kernel
   // that waits for a host flag (gate_wait); t0 is recorded after it, so the

@@ -12,7 +12,7 @@ import json
 from dataclasses import dataclass
 from typing import Sequence
 
-from ._lib import DTYPE_BF16, DTYPE_F16, DTYPE_F32, PoasError, call_str, check, lib
+from ._lib import DTYPE_BF16, DTYPE_F16, DTYPE_F32, PoasError, call_str, check, lib, take_string
 
 __all__ = [
     "PoasError", "plan", "plan_standalone", "solve_split", "oracle_grid_search", "build_tile_plan",
@@ -163,6 +163,61 @@ def profile_machine(units: str, profiling: str = "", bus: bool = True) -> str:
     """profile_machine over real units -> "poas-profile v1" text
     (reference proj/src/simulator.cpp:53-74 + proj/src/profiler.cpp:75-135)."""
     return call_str(lib.poas_b200_profile_machine, _b(units), _b(profiling), int(bus))
+
+
+GEMM_CB = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_int64)
+TRANSFER_CB = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_uint64)
+KINDS = {"cpu": 0, "gpu": 1, "xpu": 2}
+
+
+class ProbeBackend(C.Structure):
+    """poas_probe_backend (include/poas_b200.h): the C form of the reference
+    plugin DeviceBackend (proj/include/poas/backend.hpp:11-24)."""
+    _fields_ = [
+        ("id", C.c_char_p), ("kind", C.c_int), ("elem_size", C.c_uint32), ("align", C.c_int64),
+        ("cache_bytes", C.c_uint64), ("priority", C.c_int), ("probe_min_side", C.c_int64),
+        ("probe_max_side", C.c_int64), ("time_gemm", GEMM_CB), ("time_transfer", TRANSFER_CB),
+        ("ctx", C.c_void_p),
+    ]
+
+
+def profile_backends(devices, profiling: str = "", bus: bool = True) -> str:
+    """profile_machine over caller-supplied backends -> "poas-profile v1".
+    `devices`: dicts with id, kind ("cpu"|"gpu"|"xpu"), elem_size, time_gemm
+    (side -> seconds) and optionally time_transfer (bytes -> seconds),
+    align, cache_bytes, priority (None = ranked), probe_range (min, max).
+    A Python exception inside a callback is re-raised after the call."""
+    errors = []
+
+    def wrap(fn, cb_type):
+        if fn is None:
+            return cb_type()
+
+        def cb(_ctx, x):
+            try:
+                return float(fn(x))
+            except BaseException as e:  # noqa: BLE001 -- re-raised below
+                errors.append(e)
+                return float("nan")
+        return cb_type(cb)
+
+    keep = []
+    arr = (ProbeBackend * len(devices))()
+    for i, d in enumerate(devices):
+        g, t = wrap(d["time_gemm"], GEMM_CB), wrap(d.get("time_transfer"), TRANSFER_CB)
+        keep += [g, t, d["id"].encode()]
+        lo, hi = d.get("probe_range") or (0, 0)
+        prio = d.get("priority")
+        arr[i] = ProbeBackend(keep[-1], KINDS[d["kind"]], int(d["elem_size"]), int(d.get("align", 0)),
+                              int(d.get("cache_bytes", 0)), -1 if prio is None else int(prio),
+                              int(lo), int(hi), g, t, None)
+    out = C.c_void_p()
+    rc = lib.poas_b200_profile_backends(C.cast(arr, C.c_void_p), len(devices), _b(profiling),
+                                        int(bus), C.byref(out))
+    if errors:
+        raise errors[0]
+    check(rc)
+    return take_string(out)
 
 
 # ------------------------------------------------------------------- execute

@@ -451,7 +451,8 @@ def test_b_panels_with_flags_one_launch(torch_cuda, poas):
     assert oracle.rel_frobenius(C.cpu().numpy(), exp) <= TOL
 
 
-@pytest.mark.parametrize("grid", ["aligned", "ragged"])
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("grid", ["aligned", "ragged", "aligned_n_not4", "aligned_1sm"])
 @pytest.mark.parametrize("link", ["bf16", "fp32"])
 def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
     """Overlapped execution of a hand-made 3 x 3 grid of blocks (ragged row
@@ -459,17 +460,24 @@ def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
     and B panels interleaved host->device, each block's C back as soon as it
     is computed -- every element of C exact. 16-bit link + 256-aligned grid:
     ONE streamed tensor launch (producers wait on per-item flags, the
-    copy-out on per-block flags); otherwise one GEMM per block."""
+    copy-out on per-block flags); otherwise one GEMM per block.
+    "aligned_n_not4": C's pitch (n = 1002) is not a TMA pitch, so the
+    streamed launch writes C with direct stores and must still raise every
+    block flag; "aligned_1sm": a one-SM budget cannot run the pair kernel, so
+    the streamed launch is not used (both used to hang)."""
     import oracle
 
     torch = torch_cuda
     elem = 2 if link == "bf16" else 4
-    units = f"gpu0.tc=xpu:dev=0:sms=16:dtype=bf16:elem={elem}:link=pcie:probe=512-2048"
-    m, n, k = 1000, 1000, 520
+    sms = 1 if grid == "aligned_1sm" else 16
+    units = f"gpu0.tc=xpu:dev=0:sms={sms}:dtype=bf16:elem={elem}:link=pcie:probe=512-2048"
+    m, n, k = 1000, (1002 if grid == "aligned_n_not4" else 1000), 520
     profile = poas.profile_machine(units, PROF, True)
     sched = json.loads(poas.plan_policy(profile, m, n, k, "overlap"))
-    parts, panels = ([512, 256, 232], [256, 512, 232]) if grid == "aligned" else ([384, 384, 232],
-                                                                                   [256, 256, 488])
+    parts, panels = {"aligned": ([512, 256, 232], [256, 512, 232]),
+                     "aligned_1sm": ([512, 256, 232], [256, 512, 232]),
+                     "aligned_n_not4": ([512, 256, 232], [256, 512, 234]),
+                     "ragged": ([384, 384, 232], [256, 256, 488])}[grid]
     sched["devices"][0]["tiles"] = [{"m": r, "k": k, "n": w} for r in parts for w in panels]
     sched_text = poas.schedule_roundtrip(json.dumps(sched))
     d = operands(torch, poas, m, n, k)
