@@ -183,6 +183,7 @@ int poas_b200_profile_backends(const poas_probe_backend* backends, size_t count,
  * Execute: the real replacement of simulate() (simulator.hpp:68-69).
  * --------------------------------------------------------------------- */
 typedef struct poas_executor_s* poas_executor_t;
+typedef struct poas_comm_s* poas_comm_t;  /* see "Multi-GPU" below */
 
 typedef struct {
   int64_t m, n, k;
@@ -242,6 +243,14 @@ typedef struct {
    * this path (CUDA cores) still wait on b_ready. */
   const int* b_flags;
   int b_epoch;
+  /* Optional (resident == 1): row-sharded multi-GPU run. The executor
+   * broadcasts B itself every repeat over this communicator (B registered
+   * with poas_b200_comm_register_b, b_panels panels): rank 0's b16_dev /
+   * b_dev are served, the other ranks' units read the comm's receive
+   * buffers; b_flags / b_ready must be NULL (the executor signals B).
+   * b_transport: 0 = copy-engine chain over CUDA IPC (no SMs), 1 = NCCL. */
+  poas_comm_t comm;
+  int b_transport;
 } poas_gemm_io;
 
 /* One executor per process per machine description (same unit specs as
@@ -289,6 +298,52 @@ int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t 
                           int64_t k, const char* policy, const poas_gemm_io* io, int iterations,
                           int repeats, double alpha, double replan_threshold_pct,
                           char** out_json);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: the GEMM row-sharded over the GPUs of one box,
+ * one process per GPU, B broadcast from rank 0 once per GEMM. No reference
+ * counterpart beyond the private-link timeline and LP rows the level-1 plan
+ * uses (proj/src/timeline.cpp:24-35, proj/src/optimizer.cpp:108-115).
+ * --------------------------------------------------------------------- */
+
+/* Join the job's ranks: `name` is a token identical on every rank and
+ * unique per job (e.g. derived from the launcher's rendezvous); `device` is
+ * this rank's CUDA ordinal, or -1 for a host-only comm (barrier and
+ * all-gather only). Collective. */
+int poas_b200_comm_create(const char* name, int rank, int world, int device, poas_comm_t* out);
+void poas_b200_comm_destroy(poas_comm_t comm);
+int poas_b200_comm_barrier(poas_comm_t comm);
+/* Every rank's `text` (<= 64 KiB) as a JSON array of strings in rank
+ * order. Collective. */
+int poas_b200_comm_allgather(poas_comm_t comm, const char* text, char** json_array);
+/* max over ranks. Collective. */
+int poas_b200_comm_max(poas_comm_t comm, double value, double* out);
+/* NCCL (libnccl.so.2 loaded at run time): rank 0 makes the id, the caller
+ * distributes it (e.g. poas_b200_comm_allgather of its hex), every rank
+ * initialises. Needed only for b_transport = 1 and the "nccl" probe. */
+int poas_b200_nccl_unique_id(unsigned char* id, size_t capacity, size_t* length);
+int poas_b200_comm_init_nccl(poas_comm_t comm, const unsigned char* id, size_t length);
+/* Register this rank's panel-major B ([panels][k][n/panels]; b16 in the
+ * tensor units' type, b32 fp32 or NULL): rank 0's are broadcast, the other
+ * ranks receive into buffers the comm owns (two, for alternate GEMMs).
+ * Device memory from cudaMalloc (any offset). Collective. */
+int poas_b200_comm_register_b(poas_comm_t comm, const void* b16, const float* b32, int64_t k,
+                              int64_t n, int panels);
+/* The level-1 link probe (DeviceBackend::time_transfer of a GPU in the
+ * level-1 plan, backend.hpp:19-21): seconds to deliver `bytes` from rank 0
+ * to every rank by `transport` ("ce" | "nccl"), max over ranks, mean of
+ * `repetitions`. Collective. */
+int poas_b200_comm_time_broadcast(poas_comm_t comm, const char* transport, uint64_t bytes,
+                                  int repetitions, double* seconds);
+
+/* Two-level plan (poas/sharded.hpp): level 1 splits m over the GPUs (each
+ * GPU = its units' combined model on a private link of bandwidth
+ * link_bandwidth[g], the reference pipeline), level 2 plans each GPU's rows
+ * over its units with `policy`. `gpu_profiles[g]`: GPU g's poas-profile v1.
+ * Out: {"level1_profile": text, "level1": schedule, "rows": [..],
+ * "row0": [..], "plans": [schedule | null, ...]}. */
+int poas_b200_plan_sharded(const char* const* gpu_profiles, const double* link_bandwidth, int gpus,
+                           int64_t m, int64_t n, int64_t k, const char* policy, char** out_json);
 
 /* ------------------------------------------------------------------------
  * Raw unit kernels (device pointers, caller's cudaStream_t or NULL).

@@ -89,6 +89,7 @@ def oracle_lib() -> C.CDLL:
             "oracle_fill_uniform": (None, [vp, i64, i64, i64, i64, i64, i64, u64]),
             "oracle_round": (None, [vp, i64, C.c_int]),
             "oracle_gemm_rows_f64": (None, [i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int]),
+            "oracle_gemm_rows_f64_strips": (None, [i64, i64, i64, vp, i64, vp, i64, vp, i64]),
             "oracle_rel_frobenius": (C.c_double, [i64, i64, vp, i64, vp, i64]),
             "oracle_exec_tiles_f32": (None, [i64, i64, vp, i64, vp, i64, vp, i64, C.POINTER(i64), i64,
                                              i64, i64]),
@@ -253,6 +254,39 @@ def gemm_rows_f64(A: np.ndarray, B: np.ndarray, mode: int) -> np.ndarray:
     C_ = np.empty((rows, n), dtype=np.float64)
     oracle_lib().oracle_gemm_rows_f64(rows, n, k, _p(A), k, _p(B), n, _p(C_), n, mode)
     return C_
+
+
+def sampled_rows(m: int, count: int = 64, seed: int = 5) -> np.ndarray:
+    """Row indices for a full-size check: the first and last row, the
+    boundary rows of 128/256-row tiles (UMMA M, the CTA-pair tile) spread
+    over M, and random rows -- sorted, unique, `count` of them (or m)."""
+    rng = np.random.default_rng(seed)
+    picks = {0, m - 1}
+    for t in np.linspace(0, max(0, m // 256 - 1), num=12, dtype=np.int64):
+        for off in (0, 127, 128, 255):
+            r = int(t) * 256 + off
+            if r < m:
+                picks.add(r)
+    while len(picks) < min(count, m):
+        picks.add(int(rng.integers(0, m)))
+    return np.array(sorted(picks)[:count] if len(picks) > count else sorted(picks), dtype=np.int64)
+
+
+def full_size_rows_f64(rows: np.ndarray, n: int, k: int, seed_a: int, seed_b: int, mode: int) -> np.ndarray:
+    """Expected C rows of the BASELINE workload at full size: A's sampled
+    rows and all of B regenerated from the counter-based stream
+    (proj/include/poas/rng.hpp:17-25), rounded to the unit's operand
+    precision (`mode`), fp64 accumulation -- one pass over B."""
+    A = np.empty((len(rows), k), dtype=np.float32)
+    for i, r in enumerate(rows):
+        A[i] = fill_uniform(1, k, seed_a, int(r), 0, k)[0]
+    B = fill_uniform(k, n, seed_b)
+    if mode:
+        oracle_lib().oracle_round(_p(A), A.size, mode)
+        oracle_lib().oracle_round(_p(B), B.size, mode)
+    out = np.empty((len(rows), n), dtype=np.float64)
+    oracle_lib().oracle_gemm_rows_f64_strips(len(rows), n, k, _p(A), k, _p(B), n, _p(out), n)
+    return out
 
 
 def rel_frobenius(C32: np.ndarray, R: np.ndarray) -> float:

@@ -120,6 +120,31 @@ void oracle_gemm_rows_f64(int64_t rows, int64_t n, int64_t k, const float* A, in
   }
 }
 
+/* Same arithmetic as oracle_gemm_rows_f64 (mode 0: A and B already hold the
+ * unit's rounded operand values) for a few sampled rows against a large B,
+ * with B read once in total: threads own 256-column strips of B and C and
+ * walk k for all the rows, so a full-size check (B 16384^2 .. 32768^2) is
+ * one pass over B instead of one per row. Summation order per element is
+ * the same (p ascending). */
+void oracle_gemm_rows_f64_strips(int64_t rows, int64_t n, int64_t k, const float* A, int64_t lda,
+                                 const float* B, int64_t ldb, double* C, int64_t ldc) {
+  const int64_t strip = 256;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t j0 = 0; j0 < n; j0 += strip) {
+    const int64_t w = n - j0 < strip ? n - j0 : strip;
+    for (int64_t i = 0; i < rows; ++i)
+      for (int64_t j = 0; j < w; ++j) C[i * ldc + j0 + j] = 0.0;
+    for (int64_t p = 0; p < k; ++p) {
+      const float* b = B + p * ldb + j0;
+      for (int64_t i = 0; i < rows; ++i) {
+        const double ad = (double)A[i * lda + p];
+        double* c = C + i * ldc + j0;
+        for (int64_t j = 0; j < w; ++j) c[j] += ad * (double)b[j];
+      }
+    }
+  }
+}
+
 /* Relative Frobenius error ||C - R|| / ||R|| of an fp32 result. */
 double oracle_rel_frobenius(int64_t rows, int64_t n, const float* C, int64_t ldc, const double* R,
                             int64_t ldr) {

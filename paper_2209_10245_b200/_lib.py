@@ -53,6 +53,16 @@ SIGNATURES: dict[str, tuple] = {
     "poas_b200_refit_profile": (C.c_int, [cp, cp, C.c_double, C.POINTER(vp)]),
     "poas_b200_run_dynamic": (C.c_int, [vp, cp, i64, i64, i64, cp, vp, C.c_int, C.c_int, C.c_double,
                                         C.c_double, C.POINTER(vp)]),
+    "poas_b200_comm_create": (C.c_int, [cp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "poas_b200_comm_destroy": (None, [vp]),
+    "poas_b200_comm_barrier": (C.c_int, [vp]),
+    "poas_b200_comm_allgather": (C.c_int, [vp, cp, C.POINTER(vp)]),
+    "poas_b200_comm_max": (C.c_int, [vp, C.c_double, dp]),
+    "poas_b200_nccl_unique_id": (C.c_int, [vp, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "poas_b200_comm_init_nccl": (C.c_int, [vp, vp, C.c_size_t]),
+    "poas_b200_comm_register_b": (C.c_int, [vp, vp, vp, i64, i64, C.c_int]),
+    "poas_b200_comm_time_broadcast": (C.c_int, [vp, cp, u64, C.c_int, dp]),
+    "poas_b200_plan_sharded": (C.c_int, [C.POINTER(cp), dp, C.c_int, i64, i64, i64, cp, C.POINTER(vp)]),
     "poas_b200_tc_gemm": (C.c_int, [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int,
                                     C.c_int, vp]),
     "poas_b200_tc_gemm_panels": (C.c_int, [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, C.c_int,

@@ -20,6 +20,10 @@ namespace poas_b200 {
 class Unit;
 }
 
+namespace poas_b200 {
+class Comm;
+}
+
 namespace poas {
 
 struct PhaseError {
@@ -81,6 +85,10 @@ struct GemmOperands {
   std::int64_t lda16_host = 0;
   const void* b16_host = nullptr;
   std::int64_t ldb16_host = 0;
+  // Row-sharded multi-GPU run (see poas_gemm_io.comm): the executor
+  // broadcasts B itself, every repeat, over this communicator.
+  poas_b200::Comm* comm = nullptr;
+  int b_transport = 0;  // 0 copy engines (chain), 1 NCCL
 };
 
 double rel_err_pct(double measured, double predicted);

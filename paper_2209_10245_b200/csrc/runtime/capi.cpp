@@ -7,6 +7,7 @@
 #include <string>
 
 #include "capi_util.hpp"
+#include "comm.hpp"
 #include "host_gemm.hpp"
 #include "host_rng.hpp"
 #include "poas/adapter.hpp"
@@ -22,6 +23,7 @@
 
 using poas_b200::capi::dup_string;
 using poas_b200::capi::guard;
+using poas_b200::capi::json_escape;
 using poas_b200::capi::raise;
 
 struct poas_unit_s {
@@ -92,24 +94,6 @@ std::string tile_plan_json(const poas::TilePlan& p) {
   return o + "]}";
 }
 
-std::string json_escape(const std::string& s) {
-  std::string o;
-  for (const char c : s) {
-    if (c == '"' || c == '\\') {
-      o += '\\';
-      o += c;
-    } else if (c == '\n') {
-      o += "\\n";
-    } else if (static_cast<unsigned char>(c) < 0x20) {
-      char buf[8];
-      std::snprintf(buf, sizeof buf, "\\u%04x", c);
-      o += buf;
-    } else {
-      o += c;
-    }
-  }
-  return o;
-}
 
 poas::GemmOperands operands_of(const poas_gemm_io& io) {
   poas::GemmOperands op;
@@ -141,6 +125,8 @@ poas::GemmOperands operands_of(const poas_gemm_io& io) {
   op.lda16_host = io.lda16_host;
   op.b16_host = io.b16_host;
   op.ldb16_host = io.ldb16_host;
+  op.comm = io.comm ? io.comm->comm.get() : nullptr;
+  op.b_transport = io.b_transport;
   return op;
 }
 

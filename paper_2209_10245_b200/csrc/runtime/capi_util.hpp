@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -50,6 +51,25 @@ int guard(F&& f) {
     set_last_error("internal error");
     return POAS_E_INTERNAL;
   }
+}
+
+inline std::string json_escape(const std::string& s) {
+  std::string o;
+  for (const char c : s) {
+    if (c == '"' || c == '\\') {
+      o += '\\';
+      o += c;
+    } else if (c == '\n') {
+      o += "\\n";
+    } else if (static_cast<unsigned char>(c) < 0x20) {
+      char buf[8];
+      std::snprintf(buf, sizeof buf, "\\u%04x", c);
+      o += buf;
+    } else {
+      o += c;
+    }
+  }
+  return o;
 }
 
 inline char* dup_string(const std::string& s) {

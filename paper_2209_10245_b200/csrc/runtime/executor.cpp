@@ -38,6 +38,7 @@
 #include <thread>
 
 #include "capi_util.hpp"
+#include "comm.hpp"
 #include "poas/error.hpp"
 #include "poas/overlap.hpp"
 #include "units.hpp"
@@ -282,6 +283,19 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       fail(errc::invalid_argument, "host operands (a_host, b_host, c_host) are required");
   }
   const int panels = io.b_panels > 1 ? io.b_panels : 1;
+  poas_b200::Comm* const comm = io.comm;
+  const poas_b200::Transport transport =
+      io.b_transport == 1 ? poas_b200::Transport::nccl : poas_b200::Transport::ce;
+  if (comm) {
+    if (!io.resident) fail(errc::invalid_argument, "a comm (B broadcast) needs resident operands");
+    if (!comm->registered() || comm->panels() != panels)
+      fail(errc::invalid_argument, "comm: register B with the same panel count as b_panels first");
+    if (io.b_flags || io.b_ready)
+      fail(errc::invalid_argument, "comm: the executor signals B itself (no b_flags / b_ready)");
+    for (std::size_t i = 0; i < nd; ++i)
+      if (schedule.devices[i].rows > 0 && unit[i]->on_gpu() && unit[i]->spec().device != comm->device())
+        fail(errc::invalid_argument, "comm: every busy GPU unit must be on the comm's GPU");
+  }
   if (panels > 1) {
     if (!io.resident) fail(errc::invalid_argument, "B panels need resident operands");
     if (d.n % panels != 0 || (d.n / panels) % 8 != 0)
@@ -312,7 +326,8 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
   // Not while B arrives through readiness events: the idle SMs are where
   // the collective's kernels run concurrently with the GEMM.
   std::vector<int> extra_sms(nd, 0);
-  if (lend_ && !io.b_ready && !io.b_flags) {
+  // (copy-engine broadcasts need no SMs; NCCL's kernels do)
+  if (lend_ && !io.b_ready && !io.b_flags && !(comm && transport == poas_b200::Transport::nccl)) {
     std::map<int, std::vector<std::size_t>> by_dev;
     for (std::size_t i = 0; i < nd; ++i)
       if (unit[i]->on_gpu()) by_dev[unit[i]->spec().device].push_back(i);
@@ -745,6 +760,30 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
           cuda_check(cudaStreamWaitEvent(unit[i]->stream(), t0[dev][rr], 0), "cudaStreamWaitEvent");
     }
 
+    // Row-sharded run: this repeat's broadcast of B over the comm (every
+    // rank relays every epoch, busy or not), gated on the repeat's t0.
+    int bepoch = io.b_epoch;
+    const void* b16_rep = io.b16_dev;
+    const float* b32_rep = io.b_dev;
+    const int* bflags_rep = io.b_flags;
+    void* const* bready_rep = io.b_ready;
+    if (comm) {
+      bool needs32 = false;  // a busy unit reading fp32 B (CUDA cores, or converting)
+      for (std::size_t i = 0; i < nd; ++i)
+        if (schedule.devices[i].rows > 0 && unit[i]->on_gpu() &&
+            !(unit[i]->spec().kind == DeviceKind::xpu && io.a16_dev && io.b16_dev))
+          needs32 = true;
+      std::vector<cudaEvent_t> after;
+      if (auto it = t0.find(comm->device()); it != t0.end()) after.push_back(it->second[rr]);
+      if (needs32 && !comm->has_b32())
+        fail(errc::invalid_argument, "comm: a busy unit reads fp32 B but only 16-bit B is registered");
+      bepoch = comm->enqueue_broadcast(transport, needs32, after);
+      b16_rep = comm->b16_for(bepoch);
+      b32_rep = comm->b32_for(bepoch);
+      bflags_rep = comm->dev_flags();
+      bready_rep = comm->panel_events();
+    }
+
     // Copy-in + compute, in schedule order.
     std::size_t prev_in = nd;  // previous busy bus unit (link order)
     for (std::size_t i = 0; i < nd; ++i) {
@@ -803,12 +842,12 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         ldc = io.ldc_dev;
         if (tensor && io.a16_dev && io.b16_dev) {
           a = static_cast<const char*>(io.a16_dev) + r0 * io.lda16_dev * 2;
-          b = io.b16_dev;
+          b = b16_rep;
           lda = io.lda16_dev;
           ldb = io.ldb16_dev;
         } else {
           a = io.a_dev + r0 * io.lda_dev;
-          b = io.b_dev;
+          b = b32_rep;
           lda = io.lda_dev;
           ldb = io.ldb_dev;
         }
@@ -831,34 +870,35 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         lda = lda16;
         ldb = ldb16;
       }
-      if (panels > 1 && io.b_flags && tensor && !need_convert && (d.n / panels) % 256 == 0) {
+      if (panels > 1 && bflags_rep && tensor && !need_convert && (d.n / panels) % 256 == 0) {
         // Panel-major B arriving panel by panel, consumed by ONE launch:
         // the kernel's producers start on panel p once b_flags[p] reaches
         // b_epoch (written in panel order by the deliverer), so compute on
         // early panels overlaps the transfer of later ones without per-panel
         // launches (no wave-quantisation tail per panel).
-        u->gemm_panels(r, d.n, d.k, a, lda, b, d.n / panels, c, ldc, panels, io.b_flags,
-                       io.b_epoch, extra_sms[i]);
+        u->gemm_panels(r, d.n, d.k, a, lda, b, d.n / panels, c, ldc, panels, bflags_rep, bepoch,
+                       extra_sms[i]);
       } else if (panels > 1) {
         // Panel-major B arriving panel by panel: compute each column panel
         // as soon as it has landed (overlaps e.g. a chunked broadcast).
         const std::int64_t np = d.n / panels;
         const std::size_t esz = (tensor && !need_convert) ? 2 : 4;
         for (int p = 0; p < panels; ++p) {
-          if (io.b_ready && io.b_ready[p])
-            cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(io.b_ready[p]), 0),
+          if (bready_rep && bready_rep[p])
+            cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(bready_rep[p]), 0),
                        "wait B panel");
           const void* bp = static_cast<const char*>(b) + static_cast<std::size_t>(p) * d.k * np * esz;
           u->gemm(r, np, d.k, a, lda, bp, np, c + p * np, ldc, false, extra_sms[i]);
         }
       } else {
         // One readiness event for the whole of B (e.g. a single broadcast).
-        if (io.resident && io.b_ready && io.b_ready[0])
-          cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(io.b_ready[0]), 0),
+        if (io.resident && bready_rep && bready_rep[0])
+          cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(bready_rep[0]), 0),
                      "wait B");
         u->gemm(r, d.n, d.k, a, lda, b, ldb, c, ldc, false, extra_sms[i]);
       }
       cuda_check(cudaEventRecord(evr[i].cp1, s), "cudaEventRecord");
+      if (comm) comm->consumed(bepoch, s);  // the next writer of these B buffers waits for it
     }
 
     // Copy-outs, in schedule order.

@@ -238,6 +238,7 @@ class GemmIO(C.Structure):
         ("a16_host", C.c_void_p), ("lda16_host", C.c_int64),
         ("b16_host", C.c_void_p), ("ldb16_host", C.c_int64),
         ("b_flags", C.c_void_p), ("b_epoch", C.c_int),
+        ("comm", C.c_void_p), ("b_transport", C.c_int),
     ]
 
 
@@ -280,6 +281,73 @@ class Executor:
             self._h = None
 
     __del__ = close
+
+
+# ----------------------------------------------------------------- multi-GPU
+TRANSPORTS = {"ce": 0, "nccl": 1}
+
+
+class Comm:
+    """poas_comm_t: the job's ranks joined through shared memory, B moved
+    by copy engines over CUDA IPC (or NCCL). `device` -1: host-only."""
+
+    def __init__(self, name: str, rank: int, world: int, device: int = -1):
+        self._h = C.c_void_p()
+        self._destroy = lib.poas_b200_comm_destroy
+        check(lib.poas_b200_comm_create(_b(name), rank, world, device, C.byref(self._h)))
+        self.rank, self.world, self.device = rank, world, device
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def barrier(self):
+        check(lib.poas_b200_comm_barrier(self._h))
+
+    def allgather(self, text: str) -> list[str]:
+        return json.loads(call_str(lib.poas_b200_comm_allgather, self._h, _b(text)))
+
+    def max(self, value: float) -> float:
+        out = C.c_double()
+        check(lib.poas_b200_comm_max(self._h, float(value), C.byref(out)))
+        return out.value
+
+    def init_nccl(self):
+        """Rank 0 makes an NCCL id, every rank joins (collective)."""
+        hexid = ""
+        if self.rank == 0:
+            buf = (C.c_ubyte * 512)()
+            n = C.c_size_t()
+            check(lib.poas_b200_nccl_unique_id(buf, 512, C.byref(n)))
+            hexid = bytes(buf[:n.value]).hex()
+        hexid = self.allgather(hexid)[0]
+        raw = bytes.fromhex(hexid)
+        check(lib.poas_b200_comm_init_nccl(self._h, (C.c_ubyte * len(raw)).from_buffer_copy(raw), len(raw)))
+
+    def register_b(self, b16: int, b32: int | None, k: int, n: int, panels: int):
+        check(lib.poas_b200_comm_register_b(self._h, b16, b32, k, n, panels))
+
+    def time_broadcast(self, nbytes: int, transport: str = "ce", repetitions: int = 3) -> float:
+        out = C.c_double()
+        check(lib.poas_b200_comm_time_broadcast(self._h, _b(transport), nbytes, repetitions, C.byref(out)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def plan_sharded(gpu_profiles: Sequence[str], link_bandwidth: Sequence[float], m: int, n: int, k: int,
+                 policy: str = "reference") -> dict:
+    """Two-level plan (poas/sharded.hpp): rows per GPU from the level-1
+    plan, then each GPU's own plan of its rows."""
+    g = len(gpu_profiles)
+    profs = (C.c_char_p * g)(*[_b(p) for p in gpu_profiles])
+    bw = (C.c_double * g)(*[float(x) for x in link_bandwidth])
+    return json.loads(call_str(lib.poas_b200_plan_sharded, profs, bw, g, m, n, k, _b(policy)))
 
 
 # --------------------------------------------------------------- raw kernels

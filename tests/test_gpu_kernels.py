@@ -173,7 +173,7 @@ def test_full_size_tc_property(torch_cuda, poas):
     rel = ((c.double() @ x - rhs).norm() / rhs.norm()).item()
     # fp32 accumulation over K = 16384 on the tensor pipe: the stated bound
     # grows with K; cuBLAS on the same inputs for scale
-    tol = max(TOL, n * 2.0 ** -28)
+    tol = TOL * max(1.0, n / 16384)
     assert rel <= tol, rel
     ref = torch.mm(a, b, out_dtype=torch.float32)
     rel_cublas = ((ref.double() @ x - rhs).norm() / rhs.norm()).item()

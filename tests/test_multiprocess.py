@@ -66,7 +66,10 @@ def _worker(rank, world, port, out_dir):
     io = poas.GemmIO(m=m, n=n, k=k, a_host=A.ctypes.data, lda_host=k, b_host=B.data_ptr(),
                      ldb_host=n, c_host=C.ctypes.data, ldc_host=n, resident=1)
     ex = poas.Executor(units)
-    rep = shard.sharded_step(ex, sched, io, [B])
+    # B to every rank (host-CPU units read host B; the GPU path's broadcast
+    # is the library's, tests/test_gpu_multirank.py)
+    dist.broadcast(B, src=0)
+    rep = ex.execute(sched, io, 1)
     assert rep["devices"][0]["rows"] == m
     gathered = [None] * world
     dist.all_gather_object(gathered, (r0, C))
@@ -102,3 +105,120 @@ def test_level1_split_config_c4(poas, world):
                "elem_size 4\npriority 1\nops_min 134217728\nops_max 8589934592\n")
     rows = shard.shard_rows(world, 65536, 8192, 8192, per_gpu, 9e11)
     assert rows == [65536 // world] * world
+
+
+def _level1_restated(world, per_gpu_profile, link_bandwidth):
+    """The round-1 Python restatement of the level-1 profile (aggregate
+    slope = 1/sum(1/slope_u), intercept = max, align = lcm over xpu units,
+    private links; tile window from 2^40 MACs, see csrc/planner/sharded.cpp)
+    -- the C++ planner must produce the same plan."""
+    import math
+
+    devs, cur = [], None
+    for line in per_gpu_profile.splitlines():
+        if line.startswith("device "):
+            cur = {"id": line.split(" ", 1)[1]}
+            devs.append(cur)
+        elif cur is not None and " " in line:
+            key, val = line.split(" ", 1)
+            cur[key] = val
+    devs = [d for d in devs if d["kind"] != "cpu"]
+    inv = 0.0  # left-to-right (Python 3.12's sum() compensates; the C++ does not)
+    for d in devs:
+        inv += 1.0 / float(d["slope"])
+    slope = 1.0 / inv
+    intercept = max(float(d["intercept"]) for d in devs)
+    align = 1
+    for d in devs:
+        if d["kind"] == "xpu":
+            align = align * int(d["align"]) // math.gcd(align, int(d["align"]))
+    lines = ["poas-profile v1", "", "bus false"]
+    for r in range(world):
+        lines += ["", f"device gpu{r}", "kind xpu", f"slope {slope!r}", f"intercept {intercept!r}",
+                  f"bandwidth {float(link_bandwidth)!r}", "elem_size 2", f"priority {r}",
+                  f"align {align}", f"ops_min {1 << 40}", f"ops_max {1 << 62}"]
+    return "\n".join(lines) + "\n"
+
+
+def test_level1_plan_matches_round1_restatement(poas, ref):
+    """The C++ two-level planner's level 1 == the round-1 Python level-1
+    profile planned by the reference planner, on random per-GPU profiles
+    and shapes; level 2 == the reference plan of each GPU's rows."""
+    import random
+
+    from paper_2209_10245_b200 import shard
+    from test_planner_parity import random_dims, random_profile
+
+    rng = random.Random(11)
+    checked = 0
+    for _ in range(300):
+        world = rng.choice([1, 2, 3, 4, 8])
+        prof = poas.profile_roundtrip(random_profile(rng, rng.randint(1, 3), rng.random() < 0.3, True))
+        if all("kind cpu" in blk for blk in prof.split("\n\n")[2:]):
+            continue
+        m, n, k = random_dims(rng)
+        bw = rng.choice([9e11, 4.5e11, 7.7e11])
+        l1 = _level1_restated(world, prof, bw)
+        try:
+            want = json.loads(ref.plan(l1, m, n, k))
+        except Exception:
+            with pytest.raises(Exception):
+                shard.plan([prof] * world, [bw] * world, m, n, k)
+            continue
+        got = shard.plan([prof] * world, [bw] * world, m, n, k)
+        assert got["level1"] == want, (world, m, n, k)
+        assert poas.profile_roundtrip(got["level1_profile"]) == poas.profile_roundtrip(l1)
+        assert got["rows"] == [d["rows"] for d in want["devices"]]
+        for g, r in enumerate(got["rows"]):
+            if r:
+                assert got["plans"][g] == json.loads(ref.plan(prof, r, n, k))
+            else:
+                assert got["plans"][g] is None
+        checked += 1
+    assert checked >= 150
+
+
+def test_level1_heterogeneous_gpus(poas):
+    """A GPU whose units are half as fast gets fewer rows (not quite half:
+    both pay the same B transfer and per-row A transfer on their links): the
+    level-1 plan reacts to a slower (throttled) GPU, and the two finish
+    together in its timeline."""
+    from paper_2209_10245_b200 import shard
+
+    def gpu(slope):
+        return poas.profile_roundtrip(
+            "poas-profile v1\n\nbus true\n\ndevice tc\nkind xpu\n"
+            f"slope {slope!r}\nintercept 2e-05\nbandwidth 6.5e12\nelem_size 2\npriority 0\nalign 1\n"
+            "ops_min 549755813888\nops_max 4398046511104\n")
+
+    p = shard.plan([gpu(7e-16), gpu(1.4e-15)], [9e11, 9e11], 65536, 8192, 8192)
+    fast, slow = p["rows"]
+    assert fast + slow == 65536 and p["row0"] == [0, fast]
+    assert 1.4 < fast / slow < 2.0, p["rows"]
+    fin = [d["copy_out"][1] for d in p["level1"]["devices"]]
+    assert abs(fin[0] - fin[1]) / max(fin) < 0.01, fin
+
+
+def _comm_worker(rank, world, name, out_dir):
+    sys.path.insert(0, str(ROOT))
+    from paper_2209_10245_b200 import poas
+
+    c = poas.Comm(name, rank, world, -1)
+    got = c.allgather(f"rank {rank} says \"hi\"\n" * (rank + 1))
+    mx = c.max(float(rank * 10))
+    c.barrier()
+    Path(out_dir, f"r{rank}.json").write_text(json.dumps({"all": got, "max": mx}))
+    c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_comm_allgather_barrier(tmp_path, world):
+    """The library communicator's host side (shared-memory rendezvous,
+    barrier, all-gather, max) across real processes."""
+    name = f"t{os.getpid()}_{world}"
+    mp.start_processes(_comm_worker, args=(world, name, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        res = json.loads((tmp_path / f"r{r}.json").read_text())
+        assert res["all"] == [f"rank {q} says \"hi\"\n" * (q + 1) for q in range(world)]
+        assert res["max"] == 10.0 * (world - 1)
