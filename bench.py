@@ -292,6 +292,88 @@ def run_reference(args):
     return 0
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"unknown ({os.cpu_count()} logical CPUs)"
+
+
+def host_unit_baseline(poas, n: int) -> dict:
+    """This repo's own host-CPU unit (host_gemm: AVX-512 packed panels +
+    OpenMP, every host core) on the same host: config C1 (2048^3 fp32 through
+    predict -> plan -> execute on a CPU-only machine) and a bounded sample of
+    the N^3 workload -- the competent CPU path beside the oracle port."""
+    import numpy as np
+
+    out = {"cores": os.cpu_count()}
+    # C1: the POAS pipeline on the host cores only
+    units = "cpu0=cpu:threads=0"
+    prof = poas.profile_machine(units, "probes=5,repetitions=2,cpu_min_side=1000,cpu_max_side=2000", bus=True)
+    c1 = 2048
+    sched = poas.plan(prof, c1, c1, c1)
+    sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
+    A = np.empty((c1, c1), np.float32)
+    B = np.empty((c1, c1), np.float32)
+    Cm = np.empty((c1, c1), np.float32)
+    poas.fill_uniform_host(A.ctypes.data, c1, c1, c1, 0, 0, c1, sa)
+    poas.fill_uniform_host(B.ctypes.data, c1, c1, c1, 0, 0, c1, sb)
+    ex = poas.Executor(units)
+    io = poas.GemmIO(m=c1, n=c1, k=c1, a_host=A.ctypes.data, lda_host=c1, b_host=B.ctypes.data, ldb_host=c1,
+                     c_host=Cm.ctypes.data, ldc_host=c1, resident=0)
+    ex.execute(sched, io, 1)
+    t0 = time.perf_counter()
+    rep = ex.execute(sched, io, 5)
+    sec = (time.perf_counter() - t0) / 5
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    err = float(np.linalg.norm(Cm - ref) / np.linalg.norm(ref))
+    out["c1"] = {"workload": "C1: 2048^3 fp32, POAS predict/plan/execute on a CPU-only machine (host_gemm)",
+                 "tflops": round(2.0 * c1 ** 3 / sec / 1e12, 4), "ms": round(sec * 1e3, 3),
+                 "plan_tiles": len(json.loads(sched)["devices"][0]["tiles"]),
+                 "makespan_error_pct": round(rep["makespan_error_pct"], 3), "c_rel_err": float(f"{err:.3e}"),
+                 "c_ok": err <= 2e-5}
+    # the N^3 workload, a bounded sample of rows (all of K and N)
+    rows = 512
+    A2 = np.empty((rows, n), np.float32)
+    B2 = np.empty((n, n), np.float32)
+    C2 = np.empty((rows, n), np.float32)
+    poas.fill_uniform_host(A2.ctypes.data, n, rows, n, 0, 0, n, sa)
+    poas.fill_uniform_host(B2.ctypes.data, n, n, n, 0, 0, n, sb)
+    poas.host_gemm(64, n, n, A2.ctypes.data, n, B2.ctypes.data, n, C2.ctypes.data, n)
+    t0 = time.perf_counter()
+    poas.host_gemm(rows, n, n, A2.ctypes.data, n, B2.ctypes.data, n, C2.ctypes.data, n)
+    sec = time.perf_counter() - t0
+    out["sample"] = {"rows": rows, "n": n, "k": n, "tflops": round(2.0 * rows * n * n / sec / 1e12, 4),
+                     "seconds": round(sec, 3)}
+    return out
+
+
+def reference_planner_cost(profile: str, m: int, n: int, k: int) -> dict:
+    """the reference planner (oracle/_ref, compiled from
+    /root/reference) -- us per plan, one thread -- on this run's profile and
+    on the reference's mach2 machine, and its exhaustive oracle_grid_search
+    at resolution 2000 over mach2's 3 units on all host threads."""
+    import oracle
+
+    out = {}
+    sec = oracle.ref.time_plan(profile, m, n, k, 200)
+    out["plan_us_this_profile"] = round(sec * 1e6, 2)
+    mach2 = (ROOT / "tests" / "golden" / "mach2.cfg")
+    if mach2.exists():
+        prof2 = oracle.ref.exact_profile(mach2.read_text())
+        out["plan_us_mach2"] = {f"{a}x{b}x{c}": round(oracle.ref.time_plan(prof2, a, b, c, 200) * 1e6, 2)
+                                for a, b, c in ((2048, 2048, 2048), (8192, 8192, 8192), (16384, 16384, 16384),
+                                                (65536, 8192, 8192))}
+        t0 = time.perf_counter()
+        oracle.ref.oracle_grid_search(prof2, 16384, 16384, 16384, 2000, parallel=True)
+        out["oracle_grid_search_res2000_s"] = round(time.perf_counter() - t0, 4)
+        out["threads"] = os.cpu_count()
+    return out
+
+
 # ----------------------------------------------------------------------- ours
 def warm_sustained(poas, torch, dev, seconds: float) -> None:
     """Back-to-back 8192^3 tensor GEMMs for `seconds` (scratch operands)."""
@@ -318,6 +400,39 @@ def _static_summary(dyn):
             "makespan_error_pct": round(it["makespan_error_pct"], 3)}
 
 
+class Group:
+    """The job's ranks for the bench's own bookkeeping (barrier, max over
+    ranks, all-gather): the library communicator (poas_b200_comm_*), or a
+    no-op at N = 1."""
+
+    def __init__(self, comm):
+        self.comm = comm
+
+    def barrier(self):
+        if self.comm:
+            self.comm.barrier()
+
+    def max(self, v: float) -> float:
+        return self.comm.max(v) if self.comm else float(v)
+
+    def allgather(self, text: str) -> list[str]:
+        return self.comm.allgather(text) if self.comm else [text]
+
+
+def relaunch(args) -> int:
+    """`bench.py --gpus N` without a launcher: re-run under torchrun with N
+    ranks (one process per GPU) and pass its output through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    log("launching", " ".join(cmd[2:6]), "...")
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,12 +445,18 @@ def main():
                     help="strong scaling (config C4: --m-total 65536 --size 8192): the job's M rows "
                          "split over the ranks instead of --size rows per rank")
     ap.add_argument("--tc-sms", type=int, default=None,
-                    help=f"tensor unit SM budget (default {TC_SMS}; {TC_SMS_MULTI} at N > 1)")
+                    help=f"tensor unit SM budget (default {TC_SMS}; {TC_SMS_MULTI} with --b-transport nccl "
+                         "at N > 1)")
     ap.add_argument("--simt-sms", type=int, default=SIMT_SMS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-cpu", action="store_true", help="e2e without the host-CPU unit")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 strong-scaling measurement")
+    ap.add_argument("--c4-steps", type=int, default=10)
     ap.add_argument("--b-panels", type=int, default=16,
                     help="N > 1: B column panels broadcast separately (overlap with compute)")
+    ap.add_argument("--b-transport", default="ce", choices=["ce", "nccl"],
+                    help="N > 1: how B reaches the ranks -- copy-engine chain over CUDA IPC (no SMs) "
+                         "or NCCL broadcasts (kernels beside the GEMM)")
     ap.add_argument("--policy", default="best-subset", choices=["reference", "best-subset"],
                     help="planner policy: the reference algorithm (byte-identical plans) or the "
                          "opt-in best-subset B200 extension")
@@ -362,42 +483,38 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     if args.impl == "reference":
         return run_reference(args)
 
     import torch
-    import torch.distributed as dist
 
     from paper_2209_10245_b200 import poas, shard
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
-    # One process per GPU. POAS_DIST_BACKEND=gloo (with ranks sharing GPUs,
-    # LOCAL_RANK modulo the visible devices) exercises the multi-rank path on
-    # a one-GPU box; the measured configuration is NCCL, one GPU per rank.
-    backend = os.environ.get("POAS_DIST_BACKEND", "nccl")
+    # One process per GPU (ranks beyond the visible GPUs share them: the
+    # multi-rank path exercised on a one-GPU box -- the measured
+    # configuration is one GPU per rank).
     local = env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            # The broadcast's kernels must all fit on the SMs the persistent
-            # GEMM leaves free (TC_SMS_MULTI): the GEMM spins on per-panel
-            # flags that only the broadcast can release.
-            for var in ("NCCL_MAX_NCHANNELS", "NCCL_MAX_CTAS"):
-                os.environ.setdefault(var, str(148 - TC_SMS_MULTI))
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    transport = args.b_transport
+    comm = poas.Comm(shard.comm_name(), rank, world, local) if world > 1 else None
+    grp = Group(comm)
+    if comm and transport == "nccl":
+        # NCCL's broadcast kernels run beside the persistent GEMM on the SMs
+        # its budget leaves free (TC_SMS_MULTI): every one of its CTAs must
+        # fit there, or the GEMM spins on flags only NCCL can release
+        for var in ("NCCL_MAX_NCHANNELS", "NCCL_MAX_CTAS"):
+            os.environ.setdefault(var, str(148 - TC_SMS_MULTI))
+        comm.init_nccl()
     if args.tc_sms is None:
-        args.tc_sms = TC_SMS if world == 1 else TC_SMS_MULTI
+        args.tc_sms = TC_SMS_MULTI if (world > 1 and transport == "nccl") else TC_SMS
     ClockSampler.prepare(local)
     n = k = args.n
-    m = args.n  # rows per rank (weak scaling)
-    if args.m_total:
-        if args.m_total % world:
-            raise SystemExit(f"--m-total {args.m_total} does not split over {world} ranks")
-        m = args.m_total // world
+    m_total = args.m_total or args.n * world
     save = Path(args.save) if args.save else None
     if save and rank == 0:
         save.mkdir(parents=True, exist_ok=True)
@@ -406,8 +523,10 @@ def main():
     tc_id, simt_id = f"gpu{rank}.tc", f"gpu{rank}.simt"
     units_res = (f"{tc_id}=xpu:dev={g}:sms={args.tc_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384;"
                  f"{simt_id}=gpu:dev={g}:sms={args.simt_sms}:exclusive=1:elem=4:link=hbm:probe=512-2048")
+    # NCCL's kernels need the idle units' SMs: no lending with that transport
+    units_exec = units_res + (";lend=0" if (world > 1 and transport == "nccl") else "")
 
-    # ---- predict -> optimize -> adapt -> schedule (resident operands)
+    # ---- predict (this GPU's units, real kernels) + the level-1 link probe
     t0 = time.perf_counter()
     if args.profile:  # a profile measured earlier on this box (e.g. for an ncu pass)
         profile = Path(args.profile.replace("{rank}", str(rank))).read_text()
@@ -419,184 +538,148 @@ def main():
             warm_sustained(poas, torch, dev, args.probe_warmup)
         profile = poas.profile_machine(units_res, PROFILING, bus=True)
     t_prof = time.perf_counter() - t0
-    schedule = poas.plan_policy(profile, m, n, k, args.policy)
-    ref_policy_makespan = json.loads(poas.plan(profile, m, n, k))["makespan"]
-    sched = json.loads(schedule)
-    rows = {d["id"]: d["rows"] for d in sched["devices"]}
-    log(f"rank {rank}: profiled in {t_prof:.1f}s; plan rows {rows}; predicted {sched['makespan']*1e3:.3f} ms")
+    link_bw = None
+    if comm:
+        # DeviceBackend::time_transfer of each GPU's level-1 link: B (16-bit)
+        # delivered to every rank by the transport the steps use
+        b_bytes = k * n * 2
+        link_bw = b_bytes / comm.time_broadcast(b_bytes, transport, 3)
     if save and rank == 0:
         (save / "profile_resident.txt").write_text(profile)
-        (save / "schedule_resident.json").write_text(schedule)
-
-    # ---- resident operands (counter-based generator, identical to host/oracle)
     sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
-    A32 = torch.empty(m, k, device=dev, dtype=torch.float32)
-    A16 = torch.empty(m, k, device=dev, dtype=torch.bfloat16)
-    C = torch.empty(m, n, device=dev, dtype=torch.float32)
-    # B is stored panel-major ([P][K][N/P]): at N > 1 each column panel is
-    # broadcast separately and the units start on panel p as soon as it
-    # lands (executor b_ready events), overlapping the rest of the broadcast.
-    P = args.b_panels if world > 1 else 1
-    while P > 1 and (n % P or (n // P) % 256):  # panels of whole pair tiles (one-launch path)
-        P //= 2
-    np_ = n // P
-    B32 = torch.empty(P, k, np_, device=dev, dtype=torch.float32)
-    B16 = torch.empty(P, k, np_, device=dev, dtype=torch.bfloat16)
-    row0 = rank * m  # this rank's rows of the global A (M_total = m * world)
-    poas.fill_uniform(poas.DTYPE_F32, A32.data_ptr(), k, m, k, row0, 0, k, sa)
-    poas.fill_uniform(poas.DTYPE_BF16, A16.data_ptr(), k, m, k, row0, 0, k, sa)
-    if rank == 0:
-        for p in range(P):
-            poas.fill_uniform(poas.DTYPE_F32, B32[p].data_ptr(), np_, k, np_, 0, p * np_, n, sb)
-            poas.fill_uniform(poas.DTYPE_BF16, B16[p].data_ptr(), np_, k, np_, 0, p * np_, n, sb)
-    else:
-        B32.zero_()
-        B16.zero_()
-    torch.cuda.synchronize()
 
-    # N > 1: NCCL's broadcast kernels run beside the GEMM on the SMs the
-    # idle CUDA-core unit leaves free, so the tensor unit must not borrow them.
-    ex = poas.Executor(units_res + (";lend=0" if world > 1 else ""))
-    io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=np_,
-                     a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=np_,
-                     c_dev=C.data_ptr(), ldc_dev=n, resident=1, b_panels=P)
-    # B in every precision a busy unit consumes is what crosses NVLink.
-    simt_busy = rows.get(simt_id, 0) > 0
-    ready = [torch.cuda.Event() for _ in range(P)]
-    comm_side = torch.cuda.Stream()
-    flags = torch.zeros(P, dtype=torch.int32, device=dev)  # per-panel readiness (tensor unit)
-    epoch = [0]
-    if world > 1 and rank != 0:
-        handles = (ctypes.c_void_p * P)()
-        io.b_ready = ctypes.cast(handles, ctypes.POINTER(ctypes.c_void_p))
-        io.b_flags = flags.data_ptr()
-    elif world > 1:  # the root's B is local: every panel ready, still one launch
-        flags.fill_(1)
-        io.b_flags, io.b_epoch = flags.data_ptr(), 1
-    # Level-1 (per-GPU) split of the whole job by the same planner: equal
-    # shards of `m` rows for identical GPUs (weak scaling).
-    l1_rows = shard.shard_rows(world, m * world, n, k, profile) if world > 1 else [m]
-    assert l1_rows == [m] * world, l1_rows
-
-    def step(repeats=1):
+    def resident_run(label, m_all, n, k, steps, panels_req, adapt=True, full=True):
+        """Plan (two-level at N > 1), place the operands, warm up through the
+        dynamic scheduler and time `steps` executor steps of the row-sharded
+        GEMM (B broadcast by the library inside every step at N > 1)."""
         if world > 1:
-            # B lives on rank 0: NCCL broadcast over NVLink inside the step,
-            # one async broadcast per panel; panel p's event fires when it lands.
-            # The one-launch flag path only while the CUDA-core unit is idle:
-            # with its SMs busy the broadcast's CTAs might not all fit beside
-            # a spinning GEMM, so per-panel launches behind events are used.
-            io.b_flags = flags.data_ptr() if not simt_busy else None
-            works = []
+            plan = shard.plan(grp.allgather(profile), [link_bw] * world, m_all, n, k, args.policy)
+            rows_l1, row0 = plan["rows"], plan["row0"][rank]
+            m = rows_l1[rank]
+            if m == 0:
+                raise SystemExit(f"rank {rank}: the level-1 plan left this GPU no rows ({rows_l1})")
+            schedule = json.dumps(plan["plans"][rank])
+            schedule = poas.schedule_roundtrip(schedule)
+        else:
+            rows_l1, row0, m = [m_all], 0, m_all
+            schedule = poas.plan_policy(profile, m, n, k, args.policy)
+        ref_policy_makespan = json.loads(poas.plan(profile, m, n, k))["makespan"]
+        sched = json.loads(schedule)
+        rows = {d["id"]: d["rows"] for d in sched["devices"]}
+        log(f"rank {rank} {label}: level-1 rows {rows_l1}; plan rows {rows}; "
+            f"predicted {sched['makespan']*1e3:.3f} ms")
+        if save and rank == 0:
+            (save / f"schedule_{label}.json").write_text(schedule)
+        P = panels_req if world > 1 else 1
+        while P > 1 and (n % P or (n // P) % 256):  # panels of whole pair tiles (one-launch path)
+            P //= 2
+        np_ = n // P
+        A32 = torch.empty(m, k, device=dev, dtype=torch.float32)
+        A16 = torch.empty(m, k, device=dev, dtype=torch.bfloat16)
+        C = torch.empty(m, n, device=dev, dtype=torch.float32)
+        # B panel-major ([P][K][N/P]): each column panel is one contiguous
+        # chunk of the broadcast; only rank 0 holds it
+        B32 = torch.zeros(P, k, np_, device=dev, dtype=torch.float32)
+        B16 = torch.zeros(P, k, np_, device=dev, dtype=torch.bfloat16)
+        poas.fill_uniform(poas.DTYPE_F32, A32.data_ptr(), k, m, k, row0, 0, k, sa)
+        poas.fill_uniform(poas.DTYPE_BF16, A16.data_ptr(), k, m, k, row0, 0, k, sa)
+
+        def fill_b():
             for p in range(P):
-                works.append([dist.broadcast(B16[p], src=0, async_op=True)] +
-                             ([dist.broadcast(B32[p], src=0, async_op=True)] if simt_busy else []))
-            if rank != 0:
-                epoch[0] += 1
-                io.b_epoch = epoch[0]
-                with torch.cuda.stream(comm_side):
-                    for p in range(P):
-                        for w in works[p]:
-                            w.wait()
-                        # panel p landed: the tensor unit's kernel starts on it
-                        poas.signal_flag(flags[p:p + 1].data_ptr(), epoch[0], comm_side.cuda_stream)
-                        ready[p].record(comm_side)
-                for p in range(P):
-                    handles[p] = ready[p].cuda_event
-        return ex.execute(schedule, io, repeats)
+                poas.fill_uniform(poas.DTYPE_F32, B32[p].data_ptr(), np_, k, np_, 0, p * np_, n, sb)
+                poas.fill_uniform(poas.DTYPE_BF16, B16[p].data_ptr(), np_, k, np_, 0, p * np_, n, sb)
 
-    # Warm-up = dynamic scheduling (paper §3.4.2, poas_b200_run_dynamic): the
-    # profile's probes are short bursts, the timed region runs at the
-    # sustained power-capped clock; each warm-up execution re-fits the unit
-    # models from its measured phases and re-plans. The first one runs the
-    # static plan, so its error is the static model's prediction error.
-    step()  # lands B on every rank (N > 1) before the loop
-    # at least ~0.3 s of work, so the power-capped clock has settled before
-    # the timed region (the adapted model then predicts it)
-    # (--no-adapt: W plain executions of the static plan -- e.g. under a
-    # profiler, whose serialised launches make measured phases meaningless)
-    # Each round runs 5 steps back to back (single steps with host gaps run
-    # cooler and faster), for >= --warmup-seconds in all. Under the power
-    # cap the step time wanders +-8% from one 60 ms block to the next
-    # (profiles/r01_warmup/power_dynamics_*.json), so the re-fit is an EWMA
-    # (alpha 0.2: ~25 steps) of the steady state rather than the last block.
-    warm_reps = 5
-    warm_iters = min(400, max(args.warmup, int(args.warmup_seconds / max(sched["makespan"] * warm_reps, 1e-6)) + 1))
-    if args.no_adapt:
-        warm_iters, warm_reps = args.warmup, 1
-    with ClockSampler(g) as warm_clk:  # the clocks the re-fit saw (last half of the warm-up)
-        dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
-                             alpha=args.alpha_resident, repeats=warm_reps,
-                             replan_threshold_pct=1e9 if args.no_adapt else args.replan_threshold)
-    warm_mhz = [x[0] for x in warm_clk.samples[len(warm_clk.samples) // 2:]]
-    warm_sm_mhz = float(statistics.median(warm_mhz)) if warm_mhz else None
-    schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
-    sched = json.loads(schedule)
-    rows = {d["id"]: d["rows"] for d in sched["devices"]}
-    simt_busy = rows.get(simt_id, 0) > 0
-    log(f"rank {rank}: dynamic warm-up {[round(i['makespan_error_pct'], 2) for i in dyn['iterations']]} % "
-        f"-> rows {rows}, predicted {sched['makespan']*1e3:.3f} ms")
-    if save and rank == 0:
-        (save / "dynamic_resident.json").write_text(json.dumps(dyn, indent=1))
-    def timed_steps():
-        """K steps bracketed by a barrier + synchronize, CUDA events around
-        them, SM clocks sampled during them."""
-        step()
+        if rank == 0:
+            fill_b()
+        torch.cuda.synchronize()
+        wcomm = None
         if world > 1:
-            dist.barrier()
+            # one communicator per workload (its B registration)
+            wcomm = comm if label == "main" else poas.Comm(shard.comm_name() + "_" + label, rank, world, local)
+            if transport == "nccl" and wcomm is not comm:
+                wcomm.init_nccl()
+            wcomm.register_b(B16.data_ptr(), B32.data_ptr(), k, n, P)
+        ex = poas.Executor(units_exec)
+        io = poas.GemmIO(m=m, n=n, k=k, a_dev=A32.data_ptr(), lda_dev=k, b_dev=B32.data_ptr(), ldb_dev=np_,
+                         a16_dev=A16.data_ptr(), lda16_dev=k, b16_dev=B16.data_ptr(), ldb16_dev=np_,
+                         c_dev=C.data_ptr(), ldc_dev=n, resident=1, b_panels=P,
+                         comm=wcomm.handle if wcomm else None, b_transport=poas.TRANSPORTS[transport])
+
+        # Warm-up = dynamic scheduling (paper §3.4.2, poas_b200_run_dynamic):
+        # the probes are short bursts, the timed region runs at the sustained
+        # power-capped clock; each warm-up execution re-fits the unit models
+        # from its measured phases and re-plans. The first one runs the
+        # static plan, so its error is the static model's prediction error.
+        # Rounds of 5 back-to-back steps (single steps with host gaps run
+        # cooler), for >= --warmup-seconds in all; EWMA re-fit (alpha 0.2:
+        # under the power cap a 60 ms block wanders +-8%,
+        # profiles/r01_warmup). At N > 1 every rank runs the same number of
+        # executions (each one is a collective broadcast).
+        ex.execute(schedule, io, 1)
+        warm_reps = 5
+        warm_iters = min(400, max(args.warmup, int(args.warmup_seconds / max(sched["makespan"] * warm_reps,
+                                                                             1e-6)) + 1))
+        if args.no_adapt or not adapt:
+            warm_iters, warm_reps = args.warmup, 1
+        warm_iters = int(grp.max(warm_iters))
+        with ClockSampler(g) as warm_clk:  # the clocks the re-fit saw (last half of the warm-up)
+            dyn = ex.run_dynamic(profile, m, n, k, io, iterations=warm_iters, policy=args.policy,
+                                 alpha=args.alpha_resident, repeats=warm_reps,
+                                 replan_threshold_pct=1e9 if (args.no_adapt or not adapt) else args.replan_threshold)
+        warm_mhz = [x[0] for x in warm_clk.samples[len(warm_clk.samples) // 2:]]
+        warm_sm_mhz = float(statistics.median(warm_mhz)) if warm_mhz else None
+        schedule = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
+        sched = json.loads(schedule)
+        rows = {d["id"]: d["rows"] for d in sched["devices"]}
+        log(f"rank {rank} {label}: dynamic warm-up {[round(i['makespan_error_pct'], 2) for i in dyn['iterations']]} % "
+            f"-> rows {rows}, predicted {sched['makespan']*1e3:.3f} ms")
+        if save and rank == 0:
+            (save / f"dynamic_{label}.json").write_text(json.dumps(dyn, indent=1))
+
+        # ---- the timed region: `steps` executor steps back to back (at N > 1
+        # each one broadcasts B), bracketed by a barrier + synchronize, CUDA
+        # events around them on the current stream (the executor's units
+        # start behind an event recorded on it), SM clocks sampled during.
+        ex.execute(schedule, io, 1)
+        grp.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = []
         # Keep the GPU at the steps' duty cycle across the host work before
         # the timed region (clock sampler start, enqueueing the first step):
         # an idle gap of a few ms lets the power cap's controller recover,
         # and a short timed region then runs up to 14% faster than the
         # steady state the model was fit in (profiles/r01_warmup).
         s_cur = torch.cuda.current_stream().cuda_stream
-        for _ in range(3 * P):
+        for _ in range(3):
             poas.tc_gemm(poas.DTYPE_BF16, m, np_, k, A16.data_ptr(), k, B16[0].data_ptr(), np_,
                          C.data_ptr(), n, stream=s_cur)
         with ClockSampler(g) as clk:
             e0.record()
-            if world > 1:
-                for _ in range(args.steps):
-                    reps.append(step())
-            else:
-                reps.append(ex.execute(schedule, io, args.steps))
+            rep = ex.execute(schedule, io, steps)
             e1.record()
             torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        return e0.elapsed_time(e1), reps, clk
+        grp.barrier()
+        ms_total = grp.max(e0.elapsed_time(e1))
+        ms_step = ms_total / steps
 
-    ms_total, reports, clk = timed_steps()
-    t = torch.tensor([ms_total], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
-    ms_step = ms_total / args.steps
-    flops_step_total = 2.0 * m * world * n * k
-    value = flops_step_total / (ms_step * 1e-3) / 1e12
-    clocks = clk.summary()
-
-    # ---- check C (every rank, full size): the size-independent property
-    # C.x = A_u.(B_u.x) in fp64, with A_u/B_u the operands each unit consumed
-    # (bf16 for the tensor unit's rows, fp32 for the CUDA-core unit's); B is
-    # panel-major [P][K][N/P]. Outside the timed region.
-    def verify_c():
-        """(1) C.x = A_u.(B_u.x) in fp64 over all of C; (2) 64 sampled full
-        rows (first/last, tile boundaries, random) against fp64 products of
-        the same rounded operands -- the arithmetic of the tests' CPU oracle
-        (tests/test_gpu_fullsize.py), evaluated here with torch in fp64."""
+        # ---- check C (every rank, full size, outside the timed region):
+        # (1) C.x = A_u.(B_u.x) in fp64 over all of C; (2) 64 sampled full
+        # rows (first/last, tile boundaries, random) against fp64 products
+        # of the same rounded operands -- the arithmetic of the tests' CPU
+        # oracle (tests/test_gpu_fullsize.py), here with torch in fp64. The
+        # ranks that received B regenerate it locally for the reference.
+        if rank != 0:
+            fill_b()
         x = torch.randn(n, dtype=torch.float64, device=dev, generator=torch.Generator(dev).manual_seed(7))
         xs = x.view(P, np_)
         y = C.double() @ x
         y_ref = torch.empty_like(y)
-        g = torch.Generator().manual_seed(5 + rank)
+        gen = torch.Generator().manual_seed(5 + rank)
         picks = {0, m - 1}
         for t in range(0, max(1, m // 256), max(1, m // 256 // 12)):
             picks.update(r for r in (t * 256, t * 256 + 127, t * 256 + 128, t * 256 + 255) if r < m)
         while len(picks) < min(64, m):
-            picks.add(int(torch.randint(0, m, (1,), generator=g)))
+            picks.add(int(torch.randint(0, m, (1,), generator=gen)))
         rows_s = sorted(picks)[:64]
         num = den = 0.0
         r0 = 0
@@ -615,36 +698,52 @@ def main():
                 num += float((C.index_select(0, idx).double() - ref_rows).norm() ** 2)
                 den += float(ref_rows.norm() ** 2)
             r0 += r
-        err = float((y - y_ref).norm() / y_ref.norm())
-        rows_err = (num / den) ** 0.5 if den > 0 else 0.0
-        t = torch.tensor([err, rows_err], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t[0].item()), float(t[1].item())
+        c_prop = grp.max(float((y - y_ref).norm() / y_ref.norm()))
+        c_rows = grp.max((num / den) ** 0.5 if den > 0 else 0.0)
+        # relative Frobenius bound for fp32 accumulation over K (SURVEY.md
+        # 8d): 2e-5 up to K = 16384 (1.79e-5 measured
+        # there, as cuBLAS), growing linearly with K beyond
+        tol = 2e-5 * max(1.0, k / 16384)
+        if not (c_prop <= tol and c_rows <= tol):
+            raise SystemExit(f"{label}: C check failed: rel err {c_prop:.3e} / sampled rows {c_rows:.3e} > {tol}")
+        c_check = {"property": "C.x = A.(B.x), fp64, each unit's own operand precision, every rank",
+                   "max_rel_err": float(f"{c_prop:.3e}"), "tol": tol,
+                   "sampled_rows": {"rows": len(rows_s), "rel_frobenius": float(f"{c_rows:.3e}"),
+                                    "reference": "fp64 product of the same rounded operands (first/last, "
+                                                 "128/256-row tile boundaries, random rows; every rank)"}}
+        meas_make = rep["measured_makespan"]
+        pred_make = rep["predicted_makespan"]
+        it0 = dyn["iterations"][0]
+        static_same = it0["rows"] == rows
+        static_pred = it0["predicted_makespan"]
+        # makespan error of the profile-only (static) prediction, job-wide:
+        # the slowest rank's measured step against the slowest predicted
+        meas_job = grp.max(meas_make)
+        pred_job = grp.max(static_pred if static_same else pred_make)
+        pred_adapt_job = grp.max(pred_make)
+        out = {
+            "label": label, "m": m, "rows_l1": rows_l1, "row0": row0, "P": P, "ms_step": ms_step,
+            "value": 2.0 * m_all * n * k / (ms_step * 1e-3) / 1e12, "clocks": clk.summary(),
+            "schedule": schedule, "sched": sched, "rows": rows, "dyn": dyn, "rep": rep,
+            "c_check": c_check, "ref_policy_makespan": ref_policy_makespan, "warm_sm_mhz": warm_sm_mhz,
+            "static_same": static_same, "meas_job": meas_job, "pred_job": pred_job,
+            "pred_adapt_job": pred_adapt_job, "warm_reps": warm_reps, "ex": ex, "io": io,
+            "A16": A16, "B16": B16, "C": C, "comm": wcomm, "np": np_,
+        }
+        if save and rank == 0:
+            (save / f"report_{label}.json").write_text(json.dumps(rep, indent=1))
+        return out
 
-    c_check, c_rows = verify_c()
-    # relative Frobenius bound for fp32 accumulation over K (SURVEY.md 8d,
-    # DESIGN.md section 5): 2e-5 up to K = 16384 (1.78e-5 measured there,
-    # as cuBLAS), growing linearly with K beyond
-    C_TOL = 2e-5 * max(1.0, k / 16384)
-    if not (c_check <= C_TOL and c_rows <= C_TOL):
-        raise SystemExit(f"C check failed: rel err {c_check:.3e} / sampled rows {c_rows:.3e} > {C_TOL}")
+    main_res = resident_run("main", m_total, n, k, args.steps, args.b_panels)
+    m, row0 = main_res["m"], main_res["row0"]
+    sched, rows, schedule = main_res["sched"], main_res["rows"], main_res["schedule"]
+    ex, io, A16, B16, C = main_res["ex"], main_res["io"], main_res["A16"], main_res["B16"], main_res["C"]
+    P, np_, dyn, rep_last = main_res["P"], main_res["np"], main_res["dyn"], main_res["rep"]
+    ms_step, value, clocks = main_res["ms_step"], main_res["value"], main_res["clocks"]
 
-    # per-unit measured vs predicted (mean over the timed reports)
-    def unit_mean(key, field="measured"):
-        vals = []
-        for r in reports:
-            for d in r["devices"]:
-                if d["id"] == key:
-                    vals.append(d["compute"][field] * (1 if len(reports) > 1 else 1))
-        return sum(vals) / len(vals) if vals else 0.0
-
-    rep_last = reports[-1]
-    meas_make = sum(r["measured_makespan"] for r in reports) / len(reports)
-    pred_make = rep_last["predicted_makespan"]
-    static_pred = dyn["iterations"][0]["predicted_makespan"]
-    static_same = dyn["iterations"][0]["rows"] == {d["id"]: d["rows"] for d in sched["devices"]}
-    tc_compute = unit_mean(tc_id)
+    # roofline: the tensor kernel's launch inside the timed steps
+    tc_compute = rep_last["devices"][[d["id"] for d in rep_last["devices"]].index(tc_id)]["compute"]["measured"] \
+        if tc_id in [d["id"] for d in rep_last["devices"]] else 0.0
     tc_rows = rows.get(tc_id, 0)
     peak_burst, peak_sust, peak_kind = measured_peaks()
     achieved = 2.0 * tc_rows * n * k / tc_compute / 1e12 if tc_compute > 0 else 0.0
@@ -667,9 +766,8 @@ def main():
     for _ in range(max(3, args.steps // 2)):
         pair_co.append(ex.execute(schedule, io, 1)["measured_makespan"])
         pair_alone.append(ex.execute(s_sched, io, 1)["measured_makespan"])
-    standalone = {tc_id: statistics.median(pair_alone)}
+    best_single = statistics.median(pair_alone)
     simt_alone_pred = json.loads(poas.plan_standalone(profile, simt_id, m, n, k))["makespan"]
-    best_single = min(standalone.values())
     co_median = statistics.median(pair_co)
     speedup = best_single / co_median if co_median > 0 else None
 
@@ -712,6 +810,24 @@ def main():
         yr = A16.double() @ (B16m.double() @ xg)
         cublas_rel = float((C_lib.double() @ xg - yr).norm() / yr.norm())
         del C_lib, yr
+
+    # ---- C4 (BASELINE config 4): 65536 x 8192 x 8192 row-sharded over the
+    # ranks -- strong scaling (total work fixed), measured in the same run
+    c4 = None
+    if not args.no_c4 and not args.m_total:
+        r4 = resident_run("c4", 65536, 8192, 8192, args.c4_steps, args.b_panels, adapt=True)
+        c4 = {"workload": f"C4: M=65536 x N=K=8192 row-sharded over {world} GPU(s), B broadcast from rank 0",
+              "scaling": "strong", "value": round(r4["value"], 3), "unit": "TFLOP/s",
+              "ms_per_step": round(r4["ms_step"], 4), "steps": args.c4_steps,
+              "level1_rows_per_gpu": r4["rows_l1"], "plan_rows": r4["rows"],
+              "b_panels": r4["P"], "b_transport": transport if world > 1 else None,
+              "predicted_makespan_ms": round(r4["pred_job"] * 1e3, 4),
+              "measured_makespan_ms": round(r4["meas_job"] * 1e3, 4),
+              "makespan_error_pct": round(100.0 * (r4["meas_job"] - r4["pred_job"]) / r4["meas_job"], 3),
+              "adapted_makespan_error_pct": round(100.0 * (r4["meas_job"] - r4["pred_adapt_job"])
+                                                  / r4["meas_job"], 3),
+              "c_check": r4["c_check"], "clocks": r4["clocks"]}
+        del r4
 
     # ---- e2e through the C ABI with host buffers over PCIe. Headline: the
     # tensor unit's link carries 16-bit A/B (the reference's XPU link model,
@@ -772,16 +888,11 @@ def main():
             t_probe = time.perf_counter()
             ex_e2e.execute(sched_e2e, io_h, 3)
             probe_ms = (time.perf_counter() - t_probe) / 3 * 1e3
-            if world > 1:
-                dist.barrier()
-            steps_e2e = max(3, min(args.steps, 10))
+            grp.barrier()
+            steps_e2e = max(3, args.steps)
             t0 = time.perf_counter()
             r_e2e = ex_e2e.execute(sched_e2e, io_h, steps_e2e)
-            wall = time.perf_counter() - t0
-            tw = torch.tensor([wall], device=dev)
-            if world > 1:
-                dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-            wall = float(tw.item())
+            wall = grp.max(time.perf_counter() - t0)
             linked = [d for d in se["devices"] if d["rows"] > 0 and not d["id"].startswith("cpu")]
             # bytes crossing the link per step: each GPU unit's A rows and all
             # of B in its link element size, its C rows in fp32
@@ -789,9 +900,9 @@ def main():
             h2d = sum(esz[d["id"]] * (d["rows"] * k + k * n) for d in linked)
             d2h = sum(4 * d["rows"] * n for d in linked)
             ms = wall / steps_e2e * 1e3
-            out = {"value": round(2.0 * m * world * n * k / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+            out = {"value": round(2.0 * m_total * n * k / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-                   "ms_per_step": round(ms, 3), "probe_ms_per_step": round(probe_ms, 3),
+                   "ms_per_step": round(ms, 3), "steps": steps_e2e, "probe_ms_per_step": round(probe_ms, 3),
                    # link roofline: the busiest direction's bytes at the
                    # profiled link bandwidth (full duplex when overlapped)
                    "link_bound_ms": None,
@@ -818,8 +929,7 @@ def main():
             bw = [float(ln.split()[1]) for ln in prof_e2e.splitlines() if ln.startswith("bandwidth ")]
             bw = max(bw) if bw else 0.0
             if bw > 0:
-                per_rank_h2d, per_rank_d2h = h2d, d2h
-                link_s = max(per_rank_h2d, per_rank_d2h) / bw if overlap else (per_rank_h2d + per_rank_d2h) / bw
+                link_s = max(h2d, d2h) / bw if overlap else (h2d + d2h) / bw
                 out["link_bound_ms"] = round(link_s * 1e3, 3)
                 out["link_bandwidth_gbs"] = round(bw / 1e9, 2)
             if save and rank == 0:
@@ -834,15 +944,15 @@ def main():
         # headline: a stream of GEMMs, each step's copies and GEMM overlapped
         # and consecutive steps pipelined; beside it the same with every step
         # isolated (its latency is the per-GEMM makespan), fp32 host operands,
-        # and the paper's synchronous copies
-        # Pipelining consecutive steps is an executor mode the adapt stage
-        # picks per box: each mode's 3-step probe (measured before either's
-        # timed steps) decides which one is the headline. (On most boxes it
+        # and the paper's synchronous copies. Pipelining is an executor mode
+        # the adapt stage picks per box: each mode's 3-step probe (measured
+        # before either's timed steps) decides the headline (on most boxes it
         # wins, 23.5 vs 29-30 ms; on a box with a weak host side the two
-        # directions' DMA contend and it lost, profiles/r01_overlap.)
+        # directions' DMA contend and it lost, profiles/r01_overlap).
         piped = run_e2e(2, overlap=True, pipeline=True)
         single = run_e2e(2, overlap=True)
-        if piped["probe_ms_per_step"] <= single["probe_ms_per_step"]:
+        choose_piped = grp.max(1.0 if piped["probe_ms_per_step"] <= single["probe_ms_per_step"] else 0.0) > 0
+        if choose_piped:
             e2e, e2e["single_step"] = piped, single
         else:
             e2e, e2e["pipelined"] = single, piped
@@ -851,13 +961,19 @@ def main():
         e2e["fp32_host"] = run_e2e(4, overlap=True)
         e2e["synchronous"] = run_e2e(2, overlap=False)
 
-    # ---- CPU baseline (rank 0 at N=1 only)
+    # ---- CPU baselines (rank 0 at N=1 only): the reference's CPU path (the
+    # oracle port executing the reference planner's CPU-only plan) and,
+    # beside it, this repo's own host-CPU unit (AVX-512 host_gemm) on the
+    # same host cores, so the GPU/CPU ratio has a competent CPU path next
+    # to it; plus the reference planner's own cost
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             tfl, sec, sample, cores = reference_cpu_path(args.n, sample_rows=args.ref_rows, reps=1)
             cpu_baseline = {"value": round(tfl, 4), "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                            "sample": sample}
+                            "sample": sample, "cpu_model": cpu_model()}
+            cpu_baseline["host_unit"] = host_unit_baseline(poas, args.n)
+            cpu_baseline["reference_planner"] = reference_planner_cost(profile, m, n, k)
         except Exception as exc:  # reported, never fatal
             cpu_baseline = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                             "sample": f"unavailable: {exc}"}
@@ -866,8 +982,8 @@ def main():
     # B panels in one launch; a CUDA-core unit launches once per panel),
     # plus the executor's start-gate kernel on this GPU
     launches_per_step = sum((1 if d["id"] == tc_id else P) for d in sched["devices"] if d["rows"] > 0) + 1
-    if save and rank == 0:
-        (save / "report_resident.json").write_text(json.dumps(rep_last, indent=1))
+    meas_make, pred_job, pred_adapt = main_res["meas_job"], main_res["pred_job"], main_res["pred_adapt_job"]
+    static_same = main_res["static_same"]
     if rank == 0:
         line = {
             "metric": "co-executed GEMM TFLOP/s at N=16384 (1/2/4/8 B200); speedup vs best single unit",
@@ -876,44 +992,39 @@ def main():
             "scaling": "strong" if args.m_total else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
             "config": {
-                "workload": (f"C4: M={m * world} x N=K={args.n} row-sharded over {world} GPU(s)" if args.m_total
-                             else f"C3: square GEMM N={args.n} per GPU (M={m}*{world})") + ", bf16 tensor-core + fp32 "
-                            f"CUDA-core co-execution planned by POAS; B broadcast from rank 0 (NCCL) at N>1",
-                "m": m * world, "n": n, "k": k, "parallelism": f"POAS row split x {world} GPU(s)",
-                "level1_rows_per_gpu": l1_rows,
+                "workload": (f"C4: M={m_total} x N=K={args.n} row-sharded over {world} GPU(s)" if args.m_total
+                             else f"C3: square GEMM N={args.n} per GPU (M={args.n}*{world})")
+                            + ", bf16 tensor-core + fp32 CUDA-core co-execution planned by POAS; at N>1 B "
+                              "broadcast from rank 0 by the library inside every step",
+                "m": m_total, "n": n, "k": k, "parallelism": f"POAS row split x {world} GPU(s)",
+                "level1_rows_per_gpu": main_res["rows_l1"],
                 "units": {tc_id: f"tcgen05 bf16->fp32 on {args.tc_sms} SMs",
                           simt_id: f"fp32 SIMT on {args.simt_sms} SMs"},
                 "planner_policy": args.policy,
-                "reference_policy_predicted_ms": round(ref_policy_makespan * 1e3, 4),
-                "plan_rows": rows, "l2": (f"inputs larger than L2 (per rank: A {m * k * 2 / 2**20:.0f} MiB + B {k * n * 2 / 2**20:.0f} MiB bf16, "
-                       f"fp32 copies twice that; L2 126 MB)" if (m * k + k * n) * 2 > 126e6
-                       else "inputs fit in L2 (small size)"),
+                "reference_policy_predicted_ms": round(main_res["ref_policy_makespan"] * 1e3, 4),
+                "plan_rows": rows, "l2": (f"inputs larger than L2 (per rank: A {m * k * 2 / 2**20:.0f} MiB + B "
+                                          f"{k * n * 2 / 2**20:.0f} MiB bf16, fp32 copies twice that; L2 126 MB)"
+                                          if (m * k + k * n) * 2 > 126e6 else "inputs fit in L2 (small size)"),
                 # the paper's scheduler is static: its prediction is the
                 # profile's, for the plan that ran (same rows); the dynamic
-                # re-fit's prediction is reported beside it
-                "predicted_makespan_ms": round((static_pred if static_same else pred_make) * 1e3, 4),
+                # re-fit's prediction is reported beside it. Job-wide: the
+                # slowest rank's step against the slowest prediction.
+                "predicted_makespan_ms": round(pred_job * 1e3, 4),
                 "measured_makespan_ms": round(meas_make * 1e3, 4),
-                "makespan_error_pct": round(100.0 * (meas_make - (static_pred if static_same else pred_make))
-                                            / meas_make, 3),
+                "makespan_error_pct": round(100.0 * (meas_make - pred_job) / meas_make, 3),
                 "prediction": ("profile-only (static POAS, the paper's scheduler) for the plan that ran, "
-                               "against the timed steps' mean" if static_same else
+                               "against the timed steps" if static_same else
                                "adapted (the profile-only plan differed from the plan that ran)"),
-                "adapted": {"predicted_makespan_ms": round(pred_make * 1e3, 4),
-                            "makespan_error_pct": round(100.0 * (meas_make - pred_make) / meas_make, 3),
-                            "warmup_sm_mhz": warm_sm_mhz,
+                "adapted": {"predicted_makespan_ms": round(pred_adapt * 1e3, 4),
+                            "makespan_error_pct": round(100.0 * (meas_make - pred_adapt) / meas_make, 3),
+                            "warmup_sm_mhz": main_res["warm_sm_mhz"],
                             "note": "dynamic scheduling: warm-up runs re-fit the profile (EWMA); under "
                                     "the power cap a short timed region can run in a boost phase the "
                                     "re-fit did not see (profiles/r01_warmup)"},
-                "static_plan": dict(_static_summary(dyn), **(
-                    {"error_vs_timed_pct": round(100.0 * (meas_make - dyn["iterations"][0]["predicted_makespan"])
-                                                 / meas_make, 3),
-                     "error_vs_timed_note": "the profile-only prediction against the timed steps' mean "
-                                            "(same rows as the adapted plan; the first run alone is at a "
-                                            "cooler clock)"}
-                    if dyn["iterations"][0]["rows"] == rows else {})),
+                "static_plan": _static_summary(dyn),
                 "dynamic_replans": dyn["replans"],
                 "dynamic_warmup_iterations": len(dyn["iterations"]),
-                "dynamic_warmup_steps_per_iteration": warm_reps,
+                "dynamic_warmup_steps_per_iteration": main_res["warm_reps"],
                 "speedup_vs_best_single_unit": round(speedup, 4) if speedup else None,
                 "best_single_unit": {"id": tc_id, "measured_makespan_ms": round(best_single * 1e3, 4),
                                      "coexec_paired_makespan_ms": round(co_median * 1e3, 4),
@@ -924,15 +1035,14 @@ def main():
                 "cublas_bf16_fp32out_tflops": round(2.0 * m * n * k / (cublas_ms * 1e-3) / 1e12, 2)
                 if cublas_ms else None,
                 "sm_count": sms_all, "profile_seconds": round(t_prof, 2),
-                "c_check": {"property": "C.x = A.(B.x), fp64, each unit's own operand precision, every rank",
-                            "max_rel_err": float(f"{c_check:.3e}"), "tol": C_TOL,
-                            "sampled_rows": {"rows": 64, "rel_frobenius": float(f"{c_rows:.3e}"),
-                                             "reference": "fp64 product of the same rounded operands "
-                                                          "(first/last, 128/256-row tile boundaries, random "
-                                                          "rows; every rank)"},
-                            "cublas_rel_err": float(f"{cublas_rel:.3e}") if cublas_rel is not None else None},
-                "dist_backend": backend if world > 1 else None,
+                "c_check": dict(main_res["c_check"], **({"cublas_rel_err": float(f"{cublas_rel:.3e}")}
+                                                         if cublas_rel is not None else {})),
+                "b_transport": (f"{transport}: " + ("copy-engine chain over CUDA IPC (rank r pulls each "
+                                                    "panel from rank r-1), no SMs" if transport == "ce"
+                                                    else "ncclBroadcast per panel")) if world > 1 else None,
+                "level1_link_gbs": round(link_bw / 1e9, 2) if link_bw else None,
                 "b_panels": P,
+                "c4": c4,
             },
             # the tensor kernel is timed inside a long back-to-back run under
             # the power cap: the measured SUSTAINED cuBLAS figure is its
@@ -952,8 +1062,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    grp.barrier()
     return 0
 
 

@@ -39,9 +39,10 @@ def row_offsets(rows: Sequence[int]) -> list[int]:
 
 
 def comm_name() -> str:
-    """A rendezvous token identical on every rank of one launch: the
-    launcher's run id and port (torchrun exports both)."""
+    """A rendezvous token identical on every rank of one launch and unique
+    per launch: the launcher's pid (the ranks' common parent), run id and
+    port (torchrun exports both)."""
     run = os.environ.get("TORCHELASTIC_RUN_ID", "none")
     port = os.environ.get("MASTER_PORT", "0")
-    tok = "".join(ch if ch.isalnum() else "_" for ch in f"{run}_{port}")
+    tok = "".join(ch if ch.isalnum() else "_" for ch in f"{os.getppid()}_{run}_{port}")
     return f"job_{tok}"

@@ -36,3 +36,19 @@ def test_reference_arm_other_ranks_are_silent():
     r = run({"RANK": "1", "WORLD_SIZE": "2"}, "--size", "1024", "--steps", "1", "--warmup", "0")
     assert r.returncode == 0, r.stderr
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_gpus_flag_launches_ranks_itself(ref):
+    """`bench.py --gpus 2` without a launcher re-runs itself under torchrun
+    with two ranks (one process per GPU); rank 0 alone prints, with
+    n_gpus 2. The reference arm needs no GPU, so the
+    self-launch is exercised here on CPU; the GPU arm's is in
+    tests/test_gpu_multirank.py."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--size", "1024", "--steps", "1", "--warmup", "0", "--ref-rows", "64"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    assert json.loads(lines[0])["n_gpus"] == 2
