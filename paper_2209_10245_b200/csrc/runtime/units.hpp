@@ -43,6 +43,7 @@ struct UnitSpec {
   Link link = Link::pcie;       // what time_transfer measures
   std::int64_t probe_min = 0;   // own probe side range ("probe=MIN-MAX"); 0 = config's
   std::int64_t probe_max = 0;
+  double preroll_ms = 0.0;      // GPU units: back-to-back launches before each timed probe
 };
 
 // "<id>=<kind>[:key=value]*"
@@ -132,6 +133,8 @@ class Unit : public poas::DeviceBackend {
   PinnedBuffer xfer_host_;
   std::vector<float> host_a_, host_b_, host_c_;
   std::int64_t probe_side_ = 0;
+  double last_probe_s_ = 0.0;  // the previous probe (pre-roll sizing)
+  std::int64_t last_probe_side_ = 0;
   DeviceBuffer scratch_[7];  // 0-4 staging, 5 streamed-launch state, 6 second C (pipelined)
 };
 

@@ -67,18 +67,47 @@ def io_for(n, d, with_host=False):
     return poas.GemmIO(**kw)
 
 
-def c5(sizes):
-    units = ("gpu0.tc=xpu:dev=0:sms=146:dtype=bf16:elem=2:link=hbm:probe=8192-16384;"
-             "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048")
-    profile = poas.profile_machine(units, PROF, True)
-    ex = poas.Executor(units)
-    out = {"profile": profile, "rows": []}
+def tc_probe_range(n):
+    """The tensor unit's probe sides for a GEMM of side n: the sizes it
+    will run (about n/2 .. n), so the linear model is fit where it is used
+    (a fit at 8192-16384 extrapolated to 1024 or 32768 misses by 50-190%)."""
+    lo = max(512, n // 2)
+    return lo, n
+
+
+def warm(n_sec=1.0):
+    """Continuous tensor-core load: the power-capped steady state."""
+    a = torch.empty(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(8192, 8192, device="cuda")
+    poas.fill_uniform(poas.DTYPE_BF16, a.data_ptr(), 8192, 8192, 8192, 0, 0, 8192, 3)
+    st = torch.cuda.current_stream().cuda_stream
+    t_end = time.perf_counter() + n_sec
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            poas.tc_gemm(2, 8192, 8192, 8192, a.data_ptr(), 8192, a.data_ptr(), 8192, c.data_ptr(), 8192, stream=st)
+        torch.cuda.synchronize()
+
+
+def c5(sizes, preroll_ms=20, steps=10):
+    """Per size: profile the units with the tensor unit probed over the
+    sizes it will run (pre-rolled probes, after a warm-up: the sustained
+    regime), plan (static POAS prediction), run the static plan's steps
+    (its error against them), then the dynamic re-plan, timed."""
+    out = {"rows": [], "preroll_ms": preroll_ms}
     for n in sizes:
+        lo, hi = tc_probe_range(n)
+        units = (f"gpu0.tc=xpu:dev=0:sms=146:dtype=bf16:elem=2:link=hbm:probe={lo}-{hi}:preroll={preroll_ms};"
+                 "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048")
         d = operands(n)
         io = io_for(n, d)
-        it = max(2, min(50, int(2e12 / (2 * n ** 3)) + 1))
-        # static plan first run, then dynamic re-planning (warm-up), then the
-        # adapted plan timed
+        warm(0.5)
+        profile = poas.profile_machine(units, PROF, True)
+        ex = poas.Executor(units)
+        it = max(3, min(50, int(2e12 / (2 * n ** 3)) + 1))
+        static = poas.plan_policy(profile, n, n, n, POLICY)
+        ex.execute(static, io, 2)
+        rep_s = ex.execute(static, io, it)
+        # the dynamic re-plan (warm-up), then the adapted plan timed
         dyn = ex.run_dynamic(profile, n, n, n, io, iterations=max(4, it), alpha=1.0, policy=POLICY,
                              replan_threshold_pct=2.0)
         sched = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
@@ -94,11 +123,15 @@ def c5(sizes):
         cublas_fn = lambda: torch.mm(d["A16"], d["B16"], out_dtype=torch.float32, out=c_lib)  # noqa: E731
         cublas_fn()
         cb_s = ev_time(cublas_fn, it)
-        row = {"n": n, "plan_rows": {x["id"]: x["rows"] for x in s["devices"]},
+        row = {"n": n, "tc_probe": [lo, hi], "steps": it,
+               "static_plan_rows": {x["id"]: x["rows"] for x in json.loads(static)["devices"]},
+               "static_predicted_ms": rep_s["predicted_makespan"] * 1e3,
+               "static_measured_ms": rep_s["measured_makespan"] * 1e3,
+               "static_error_pct": rep_s["makespan_error_pct"],
+               "plan_rows": {x["id"]: x["rows"] for x in s["devices"]},
                "poas_tflops": 2 * n ** 3 / poas_s / 1e12, "poas_pred_ms": rep["predicted_makespan"] * 1e3,
-               "poas_meas_ms": poas_s * 1e3, "makespan_error_pct": rep["makespan_error_pct"],
-               "static_plan_error_pct": dyn["iterations"][0]["makespan_error_pct"],
-               "static_plan_rows": dyn["iterations"][0]["rows"], "replans": dyn["replans"],
+               "poas_meas_ms": poas_s * 1e3, "adapted_error_pct": rep["makespan_error_pct"],
+               "replans": dyn["replans"],
                "tc_only_148sm_tflops": 2 * n ** 3 / tc_s / 1e12,
                "cublas_bf16_fp32out_tflops": 2 * n ** 3 / cb_s / 1e12}
         if n <= 4096:
@@ -111,7 +144,7 @@ def c5(sizes):
             row["host_cores"] = os.cpu_count()
         out["rows"].append(row)
         print(json.dumps(row), file=sys.stderr, flush=True)
-        del d
+        del d, c_lib
         torch.cuda.empty_cache()
     return out
 
@@ -165,7 +198,13 @@ def simt_vs_cublas_fp32(n=8192):
 
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
+    only_c5 = "--c5" in sys.argv
+    pre = 20
+    for a in sys.argv:
+        if a.startswith("--preroll="):
+            pre = int(a.split("=")[1])
     sizes = [1024, 2048, 4096, 8192, 16384] + ([] if quick else [32768])
-    res = {"gpu": torch.cuda.get_device_name(), "c5": c5(sizes), "c2": c2(),
-           "simt_vs_cublas_fp32": simt_vs_cublas_fp32()}
+    res = {"gpu": torch.cuda.get_device_name(), "c5": c5(sizes, pre)}
+    if not only_c5:
+        res.update({"c2": c2(), "simt_vs_cublas_fp32": simt_vs_cublas_fp32()})
     print(json.dumps(res, indent=1))
