@@ -472,6 +472,8 @@ def main():
                     help="dynamic scheduling of the resident run: EWMA weight of the newest round")
     ap.add_argument("--warmup-seconds", type=float, default=1.0,
                     help="minimum length of the dynamic warm-up (steady power-capped state)")
+    ap.add_argument("--preroll", type=int, default=20,
+                    help="ms of back-to-back launches before each timed GPU-unit probe (0: cold probes)")
     ap.add_argument("--probe-warmup", type=float, default=0.5,
                     help="seconds of tensor-core GEMMs before profiling (0: probe a cool GPU)")
     ap.add_argument("--no-adapt", action="store_true",
@@ -521,8 +523,13 @@ def main():
 
     g = local  # CUDA ordinal inside this process (CUDA_VISIBLE_DEVICES respected)
     tc_id, simt_id = f"gpu{rank}.tc", f"gpu{rank}.simt"
-    units_res = (f"{tc_id}=xpu:dev={g}:sms={args.tc_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384;"
-                 f"{simt_id}=gpu:dev={g}:sms={args.simt_sms}:exclusive=1:elem=4:link=hbm:probe=512-2048")
+    # probes pre-rolled (preroll=<ms>: each timed probe follows back-to-back
+    # launches of the same GEMM): the sustained, power-capped regime the
+    # timed steps run in, not the boost clock of a launch after an idle gap
+    units_res = (f"{tc_id}=xpu:dev={g}:sms={args.tc_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384:"
+                 f"preroll={args.preroll};"
+                 f"{simt_id}=gpu:dev={g}:sms={args.simt_sms}:exclusive=1:elem=4:link=hbm:probe=512-2048:"
+                 f"preroll={args.preroll}")
     # NCCL's kernels need the idle units' SMs: no lending with that transport
     units_exec = units_res + (";lend=0" if (world > 1 and transport == "nccl") else "")
 

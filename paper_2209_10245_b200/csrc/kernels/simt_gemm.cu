@@ -5,11 +5,13 @@
 // Replaces the GPU-kind synthetic law of the reference (SyntheticBackend::
 // time_gemm, /root/reference/proj/src/simulator.cpp:30-34).
 //
-// 128 x 128 x 16 CTA tile, 256 threads, 8 x 8 register micro-tile per thread
-// (two 4 x 4 quadrants 64 apart so the float4 shared-memory reads stay
-// conflict-free), 128-bit coalesced global loads prefetched into registers
-// one K-step ahead, shared memory double buffered (one barrier per K-step).
-// Persistent over tiles so the grid size is the unit's SM budget.
+// Default kernel: simt_gemm2_kernel (FFMA2, 128 x 256 tiles, grouped
+// raster; below). simt_gemm_kernel: the earlier plain-FFMA kernel, 128 x 128
+// (or 128 x 256) x 16 CTA tiles, 256 threads, 8 x 8 (8 x 16) register
+// micro-tile per thread (4-column quadrants 64 apart so the float4
+// shared-memory reads stay conflict-free), 128-bit coalesced global loads
+// prefetched into registers one K-step ahead, shared memory double buffered
+// (one barrier per K-step). Persistent over tiles: grid = the SM budget.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -169,6 +171,164 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) simt_gemm_kernel(const S
           for (int e = 0; e < 4; ++e) {
             if (c + e < p.N) {
               float o = acc[i][4 * h + e];
+              if (p.accumulate) o += crow[c + e];
+              crow[c + e] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// FFMA2 kernel (default for M >= 128). Blackwell's fp32 pipe takes packed
+// pairs: fma.rn.f32x2 (SASS FFMA2) does two FMAs per lane per issue, with a
+// scalar operand broadcast to both halves -- exactly the outer-product step
+// acc[i][j..j+1] += a[i] * b[j..j+1]. With plain FFMA every FMA costs an
+// issue slot and the loop sat at ~65% of the FMA pipe (shared-memory loads,
+// address arithmetic and barriers compete for the same slots); with FFMA2
+// the 128 FMAs of a thread's k-step are 64 issues.
+//   CTA tile 128 x 256 x 16, 256 threads, 8 x 16 accumulators per thread
+//   (acc2[8][8] float2 pairs: four 4-column quadrants 64 apart, so the
+//   float4 shared-memory reads stay conflict-free), A transposed into shared
+//   memory, 128-bit global loads one K-step ahead in registers, two shared
+//   buffers (one barrier per K-step), persistent over tiles in a grouped
+//   raster (8 M-tiles per group: the ~148 tiles in flight share their A and
+//   B panels through L2 instead of streaming all of B per M-row of tiles).
+constexpr int kGroupM2 = 8;
+
+template <bool kVec>
+__global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs p) {
+  constexpr int kTN = 256;
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  float* As = smem;                          // [2][kBK][kBM + kPad]  (A transposed)
+  float* Bs = smem + 2 * kBK * (kBM + kPad);  // [2][kBK][kTN]
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15;
+  const int ty = tid >> 4;
+  const int a_row = tid >> 1;
+  const int a_k = (tid & 1) * 8;
+  const int b_k = tid >> 4;
+  const int b_col = (tid & 15) * 4;
+
+  const int tiles_n = (p.N + kTN - 1) / kTN;
+  const int total = p.tiles_m * tiles_n;
+  const int per_group = kGroupM2 * tiles_n;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int group = t / per_group;
+    const int first_m = group * kGroupM2;
+    const int gm = min(p.tiles_m - first_m, kGroupM2);
+    const int in_group = t - group * per_group;
+    const int mb = first_m + in_group % gm;
+    const int nb = in_group / gm;
+    const int m0 = mb * kBM;
+    const int n0 = nb * kTN;
+
+    float2 acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+
+    float4 ra[2], rb[4];
+    auto load_global = [&](int k0) {
+      const int gr = m0 + a_row;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gk = k0 + a_k + h * 4;
+        if (kVec && gr < p.M && gk + 3 < p.K) {
+          ra[h] = __ldg(reinterpret_cast<const float4*>(p.A + (long long)gr * p.lda + gk));
+        } else {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = (gr < p.M && gk + e < p.K) ? p.A[(long long)gr * p.lda + gk + e] : 0.f;
+          ra[h] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      }
+      const int gk = k0 + b_k;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int gc = n0 + b_col + h * 64;
+        if (kVec && gk < p.K && gc + 3 < p.N) {
+          rb[h] = __ldg(reinterpret_cast<const float4*>(p.B + (long long)gk * p.ldb + gc));
+        } else {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = (gk < p.K && gc + e < p.N) ? p.B[(long long)gk * p.ldb + gc + e] : 0.f;
+          rb[h] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      }
+    };
+    auto store_shared = [&](int buf) {
+      float* as = As + buf * kBK * (kBM + kPad) + a_row;
+      const float av[8] = {ra[0].x, ra[0].y, ra[0].z, ra[0].w, ra[1].x, ra[1].y, ra[1].z, ra[1].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) as[(a_k + e) * (kBM + kPad)] = av[e];
+      float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + b_k * kTN + b_col);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) bs[16 * h] = rb[h];
+    };
+
+    const int k_steps = (p.K + kBK - 1) / kBK;
+    load_global(0);
+    __syncthreads();  // previous tile's readers are done with both buffers
+    store_shared(0);
+    __syncthreads();
+
+    for (int ks = 0; ks < k_steps; ++ks) {
+      const int buf = ks & 1;
+      if (ks + 1 < k_steps) load_global((ks + 1) * kBK);
+      const float* as = As + buf * kBK * (kBM + kPad) + ty * 4;
+      const float4* bs = reinterpret_cast<const float4*>(Bs + buf * kBK * kTN) + tx;
+#pragma unroll
+      for (int k = 0; k < kBK; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad));
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + 64);
+        float2 b[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float4 v = bs[k * (kTN / 4) + 16 * h];
+          b[2 * h] = make_float2(v.x, v.y);
+          b[2 * h + 1] = make_float2(v.z, v.w);
+        }
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 ai = make_float2(a[i], a[i]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = __ffma2_rn(ai, b[j], acc[i][j]);
+        }
+      }
+      if (ks + 1 < k_steps) store_shared(buf ^ 1);
+      __syncthreads();
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+      if (r >= p.M) continue;
+      float* crow = p.C + (long long)r * p.ldc;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int c = n0 + h * 64 + tx * 4;
+        const float2 lo = acc[i][2 * h], hi = acc[i][2 * h + 1];
+        if (kVec && c + 3 < p.N) {
+          float4 o = make_float4(lo.x, lo.y, hi.x, hi.y);
+          if (p.accumulate) {
+            const float4 q = *reinterpret_cast<const float4*>(crow + c);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4*>(crow + c) = o;
+        } else {
+          const float v[4] = {lo.x, lo.y, hi.x, hi.y};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c + e < p.N) {
+              float o = v[e];
               if (p.accumulate) o += crow[c + e];
               crow[c + e] = o;
             }
@@ -462,7 +622,9 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
                           reinterpret_cast<const void*>(simt_gemm_kernel<true, 4>),
                           reinterpret_cast<const void*>(simt_gemm_kernel<false, 4>),
                           reinterpret_cast<const void*>(simt_gemm_kernel<true, 2, 2>),
-                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 2, 2>)})
+                          reinterpret_cast<const void*>(simt_gemm_kernel<false, 2, 2>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<true>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false>)})
       if (attr_err == cudaSuccess)
         attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
   });
@@ -483,13 +645,23 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
     const size_t dyn = exclusive_sm ? 100 * 1024 : 0;
     return launch_skinny(vec, rg, grid, dyn, stream, p);
   }
-  // Tile: 128 x 256 (8 x 16 per thread, one CTA per SM) by default;
-  // POAS_SIMT_TILE=128: 128 x 128 (8 x 8), one CTA per SM; =128x2: 128 x 128
-  // with registers capped so two CTAs share an SM (16 warps to hide
-  // shared-memory latency). Exclusive units pad shared memory so that no
-  // tensor-core CTA (210 KB) fits beside them.
+  // Default: the FFMA2 kernel (128 x 256 tiles, grouped raster). Earlier
+  // FFMA kernels for A/B comparisons: POAS_SIMT_TILE=256: 128 x 256 (8 x 16
+  // per thread, one CTA per SM); =128: 128 x 128 (8 x 8); =128x2: 128 x 128
+  // with registers capped so two CTAs share an SM. Exclusive units pad
+  // shared memory so that no tensor-core CTA (210 KB) fits beside them.
   const char* tw = std::getenv("POAS_SIMT_TILE");
-  const std::string tile = tw ? tw : "256";
+  const std::string tile = tw ? tw : "ffma2";
+  if (tile == "ffma2") {
+    const int tiles2 = p.tiles_m * static_cast<int>((N + 255) / 256);
+    if (grid > tiles2) grid = tiles2;
+    const size_t smem2 = exclusive_sm ? 120 * 1024 : (2 * kBK * (kBM + kPad) + 2 * kBK * 256) * sizeof(float);
+    if (vec)
+      simt_gemm2_kernel<true><<<grid, kThreads, smem2, stream>>>(p);
+    else
+      simt_gemm2_kernel<false><<<grid, kThreads, smem2, stream>>>(p);
+    return cudaGetLastError();
+  }
   const bool wide = tile != "128" && tile != "128x2";
   const bool two = tile == "128x2";
   const int tn = wide ? 256 : 128;

@@ -103,13 +103,15 @@ def c5(sizes, preroll_ms=20, steps=10):
         warm(0.5)
         profile = poas.profile_machine(units, PROF, True)
         ex = poas.Executor(units)
-        it = max(3, min(50, int(2e12 / (2 * n ** 3)) + 1))
+        # timed runs last >= ~0.25 s back to back (the sustained regime the
+        # pre-rolled probes were taken in; a 1 ms burst runs at boost clock)
+        it = max(3, min(2000, int(0.25 / (2 * n ** 3 / 1.3e15)) + 1))
         static = poas.plan_policy(profile, n, n, n, POLICY)
-        ex.execute(static, io, 2)
+        ex.execute(static, io, max(3, it // 2))
         rep_s = ex.execute(static, io, it)
         # the dynamic re-plan (warm-up), then the adapted plan timed
-        dyn = ex.run_dynamic(profile, n, n, n, io, iterations=max(4, it), alpha=1.0, policy=POLICY,
-                             replan_threshold_pct=2.0)
+        dyn = ex.run_dynamic(profile, n, n, n, io, iterations=6, alpha=1.0, policy=POLICY,
+                             replan_threshold_pct=2.0, repeats=max(1, it // 6))
         sched = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
         s = json.loads(sched)
         rep = ex.execute(sched, io, it)
