@@ -66,6 +66,7 @@ def ref_lib() -> C.CDLL:
             "ref_profile_synthetic": (C.c_int, [cp, u64, C.POINTER(vp)]),
             "ref_exact_profile": (C.c_int, [cp, C.POINTER(vp)]),
             "ref_probe_trace": (C.c_int, [cp, u64, C.POINTER(vp)]),
+            "ref_evaluate_report": (C.c_int, [cp, cp, C.c_int, u64, C.POINTER(vp)]),
             "ref_machine_config_roundtrip": (C.c_int, [cp, C.POINTER(vp)]),
             "ref_rng_draw": (u64, [u64, cp, C.c_int, dp]),
             "ref_time_plan": (C.c_int, [cp, i64, i64, i64, C.c_int, dp]),
@@ -198,6 +199,14 @@ class ref:
         """Every synthetic-backend measurement the reference profile_machine
         takes, in call order (oracle/ref_shim.cpp ref_probe_trace)."""
         return json.loads(_rcall(ref_lib().ref_probe_trace, machine_cfg.encode(), seed))
+
+    @staticmethod
+    def evaluate_report(machine_cfg, inputs, repeats=2, seed=1):
+        """The reference evaluate report (format_report_json) for
+        `inputs` = [(name, m, n, k), ...] on a synthetic machine."""
+        spec = ";".join(f"{nm}:{m}x{n}x{k}" for nm, m, n, k in inputs)
+        return json.loads(_rcall(ref_lib().ref_evaluate_report, machine_cfg.encode(), spec.encode(),
+                                 repeats, seed))
 
     @staticmethod
     def exact_profile(machine_cfg):

@@ -273,6 +273,35 @@ int ref_probe_trace(const char* machine_cfg, uint64_t seed, char** out) {
   });
 }
 
+// The reference's evaluate report (format_report_json, proj/src/simulator.cpp:
+// 448-490) for a synthetic machine and "name:MxNxK;..." inputs -- the schema
+// the B200 CLI's `poas evaluate` report follows.
+int ref_evaluate_report(const char* machine_cfg, const char* inputs, int repeats, uint64_t seed,
+                        char** out) {
+  return guarded([&] {
+    const poas::MachineConfig cfg = poas::parse_machine_config(machine_cfg);
+    const poas::MachineProfile prof = poas::profile_machine(cfg, seed);
+    std::vector<poas::EvalInput> in;
+    std::string list(inputs);
+    std::size_t at = 0;
+    while (at < list.size()) {
+      std::size_t end = list.find(';', at);
+      if (end == std::string::npos) end = list.size();
+      const std::string item = list.substr(at, end - at);
+      const std::size_t colon = item.find(':');
+      poas::EvalInput e;
+      e.name = item.substr(0, colon);
+      e.dims = poas::parse_dims(item.substr(colon + 1));
+      in.push_back(e);
+      at = end + 1;
+    }
+    poas::EvalOptions opt;
+    opt.repeats = repeats;
+    opt.seed = seed;
+    *out = dup(poas::format_report_json(poas::evaluate_inputs(prof, cfg, in, opt)));
+  });
+}
+
 // The reference test fixture's exact (noise-free) profile of a machine config.
 int ref_exact_profile(const char* machine_cfg, char** out) {
   return guarded([&] {

@@ -4,12 +4,14 @@
 //   poas profile  --units SPEC [--profiling k=v,..] [--bus true|false] --out FILE
 //   poas plan     --profile FILE --dims MxNxK --out FILE [--policy reference|best-subset]
 //   poas run      --schedule FILE --units SPEC [--repeats N] [--seed S] [--host]
+//                 [--out-c FILE]   (C as raw fp32, row-major)
 //   poas evaluate --units SPEC [--inputs FILE] [--repeats N] [--seed S]
 //                 [--policy P] [--profiling k=v,..] [--adapt N] --out-dir DIR
 //   poas adapt    --profile FILE --units SPEC --dims MxNxK [--iterations N]
 //                 [--alpha A] [--threshold PCT] [--policy P] [--seed S] [--host]
 //                 [--out-profile FILE] [--out FILE]
-// Exit codes as the reference: 0 success, 1 domain or usage error, 2 internal.
+// Exit codes as the reference: 0 success, 1 domain or usage error (a
+// poas::Error), 2 anything else -- CUDA failures included.
 // `run` replaces `simulate` (poas.cpp:116-151): it executes the schedule on
 // the box (inputs from the seeded counter generator) and writes
 // <schedule>.report.json in the simulate report's shape.
@@ -328,6 +330,27 @@ int cmd_run(const Args& a) {
   std::printf("%.3f TFLOP/s\nwrote %s\n",
               2.0 * static_cast<double>(s.dims.total_ops()) / r.measured_makespan / 1e12,
               report.c_str());
+  if (a.has("out-c")) {
+    // C (fp32, row-major m x n) as the units left it: GPU units' rows in
+    // device memory for resident runs, host-CPU units' (and every unit's,
+    // for --host runs) in host memory; rows contiguous in schedule order
+    const poas::MatrixDims& d = s.dims;
+    std::vector<float> c(static_cast<std::size_t>(d.m) * static_cast<std::size_t>(d.n));
+    const std::vector<std::int64_t> row0 = poas::row_offsets(s);
+    for (std::size_t i = 0; i < s.devices.size(); ++i) {
+      const std::int64_t r0 = row0[i], rows = s.devices[i].rows;
+      if (rows == 0) continue;
+      const Unit* u = ex.find(s.devices[i].id);
+      float* dst = c.data() + r0 * d.n;
+      const std::size_t bytes = static_cast<std::size_t>(rows) * static_cast<std::size_t>(d.n) * 4;
+      if (ops->io.resident && u->on_gpu())
+        cuda_ok(cudaMemcpy(dst, ops->io.c_dev + r0 * ops->io.ldc_dev, bytes, cudaMemcpyDeviceToHost), "copy C");
+      else
+        std::memcpy(dst, ops->io.c_host + r0 * ops->io.ldc_host, bytes);
+    }
+    write_atomic(a.get("out-c"), std::string(reinterpret_cast<const char*>(c.data()), c.size() * 4));
+    std::printf("wrote %s\n", a.get("out-c").c_str());
+  }
   return 0;
 }
 
@@ -438,12 +461,19 @@ int cmd_evaluate(const Args& a) {
   std::vector<const Unit*> all_units;
   for (const auto& u : ex.units()) all_units.push_back(u.get());
 
-  std::string j = "{\n  \"machine_hash\": \"" + ex.machine_hash() + "\",\n  \"seed\": " +
+  // report.json: the reference's evaluate report (format_report_json,
+  // proj/src/simulator.cpp:448-490) key for key -- machine_hash, seed,
+  // repeats, devices, inputs[{name, dims, tops, predicted/measured makespan,
+  // makespan_error_pct, devices[{id, rows, share_pct, finish/compute/copy
+  // error, standalone_makespan, speedup}]}], rmse[{id, finish, compute,
+  // copy}] -- plus a "b200" object per input and at the top for what only
+  // this implementation has (policy, dynamic re-fit, measured TFLOP/s, which
+  // standalone runs were measured and which predicted).
+  const auto q = [](const std::string& x) { return "\"" + poas_b200::capi::json_escape(x) + "\""; };
+  std::string j = "{\n  \"machine_hash\": " + q(ex.machine_hash()) + ",\n  \"seed\": " +
                   std::to_string(seed) + ",\n  \"repeats\": " + std::to_string(repeats) +
-                  ",\n  \"policy\": \"" + policy + "\",\n  \"adapt\": " + std::to_string(adapt) +
                   ",\n  \"devices\": [";
-  for (std::size_t i = 0; i < prof.devices.size(); ++i)
-    j += (i ? ", " : "") + std::string("\"") + prof.devices[i].id + "\"";
+  for (std::size_t i = 0; i < prof.devices.size(); ++i) j += (i ? ", " : "") + q(prof.devices[i].id);
   j += "],\n  \"inputs\": [\n";
   std::string txt = "machine " + ex.machine_hash() + "  seed " + std::to_string(seed) +
                     "  repeats " + std::to_string(repeats) + "  policy " + policy + "\n\n";
@@ -451,7 +481,7 @@ int cmd_evaluate(const Args& a) {
   std::snprintf(line, sizeof line, "%-6s %-22s %8s %12s %12s %8s %10s %8s\n", "input", "dims",
                 "TOps", "predicted s", "measured s", "err %", "TFLOP/s", "speedup");
   txt += line;
-  std::map<std::string, std::vector<double>> e_fin, e_cp;
+  std::map<std::string, std::vector<double>> e_fin, e_cp, e_cy;
   for (std::size_t ii = 0; ii < inputs.size(); ++ii) {
     const EvalInput& in = inputs[ii];
     poas::Schedule s = poas::plan_with_policy(live, in.dims, policy);
@@ -474,20 +504,22 @@ int cmd_evaluate(const Args& a) {
       ex.run(s, ops->io, 1);
     }
     const poas::SimulationResult r = ex.run(s, ops->io, repeats);
+    // standalone run of every unit (evaluate_one, simulator.cpp:224-232):
+    // measured when its predicted standalone makespan is at most
+    // --max-standalone seconds, else its prediction stands in
+    std::vector<double> alone(prof.devices.size(), 0.0);
+    std::vector<char> alone_measured(prof.devices.size(), 0);
     double best_alone = 0.0;
-    std::string alone_json;
-    for (const poas::DeviceProfile& d : prof.devices) {
-      const poas::Schedule sa = poas::standalone_schedule(live, d.id, in.dims);
-      double meas = -1.0;
+    for (std::size_t di = 0; di < prof.devices.size(); ++di) {
+      const poas::Schedule sa = poas::standalone_schedule(live, prof.devices[di].id, in.dims);
+      alone[di] = sa.makespan;
       if (sa.makespan <= max_alone) {
         auto oa = operands_for(ex, sa, seed + ii, false);
         ex.run(sa, oa->io, 1);
-        meas = ex.run(sa, oa->io, repeats).measured_makespan;
-        if (best_alone == 0.0 || meas < best_alone) best_alone = meas;
+        alone[di] = ex.run(sa, oa->io, repeats).measured_makespan;
+        alone_measured[di] = 1;
       }
-      alone_json += (alone_json.empty() ? "" : ", ") + std::string("{\"id\": \"") + d.id +
-                    "\", \"predicted\": " + g(sa.makespan) + ", \"measured\": " +
-                    (meas < 0 ? "null" : g(meas)) + "}";
+      if (best_alone == 0.0 || alone[di] < best_alone) best_alone = alone[di];
     }
     const double tops = static_cast<double>(in.dims.total_ops()) / 1e12;
     const double speedup = best_alone > 0 ? best_alone / r.measured_makespan : 0.0;
@@ -498,30 +530,40 @@ int cmd_evaluate(const Args& a) {
                   tops, r.predicted_makespan, r.measured_makespan, r.makespan_error_pct,
                   2 * tops / r.measured_makespan, speedup);
     txt += line;
-    j += std::string(ii ? ",\n" : "") + "    {\"name\": \"" + in.name + "\", \"dims\": {\"m\": " +
-         std::to_string(in.dims.m) + ", \"n\": " + std::to_string(in.dims.n) + ", \"k\": " +
-         std::to_string(in.dims.k) + "}, \"tops\": " + g(tops) + ", \"predicted_makespan\": " +
-         g(r.predicted_makespan) + ", \"measured_makespan\": " + g(r.measured_makespan) +
-         ", \"makespan_error_pct\": " + g(r.makespan_error_pct) +
-         (adapt > 0 ? ", \"static_plan_error_pct\": " + g(static_err) : std::string()) +
-         ", \"speedup_vs_best_single\": " +
-         g(speedup) + ", \"standalone\": [" + alone_json + "], \"devices\": [";
-    for (std::size_t k = 0; k < r.devices.size(); ++k) {
-      const poas::DeviceOutcome& d = r.devices[k];
-      j += std::string(k ? ", " : "") + "{\"id\": \"" + d.id + "\", \"rows\": " +
-           std::to_string(d.rows) + ", \"share_pct\": " +
-           g(100.0 * static_cast<double>(d.rows) / static_cast<double>(in.dims.m)) +
-           ", \"finish_error_pct\": " + g(d.finish.error_pct) + ", \"compute_error_pct\": " +
-           g(d.compute.error_pct) + ", \"copy_error_pct\": " + g(d.copy.error_pct) + "}";
-      if (d.rows > 0) {
-        e_fin[d.id].push_back(d.finish.error_pct);
-        e_cp[d.id].push_back(d.compute.error_pct);
+    j += std::string(ii ? ",\n" : "") + "    {\n      \"name\": " + q(in.name) +
+         ",\n      \"dims\": {\"m\": " + std::to_string(in.dims.m) + ", \"n\": " +
+         std::to_string(in.dims.n) + ", \"k\": " + std::to_string(in.dims.k) + "},\n      \"tops\": " +
+         g(tops) + ",\n      \"predicted_makespan\": " + g(r.predicted_makespan) +
+         ",\n      \"measured_makespan\": " + g(r.measured_makespan) +
+         ",\n      \"makespan_error_pct\": " + g(r.makespan_error_pct) + ",\n      \"devices\": [";
+    std::string measured_ids;
+    for (std::size_t di = 0; di < prof.devices.size(); ++di) {
+      const std::string& id = prof.devices[di].id;
+      const poas::DeviceOutcome* d = nullptr;
+      for (const poas::DeviceOutcome& o : r.devices)
+        if (o.id == id) d = &o;
+      const std::int64_t rows = d ? d->rows : 0;
+      j += std::string(di ? ", " : "") + "\n        {\"id\": " + q(id) + ", \"rows\": " +
+           std::to_string(rows) + ", \"share_pct\": " +
+           g(100.0 * static_cast<double>(rows) / static_cast<double>(in.dims.m)) +
+           ", \"finish_error_pct\": " + g(d ? d->finish.error_pct : 0.0) +
+           ", \"compute_error_pct\": " + g(d ? d->compute.error_pct : 0.0) +
+           ", \"copy_error_pct\": " + g(d ? d->copy.error_pct : 0.0) +
+           ", \"standalone_makespan\": " + g(alone[di]) +
+           ", \"speedup\": " + g(alone[di] / r.measured_makespan) + "}";
+      if (d) {  // the reference's RMSE takes every device of the co-executed run
+        e_fin[id].push_back(d->finish.error_pct);
+        e_cp[id].push_back(d->compute.error_pct);
+        e_cy[id].push_back(d->copy.error_pct);
       }
+      if (alone_measured[di]) measured_ids += (measured_ids.empty() ? "" : ", ") + q(id);
     }
-    j += "]}";
+    j += "\n      ],\n      \"b200\": {\"tflops\": " + g(2 * tops / r.measured_makespan) +
+         ", \"speedup_vs_best_single\": " + g(speedup) + ", \"standalone_measured\": [" + measured_ids +
+         "]" + (adapt > 0 ? ", \"static_plan_error_pct\": " + g(static_err) : std::string()) + "}\n    }";
   }
   j += "\n  ],\n  \"rmse\": [";
-  txt += "\nRMSE % across inputs, finish (compute)\n";
+  txt += "\nRMSE % across inputs, finish (compute, copy)\n";
   std::size_t idx = 0;
   for (const poas::DeviceProfile& d : prof.devices) {
     auto rms = [](const std::vector<double>& v) {
@@ -529,13 +571,14 @@ int cmd_evaluate(const Args& a) {
       for (double x : v) s += x * x;
       return v.empty() ? 0.0 : std::sqrt(s / static_cast<double>(v.size()));
     };
-    const double f = rms(e_fin[d.id]), c = rms(e_cp[d.id]);
-    j += std::string(idx++ ? ", " : "") + "{\"id\": \"" + d.id + "\", \"finish\": " + g(f) +
-         ", \"compute\": " + g(c) + "}";
-    std::snprintf(line, sizeof line, "%-14s %.2f (%.2f)\n", d.id.c_str(), f, c);
+    const double f = rms(e_fin[d.id]), c = rms(e_cp[d.id]), y = rms(e_cy[d.id]);
+    j += std::string(idx++ ? ", " : "") + "\n    {\"id\": " + q(d.id) + ", \"finish\": " + g(f) +
+         ", \"compute\": " + g(c) + ", \"copy\": " + g(y) + "}";
+    std::snprintf(line, sizeof line, "%-14s %.2f (%.2f, %.2f)\n", d.id.c_str(), f, c, y);
     txt += line;
   }
-  j += "]\n}\n";
+  j += "\n  ],\n  \"b200\": {\"policy\": " + q(policy) + ", \"adapt\": " + std::to_string(adapt) +
+       ", \"max_standalone_s\": " + g(max_alone) + "}\n}\n";
   mkdir(out_dir.c_str(), 0755);
   write_atomic(out_dir + "/report.json", j);
   write_atomic(out_dir + "/report.txt", txt);
@@ -564,8 +607,10 @@ int main(int argc, char** argv) {
     std::fprintf(stderr, "poas: error: %s\n", e.what());
     return 1;
   } catch (const poas_b200::capi::AbiError& e) {
-    std::fprintf(stderr, "poas: error: %s\n", e.what());
-    return 1;
+    // CUDA / internal failures are not domain errors: exit 2 as any other
+    // non-poas::Error exception (proj/tools/poas.cpp:251-260)
+    std::fprintf(stderr, "poas: internal error: %s\n", e.what());
+    return 2;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "poas: internal error: %s\n", e.what());
     return 2;
