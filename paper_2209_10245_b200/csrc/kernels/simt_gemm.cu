@@ -195,6 +195,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) simt_gemm_kernel(const S
 //   buffers (one barrier per K-step), persistent over tiles in a grouped
 //   raster (8 M-tiles per group: the ~148 tiles in flight share their A and
 //   B panels through L2 instead of streaming all of B per M-row of tiles).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int kN>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
+}
+
 constexpr int kGroupM2 = 8;
 
 template <bool kVec>
@@ -208,8 +222,10 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
   const int tid = threadIdx.x;
   const int tx = tid & 15;
   const int ty = tid >> 4;
-  const int a_row = tid >> 1;
-  const int a_k = (tid & 1) * 8;
+  // a warp loads 32 consecutive rows of A at one k offset: its transposed
+  // shared stores hit 32 distinct banks
+  const int a_row = tid & 127;
+  const int a_k = (tid >> 7) * 8;
   const int b_k = tid >> 4;
   const int b_col = (tid & 15) * 4;
 
@@ -232,29 +248,45 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
+    // A: 128-bit loads into registers one K-step ahead (unconditional for
+    // interior tiles), stored transposed at the end of the step. B: cp.async
+    // straight into the other shared buffer (no registers, no transpose;
+    // out-of-range bytes zero-filled) for 16-byte aligned operands.
+    const bool full_m = kVec && m0 + kBM <= p.M;
     float4 ra[2], rb[4];
-    auto load_global = [&](int k0) {
+    auto load_a = [&](int k0) {
       const int gr = m0 + a_row;
+      if (full_m && k0 + kBK <= p.K) {
+        const float4* src = reinterpret_cast<const float4*>(p.A + (long long)gr * p.lda + k0 + a_k);
+        ra[0] = __ldg(src);
+        ra[1] = __ldg(src + 1);
+        return;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int gk = k0 + a_k + h * 4;
-        if (kVec && gr < p.M && gk + 3 < p.K) {
-          ra[h] = __ldg(reinterpret_cast<const float4*>(p.A + (long long)gr * p.lda + gk));
-        } else {
-          float v[4];
+        float v[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[e] = (gr < p.M && gk + e < p.K) ? p.A[(long long)gr * p.lda + gk + e] : 0.f;
-          ra[h] = make_float4(v[0], v[1], v[2], v[3]);
-        }
+        for (int e = 0; e < 4; ++e)
+          v[e] = (gr < p.M && gk + e < p.K) ? p.A[(long long)gr * p.lda + gk + e] : 0.f;
+        ra[h] = make_float4(v[0], v[1], v[2], v[3]);
       }
+    };
+    auto load_b = [&](int k0, int buf) {
       const int gk = k0 + b_k;
+      if constexpr (kVec) {
+        float* bs = Bs + buf * kBK * kTN + b_k * kTN + b_col;
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int gc = n0 + b_col + h * 64;
-        if (kVec && gk < p.K && gc + 3 < p.N) {
-          rb[h] = __ldg(reinterpret_cast<const float4*>(p.B + (long long)gk * p.ldb + gc));
-        } else {
+        for (int h = 0; h < 4; ++h) {
+          const int gc = n0 + b_col + h * 64;
+          const int bytes = gk < p.K ? max(0, min(16, (p.N - gc) * 4)) : 0;
+          cp_async16(bs + 64 * h, bytes ? p.B + (long long)gk * p.ldb + gc : p.B, bytes);
+        }
+        cp_async_commit();
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int gc = n0 + b_col + h * 64;
           float v[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e)
@@ -268,20 +300,28 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
       const float av[8] = {ra[0].x, ra[0].y, ra[0].z, ra[0].w, ra[1].x, ra[1].y, ra[1].z, ra[1].w};
 #pragma unroll
       for (int e = 0; e < 8; ++e) as[(a_k + e) * (kBM + kPad)] = av[e];
-      float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + b_k * kTN + b_col);
+      if constexpr (kVec) {
+        cp_async_wait<0>();  // this thread's B copies for the step have landed
+      } else {
+        float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + b_k * kTN + b_col);
 #pragma unroll
-      for (int h = 0; h < 4; ++h) bs[16 * h] = rb[h];
+        for (int h = 0; h < 4; ++h) bs[16 * h] = rb[h];
+      }
     };
 
     const int k_steps = (p.K + kBK - 1) / kBK;
-    load_global(0);
     __syncthreads();  // previous tile's readers are done with both buffers
+    load_a(0);
+    load_b(0, 0);
     store_shared(0);
     __syncthreads();
 
     for (int ks = 0; ks < k_steps; ++ks) {
       const int buf = ks & 1;
-      if (ks + 1 < k_steps) load_global((ks + 1) * kBK);
+      if (ks + 1 < k_steps) {
+        load_a((ks + 1) * kBK);
+        load_b((ks + 1) * kBK, buf ^ 1);
+      }
       const float* as = As + buf * kBK * (kBM + kPad) + ty * 4;
       const float4* bs = reinterpret_cast<const float4*>(Bs + buf * kBK * kTN) + tx;
 #pragma unroll
@@ -315,6 +355,152 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const int c = n0 + h * 64 + tx * 4;
+        const float2 lo = acc[i][2 * h], hi = acc[i][2 * h + 1];
+        if (kVec && c + 3 < p.N) {
+          float4 o = make_float4(lo.x, lo.y, hi.x, hi.y);
+          if (p.accumulate) {
+            const float4 q = *reinterpret_cast<const float4*>(crow + c);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4*>(crow + c) = o;
+        } else {
+          const float v[4] = {lo.x, lo.y, hi.x, hi.y};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c + e < p.N) {
+              float o = v[e];
+              if (p.accumulate) o += crow[c + e];
+              crow[c + e] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// FFMA2 with 16 warps per SM: the same 128 x 256 x 16 CTA tile over 512
+// threads, 8 x 8 accumulators each (two 4-row groups 64 apart x two
+// 4-column quadrants 128 apart). With 8 warps (two per scheduler) a
+// warp's shared-memory latency and fixed-latency waits leave the FP32 pipe
+// idle ~25% of the time (ncu: stall "wait" 1.2 + short scoreboard 0.35 per
+// issue); four warps per scheduler cover them, at 1/3 more shared-memory
+// loads per FMA (still ~60% of the smem wavefront budget).
+constexpr int kThreads3 = 512;
+
+template <bool kVec>
+__global__ void __launch_bounds__(kThreads3, 1) simt_gemm3_kernel(const SimtArgs p) {
+  constexpr int kTN = 256;
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  float* As = smem;                          // [2][kBK][kBM + kPad]  (A transposed)
+  float* Bs = smem + 2 * kBK * (kBM + kPad);  // [2][kBK][kTN]
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 31;  // columns tx*4 + {0..3} and 128 + tx*4 + {0..3}
+  const int ty = tid >> 5;  // rows ty*4 + {0..3} and 64 + ty*4 + {0..3}
+  // global loads: A 128 x 16 (one float4 per thread: a warp = 32 rows, so
+  // the transposed shared stores hit 32 distinct banks); B 16 x 256 (two)
+  const int a_row = tid & 127;
+  const int a_k = (tid >> 7) * 4;
+  const int b_k = tid >> 5;
+  const int b_col = tx * 4;
+
+  const int tiles_n = (p.N + kTN - 1) / kTN;
+  const int total = p.tiles_m * tiles_n;
+  const int per_group = kGroupM2 * tiles_n;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int group = t / per_group;
+    const int first_m = group * kGroupM2;
+    const int gm = min(p.tiles_m - first_m, kGroupM2);
+    const int in_group = t - group * per_group;
+    const int m0 = (first_m + in_group % gm) * kBM;
+    const int n0 = (in_group / gm) * kTN;
+
+    float2 acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+
+    float4 ra, rb[2];
+    auto load_global = [&](int k0) {
+      const int gr = m0 + a_row;
+      const int gk = k0 + a_k;
+      if (kVec && gr < p.M && gk + 3 < p.K) {
+        ra = __ldg(reinterpret_cast<const float4*>(p.A + (long long)gr * p.lda + gk));
+      } else {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          v[e] = (gr < p.M && gk + e < p.K) ? p.A[(long long)gr * p.lda + gk + e] : 0.f;
+        ra = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      const int bk = k0 + b_k;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gc = n0 + b_col + h * 128;
+        if (kVec && bk < p.K && gc + 3 < p.N) {
+          rb[h] = __ldg(reinterpret_cast<const float4*>(p.B + (long long)bk * p.ldb + gc));
+        } else {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = (bk < p.K && gc + e < p.N) ? p.B[(long long)bk * p.ldb + gc + e] : 0.f;
+          rb[h] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      }
+    };
+    auto store_shared = [&](int buf) {
+      float* as = As + buf * kBK * (kBM + kPad) + a_k * (kBM + kPad) + a_row;
+      as[0] = ra.x;
+      as[kBM + kPad] = ra.y;
+      as[2 * (kBM + kPad)] = ra.z;
+      as[3 * (kBM + kPad)] = ra.w;
+      float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + b_k * kTN + b_col);
+      bs[0] = rb[0];
+      bs[32] = rb[1];
+    };
+
+    const int k_steps = (p.K + kBK - 1) / kBK;
+    load_global(0);
+    __syncthreads();  // previous tile's readers are done with both buffers
+    store_shared(0);
+    __syncthreads();
+
+    for (int ks = 0; ks < k_steps; ++ks) {
+      const int buf = ks & 1;
+      if (ks + 1 < k_steps) load_global((ks + 1) * kBK);
+      const float* as = As + buf * kBK * (kBM + kPad) + ty * 4;
+      const float4* bs = reinterpret_cast<const float4*>(Bs + buf * kBK * kTN) + tx;
+#pragma unroll
+      for (int k = 0; k < kBK; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad));
+        const float4 a1 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + 64);
+        const float4 v0 = bs[k * (kTN / 4)];
+        const float4 v1 = bs[k * (kTN / 4) + 32];
+        const float2 b[4] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
+                             make_float2(v1.z, v1.w)};
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 ai = make_float2(a[i], a[i]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(ai, b[j], acc[i][j]);
+        }
+      }
+      if (ks + 1 < k_steps) store_shared(buf ^ 1);
+      __syncthreads();
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+      if (r >= p.M) continue;
+      float* crow = p.C + (long long)r * p.ldc;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = n0 + h * 128 + tx * 4;
         const float2 lo = acc[i][2 * h], hi = acc[i][2 * h + 1];
         if (kVec && c + 3 < p.N) {
           float4 o = make_float4(lo.x, lo.y, hi.x, hi.y);
@@ -431,20 +617,6 @@ __global__ void __launch_bounds__(kThreads, 1) simt_skinny_kernel(const SimtArgs
 // block barrier -- only per-thread cp.async group waits. A values come
 // through L1 as warp-uniform 128-bit loads.
 constexpr int kPipeK = 8;  // B rows per stage: 8 x 1024 x 4 B = 32 KB per stage
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-               "l"(gmem), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int kN>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
-}
 
 template <int kRows>
 __global__ void __launch_bounds__(kThreads, 1) simt_skinny_pipe_kernel(const SimtArgs p,
@@ -624,7 +796,9 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
                           reinterpret_cast<const void*>(simt_gemm_kernel<true, 2, 2>),
                           reinterpret_cast<const void*>(simt_gemm_kernel<false, 2, 2>),
                           reinterpret_cast<const void*>(simt_gemm2_kernel<true>),
-                          reinterpret_cast<const void*>(simt_gemm2_kernel<false>)})
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false>),
+                          reinterpret_cast<const void*>(simt_gemm3_kernel<true>),
+                          reinterpret_cast<const void*>(simt_gemm3_kernel<false>)})
       if (attr_err == cudaSuccess)
         attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
   });
@@ -652,6 +826,16 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
   // shared memory so that no tensor-core CTA (210 KB) fits beside them.
   const char* tw = std::getenv("POAS_SIMT_TILE");
   const std::string tile = tw ? tw : "ffma2";
+  if (tile == "ffma2x512") {
+    const int tiles3 = p.tiles_m * static_cast<int>((N + 255) / 256);
+    if (grid > tiles3) grid = tiles3;
+    const size_t smem3 = exclusive_sm ? 120 * 1024 : (2 * kBK * (kBM + kPad) + 2 * kBK * 256) * sizeof(float);
+    if (vec)
+      simt_gemm3_kernel<true><<<grid, kThreads3, smem3, stream>>>(p);
+    else
+      simt_gemm3_kernel<false><<<grid, kThreads3, smem3, stream>>>(p);
+    return cudaGetLastError();
+  }
   if (tile == "ffma2") {
     const int tiles2 = p.tiles_m * static_cast<int>((N + 255) / 256);
     if (grid > tiles2) grid = tiles2;

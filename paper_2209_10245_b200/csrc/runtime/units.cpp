@@ -320,6 +320,34 @@ double Unit::time_transfer(std::uint64_t bytes) {
     // makes receiving all of B (the model's copy-in) expensive for it.
     const std::size_t rounded = (bytes + 15) / 16 * 16;
     void* src = xfer_dev2_.ensure(rounded);
+    if (spec_.kind == poas::DeviceKind::gpu) {
+      // A CUDA-core unit's operand path for the few rows a co-executed share
+      // gives it IS its skinny GEMM streaming all of B (each B element feeds
+      // only those rows): time exactly that -- 8 rows against a B of `bytes`
+      // (16384 columns) -- rather than a bare streaming read, which it
+      // outruns (a 4-row share at 32768^3 read B at 0.6x the bare rate).
+      const std::int64_t n = 16384;
+      const std::int64_t k = std::max<std::int64_t>(1, static_cast<std::int64_t>(rounded / 4 / n));
+      const std::int64_t rows = 8;
+      float* a = static_cast<float*>(xfer_dev_.ensure(static_cast<std::size_t>(rows * k) * 4 +
+                                                      static_cast<std::size_t>(rows * n) * 4));
+      float* c = a + rows * k;
+      const float* b = static_cast<const float*>(src);
+      const int sms = spec_.sms > 0 ? spec_.sms : 0;
+      if (xfer_warm_bytes_ != rounded) {  // one untimed pass: clocks, L2 and TLB state
+        cuda_check(simt_gemm(rows, n, k, a, k, b, n, c, n, false, sms, spec_.exclusive, stream_), "simt_gemm");
+        xfer_warm_bytes_ = rounded;
+      }
+      cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+      cuda_check(simt_gemm(rows, n, k, a, k, b, n, c, n, false, sms, spec_.exclusive, stream_), "simt_gemm");
+      cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+      cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "cudaEventElapsedTime");
+      // scaled to exactly `bytes` (B was k * 16384 fp32 elements)
+      return static_cast<double>(ms) * 1e-3 * static_cast<double>(bytes) /
+             static_cast<double>(k * n * 4);
+    }
     float* sink = static_cast<float*>(xfer_dev_.ensure(64));
     cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
     cuda_check(stream_read(src, rounded, spec_.sms, sink, stream_), "stream_read");

@@ -134,6 +134,7 @@ class Unit : public poas::DeviceBackend {
   std::vector<float> host_a_, host_b_, host_c_;
   std::int64_t probe_side_ = 0;
   double last_probe_s_ = 0.0;  // the previous probe (pre-roll sizing)
+  std::size_t xfer_warm_bytes_ = 0;  // link probe buffers warmed for this size
   std::int64_t last_probe_side_ = 0;
   DeviceBuffer scratch_[7];  // 0-4 staging, 5 streamed-launch state, 6 second C (pipelined)
 };

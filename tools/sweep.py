@@ -71,7 +71,13 @@ def tc_probe_range(n):
     """The tensor unit's probe sides for a GEMM of side n: the sizes it
     will run (about n/2 .. n), so the linear model is fit where it is used
     (a fit at 8192-16384 extrapolated to 1024 or 32768 misses by 50-190%)."""
-    lo = max(512, n // 2)
+    # small sizes: a wider ratio (n/4 .. n) so the fit sees enough spread of
+    # work above the launch-latency floor (n/2 .. n at 1024 fit a negative
+    # slope in noise)
+    # larger sizes: the top quarter (n*3/4 .. n): the tensor unit's time is
+    # concave in ops (efficiency still rising with size), and a line fit over
+    # n/2 .. n overestimates its end point by 12-17% at 4096 / 8192
+    lo = max(256, n // 4) if n <= 2048 else n * 3 // 4
     return lo, n
 
 
