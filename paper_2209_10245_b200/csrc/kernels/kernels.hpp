@@ -58,6 +58,9 @@ cudaError_t tc_gemm_stream(AbType t, int64_t M, int64_t N, int64_t K, const void
 
 // *flag = value in stream order (cuStreamWriteValue32).
 cudaError_t signal_flag(int* flag, int value, cudaStream_t stream);
+// Creates the per-stream state tc_gemm launches on `stream` use (its tile
+// scheduler counter), so that a launch can be captured into a CUDA graph.
+cudaError_t tc_prepare_stream(cudaStream_t stream);
 // The stream waits until *flag >= value (cuStreamWaitValue32, GEQ).
 cudaError_t wait_flag(const int* flag, int value, cudaStream_t stream);
 

@@ -1035,6 +1035,10 @@ const char* variant_name(TcVariant v) {
 }
 }  // namespace
 
+cudaError_t tc_prepare_stream(cudaStream_t stream) {
+  return next_tile_counter(stream) ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
 const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t) {
   return variant_name(choose_variant(M, N, device_sm_count()));
 }

@@ -422,7 +422,10 @@ std::vector<EvalInput> load_inputs(const std::string& path) {
   return out;
 }
 
+// %.17g; JSON has no inf/nan: a phase that was not measured (a resident
+// run's zero-length copies give e = 100 (0 - p) / 0) is written as null
 std::string g(double v) {
+  if (!std::isfinite(v)) return "null";
   char b[40];
   std::snprintf(b, sizeof b, "%.17g", v);
   return b;
@@ -552,9 +555,9 @@ int cmd_evaluate(const Args& a) {
            ", \"standalone_makespan\": " + g(alone[di]) +
            ", \"speedup\": " + g(alone[di] / r.measured_makespan) + "}";
       if (d) {  // the reference's RMSE takes every device of the co-executed run
-        e_fin[id].push_back(d->finish.error_pct);
-        e_cp[id].push_back(d->compute.error_pct);
-        e_cy[id].push_back(d->copy.error_pct);
+        for (auto [vec, v] : {std::pair{&e_fin, d->finish.error_pct}, std::pair{&e_cp, d->compute.error_pct},
+                              std::pair{&e_cy, d->copy.error_pct}})
+          if (std::isfinite(v)) (*vec)[id].push_back(v);  // unmeasured phases (null) left out
       }
       if (alone_measured[di]) measured_ids += (measured_ids.empty() ? "" : ", ") + q(id);
     }
