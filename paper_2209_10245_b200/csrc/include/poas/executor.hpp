@@ -130,15 +130,12 @@ class Executor {
     std::vector<int*> retired;
   };
 
-  // One repeat of a resident GPU-only plan captured as a CUDA graph (see
-  // Executor::run): replayed per repeat with its timing-event nodes
-  // pointed at that repeat's events.
+  // The device-side repeat of a one-unit resident plan captured as a CUDA
+  // graph (see Executor::run), replayed per repeat.
   struct RepeatGraph {
     std::string key;
     void* graph = nullptr;  // cudaGraph_t
     void* exec = nullptr;   // cudaGraphExec_t
-    std::vector<std::pair<void*, int>> nodes;  // (event-record node, role: -1 = t0, 2i / 2i+1 = unit i cp0 / cp1)
-    std::vector<void*> placeholders;           // the events recorded at capture
     int device = 0;
   };
 

@@ -14,6 +14,7 @@
 // (one barrier per K-step). Persistent over tiles: grid = the SM budget.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -211,9 +212,12 @@ __device__ __forceinline__ void cp_async_wait() {
 
 constexpr int kGroupM2 = 8;
 
-template <bool kVec>
+template <bool kVec, int kBK2 = 16>
 __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs p) {
   constexpr int kTN = 256;
+  constexpr int kBK = kBK2;  // K depth of a step (16 or 32)
+  constexpr int kAV = kBK / 8;  // A float4 loads per thread per step
+  constexpr int kBP = kBK / 16;  // B row passes per step
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float* As = smem;                          // [2][kBK][kBM + kPad]  (A transposed)
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
   // a warp loads 32 consecutive rows of A at one k offset: its transposed
   // shared stores hit 32 distinct banks
   const int a_row = tid & 127;
-  const int a_k = (tid >> 7) * 8;
+  const int a_k = (tid >> 7) * (kBK / 2);
   const int b_k = tid >> 4;
   const int b_col = (tid & 15) * 4;
 
@@ -253,17 +257,17 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
     // straight into the other shared buffer (no registers, no transpose;
     // out-of-range bytes zero-filled) for 16-byte aligned operands.
     const bool full_m = kVec && m0 + kBM <= p.M;
-    float4 ra[2], rb[4];
+    float4 ra[kAV], rb[4 * kBP];
     auto load_a = [&](int k0) {
       const int gr = m0 + a_row;
       if (full_m && k0 + kBK <= p.K) {
         const float4* src = reinterpret_cast<const float4*>(p.A + (long long)gr * p.lda + k0 + a_k);
-        ra[0] = __ldg(src);
-        ra[1] = __ldg(src + 1);
+#pragma unroll
+        for (int h = 0; h < kAV; ++h) ra[h] = __ldg(src + h);
         return;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kAV; ++h) {
         const int gk = k0 + a_k + h * 4;
         float v[4];
 #pragma unroll
@@ -273,39 +277,49 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
       }
     };
     auto load_b = [&](int k0, int buf) {
-      const int gk = k0 + b_k;
-      if constexpr (kVec) {
-        float* bs = Bs + buf * kBK * kTN + b_k * kTN + b_col;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int gc = n0 + b_col + h * 64;
-          const int bytes = gk < p.K ? max(0, min(16, (p.N - gc) * 4)) : 0;
-          cp_async16(bs + 64 * h, bytes ? p.B + (long long)gk * p.ldb + gc : p.B, bytes);
-        }
-        cp_async_commit();
-      } else {
+      for (int q = 0; q < kBP; ++q) {
+        const int gk = k0 + b_k + 16 * q;
+        if constexpr (kVec) {
+          float* bs = Bs + buf * kBK * kTN + (b_k + 16 * q) * kTN + b_col;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int gc = n0 + b_col + h * 64;
-          float v[4];
+          for (int h = 0; h < 4; ++h) {
+            const int gc = n0 + b_col + h * 64;
+            const int bytes = gk < p.K ? max(0, min(16, (p.N - gc) * 4)) : 0;
+            cp_async16(bs + 64 * h, bytes ? p.B + (long long)gk * p.ldb + gc : p.B, bytes);
+          }
+        } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[e] = (gk < p.K && gc + e < p.N) ? p.B[(long long)gk * p.ldb + gc + e] : 0.f;
-          rb[h] = make_float4(v[0], v[1], v[2], v[3]);
+          for (int h = 0; h < 4; ++h) {
+            const int gc = n0 + b_col + h * 64;
+            float v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              v[e] = (gk < p.K && gc + e < p.N) ? p.B[(long long)gk * p.ldb + gc + e] : 0.f;
+            rb[4 * q + h] = make_float4(v[0], v[1], v[2], v[3]);
+          }
         }
       }
+      if constexpr (kVec) cp_async_commit();
     };
     auto store_shared = [&](int buf) {
       float* as = As + buf * kBK * (kBM + kPad) + a_row;
-      const float av[8] = {ra[0].x, ra[0].y, ra[0].z, ra[0].w, ra[1].x, ra[1].y, ra[1].z, ra[1].w};
 #pragma unroll
-      for (int e = 0; e < 8; ++e) as[(a_k + e) * (kBM + kPad)] = av[e];
+      for (int h = 0; h < kAV; ++h) {
+        as[(a_k + 4 * h) * (kBM + kPad)] = ra[h].x;
+        as[(a_k + 4 * h + 1) * (kBM + kPad)] = ra[h].y;
+        as[(a_k + 4 * h + 2) * (kBM + kPad)] = ra[h].z;
+        as[(a_k + 4 * h + 3) * (kBM + kPad)] = ra[h].w;
+      }
       if constexpr (kVec) {
         cp_async_wait<0>();  // this thread's B copies for the step have landed
       } else {
-        float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + b_k * kTN + b_col);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) bs[16 * h] = rb[h];
+        for (int q = 0; q < kBP; ++q) {
+          float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + (b_k + 16 * q) * kTN + b_col);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) bs[16 * h] = rb[4 * q + h];
+        }
       }
     };
 
@@ -797,6 +811,8 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
                           reinterpret_cast<const void*>(simt_gemm_kernel<false, 2, 2>),
                           reinterpret_cast<const void*>(simt_gemm2_kernel<true>),
                           reinterpret_cast<const void*>(simt_gemm2_kernel<false>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<true, 32>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false, 32>),
                           reinterpret_cast<const void*>(simt_gemm3_kernel<true>),
                           reinterpret_cast<const void*>(simt_gemm3_kernel<false>)})
       if (attr_err == cudaSuccess)
@@ -836,14 +852,22 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
       simt_gemm3_kernel<false><<<grid, kThreads3, smem3, stream>>>(p);
     return cudaGetLastError();
   }
-  if (tile == "ffma2") {
+  if (tile == "ffma2" || tile == "ffma2k32") {
     const int tiles2 = p.tiles_m * static_cast<int>((N + 255) / 256);
     if (grid > tiles2) grid = tiles2;
-    const size_t smem2 = exclusive_sm ? 120 * 1024 : (2 * kBK * (kBM + kPad) + 2 * kBK * 256) * sizeof(float);
-    if (vec)
+    const int bk = tile == "ffma2k32" ? 32 : 16;
+    const size_t need = (2 * bk * (kBM + kPad) + 2 * bk * 256) * sizeof(float);
+    const size_t smem2 = exclusive_sm ? std::max<size_t>(120 * 1024, need) : need;
+    if (bk == 32) {
+      if (vec)
+        simt_gemm2_kernel<true, 32><<<grid, kThreads, smem2, stream>>>(p);
+      else
+        simt_gemm2_kernel<false, 32><<<grid, kThreads, smem2, stream>>>(p);
+    } else if (vec) {
       simt_gemm2_kernel<true><<<grid, kThreads, smem2, stream>>>(p);
-    else
+    } else {
       simt_gemm2_kernel<false><<<grid, kThreads, smem2, stream>>>(p);
+    }
     return cudaGetLastError();
   }
   const bool wide = tile != "128" && tile != "128x2";

@@ -225,7 +225,6 @@ void Executor::release_graph() {
   DeviceGuard g(graph_->device);
   if (graph_->exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_->exec));
   if (graph_->graph) cudaGraphDestroy(static_cast<cudaGraph_t>(graph_->graph));
-  for (void* e : graph_->placeholders) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   graph_.reset();
 }
 
@@ -750,156 +749,99 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         cuda_check(cudaStreamWaitEvent(unit[i]->stream(), entry[dev], 0), "cudaStreamWaitEvent");
   }
 
-  // ---- CUDA-graph replay. A resident, GPU-only plan on one GPU with B in
-  // place (no delivery events, flags or broadcast) has a fixed device-side
-  // repeat: capture it once as a graph (its timing events as event-record
-  // nodes) and replay it per repeat with those nodes pointed at the
-  // repeat's events -- one graph launch instead of a start-gate kernel,
-  // event records and the units' launches (tensor-map encoding included)
-  // per repeat, so the host never paces small GEMMs. No gate is needed: a
-  // launched graph starts with everything already enqueued. The graph is
-  // kept while the schedule and operands stay the same. POAS_EXEC_GRAPH=0
-  // turns it off.
+  // ---- CUDA-graph replay. A resident plan with ONE busy unit (a GPU unit,
+  // B in place: no delivery events, flags or broadcast) repeats a fixed
+  // device-side sequence: the unit's (conversion +) GEMM launch. It is
+  // captured once as a CUDA graph and replayed per repeat between the
+  // repeat's t0 / cp0 and cp1 event records on the unit's stream -- one
+  // graph launch instead of a start-gate kernel plus the launch sequence
+  // (tensor-map encoding included) per repeat, so the host never paces a
+  // small GEMM. No gate is needed: each repeat's events and launch are
+  // enqueued together and the GPU runs them back to back. The graph is kept
+  // while the schedule and operands stay the same. POAS_EXEC_GRAPH=0 turns
+  // it off.
   const char* graph_env = std::getenv("POAS_EXEC_GRAPH");
+  std::size_t graph_unit = nd;
+  for (std::size_t i = 0; i < nd; ++i)
+    if (schedule.devices[i].rows > 0) graph_unit = graph_unit == nd ? i : nd + 1;
   const bool graph_mode = io.resident && !any_cpu && !overlapped && !comm && !io.b_flags && !io.b_ready &&
-                          panels <= 1 && host_unit.size() == 1 &&
+                          panels <= 1 && graph_unit < nd && unit[graph_unit]->on_gpu() &&
                           !(graph_env && std::string(graph_env) == "0");
   if (graph_mode) {
-    const int dev = host_unit.begin()->first;
-    const std::size_t h = host_unit.begin()->second;
+    const std::size_t i = graph_unit;
+    Unit* u = unit[i];
+    const int dev = u->spec().device;
     DeviceGuard g(dev);
-    cudaStream_t hs = unit[h]->stream();
-    std::vector<std::size_t> busy;
-    for (std::size_t i = 0; i < nd; ++i)
-      if (unit[i]->on_gpu() && schedule.devices[i].rows > 0) busy.push_back(i);
+    cudaStream_t s = u->stream();
     char buf[512];
-    std::snprintf(buf, sizeof buf, "|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%p,%lld", static_cast<const void*>(io.a_dev),
+    std::snprintf(buf, sizeof buf, "|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%d", static_cast<const void*>(io.a_dev),
                   static_cast<long long>(io.lda_dev), static_cast<const void*>(io.b_dev),
                   static_cast<long long>(io.ldb_dev), io.a16_dev, static_cast<long long>(io.lda16_dev),
                   io.b16_dev, static_cast<long long>(io.ldb16_dev), static_cast<const void*>(io.c_dev),
-                  static_cast<long long>(io.ldc_dev));
-    std::string key = format_schedule(schedule) + buf;
-    for (std::size_t i : busy) key += "|" + std::to_string(extra_sms[i]);
+                  static_cast<long long>(io.ldc_dev), extra_sms[i]);
+    const std::string key = format_schedule(schedule) + buf;
     if (!graph_ || graph_->key != key) {
       release_graph();
       auto rg = std::make_unique<RepeatGraph>();
       rg->key = key;
       rg->device = dev;
-      for (std::size_t i : busy)  // per-stream state the capture must not create
-        if (unit[i]->spec().kind == DeviceKind::xpu)
-          cuda_check(poas_b200::tc_prepare_stream(unit[i]->stream()), "tc_prepare_stream");
-      const auto make_ev = [&](unsigned flags) {
-        cudaEvent_t e = nullptr;
-        cuda_check(cudaEventCreateWithFlags(&e, flags), "cudaEventCreate");
-        return e;
-      };
-      cudaEvent_t t0p = make_ev(cudaEventDefault);
-      rg->placeholders.push_back(t0p);
-      std::vector<cudaEvent_t> cp0p(nd, nullptr), cp1p(nd, nullptr), joins;
-      for (std::size_t i : busy) {
-        cp0p[i] = make_ev(cudaEventDefault);
-        cp1p[i] = make_ev(cudaEventDefault);
-        rg->placeholders.push_back(cp0p[i]);
-        rg->placeholders.push_back(cp1p[i]);
+      if (u->spec().kind == DeviceKind::xpu)  // per-stream state the capture must not create
+        cuda_check(poas_b200::tc_prepare_stream(s), "tc_prepare_stream");
+      const bool tensor = u->spec().kind == DeviceKind::xpu;
+      const std::int64_t r = schedule.devices[i].rows, r0 = row0[i];
+      float* c = io.c_dev + r0 * io.ldc_dev;
+      const void* a = nullptr;
+      const void* b = nullptr;
+      std::int64_t lda = 0, ldb = 0;
+      const bool sixteen = tensor && io.a16_dev && io.b16_dev;
+      if (sixteen) {
+        a = static_cast<const char*>(io.a16_dev) + r0 * io.lda16_dev * 2;
+        b = io.b16_dev;
+        lda = io.lda16_dev;
+        ldb = io.ldb16_dev;
+      } else {
+        a = io.a_dev + r0 * io.lda_dev;
+        b = io.b_dev;
+        lda = io.lda_dev;
+        ldb = io.ldb_dev;
       }
-      cudaEvent_t fork = make_ev(cudaEventDisableTiming);
       cudaGraph_t graph = nullptr;
-      cuda_check(cudaStreamBeginCapture(hs, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+      cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
       try {
-        cuda_check(cudaEventRecordWithFlags(t0p, hs, cudaEventRecordExternal), "cudaEventRecord");
-        cuda_check(cudaEventRecord(fork, hs), "cudaEventRecord");
-        for (std::size_t i : busy) {
-          Unit* u = unit[i];
-          cudaStream_t s = u->stream();
-          if (s != hs) cuda_check(cudaStreamWaitEvent(s, fork, 0), "cudaStreamWaitEvent");
-          const bool tensor = u->spec().kind == DeviceKind::xpu;
-          const std::int64_t r = schedule.devices[i].rows, r0 = row0[i];
-          float* c = io.c_dev + r0 * io.ldc_dev;
-          const void* a = nullptr;
-          const void* b = nullptr;
-          std::int64_t lda = 0, ldb = 0;
-          const bool sixteen = tensor && io.a16_dev && io.b16_dev;
-          if (sixteen) {
-            a = static_cast<const char*>(io.a16_dev) + r0 * io.lda16_dev * 2;
-            b = io.b16_dev;
-            lda = io.lda16_dev;
-            ldb = io.ldb16_dev;
-          } else {
-            a = io.a_dev + r0 * io.lda_dev;
-            b = io.b_dev;
-            lda = io.lda_dev;
-            ldb = io.ldb_dev;
-          }
-          cuda_check(cudaEventRecordWithFlags(cp0p[i], s, cudaEventRecordExternal), "cudaEventRecord");
-          if (tensor && !sixteen) {  // fp32 operands: converted inside the compute phase
-            const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
-            void* a16 = u->scratch(2).get();
-            void* b16 = u->scratch(3).get();
-            cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(a), lda, a16, lda16, r,
-                                              d.k, s), "convert A");
-            cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(b), ldb, b16, ldb16,
-                                              d.k, d.n, s), "convert B");
-            a = a16;
-            b = b16;
-            lda = lda16;
-            ldb = ldb16;
-          }
-          u->gemm(r, d.n, d.k, a, lda, b, ldb, c, io.ldc_dev, false, extra_sms[i]);
-          cuda_check(cudaEventRecordWithFlags(cp1p[i], s, cudaEventRecordExternal), "cudaEventRecord");
-          if (s != hs) {
-            joins.push_back(make_ev(cudaEventDisableTiming));
-            cuda_check(cudaEventRecord(joins.back(), s), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(hs, joins.back(), 0), "cudaStreamWaitEvent");
-          }
+        if (tensor && !sixteen) {  // fp32 operands: converted inside the compute phase
+          const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
+          void* a16 = u->scratch(2).get();
+          void* b16 = u->scratch(3).get();
+          cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(a), lda, a16, lda16, r,
+                                            d.k, s), "convert A");
+          cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(b), ldb, b16, ldb16,
+                                            d.k, d.n, s), "convert B");
+          a = a16;
+          b = b16;
+          lda = lda16;
+          ldb = ldb16;
         }
+        u->gemm(r, d.n, d.k, a, lda, b, ldb, c, io.ldc_dev, false, extra_sms[i]);
       } catch (...) {
-        cudaStreamEndCapture(hs, &graph);
+        cudaStreamEndCapture(s, &graph);
         if (graph) cudaGraphDestroy(graph);
-        cudaEventDestroy(fork);
-        for (cudaEvent_t e : joins) cudaEventDestroy(e);
-        for (void* e : rg->placeholders) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         throw;
       }
-      cuda_check(cudaStreamEndCapture(hs, &graph), "cudaStreamEndCapture");
-      cudaEventDestroy(fork);
-      for (cudaEvent_t e : joins) cudaEventDestroy(e);
+      cuda_check(cudaStreamEndCapture(s, &graph), "cudaStreamEndCapture");
       rg->graph = graph;
       cudaGraphExec_t exec = nullptr;
       cuda_check(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
       rg->exec = exec;
-      std::size_t count = 0;
-      cuda_check(cudaGraphGetNodes(graph, nullptr, &count), "cudaGraphGetNodes");
-      std::vector<cudaGraphNode_t> nodes(count);
-      cuda_check(cudaGraphGetNodes(graph, nodes.data(), &count), "cudaGraphGetNodes");
-      for (cudaGraphNode_t nd_ : nodes) {
-        cudaGraphNodeType type;
-        cuda_check(cudaGraphNodeGetType(nd_, &type), "cudaGraphNodeGetType");
-        if (type != cudaGraphNodeTypeEventRecord) continue;
-        cudaEvent_t e = nullptr;
-        cuda_check(cudaGraphEventRecordNodeGetEvent(nd_, &e), "cudaGraphEventRecordNodeGetEvent");
-        int role = -2;
-        if (e == t0p) role = -1;
-        for (std::size_t i : busy) {
-          if (e == cp0p[i]) role = static_cast<int>(2 * i);
-          if (e == cp1p[i]) role = static_cast<int>(2 * i + 1);
-        }
-        if (role != -2) rg->nodes.emplace_back(nd_, role);
-      }
-      if (rg->nodes.size() != 1 + 2 * busy.size())
-        fail(errc::numerical_failure, "executor graph: timing nodes not found");
       graph_ = std::move(rg);
     }
     const auto exec = static_cast<cudaGraphExec_t>(graph_->exec);
     first_open = std::chrono::steady_clock::now();
     for (int rep = 0; rep < repeats; ++rep) {
       const std::size_t rr = static_cast<std::size_t>(rep);
-      for (const auto& [node, role] : graph_->nodes) {
-        const std::size_t i = role < 0 ? 0 : static_cast<std::size_t>(role / 2);
-        cudaEvent_t e = role < 0 ? t0[dev][rr] : (role % 2 == 0 ? ev[rr][i].cp0 : ev[rr][i].cp1);
-        cuda_check(cudaGraphExecEventRecordNodeSetEvent(exec, static_cast<cudaGraphNode_t>(node), e),
-                   "cudaGraphExecEventRecordNodeSetEvent");
-      }
-      cuda_check(cudaGraphLaunch(exec, hs), "cudaGraphLaunch");
+      cuda_check(cudaEventRecord(t0[dev][rr], s), "cudaEventRecord");
+      cuda_check(cudaEventRecord(ev[rr][i].cp0, s), "cudaEventRecord");
+      cuda_check(cudaGraphLaunch(exec, s), "cudaGraphLaunch");
+      cuda_check(cudaEventRecord(ev[rr][i].cp1, s), "cudaEventRecord");
     }
   }
 
