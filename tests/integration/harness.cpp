@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "poas/adapter.hpp"
 #include "poas/backend.hpp"
 #include "poas/device_model.hpp"
@@ -66,6 +68,38 @@ std::string run_dynamic(poas_executor_t ex, const std::string& profile_text,
 void run_overlap(const char* units, const std::string& profile_text, const poas::MatrixDims& dims,
                  const poas_gemm_io& io, int repeats) {
 #include "snippet_overlap.inc"
+}
+
+// the caller's JSON reader for the snippet: a flat array of strings
+std::vector<std::string> parse_string_array(const char* json) {
+  std::vector<std::string> out;
+  std::string cur;
+  bool in = false, esc = false;
+  for (const char* p = json; *p; ++p) {
+    const char ch = *p;
+    if (!in) {
+      if (ch == '"') in = true, cur.clear();
+      continue;
+    }
+    if (esc) {
+      cur += ch == 'n' ? '\n' : ch;
+      esc = false;
+    } else if (ch == '\\') {
+      esc = true;
+    } else if (ch == '"') {
+      in = false;
+      out.push_back(cur);
+    } else {
+      cur += ch;
+    }
+  }
+  return out;
+}
+
+std::string run_sharded(const char* job_token, int rank, int world, int device, const std::string& profile_text,
+                        const poas::MatrixDims& dims) {
+#include "snippet_sharded.inc"
+  return sharded_json;
 }
 
 }  // namespace
@@ -121,6 +155,16 @@ int main(int argc, char** argv) {
     std::fill(C2.begin(), C2.end(), -1.0f);
     run_overlap(units, profile_text, dims, io, 2);
     put("C_ovl.bin", C2.data(), nc * 4);
+
+    // a one-GPU box's profile (tensor + CUDA-core units) for the sharded plan
+    const std::string gpu_profile =
+        "poas-profile v1\n\nbus true\n\ndevice gpu0.tc\nkind xpu\nslope 7e-16\nintercept 2e-05\n"
+        "bandwidth 6500000000000\nelem_size 2\npriority 0\nalign 1\nops_min 1000000\n"
+        "ops_max 4398046511104\n\ndevice gpu0.simt\nkind gpu\nslope 3.5e-14\nintercept 2e-05\n"
+        "bandwidth 107000000000\nelem_size 4\npriority 1\nops_min 134217728\nops_max 8589934592\n";
+    const std::string token = "harness_" + std::to_string(::getpid());
+    const std::string sharded = run_sharded(token.c_str(), 0, 1, -1, gpu_profile, dims);
+    put("sharded.json", sharded.data(), sharded.size());
   } catch (const std::exception& e) {
     std::cerr << "harness: " << e.what() << "\n";
     return 1;

@@ -35,7 +35,7 @@ def snippets() -> dict:
 
 def test_snippets_present():
     s = snippets()
-    assert set(s) >= {"backend", "execute", "ctypes", "dynamic", "overlap"}, sorted(s)
+    assert set(s) >= {"backend", "execute", "ctypes", "dynamic", "overlap", "sharded"}, sorted(s)
 
 
 def test_cpp_snippets_compile_and_run_against_reference(tmp_path):
@@ -73,6 +73,9 @@ def test_cpp_snippets_compile_and_run_against_reference(tmp_path):
     assert rep["repeats"] == 2 and rep["measured_makespan"] > 0
     dyn = json.loads((tmp_path / "dynamic.json").read_text())
     assert len(dyn["iterations"]) == 2 and "profile" in dyn
+    sh = json.loads((tmp_path / "sharded.json").read_text())
+    assert sh["rows"] == [m] and sh["row0"] == [0]
+    assert sum(d["rows"] for d in sh["plans"][0]["devices"]) == m
 
 
 def test_ctypes_snippet_runs(poas):
