@@ -647,7 +647,10 @@ def main():
         # each one broadcasts B), bracketed by a barrier + synchronize, CUDA
         # events around them on the current stream (the executor's units
         # start behind an event recorded on it), SM clocks sampled during.
-        ex.execute(schedule, io, 1)
+        # the run's one-time costs, untimed: a one-unit resident plan replays
+        # its steps as one CUDA graph, captured for this schedule, operands
+        # and step count on first use
+        ex.execute(schedule, io, steps)
         grp.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -130,20 +130,21 @@ class Executor {
     std::vector<int*> retired;
   };
 
-  // The device-side repeat of a one-unit resident plan captured as a CUDA
-  // graph (see Executor::run), replayed per repeat.
+  // The repeats of a one-unit resident plan captured as one CUDA graph (see
+  // Executor::run), with the timing events its record nodes use.
   struct RepeatGraph {
     std::string key;
     void* graph = nullptr;  // cudaGraph_t
     void* exec = nullptr;   // cudaGraphExec_t
+    std::vector<void*> events;  // per repeat: t0, cp0, cp1 (cudaEvent_t)
     int device = 0;
   };
 
  private:
-  void release_graph();
+  static void release_graph(RepeatGraph& g);
   GateBuffer gates_;
   std::string hash_;
-  std::unique_ptr<RepeatGraph> graph_;
+  std::vector<std::unique_ptr<RepeatGraph>> graphs_;  // most recent last
 };
 
 // The reference's simulate report JSON (proj/tools/poas.cpp:85-114) for a

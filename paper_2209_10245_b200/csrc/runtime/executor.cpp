@@ -220,16 +220,16 @@ Executor::Executor(const std::string& spec) {
     }
 }
 
-void Executor::release_graph() {
-  if (!graph_) return;
-  DeviceGuard g(graph_->device);
-  if (graph_->exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_->exec));
-  if (graph_->graph) cudaGraphDestroy(static_cast<cudaGraph_t>(graph_->graph));
-  graph_.reset();
+void Executor::release_graph(RepeatGraph& g) {
+  DeviceGuard dg(g.device);
+  if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
+  if (g.graph) cudaGraphDestroy(static_cast<cudaGraph_t>(g.graph));
+  for (void* e : g.events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  g = RepeatGraph{};
 }
 
 Executor::~Executor() {
-  release_graph();
+  for (auto& gr : graphs_) release_graph(*gr);
   for (std::size_t i = 0; i < units_.size(); ++i)
     for (void* s : {h2d_[i], d2h_[i]})
       if (s) {
@@ -376,17 +376,20 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     std::map<int, cudaEvent_t>& entry;
     std::vector<std::vector<PhaseEvents>>& ev;
     std::vector<Unit*>& unit;
+    bool borrowed = false;  // graph replay: t0 / cp0 / cp1 belong to the cached graph
     ~Cleanup() {
       for (auto& per_rep : ev)
         for (std::size_t i = 0; i < per_rep.size(); ++i) {
           if (!unit[i]->on_gpu()) continue;
           DeviceGuard g(unit[i]->spec().device);
+          if (borrowed) per_rep[i].cp0 = per_rep[i].cp1 = nullptr;
           per_rep[i].destroy();
         }
       for (auto& [dev, v] : t0) {
         DeviceGuard g(dev);
-        for (cudaEvent_t e : v)
-          if (e) cudaEventDestroy(e);
+        if (!borrowed)
+          for (cudaEvent_t e : v)
+            if (e) cudaEventDestroy(e);
         if (entry.count(dev) && entry[dev]) cudaEventDestroy(entry[dev]);
       }
     }
@@ -750,22 +753,21 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
   }
 
   // ---- CUDA-graph replay. A resident plan with ONE busy unit (a GPU unit,
-  // B in place: no delivery events, flags or broadcast) repeats a fixed
-  // device-side sequence: the unit's (conversion +) GEMM launch. It is
-  // captured once as a CUDA graph and replayed per repeat between the
-  // repeat's t0 / cp0 and cp1 event records on the unit's stream -- one
-  // graph launch instead of a start-gate kernel plus the launch sequence
-  // (tensor-map encoding included) per repeat, so the host never paces a
-  // small GEMM. No gate is needed: each repeat's events and launch are
-  // enqueued together and the GPU runs them back to back. The graph is kept
-  // while the schedule and operands stay the same. POAS_EXEC_GRAPH=0 turns
-  // it off.
+  // B in place: no delivery events, flags or broadcast) runs a fixed
+  // device-side sequence per repeat: t0 / cp0 event records, the unit's
+  // (conversion +) GEMM launch, cp1. All `repeats` of them are captured once
+  // as one CUDA graph (the records as event-record nodes on events the
+  // graph owns) and launched at once: no start-gate kernel, no per-repeat
+  // host enqueue (tensor-map encoding included) pacing a small GEMM, and
+  // the kernels follow each other inside the graph. The last few graphs
+  // (schedule, operands, repeats) are kept for reuse. POAS_EXEC_GRAPH=0
+  // turns it off.
   const char* graph_env = std::getenv("POAS_EXEC_GRAPH");
   std::size_t graph_unit = nd;
   for (std::size_t i = 0; i < nd; ++i)
     if (schedule.devices[i].rows > 0) graph_unit = graph_unit == nd ? i : nd + 1;
   const bool graph_mode = io.resident && !any_cpu && !overlapped && !comm && !io.b_flags && !io.b_ready &&
-                          panels <= 1 && graph_unit < nd && unit[graph_unit]->on_gpu() &&
+                          panels <= 1 && graph_unit < nd && unit[graph_unit]->on_gpu() && repeats <= 256 &&
                           !(graph_env && std::string(graph_env) == "0");
   if (graph_mode) {
     const std::size_t i = graph_unit;
@@ -774,19 +776,27 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     DeviceGuard g(dev);
     cudaStream_t s = u->stream();
     char buf[512];
-    std::snprintf(buf, sizeof buf, "|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%d", static_cast<const void*>(io.a_dev),
-                  static_cast<long long>(io.lda_dev), static_cast<const void*>(io.b_dev),
-                  static_cast<long long>(io.ldb_dev), io.a16_dev, static_cast<long long>(io.lda16_dev),
-                  io.b16_dev, static_cast<long long>(io.ldb16_dev), static_cast<const void*>(io.c_dev),
-                  static_cast<long long>(io.ldc_dev), extra_sms[i]);
+    std::snprintf(buf, sizeof buf, "|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%p,%lld|%d|%d",
+                  static_cast<const void*>(io.a_dev), static_cast<long long>(io.lda_dev),
+                  static_cast<const void*>(io.b_dev), static_cast<long long>(io.ldb_dev), io.a16_dev,
+                  static_cast<long long>(io.lda16_dev), io.b16_dev, static_cast<long long>(io.ldb16_dev),
+                  static_cast<const void*>(io.c_dev), static_cast<long long>(io.ldc_dev), extra_sms[i], repeats);
     const std::string key = format_schedule(schedule) + buf;
-    if (!graph_ || graph_->key != key) {
-      release_graph();
+    RepeatGraph* hit = nullptr;
+    for (auto& gr : graphs_)
+      if (gr->key == key) hit = gr.get();
+    if (!hit) {
       auto rg = std::make_unique<RepeatGraph>();
       rg->key = key;
       rg->device = dev;
       if (u->spec().kind == DeviceKind::xpu)  // per-stream state the capture must not create
         cuda_check(poas_b200::tc_prepare_stream(s), "tc_prepare_stream");
+      for (int r = 0; r < repeats; ++r)
+        for (int k = 0; k < 3; ++k) {
+          cudaEvent_t e = nullptr;
+          cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+          rg->events.push_back(e);
+        }
       const bool tensor = u->spec().kind == DeviceKind::xpu;
       const std::int64_t r = schedule.devices[i].rows, r0 = row0[i];
       float* c = io.c_dev + r0 * io.ldc_dev;
@@ -805,26 +815,34 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
         lda = io.lda_dev;
         ldb = io.ldb_dev;
       }
+      const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
       cudaGraph_t graph = nullptr;
       cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
       try {
-        if (tensor && !sixteen) {  // fp32 operands: converted inside the compute phase
-          const std::int64_t lda16 = round_up(d.k, 8), ldb16 = round_up(d.n, 8);
-          void* a16 = u->scratch(2).get();
-          void* b16 = u->scratch(3).get();
-          cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(a), lda, a16, lda16, r,
-                                            d.k, s), "convert A");
-          cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(b), ldb, b16, ldb16,
-                                            d.k, d.n, s), "convert B");
-          a = a16;
-          b = b16;
-          lda = lda16;
-          ldb = ldb16;
+        for (int rep = 0; rep < repeats; ++rep) {
+          const auto rec = [&](int k) {
+            cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(rg->events[3 * rep + k]), s,
+                                                cudaEventRecordExternal), "cudaEventRecord");
+          };
+          rec(0);
+          rec(1);
+          if (tensor && !sixteen) {  // fp32 operands: converted inside the compute phase
+            void* a16 = u->scratch(2).get();
+            void* b16 = u->scratch(3).get();
+            cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(a), lda, a16, lda16, r,
+                                              d.k, s), "convert A");
+            cuda_check(poas_b200::convert_f32(u->spec().dtype, static_cast<const float*>(b), ldb, b16, ldb16,
+                                              d.k, d.n, s), "convert B");
+            u->gemm(r, d.n, d.k, a16, lda16, b16, ldb16, c, io.ldc_dev, false, extra_sms[i]);
+          } else {
+            u->gemm(r, d.n, d.k, a, lda, b, ldb, c, io.ldc_dev, false, extra_sms[i]);
+          }
+          rec(2);
         }
-        u->gemm(r, d.n, d.k, a, lda, b, ldb, c, io.ldc_dev, false, extra_sms[i]);
       } catch (...) {
         cudaStreamEndCapture(s, &graph);
         if (graph) cudaGraphDestroy(graph);
+        for (void* e : rg->events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         throw;
       }
       cuda_check(cudaStreamEndCapture(s, &graph), "cudaStreamEndCapture");
@@ -832,17 +850,27 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
       cudaGraphExec_t exec = nullptr;
       cuda_check(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
       rg->exec = exec;
-      graph_ = std::move(rg);
+      if (graphs_.size() >= 4) {
+        release_graph(*graphs_.front());
+        graphs_.erase(graphs_.begin());
+      }
+      graphs_.push_back(std::move(rg));
+      hit = graphs_.back().get();
     }
-    const auto exec = static_cast<cudaGraphExec_t>(graph_->exec);
-    first_open = std::chrono::steady_clock::now();
+    // the run's timing events are the graph's
     for (int rep = 0; rep < repeats; ++rep) {
       const std::size_t rr = static_cast<std::size_t>(rep);
-      cuda_check(cudaEventRecord(t0[dev][rr], s), "cudaEventRecord");
-      cuda_check(cudaEventRecord(ev[rr][i].cp0, s), "cudaEventRecord");
-      cuda_check(cudaGraphLaunch(exec, s), "cudaGraphLaunch");
-      cuda_check(cudaEventRecord(ev[rr][i].cp1, s), "cudaEventRecord");
+      cudaEventDestroy(t0[dev][rr]);
+      t0[dev][rr] = static_cast<cudaEvent_t>(hit->events[3 * rep]);
+      PhaseEvents& pe = ev[rr][i];
+      cudaEventDestroy(pe.cp0);
+      cudaEventDestroy(pe.cp1);
+      pe.cp0 = static_cast<cudaEvent_t>(hit->events[3 * rep + 1]);
+      pe.cp1 = static_cast<cudaEvent_t>(hit->events[3 * rep + 2]);
     }
+    cleanup.borrowed = true;
+    first_open = std::chrono::steady_clock::now();
+    cuda_check(cudaGraphLaunch(static_cast<cudaGraphExec_t>(hit->exec), s), "cudaGraphLaunch");
   }
 
   for (int rep = 0; rep < (graph_mode ? 0 : repeats); ++rep) {

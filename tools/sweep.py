@@ -111,15 +111,18 @@ def c5(sizes, preroll_ms=20, steps=10):
         ex = poas.Executor(units)
         # timed runs last >= ~0.25 s back to back (the sustained regime the
         # pre-rolled probes were taken in; a 1 ms burst runs at boost clock)
-        it = max(3, min(2000, int(0.25 / (2 * n ** 3 / 1.3e15)) + 1))
+        # (<= 256 steps: one CUDA graph per run; warm() keeps the regime)
+        it = max(3, min(256, int(0.25 / (2 * n ** 3 / 1.3e15)) + 1))
         static = poas.plan_policy(profile, n, n, n, POLICY)
-        ex.execute(static, io, max(3, it // 2))
+        ex.execute(static, io, it)
+        warm(0.2)
         rep_s = ex.execute(static, io, it)
         # the dynamic re-plan (warm-up), then the adapted plan timed
         dyn = ex.run_dynamic(profile, n, n, n, io, iterations=6, alpha=1.0, policy=POLICY,
                              replan_threshold_pct=2.0, repeats=max(1, it // 6))
         sched = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
         s = json.loads(sched)
+        ex.execute(sched, io, it)
         rep = ex.execute(sched, io, it)
         poas_s = rep["measured_makespan"]
         st = torch.cuda.current_stream().cuda_stream
