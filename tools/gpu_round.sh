@@ -19,7 +19,7 @@ timeout 900 paper_2209_10245_b200/bin/poas evaluate \
   --units "gpu0.tc=xpu:dev=0:sms=146:dtype=bf16:elem=2:link=hbm:probe=4096-12288;gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048" \
   --profiling probes=9,repetitions=3 --policy best-subset --repeats 5 --adapt 3 --out-dir "$OUT/evaluate" > "$OUT/evaluate.txt" 2>&1
 # ncu evidence (single launches; numbers under ncu are never bench values)
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt_gemm_kernel -s 1 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt_gemm2_kernel -s 1 -c 1 \
   -o "$OUT/prof_simt_square" python tools/ncu_target.py simt 8192 8192 0 > "$OUT/ncu_simt_square.log" 2>&1
 timeout 300 ncu --set full --clock-control none -k regex:simt_skinny -s 1 -c 1 \
   -o "$OUT/prof_simt_skinny" python tools/ncu_target.py simt 8 16384 2 > "$OUT/ncu_simt_skinny.log" 2>&1
