@@ -5,8 +5,9 @@
 // Replaces the GPU-kind synthetic law of the reference (SyntheticBackend::
 // time_gemm, /root/reference/proj/src/simulator.cpp:30-34).
 //
-// Default kernel: simt_gemm2_kernel (FFMA2, 128 x 256 tiles, grouped
-// raster; below). simt_gemm_kernel: the earlier plain-FFMA kernel, 128 x 128
+// Default kernel: simt_gemm2_kernel<.., 32, 256, 4, true> (FFMA2, 128 x 256
+// x 32 tiles, fragments double buffered in registers, B-pair-major FFMA2
+// order, grouped raster; below). simt_gemm_kernel: the earlier plain-FFMA kernel, 128 x 128
 // (or 128 x 256) x 16 CTA tiles, 256 threads, 8 x 8 (8 x 16) register
 // micro-tile per thread (4-column quadrants 64 apart so the float4
 // shared-memory reads stay conflict-free), 128-bit coalesced global loads
@@ -212,26 +213,38 @@ __device__ __forceinline__ void cp_async_wait() {
 
 constexpr int kGroupM2 = 8;
 
-template <bool kVec, int kBK2 = 16>
-__global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs p) {
-  constexpr int kTN = 256;
-  constexpr int kBK = kBK2;  // K depth of a step (16 or 32)
-  constexpr int kAV = kBK / 8;  // A float4 loads per thread per step
-  constexpr int kBP = kBK / 16;  // B row passes per step
+// FFMA2 kernel family. A CTA of kThr threads computes a 128 x kTN tile;
+// each thread owns 8 rows (two 4-row groups 64 apart) x 4*kNQ columns
+// (kNQ 4-column quadrants kTN/kNQ apart) as float2 accumulators, and the
+// float4 shared-memory reads stay conflict-free. Variants (POAS_SIMT_TILE):
+//   ffma2    kThr 256, kNQ 4: 128 x 256, one CTA per SM (8 x 16 per thread)
+//   ffma2x2  kThr 128, kNQ 4: 128 x 128, two CTAs per SM (8 x 16 per thread)
+//   ffma2w16 kThr 256, kNQ 2: 128 x 128, two CTAs per SM (8 x 8 per thread,
+//            16 warps per SM: twice the warps to hide shared-memory and
+//            fixed-latency waits, 1/3 more shared-memory reads per FMA)
+template <bool kVec, int kBK2 = 16, int kThr = kThreads, int kNQ = 4, bool kJOuter = false>
+__global__ void __launch_bounds__(kThr, (kThr * kNQ) == 1024 ? 1 : 2) simt_gemm2_kernel(const SimtArgs p) {
+  constexpr int kTX = kThr / 16;      // threads across a row of the tile (16 down)
+  constexpr int kQ = kTX * 4;         // column distance of a thread's quadrants
+  constexpr int kTN = kQ * kNQ;       // CTA tile width (columns)
+  constexpr int kBK = kBK2;           // K depth of a step (16 or 32)
+  constexpr int kAV = kBM * kBK / (4 * kThr);  // A float4 loads per thread per step
+  constexpr int kBP = kBK / 16;       // B passes per step (16 rows, kNQ float4 per thread each)
+  static_assert(kAV >= 1 && kBM * kBK == 4 * kThr * kAV, "A tile split");
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float* As = smem;                          // [2][kBK][kBM + kPad]  (A transposed)
   float* Bs = smem + 2 * kBK * (kBM + kPad);  // [2][kBK][kTN]
 
   const int tid = threadIdx.x;
-  const int tx = tid & 15;
-  const int ty = tid >> 4;
+  const int tx = tid % kTX;
+  const int ty = tid / kTX;
   // a warp loads 32 consecutive rows of A at one k offset: its transposed
   // shared stores hit 32 distinct banks
   const int a_row = tid & 127;
-  const int a_k = (tid >> 7) * (kBK / 2);
-  const int b_k = tid >> 4;
-  const int b_col = (tid & 15) * 4;
+  const int a_k = (tid >> 7) * (kAV * 4);
+  const int b_k = tid / kTX;
+  const int b_col = tx * 4;
 
   const int tiles_n = (p.N + kTN - 1) / kTN;
   const int total = p.tiles_m * tiles_n;
@@ -246,18 +259,18 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
     const int m0 = mb * kBM;
     const int n0 = nb * kTN;
 
-    float2 acc[8][8];
+    float2 acc[8][2 * kNQ];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < 2 * kNQ; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
     // A: 128-bit loads into registers one K-step ahead (unconditional for
     // interior tiles), stored transposed at the end of the step. B: cp.async
     // straight into the other shared buffer (no registers, no transpose;
     // out-of-range bytes zero-filled) for 16-byte aligned operands.
     const bool full_m = kVec && m0 + kBM <= p.M;
-    float4 ra[kAV], rb[4 * kBP];
+    float4 ra[kAV], rb[kNQ * kBP];
     auto load_a = [&](int k0) {
       const int gr = m0 + a_row;
       if (full_m && k0 + kBK <= p.K) {
@@ -283,20 +296,20 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
         if constexpr (kVec) {
           float* bs = Bs + buf * kBK * kTN + (b_k + 16 * q) * kTN + b_col;
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int gc = n0 + b_col + h * 64;
+          for (int h = 0; h < kNQ; ++h) {
+            const int gc = n0 + b_col + h * kQ;
             const int bytes = gk < p.K ? max(0, min(16, (p.N - gc) * 4)) : 0;
-            cp_async16(bs + 64 * h, bytes ? p.B + (long long)gk * p.ldb + gc : p.B, bytes);
+            cp_async16(bs + kQ * h, bytes ? p.B + (long long)gk * p.ldb + gc : p.B, bytes);
           }
         } else {
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int gc = n0 + b_col + h * 64;
+          for (int h = 0; h < kNQ; ++h) {
+            const int gc = n0 + b_col + h * kQ;
             float v[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e)
               v[e] = (gk < p.K && gc + e < p.N) ? p.B[(long long)gk * p.ldb + gc + e] : 0.f;
-            rb[4 * q + h] = make_float4(v[0], v[1], v[2], v[3]);
+            rb[kNQ * q + h] = make_float4(v[0], v[1], v[2], v[3]);
           }
         }
       }
@@ -318,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
         for (int q = 0; q < kBP; ++q) {
           float4* bs = reinterpret_cast<float4*>(Bs + buf * kBK * kTN + (b_k + 16 * q) * kTN + b_col);
 #pragma unroll
-          for (int h = 0; h < 4; ++h) bs[16 * h] = rb[4 * q + h];
+          for (int h = 0; h < kNQ; ++h) bs[(kQ / 4) * h] = rb[kNQ * q + h];
         }
       }
     };
@@ -330,35 +343,62 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
     store_shared(0);
     __syncthreads();
 
+    // Fragments (one k's 8 A values and 4*kNQ B values) are double
+    // buffered in registers: the next k's are read while this k's FFMA2s
+    // issue, and the step's barrier sits before its LAST k, so the next
+    // step's first fragment is read (after the barrier) while that k's
+    // FFMA2s still have work -- no warp waits on shared memory right after
+    // the barrier.
+    float4 fa[2][2], fb[2][kNQ];
+    auto load_frag = [&](int buf, int k, int slot) {
+      const float* as = As + buf * kBK * (kBM + kPad) + ty * 4 + k * (kBM + kPad);
+      const float4* bs = reinterpret_cast<const float4*>(Bs + buf * kBK * kTN) + tx + k * (kTN / 4);
+      fa[slot][0] = *reinterpret_cast<const float4*>(as);
+      fa[slot][1] = *reinterpret_cast<const float4*>(as + 64);
+#pragma unroll
+      for (int h = 0; h < kNQ; ++h) fb[slot][h] = bs[(kQ / 4) * h];
+    };
+    load_frag(0, 0, 0);
     for (int ks = 0; ks < k_steps; ++ks) {
       const int buf = ks & 1;
-      if (ks + 1 < k_steps) {
+      const bool more = ks + 1 < k_steps;
+      if (more) {
         load_a((ks + 1) * kBK);
         load_b((ks + 1) * kBK, buf ^ 1);
       }
-      const float* as = As + buf * kBK * (kBM + kPad) + ty * 4;
-      const float4* bs = reinterpret_cast<const float4*>(Bs + buf * kBK * kTN) + tx;
 #pragma unroll
       for (int k = 0; k < kBK; ++k) {
-        const float4 a0 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad));
-        const float4 a1 = *reinterpret_cast<const float4*>(as + k * (kBM + kPad) + 64);
-        float2 b[8];
+        const int cur = k & 1;
+        if (k + 1 < kBK) {
+          load_frag(buf, k + 1, cur ^ 1);
+        } else {
+          if (more) store_shared(buf ^ 1);
+          __syncthreads();
+          if (more) load_frag(buf ^ 1, 0, cur ^ 1);
+        }
+        const float4 a0 = fa[cur][0], a1 = fa[cur][1];
+        float2 b[2 * kNQ];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const float4 v = bs[k * (kTN / 4) + 16 * h];
+        for (int h = 0; h < kNQ; ++h) {
+          const float4 v = fb[cur][h];
           b[2 * h] = make_float2(v.x, v.y);
           b[2 * h + 1] = make_float2(v.z, v.w);
         }
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        if constexpr (kJOuter) {  // consecutive FFMA2s share the B pair
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float2 ai = make_float2(a[i], a[i]);
+          for (int j = 0; j < 2 * kNQ; ++j)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = __ffma2_rn(ai, b[j], acc[i][j]);
+            for (int i = 0; i < 8; ++i) acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), b[j], acc[i][j]);
+        } else {  // consecutive FFMA2s share the A scalar
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float2 ai = make_float2(a[i], a[i]);
+#pragma unroll
+            for (int j = 0; j < 2 * kNQ; ++j) acc[i][j] = __ffma2_rn(ai, b[j], acc[i][j]);
+          }
         }
       }
-      if (ks + 1 < k_steps) store_shared(buf ^ 1);
-      __syncthreads();
     }
 
 #pragma unroll
@@ -367,8 +407,8 @@ __global__ void __launch_bounds__(kThreads, 1) simt_gemm2_kernel(const SimtArgs 
       if (r >= p.M) continue;
       float* crow = p.C + (long long)r * p.ldc;
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int c = n0 + h * 64 + tx * 4;
+      for (int h = 0; h < kNQ; ++h) {
+        const int c = n0 + h * kQ + tx * 4;
         const float2 lo = acc[i][2 * h], hi = acc[i][2 * h + 1];
         if (kVec && c + 3 < p.N) {
           float4 o = make_float4(lo.x, lo.y, hi.x, hi.y);
@@ -813,6 +853,14 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
                           reinterpret_cast<const void*>(simt_gemm2_kernel<false>),
                           reinterpret_cast<const void*>(simt_gemm2_kernel<true, 32>),
                           reinterpret_cast<const void*>(simt_gemm2_kernel<false, 32>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<true, 16, 128>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false, 16, 128>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<true, 16, 256, 2>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<true, 32, 256, 4, true>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false, 32, 256, 4, true>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<true, 16, 256, 4, true>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false, 16, 256, 4, true>),
+                          reinterpret_cast<const void*>(simt_gemm2_kernel<false, 16, 256, 2>),
                           reinterpret_cast<const void*>(simt_gemm3_kernel<true>),
                           reinterpret_cast<const void*>(simt_gemm3_kernel<false>)})
       if (attr_err == cudaSuccess)
@@ -852,22 +900,45 @@ cudaError_t simt_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t l
       simt_gemm3_kernel<false><<<grid, kThreads3, smem3, stream>>>(p);
     return cudaGetLastError();
   }
-  if (tile == "ffma2" || tile == "ffma2k32") {
+  if (tile == "ffma2x2" || tile == "ffma2w16") {  // 128 x 128 tiles, two CTAs per SM
+    const int tiles2 = p.tiles_m * static_cast<int>((N + 127) / 128);
+    grid *= 2;
+    if (grid > tiles2) grid = tiles2;
+    const size_t need = (2 * kBK * (kBM + kPad) + 2 * kBK * 128) * sizeof(float);
+    // exclusive: two of these fit an SM (2 x 100 KB), a tensor CTA does not
+    const size_t smem2 = exclusive_sm ? std::max<size_t>(100 * 1024, need) : need;
+    if (tile == "ffma2w16") {
+      if (vec)
+        simt_gemm2_kernel<true, 16, 256, 2><<<grid, 256, smem2, stream>>>(p);
+      else
+        simt_gemm2_kernel<false, 16, 256, 2><<<grid, 256, smem2, stream>>>(p);
+    } else if (vec) {
+      simt_gemm2_kernel<true, 16, 128><<<grid, 128, smem2, stream>>>(p);
+    } else {
+      simt_gemm2_kernel<false, 16, 128><<<grid, 128, smem2, stream>>>(p);
+    }
+    return cudaGetLastError();
+  }
+  // The FFMA2 128 x 256 kernel: default K depth 32 with B-pair-major FFMA2
+  // order (8192^3: 58.4 TFLOP/s, 0.91x cuBLAS SGEMM; A-scalar-major order
+  // 56.3, K depth 16 56.0 -- profiles/r02_simt). "ffma2k16" / "ffma2k16j" /
+  // "ffma2k32": the other (depth, order) pairs.
+  if (tile == "ffma2" || tile == "ffma2k32j" || tile == "ffma2k32" || tile == "ffma2k16" ||
+      tile == "ffma2k16j") {
     const int tiles2 = p.tiles_m * static_cast<int>((N + 255) / 256);
     if (grid > tiles2) grid = tiles2;
-    const int bk = tile == "ffma2k32" ? 32 : 16;
+    const int bk = (tile == "ffma2k16" || tile == "ffma2k16j") ? 16 : 32;
+    const bool jouter = tile == "ffma2" || tile == "ffma2k32j" || tile == "ffma2k16j";
     const size_t need = (2 * bk * (kBM + kPad) + 2 * bk * 256) * sizeof(float);
     const size_t smem2 = exclusive_sm ? std::max<size_t>(120 * 1024, need) : need;
-    if (bk == 32) {
-      if (vec)
-        simt_gemm2_kernel<true, 32><<<grid, kThreads, smem2, stream>>>(p);
-      else
-        simt_gemm2_kernel<false, 32><<<grid, kThreads, smem2, stream>>>(p);
-    } else if (vec) {
-      simt_gemm2_kernel<true><<<grid, kThreads, smem2, stream>>>(p);
-    } else {
-      simt_gemm2_kernel<false><<<grid, kThreads, smem2, stream>>>(p);
-    }
+#define POAS_SIMT2(BK, J)                                                           \
+  (vec ? (simt_gemm2_kernel<true, BK, 256, 4, J><<<grid, kThreads, smem2, stream>>>(p), 0) \
+       : (simt_gemm2_kernel<false, BK, 256, 4, J><<<grid, kThreads, smem2, stream>>>(p), 0))
+    if (bk == 32)
+      jouter ? POAS_SIMT2(32, true) : POAS_SIMT2(32, false);
+    else
+      jouter ? POAS_SIMT2(16, true) : POAS_SIMT2(16, false);
+#undef POAS_SIMT2
     return cudaGetLastError();
   }
   const bool wide = tile != "128" && tile != "128x2";

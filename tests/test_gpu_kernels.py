@@ -142,6 +142,31 @@ def test_simt_gemm_vs_oracle(torch_cuda, poas, shape, ctas):
     assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
 
 
+SIMT_VARIANTS = ["ffma2", "ffma2k32", "ffma2k16", "ffma2k16j", "ffma2x2", "ffma2w16", "ffma2x512", "256", "128"]
+
+
+@pytest.mark.parametrize("variant", SIMT_VARIANTS)
+@pytest.mark.parametrize("shape", [(1000, 1000, 1000), (129, 300, 72), (640, 1024, 512), (333, 777, 100)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_simt_variants_vs_oracle(torch_cuda, poas, monkeypatch, variant, shape, accumulate):
+    """Every CUDA-core kernel variant (POAS_SIMT_TILE, read per launch) on
+    square, ragged and strided shapes, overwrite and accumulate."""
+    import oracle
+
+    torch = torch_cuda
+    monkeypatch.setenv("POAS_SIMT_TILE", variant)
+    m, n, k = shape
+    lda, ldb = k + (4 if m % 2 else 0), n + (8 if n % 2 else 0)
+    A, B = oracle.fill_uniform(m, lda, 31), oracle.fill_uniform(k, ldb, 32)
+    C0 = oracle.fill_uniform(m, n, 33)
+    a, b = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    c = torch.from_numpy(C0).cuda() if accumulate else torch.full((m, n), float("nan"), device="cuda")
+    poas.simt_gemm(m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), n, accumulate=accumulate)
+    torch.cuda.synchronize()
+    ref = oracle.gemm_rows_f64(A[:, :k], B[:, :n], 0) + (C0 if accumulate else 0)
+    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+
+
 def test_simt_accumulate_and_strided(torch_cuda, poas):
     import oracle
 

@@ -37,7 +37,7 @@ def main():
         poas.fill_uniform(0, b.data_ptr(), n, n, n, 0, 0, n, 2)
         st = torch.cuda.current_stream().cuda_stream
         res = {"n": n}
-        for variant in ("ffma2", "ffma2k32", "256"):
+        for variant in ("ffma2", "ffma2k32", "ffma2k16j", "ffma2k16"):
             os.environ["POAS_SIMT_TILE"] = variant
             ours = lambda: poas.simt_gemm(n, n, n, a.data_ptr(), n, b.data_ptr(), n, c.data_ptr(), n,  # noqa
                                           stream=st)
@@ -56,7 +56,7 @@ def main():
             res[variant] = {"tflops": f / min(t_o) / 1e12, "rel_err": err}
             res["cublas_sgemm_tflops"] = f / min(t_l) / 1e12
             del ref
-        for v in ("ffma2", "ffma2k32"):
+        for v in ("ffma2", "ffma2k32", "ffma2k16j", "ffma2k16"):
             res[v + "_vs_cublas"] = res[v]["tflops"] / res["cublas_sgemm_tflops"]
         print(json.dumps(res), flush=True)
         del a, b, c
