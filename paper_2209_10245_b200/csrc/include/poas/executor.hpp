@@ -136,7 +136,7 @@ class Executor {
     std::string key;
     void* graph = nullptr;  // cudaGraph_t
     void* exec = nullptr;   // cudaGraphExec_t
-    std::vector<void*> events;  // per repeat: t0, cp0, cp1 (cudaEvent_t)
+    std::vector<void*> events;  // t0, cp0 (before the first repeat), cp1 (after the last)
     int device = 0;
   };
 

@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic launch: the prologue above overlapped the previous kernel
+  // of the stream; global memory only from here on
+  griddep_launch();
+  griddep_wait();
 
   const int total = args.tiles_m * args.tiles_n;
   const int k_blocks = (args.K + kBK - 1) / kBK;
@@ -522,6 +526,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic launch: the prologue above overlapped the previous kernel
+  // of the stream; global memory only from here on
+  griddep_launch();
+  griddep_wait();
   if (threadIdx.x == 0) trace_stamp(args, 1);
 
   const int total = args.tiles_m * args.tiles_n;
@@ -1080,6 +1088,30 @@ cudaError_t tc_gemm_panels(AbType t, int64_t M, int64_t N, int64_t K, const void
 }
 
 namespace {
+// Launch with programmatic stream serialization (the kernels call
+// griddepcontrol.wait before touching global memory), so a GEMM's launch
+// and prologue overlap the previous kernel of its stream. POAS_TC_PDL=0
+// launches plainly.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  static const bool pdl = [] {
+    const char* e = std::getenv("POAS_TC_PDL");
+    return !(e && std::string(e) == "0");
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                          const void* B, int64_t ldb, float* C, int64_t ldc, bool accumulate,
                          int num_ctas, const TcPanels* ps, const TcStream* ss, cudaStream_t stream) {
@@ -1230,9 +1262,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       cudaMemsetAsync(trace_buf, 0, 2 * pairs * 16 * sizeof(unsigned long long), stream);
       args.trace = trace_buf;
     }
-    tc_gemm_2cta_kernel<<<2 * pairs, kThreads, k2SmemBytes, stream>>>(ma, mb, mc, args);
+    const cudaError_t e = launch_pdl(tc_gemm_2cta_kernel, 2 * pairs, k2SmemBytes, stream, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
-    return cudaGetLastError();
+    return e;
   }
   const int bn = variant == TcVariant::single128 ? 128 : 256;
   args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
@@ -1242,11 +1274,8 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
-  if (bn == 128)
-    tc_gemm_kernel<128, 6><<<grid, kThreads, Tile1<128, 6>::kSmem, stream>>>(ma, mb, args);
-  else
-    tc_gemm_kernel<256, 4><<<grid, kThreads, Tile1<256, 4>::kSmem, stream>>>(ma, mb, args);
-  return cudaGetLastError();
+  if (bn == 128) return launch_pdl(tc_gemm_kernel<128, 6>, grid, Tile1<128, 6>::kSmem, stream, ma, mb, args);
+  return launch_pdl(tc_gemm_kernel<256, 4>, grid, Tile1<256, 4>::kSmem, stream, ma, mb, args);
 }
 }  // namespace
 

@@ -282,6 +282,11 @@ double Unit::time_gemm(std::int64_t side) {
   // runs in the continuous-load regime a co-executed step runs in (under
   // the power cap a launch after an idle gap sees a boost clock the
   // sustained run never gets, profiles/r01_warmup); 0 = one cold launch.
+  // In that regime a short GEMM is also timed the way the executor replays
+  // back-to-back steps (one event pair around consecutive launches, each
+  // launch staged while the previous runs): the mean of `reps` launches
+  // spanning >= ~100 us (1 once a launch alone lasts that long).
+  int reps = 1;
   if (spec_.preroll_ms > 0.0) {
     // one launch's time: the previous probe, scaled by ops to this side
     double est = 0.0;
@@ -291,14 +296,15 @@ double Unit::time_gemm(std::int64_t side) {
     }
     const int pre = est > 0.0 ? static_cast<int>(spec_.preroll_ms * 1e-3 / est) + 1 : 2;
     for (int i = 0; i < std::min(pre, 4096); ++i) one();
+    if (est > 0.0) reps = std::clamp(static_cast<int>(100e-6 / est) + 1, 1, 32);
   }
   cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
-  one();
+  for (int i = 0; i < reps; ++i) one();
   cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
   cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
   float ms = 0.f;
   cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "cudaEventElapsedTime");
-  last_probe_s_ = static_cast<double>(ms) * 1e-3;
+  last_probe_s_ = static_cast<double>(ms) * 1e-3 / reps;
   last_probe_side_ = side;
   return last_probe_s_;
 }
