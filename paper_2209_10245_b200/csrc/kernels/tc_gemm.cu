@@ -105,6 +105,18 @@ __device__ __forceinline__ void wait_panel_flag(const int* flag, int epoch) {
 //   empty-slot wait passed
 // Write-only (no global read on the traced thread's path); callers stamp
 // each event once.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Slots 10..13 accumulate durations (ns) over the CTA's tiles: 10 MMA
+// blocked on the accumulator (half 0), 11 MMA blocked on half 1 (wide
+// tiles), 12 epilogue from accumulator-full to the release of its first
+// half, 13 ... to the release of its last half.
+__device__ __forceinline__ void trace_add(const TcArgs& a, int idx, unsigned long long d) {
+  if (a.trace) a.trace[blockIdx.x * 16 + idx] += d;
+}
 __device__ __forceinline__ void trace_stamp(const TcArgs& a, int idx) {
   if (!a.trace) return;
   unsigned long long t;
@@ -460,28 +472,51 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------- 2-SM (cta_group::2) kernel
-// A CTA pair (cluster of 2 on one TPC) owns a 256 x 256 output tile. Each
-// CTA stages 128 rows of A and 128 columns of B per 64-deep K block (32 KB
-// per stage per CTA, 6 stages); the leader's single thread issues
-// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), which reads both CTAs'
-// shared memory and writes both CTAs' TMEM (each holds its 128 rows x 256
-// fp32 columns, double buffered). Versus two independent 128 x 256 CTAs this
-// moves 1/3 fewer operand bytes from L2 into shared memory per MAC.
-constexpr int k2Stages = 6;
+// A CTA pair (cluster of 2 on one TPC) owns a 256 x W output tile. Each CTA
+// stages 128 rows of A and W/2 columns of B per 64-deep K block; the
+// leader's single thread issues tcgen05.mma.cta_group::2 (M=256, N=256,
+// K=16) once per 256-column half of the tile, which reads both CTAs' shared
+// memory and writes both CTAs' TMEM (each holds its 128 rows x W fp32
+// columns).
+//
+//   W = 256: 6 stages of 32 KB per CTA; two 256-column accumulators, double
+//            buffered (the epilogue of tile i overlaps the MMAs of tile i+1).
+//            Versus two independent 128 x 256 CTAs: 1/3 fewer operand bytes
+//            from L2 into shared memory per MAC.
+//   W = 512: 4 stages of 48 KB; the accumulator fills all 512 TMEM columns.
+//            Another 1/4 fewer operand bytes from L2 per MAC than W = 256
+//            (16384^3: 68.7 -> 51.5 GB through the L2 -> SM crossbar), which
+//            under the power cap is energy and therefore clock. The epilogue
+//            releases each 256-column half as soon as it is in registers; the
+//            next tile's MMAs start on half 0 and catch half 1 up (its
+//            k-blocks stay staged, at most a ring's worth) once it is free.
 constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
-constexpr int k2BBytes = 128 * kBK * 2;  // this CTA's 128 columns of B: 16 KB
-constexpr int k2StageBytes = k2ABytes + k2BBytes;
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
-// Epilogue staging (TMA-store path): per epilogue warp two 32-row x 16-column
-// fp32 boxes, 64-byte swizzled rows (2 x 2 KB).
-constexpr int k2StagingBytes = 4 * 32 * 32 * 4;
-constexpr size_t k2SmemBytes = 1024 + k2Stages * k2StageBytes + k2StagingBytes + 256;
+// Epilogue staging (TMA-store path): per epilogue warp two 32-row x 32-column
+// fp32 boxes, 128-byte swizzled rows (2 x 4 KB).
 
+template <int W>
+struct Pair {
+  static_assert(W == 256 || W == 512, "pair tile width");
+  static constexpr int kHalves = W / 256;
+  static constexpr int kStages = W == 256 ? 6 : 4;
+  static constexpr int kBBytes = (W / 2) * kBK * 2;  // this CTA's W/2 columns of B
+  static constexpr int kStageBytes = k2ABytes + kBBytes;
+  static constexpr int kStagingBytes = 4 * 2 * 4096;
+  static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 256;
+  static_assert(kSmem <= 232448, "shared memory per CTA");
+};
 
+template <int W>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
+  using P = Pair<W>;
+  constexpr int k2StagingBytes = P::kStagingBytes;
+  constexpr int k2Stages = P::kStages;
+  constexpr int k2BBytes = P::kBBytes;
+  constexpr int k2StageBytes = P::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -491,7 +526,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(s_c + k2StagingBytes);
   uint64_t* empty = full + k2Stages;
   uint64_t* acc_full = empty + k2Stages;
-  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* acc_empty = acc_full + 2;  // W = 256: per accumulator; W = 512: per half
   uint64_t* tile_full = acc_empty + 2;
   uint64_t* tile_empty = tile_full + kTileSlots;
   int* tile_ring = reinterpret_cast<int*>(tile_empty + kTileSlots);
@@ -582,7 +617,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           confirmed = pnl;
         }
         const int row0 = mb * 256 + static_cast<int>(rank) * 128;
-        const int col0 = nbl * 256 + static_cast<int>(rank) * 128;  // inside the panel
+        // this CTA's columns of each 256-column half: [h*256 + rank*128, +128)
+        const int col0 = nbl * W + static_cast<int>(rank) * 128;  // inside the panel
         // K serpentine: the tiles of a wave that follows one sweeping K
         // forwards start where it ended, on the K-slices still in L2
         const bool rev = args.kserp && ((t / step) & 1);
@@ -593,16 +629,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
           tma_load_2d_pair(s_a + stage * k2ABytes, &map_a, &full[stage], kc, row0,
                            args.hint_a);
-          if (args.panels > 1) {
-            tma_load_3d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kc, pnl,
-                             args.hint_b);
-            tma_load_3d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
-                             col0 + 64, kc, pnl, args.hint_b);
-          } else {
-            tma_load_2d_pair(s_b + stage * k2BBytes, &map_b, &full[stage], col0, kc,
-                             args.hint_b);
-            tma_load_2d_pair(s_b + stage * k2BBytes + kBChunkBytes, &map_b, &full[stage],
-                             col0 + 64, kc, args.hint_b);
+          uint8_t* sb = s_b + stage * k2BBytes;
+#pragma unroll
+          for (int j = 0; j < W / 128; ++j) {  // 64-column chunks: half j/2, chunk j%2
+            const int cj = col0 + (j >> 1) * 256 + (j & 1) * 64;
+            if (args.panels > 1)
+              tma_load_3d_pair(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, pnl,
+                               args.hint_b);
+            else
+              tma_load_2d_pair(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, args.hint_b);
           }
           if (wave == 1 && kb == 0) trace_stamp(args, 2);
           if (kb == 0 && leader) t_next = claim_tile(args, next_static, step);  // behind the first loads
@@ -641,10 +676,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int slot = 0;
       uint32_t tphase = 0;
       bool traced = false;
+      // one 256-column half of the tile for the k-block staged in `st`
+      auto issue = [&](uint32_t d_tmem, int st, int kb, int h) {
+        const uint32_t a0 = smem_addr(s_a + st * k2ABytes);
+        const uint32_t b0 = smem_addr(s_b + st * k2BBytes) + static_cast<uint32_t>(h * 2 * kBChunkBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / kUmmaK; ++k) {
+          const uint64_t ad = sdesc_sw128(a0 + k * kUmmaK * 2, 16, 1024);
+          const uint64_t bd = sdesc_sw128(b0 + k * 2 * 1024, kBChunkBytes, 1024);
+          umma_f16_pair(d_tmem + static_cast<uint32_t>(h * 256), ad, bd, args.idesc,
+                        (kb | k) != 0 ? 1u : 0u);
+        }
+      };
       for (int t = first < total ? first : -1; t >= 0;) {
-        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        const unsigned long long tw0 = args.trace ? gtimer() : 0;
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);  // W = 512: half 0
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
+        if (args.trace) trace_add(args, 10, gtimer() - tw0);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(W == 256 ? acc * 256 : 0);
+        // W = 512: half 1 of the previous tile may still be draining; its
+        // MMAs trail half 0's by the k-blocks held in `npend` stages (each
+        // stage is released once both halves have consumed it)
+        bool h1 = W == 256;
+        int npend = 0, pend_kb = 0, pend_stage = 0;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -652,18 +706,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             trace_stamp(args, 3);
             traced = true;
           }
-          const uint32_t a0 = smem_addr(s_a + stage * k2ABytes);
-          const uint32_t b0 = smem_addr(s_b + stage * k2BBytes);
-#pragma unroll
-          for (int k = 0; k < kBK / kUmmaK; ++k) {
-            const uint64_t ad = sdesc_sw128(a0 + k * kUmmaK * 2, 16, 1024);
-            const uint64_t bd = sdesc_sw128(b0 + k * 2 * 1024, kBChunkBytes, 1024);
-            umma_f16_pair(d_tmem, ad, bd, args.idesc, (kb | k) != 0 ? 1u : 0u);
+          issue(d_tmem, stage, kb, 0);
+          if constexpr (W == 256) {
+            umma_commit_pair(&empty[stage], 0x3);
+          } else {
+            if (npend++ == 0) {
+              pend_kb = kb;
+              pend_stage = stage;
+            }
+            if (!h1 && (npend == k2Stages || mbar_test_wait(&acc_empty[1], acc_phase ^ 1))) {
+              const unsigned long long tw1 = args.trace ? gtimer() : 0;
+              mbar_wait(&acc_empty[1], acc_phase ^ 1);
+              tc_fence_after();
+              if (args.trace) trace_add(args, 11, gtimer() - tw1);
+              h1 = true;
+            }
+            if (h1) {
+              for (int i = 0, st = pend_stage; i < npend; ++i) {
+                issue(d_tmem, st, pend_kb + i, 1);
+                umma_commit_pair(&empty[st], 0x3);
+                if (++st == k2Stages) st = 0;
+              }
+              npend = 0;
+            }
           }
-          umma_commit_pair(&empty[stage], 0x3);
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
+          }
+        }
+        if constexpr (W == 512) {
+          if (npend) {  // a tile shorter than the drain of half 1
+            mbar_wait(&acc_empty[1], acc_phase ^ 1);
+            tc_fence_after();
+            for (int i = 0, st = pend_stage; i < npend; ++i) {
+              issue(d_tmem, st, pend_kb + i, 1);
+              umma_commit_pair(&empty[st], 0x3);
+              if (++st == k2Stages) st = 0;
+            }
           }
         }
         umma_commit_pair(&acc_full[acc], 0x3);
@@ -672,8 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           args.trace[blockIdx.x * 16 + 4] = tt;
         }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
         mbar_wait_cluster(&tile_full[slot], tphase);  // the next tile
         t = tile_ring[slot];
         mbar_arrive(&tile_empty[slot]);
@@ -713,63 +792,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
+      const unsigned long long te0 = args.trace ? gtimer() : 0;
       if (quad == 0 && lane == 0 && !epi_traced) {
         trace_stamp(args, 5);
         epi_traced = true;
       }
       const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
       if (args.tma_store) {
-        // TMEM -> registers -> a 32-row x 16-column staging box of this
-        // warp (64-byte swizzled rows: conflict-free, the TMA's layout) ->
-        // one TMA store (or f32 add-reduction) per box: full-line writes,
-        // the threads never wait on global memory. Two boxes per warp, so a
-        // box's store drains while the next one fills; the TMEM load of the
-        // next 32 columns is in flight while the current ones are written
-        // (TMEM reads at 64 B/clk/SM are the floor). The accumulator is
-        // released as soon as its last columns are in registers.
-        uint8_t* boxes = s_c + quad * 4096;
+        // TMEM -> registers, 64 columns per step (two 32x32b.x32 loads, the
+        // next step's in flight while this one is written) -> two 32-row x
+        // 32-column staging boxes of this warp (128-byte rows, 128-byte
+        // swizzle: conflict-free, the TMA's layout) -> ONE proxy fence ->
+        // two TMA stores (or f32 add-reductions). The fence is the expensive
+        // part of a step, so a step covers 8 KB. Each 256-column half of
+        // the accumulator is released as soon as its last columns are in
+        // registers (TMEM reads, 64 B/clk/SM, are the floor of the drain).
+        uint8_t* slots = s_c + quad * 8192;
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(acc * kBN);
-        auto put_box = [&](const uint32_t* w, int c) {  // 16 columns, box (c & 1)
-          uint8_t* box = boxes + (c & 1) * 2048;
-          if (lane == 0) bulk_wait_read<1>();  // the store two boxes back has left smem
+                               static_cast<uint32_t>(W == 256 ? acc * 256 : 0);
+        auto put = [&](const uint32_t* w, int c) {  // columns [c*64, c*64+64)
+          if (lane == 0) bulk_wait_read<0>();  // the previous step's stores have left smem
           __syncwarp();
-          uint8_t* my_row = box + lane * 64;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint4*>(my_row + ((j ^ ((lane >> 1) & 3)) << 4)) =
-                make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+          for (int bx = 0; bx < 2; ++bx) {
+            uint8_t* my_row = slots + bx * 4096 + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(w[32 * bx + 4 * j], w[32 * bx + 4 * j + 1], w[32 * bx + 4 * j + 2],
+                             w[32 * bx + 4 * j + 3]);
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && !args.epi_skip) {
-            const int col0 = nb * kBN + c * 16;
-            if (args.accumulate)
-              tma_reduce_add_2d(&map_c, box, col0, row_base);
-            else if (args.hint_c != kEvictNormal)
-              tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
-            else
-              tma_store_2d(&map_c, box, col0, row_base);
+#pragma unroll
+            for (int bx = 0; bx < 2; ++bx) {
+              const int col0 = nb * W + c * 64 + bx * 32;
+              uint8_t* box = slots + bx * 4096;
+              if (args.accumulate)
+                tma_reduce_add_2d(&map_c, box, col0, row_base);
+              else if (args.hint_c != kEvictNormal)
+                tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
+              else
+                tma_store_2d(&map_c, box, col0, row_base);
+            }
             bulk_commit();
           }
         };
-        uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(taddr, va);
+        uint32_t va[64], vb[64];
+        auto load64 = [&](uint32_t (&v)[64], int c) {
+          tmem_ld_32x32b_x32(taddr + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_ld_32x32b_x32(taddr + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        };
+        load64(va, 0);
         tmem_wait_ld();
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; c += 2) {
-          tmem_ld_32x32b_x32(taddr + (c + 1) * 32, vb);
-          put_box(va, 2 * c);
-          put_box(va + 16, 2 * c + 1);
+        for (int c = 0; c < W / 64; c += 2) {
+          load64(vb, c + 1);
+          put(va, c);
           tmem_wait_ld();
-          if (c + 2 < kBN / 32) {
-            tmem_ld_32x32b_x32(taddr + (c + 2) * 32, va);
-          } else {  // all 256 columns are in registers: free the accumulator
+          if ((c + 2) % 4 == 0) {  // a 256-column half is in registers: free it
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
+            if (lane == 0)  // the leader's barrier
+              mbar_arrive_cluster(&acc_empty[W == 256 ? acc : (c + 2) / 4 - 1], 0);
+            if (args.trace && quad == 0 && lane == 0)
+              trace_add(args, (c + 2) == 4 ? 12 : 13, gtimer() - te0);
           }
-          put_box(vb, 2 * c + 2);
-          put_box(vb + 16, 2 * c + 3);
+          if (c + 2 < W / 64) load64(va, c + 2);
+          put(vb, c + 1);
           tmem_wait_ld();
         }
         if (args.trace && quad == 0 && lane == 0) {
@@ -790,21 +881,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             atomicExch(args.block_flags + blk, args.stream_epoch);
           }
         }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
         continue;  // (the for-increment fetches the next tile)
       }
       const int row = row_base + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
 #pragma unroll 1
-      for (int c = 0; c < kBN / 32; ++c) {
+      for (int c = 0; c < W / 32; ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(acc * kBN + c * 32),
+                               static_cast<uint32_t>((W == 256 ? acc * 256 : 0) + c * 32),
                            v);
         tmem_wait_ld();
         if (row < args.M) {
-          const int col0 = nb * kBN + c * 32;
+          const int col0 = nb * W + c * 32;
           if (vec && col0 + 32 <= args.N) {
             float4* dst = reinterpret_cast<float4*>(crow + col0);
 #pragma unroll
@@ -836,7 +926,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], 0);  // the leader's barrier
+      if (lane == 0) {  // the leader's barrier(s)
+        mbar_arrive_cluster(&acc_empty[W == 256 ? acc : 0], 0);
+        if (W == 512) mbar_arrive_cluster(&acc_empty[1], 0);
+      }
       if (args.sblocks) {
         // direct stores (C pitch TMA cannot map): the same per-block count
         // as the TMA-store path, after this warp's st.global are visible
@@ -850,8 +943,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
     }
     if (args.tma_store && lane == 0) bulk_wait_all();  // C written before the CTA retires
   }
@@ -923,17 +1015,17 @@ bool make_map_panels(CUtensorMap* map, AbType t, const void* base, int64_t K, in
 }
 
 // 2-D map over a row-major fp32 [rows x cols] C with leading dim `ld`
-// (elements): 16-column x 32-row boxes, 64-byte swizzle (the epilogue
+// (elements): 32-column x 32-row boxes, 128-byte swizzle (the epilogue
 // staging layout).
 bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  const cuuint32_t box[2] = {16, 32};
+  const cuuint32_t box[2] = {32, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -947,14 +1039,15 @@ void print_trace(unsigned long long* dev, int ctas, cudaStream_t stream, int64_t
   unsigned long long t0 = ~0ull;
   for (int c = 0; c < ctas; ++c)
     if (h[c * 16]) t0 = std::min(t0, h[c * 16]);
-  static const char* names[10] = {"entry", "prologue", "first_tma", "first_full", "last_commit",
-                                  "epi_acc", "epi_issued", "exit", "published", "empty_ok"};
+  static const char* names[14] = {"entry", "prologue", "first_tma", "first_full", "last_commit",
+                                  "epi_acc", "epi_issued", "exit", "published", "empty_ok",
+                                  "sum_mma_wait_h0", "sum_mma_wait_h1", "sum_epi_h0", "sum_epi_h1"};
   std::fprintf(stderr, "tc_trace M=%lld N=%lld K=%lld ctas=%d:", static_cast<long long>(M),
                static_cast<long long>(N), static_cast<long long>(K), ctas);
-  for (int e = 0; e < 10; ++e) {
+  for (int e = 0; e < 14; ++e) {
     std::vector<double> v;
     for (int c = 0; c < ctas; ++c)
-      if (h[c * 16 + e]) v.push_back((h[c * 16 + e] - t0) * 1e-3);
+      if (h[c * 16 + e]) v.push_back((h[c * 16 + e] - (e < 10 ? t0 : 0)) * 1e-3);
     std::sort(v.begin(), v.end());
     if (v.empty()) continue;
     std::fprintf(stderr, " %s[min %.2f med %.2f max %.2f n %zu]", names[e], v.front(),
@@ -1010,14 +1103,15 @@ int* next_tile_counter(cudaStream_t stream) {
 }  // namespace
 
 namespace {
-// Kernel variants: the CTA-pair kernel (256 x 256 tiles; 1/3 fewer operand
-// bytes into shared memory per MAC than a single SM's 128 x 256) wherever
-// its tiles keep the SM budget reasonably busy; when at most a quarter of
-// the pairs would have a tile (e.g. 1024^3: 16 tiles for 74 pairs) the
-// single-SM kernel with 128 x 128 tiles spreads the work over 4x as many
-// CTAs. POAS_TC_KERNEL = 2cta |
+// Kernel variants: the CTA-pair kernel wherever its tiles keep the SM budget
+// reasonably busy -- 256 x 512 tiles (1/4 fewer operand bytes from L2 per
+// MAC than 256 x 256, whose tiles in turn move 1/3 fewer than a single SM's
+// 128 x 256) once there are at least two waves of them, 256 x 256 below;
+// when at most a quarter of the pairs would have a 256 x 256 tile (e.g.
+// 1024^3: 16 tiles for 74 pairs) the single-SM kernel with 128 x 128 tiles
+// spreads the work over 4x as many CTAs. POAS_TC_KERNEL = 2cta512 | 2cta |
 // 1cta (128 x 256) | 1cta128 overrides.
-enum class TcVariant { pair, single256, single128 };
+enum class TcVariant { pair512, pair, single256, single128 };
 
 TcVariant choose_variant(int64_t M, int64_t N, int budget) {
   if (const char* v = std::getenv("POAS_TC_KERNEL")) {
@@ -1025,21 +1119,25 @@ TcVariant choose_variant(int64_t M, int64_t N, int budget) {
     if (s == "1cta") return TcVariant::single256;
     if (s == "1cta128") return TcVariant::single128;
     if (s == "2cta") return TcVariant::pair;
+    if (s == "2cta512") return TcVariant::pair512;
   }
   // Single-SM 128 x 128 tiles only when the pairs would be mostly idle (at
   // most a quarter busy): measured (profiles/r01_small_variants) 1024^3
   // 16.1 -> 12.4 us, but 2048^3 22.3 -> 29.6 us (64 pair tiles for 74 pairs).
   const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  return 4 * pair_tiles <= budget / 2 ? TcVariant::single128 : TcVariant::pair;
+  if (4 * pair_tiles <= budget / 2) return TcVariant::single128;
+  const int64_t wide_tiles = ((M + 255) / 256) * ((N + 511) / 512);
+  return wide_tiles >= 2 * (budget / 2) ? TcVariant::pair512 : TcVariant::pair;
 }
 
 const char* variant_name(TcVariant v) {
   switch (v) {
     case TcVariant::single256: return "tc_gemm_kernel";
     case TcVariant::single128: return "tc_gemm_kernel_n128";
+    case TcVariant::pair512: return "tc_gemm_2cta_kernel<512>";
     case TcVariant::pair: break;
   }
-  return "tc_gemm_2cta_kernel";
+  return "tc_gemm_2cta_kernel<256>";
 }
 }  // namespace
 
@@ -1150,9 +1248,13 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Tile1<128, 6>::kSmem));
     if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel,
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<256>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(k2SmemBytes));
+                                      static_cast<int>(Pair<256>::kSmem));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<512>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Pair<512>::kSmem));
   });
   if (attr_err != cudaSuccess) return attr_err;
   // Kernel choice: the CTA-pair kernel (1/3 fewer operand bytes into shared
@@ -1161,12 +1263,16 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const int budget_all = num_ctas > 0 ? num_ctas : device_sm_count();
   TcVariant variant = choose_variant(M, N, budget_all);
-  if (P > 1 || ss) {  // panels / streamed operands: the pair kernel only
+  if (P > 1 || ss) {
+    // panels / streamed operands: the pair kernel only; streamed block
+    // tables are in 256 x 256 tiles, panels take 512-wide tiles when every
+    // panel is a whole number of them
     const char* v = std::getenv("POAS_TC_KERNEL");
-    if (v && std::string(v) != "2cta") return cudaErrorNotSupported;
-    variant = TcVariant::pair;
+    if (v && std::string(v) != "2cta" && std::string(v) != "2cta512") return cudaErrorNotSupported;
+    const bool wide = variant == TcVariant::pair512 && !ss && np % 512 == 0;
+    variant = wide ? TcVariant::pair512 : TcVariant::pair;
   }
-  const bool force_1cta = variant != TcVariant::pair;
+  const bool force_1cta = variant != TcVariant::pair && variant != TcVariant::pair512;
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -1212,7 +1318,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.tma_store = 0;
   args.trace = nullptr;
   args.panels = P;
-  args.tiles_n_panel = static_cast<int>(np / 256);
+  args.tiles_n_panel = static_cast<int>(np / (variant == TcVariant::pair512 ? 512 : 256));
   args.panel_flags = ps ? ps->flags : nullptr;
   args.panel_epoch = ps ? ps->epoch : 0;
   args.sblocks = nullptr;
@@ -1247,9 +1353,11 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     args.tma_store = !direct && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 &&
                      make_map_c(&mc, C, M, N, ldc);
     if (!args.tma_store) mc = ma;  // unused
+    const bool wide = variant == TcVariant::pair512;
+    const int w = wide ? 512 : 256;
     args.tiles_m = static_cast<int>((M + 255) / 256);
-    args.tiles_n = static_cast<int>((N + kBN - 1) / kBN);
-    args.idesc = idesc_f16(t == AbType::bf16, 256, kBN, false, true);
+    args.tiles_n = static_cast<int>((N + w - 1) / w);
+    args.idesc = idesc_f16(t == AbType::bf16, 256, 256, false, true);  // per 256-column half
     args.group = group_override > 0 ? group_override : kGroupM2;
     const int tiles = args.tiles_m * args.tiles_n;
     int pairs = budget / 2;
@@ -1262,7 +1370,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       cudaMemsetAsync(trace_buf, 0, 2 * pairs * 16 * sizeof(unsigned long long), stream);
       args.trace = trace_buf;
     }
-    const cudaError_t e = launch_pdl(tc_gemm_2cta_kernel, 2 * pairs, k2SmemBytes, stream, ma, mb, mc, args);
+    const cudaError_t e =
+        wide ? launch_pdl(tc_gemm_2cta_kernel<512>, 2 * pairs, Pair<512>::kSmem, stream, ma, mb, mc, args)
+             : launch_pdl(tc_gemm_2cta_kernel<256>, 2 * pairs, Pair<256>::kSmem, stream, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return e;
   }

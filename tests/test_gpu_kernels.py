@@ -205,7 +205,7 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
-@pytest.mark.parametrize("variant", ["1cta", "2cta"])
+@pytest.mark.parametrize("variant", ["1cta", "2cta", "2cta512"])
 def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
     """POAS_TC_KSERP=0: every tile sweeps K forwards (the default alternates
     the direction per wave of tiles); both orders agree with the oracle and
@@ -231,14 +231,16 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 
 
 # (variant, epilogue): the single-SM kernels have one epilogue
-_TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct")]
+_TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct"),
+                ("2cta512", "tma"), ("2cta512", "direct")]
 
 
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
 @pytest.mark.parametrize("variant,epilogue", _TC_VARIANTS)
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
 def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched, epilogue):
-    """Both tensor kernels (single-SM 128x256 and CTA-pair 256x256) under
+    """The tensor kernels (single-SM 128x256 / 128x128, CTA-pair 256x256 and
+    256x512) under
     every tile scheduler and both pair-kernel epilogues (TMA store; direct
     register stores) agree with the oracle, including partial pair tiles,
     odd SM budgets and a C pitch TMA cannot map (n = 777)."""
@@ -263,8 +265,9 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
         assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, (variant, ctas)
 
 
+@pytest.mark.parametrize("variant", [None, "2cta512"])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_tc_epilogue_pitch_and_alignment(torch_cuda, poas, accumulate):
+def test_tc_epilogue_pitch_and_alignment(torch_cuda, poas, monkeypatch, accumulate, variant):
     """C inside a wider buffer: a padded pitch (TMA-store epilogue, tails
     clipped: the padding is never written) and a 4-byte-offset base (no
     tensor map: direct stores); both plain and accumulating (TMA f32 add
@@ -272,6 +275,8 @@ def test_tc_epilogue_pitch_and_alignment(torch_cuda, poas, accumulate):
     import oracle
 
     torch = torch_cuda
+    if variant:
+        monkeypatch.setenv("POAS_TC_KERNEL", variant)
     m, n, k = 700, 600, 320
     A, B = oracle.fill_uniform(m, k, 41), oracle.fill_uniform(k, n, 42)
     a = torch.from_numpy(A).cuda().bfloat16()
@@ -349,15 +354,20 @@ def _panel_major(torch, B16, panels):
     return torch.stack([B16[:, p * np_:(p + 1) * np_] for p in range(panels)]).contiguous()
 
 
+@pytest.mark.parametrize("variant", [None, "2cta512"])
 @pytest.mark.parametrize("panels", [2, 4])
 @pytest.mark.parametrize("shape", [(1000, 1024, 320), (300, 2048, 136)])
-def test_tc_gemm_panels(torch_cuda, poas, shape, panels):
+def test_tc_gemm_panels(torch_cuda, poas, monkeypatch, shape, panels, variant):
     """One launch over panel-major B (the layout a per-panel broadcast
     lands): tiles are ordered panel by panel and B is read through a 3-D
-    tensor map; with readiness flags already set and without flags."""
+    tensor map; with readiness flags already set and without flags. With
+    2cta512, panels that are whole 512-column tiles run the wide pair tile
+    and the others the 256-wide one."""
     import oracle
 
     torch = torch_cuda
+    if variant:
+        monkeypatch.setenv("POAS_TC_KERNEL", variant)
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 51), oracle.fill_uniform(k, n, 52)
     a = torch.from_numpy(A).cuda().bfloat16()
@@ -377,7 +387,8 @@ def test_tc_gemm_panels(torch_cuda, poas, shape, panels):
         poas.tc_gemm_panels(2, m, 768, k, a.data_ptr(), k, bp.data_ptr(), 384, c.data_ptr(), n, 2)
 
 
-def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
+@pytest.mark.parametrize("variant", ["2cta", "2cta512"])
+def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas, monkeypatch, variant):
     """The fused consumer: the GEMM is queued first with every flag clear;
     another stream delivers the panels later (a ~spin, then one flag per
     panel in order, each after the panel's bytes were written). The kernel
@@ -385,6 +396,7 @@ def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
     import oracle
 
     torch = torch_cuda
+    monkeypatch.setenv("POAS_TC_KERNEL", variant)
     m, n, k, panels = 2048, 2048, 512, 4
     A, B = oracle.fill_uniform(m, k, 61), oracle.fill_uniform(k, n, 62)
     a = torch.from_numpy(A).cuda().bfloat16()
@@ -422,13 +434,48 @@ def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas):
 
 
 def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
-    """Pair tiles unless at most a quarter of the pairs would be busy, then
-    128 x 128 single-SM tiles; the env override wins."""
+    """256 x 512 pair tiles from two waves of them, 256 x 256 pair tiles
+    below, 128 x 128 single-SM tiles when at most a quarter of the pairs
+    would be busy; the env override wins."""
     monkeypatch.delenv("POAS_TC_KERNEL", raising=False)
-    assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel"
-    assert poas.tc_kernel_name(4096, 4096, 4096) == "tc_gemm_2cta_kernel"
+    assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel<512>"
+    assert poas.tc_kernel_name(65536, 8192, 8192) == "tc_gemm_2cta_kernel<512>"
+    assert poas.tc_kernel_name(8192, 8192, 8192) == "tc_gemm_2cta_kernel<512>"
+    assert poas.tc_kernel_name(4096, 4096, 4096) == "tc_gemm_2cta_kernel<256>"
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_kernel_n128"
-    assert poas.tc_kernel_name(2048, 2048, 2048) == "tc_gemm_2cta_kernel"
+    assert poas.tc_kernel_name(2048, 2048, 2048) == "tc_gemm_2cta_kernel<256>"
     assert poas.tc_kernel_name(256, 4096, 16384) == "tc_gemm_kernel_n128"
     monkeypatch.setenv("POAS_TC_KERNEL", "2cta")
-    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel"
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<256>"
+    assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel<256>"
+    monkeypatch.setenv("POAS_TC_KERNEL", "2cta512")
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<512>"
+
+
+@pytest.mark.parametrize("shape,ctas", [((2048, 4096, 2048), 4), ((1024, 2048, 64), 2),
+                                        ((777, 1536, 4104), 6), ((4096, 1000, 192), 148)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_tc_wide_pair_half_release(torch_cuda, poas, monkeypatch, shape, ctas, accumulate):
+    """256 x 512 pair tiles: the epilogue frees each 256-column half of the
+    TMEM accumulator separately and the next tile's MMAs for half 1 trail
+    half 0's by up to a ring of staged k-blocks. Many tiles per pair (long
+    and short K -- one k-block: the end-of-tile catch-up), ragged N, and a
+    budget of every SM; exact vs the oracle, plain and accumulating."""
+    import oracle
+
+    torch = torch_cuda
+    monkeypatch.setenv("POAS_TC_KERNEL", "2cta512")
+    m, n, k = shape
+    A, B = oracle.fill_uniform(m, k, 71), oracle.fill_uniform(k, n, 72)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    c = torch.full((m, n), 1.0 if accumulate else float("nan"), device="cuda")
+    for _ in range(2):  # the second launch reuses the self-reset tile counter
+        if accumulate:
+            c.fill_(1.0)
+        poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n,
+                     accumulate=accumulate, num_ctas=ctas)
+        torch.cuda.synchronize()
+        got = c.cpu().numpy() - (1.0 if accumulate else 0.0)
+        assert oracle.rel_frobenius(got, ref) <= TOL, (shape, ctas)
