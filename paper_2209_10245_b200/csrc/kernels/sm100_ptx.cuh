@@ -43,10 +43,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return done != 0;
 }
 
+// Watchdog for the spin loops: a wait that has not completed after ~16M
+// polls checks %globaltimer every ~1M polls and traps after 10 s, so a lost
+// signal fails the launch (a CUDA error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_watchdog(uint32_t& polls, unsigned long long& since) {
+  if (++polls < (1u << 24) || (polls & ((1u << 20) - 1)) != 0) return;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  if (since == 0) since = now;
+  else if (now - since > 10000000000ull) __trap();
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
-  while (!mbar_try_wait(a, parity)) {
-  }
+  uint32_t polls = 0;
+  unsigned long long since = 0;
+  while (!mbar_try_wait(a, parity)) mbar_watchdog(polls, since);
 }
 
 // --------------------------------------------------------------------- TMA
@@ -227,7 +239,9 @@ __device__ __forceinline__ void st_shared_cluster(const void* p, uint32_t rank, 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
   uint32_t done;
-  do {
+  uint32_t polls = 0;
+  unsigned long long since = 0;
+  while (true) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
@@ -235,7 +249,9 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) break;
+    mbar_watchdog(polls, since);
+  }
 }
 // Non-blocking parity test (never suspends the thread), cluster-scope
 // acquire: true once the phase with `parity` has completed.
@@ -270,6 +286,29 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
       ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_addr(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
       "r"(c2), "l"(cache_hint)
+      : "memory");
+}
+// Multicast variants: the box lands at the same offset in every CTA of
+// `mask`; each destination's bytes complete on ITS pair leader's barrier at
+// this offset (peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                    int32_t c0, int32_t c1, uint16_t mask,
+                                                    uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "h"(mask), "l"(cache_hint)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                    int32_t c0, int32_t c1, int32_t c2, uint16_t mask,
+                                                    uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "r"(c2), "h"(mask), "l"(cache_hint)
       : "memory");
 }
 // Generic-proxy global state (e.g. data another kernel wrote, observed via

@@ -507,8 +507,17 @@ struct Pair {
   static_assert(kSmem <= 232448, "shared memory per CTA");
 };
 
-template <int W>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// PAIRS = 2 (W = 512 only): a cluster of two CTA pairs stacked in M (a
+// 512 x 512 cluster tile) shares B: each CTA loads the 256-column half of its
+// B slice that matches its pair index and multicasts it to the same-rank CTA
+// of the other pair, so B crosses the L2 -> SM crossbar once per cluster
+// (1/3 fewer operand bytes per MAC than PAIRS = 1). A stage of a CTA is then
+// written by both pairs' producers: it is free once BOTH pairs' MMAs have
+// consumed it (every MMA commit is multicast to the four CTAs). The cluster
+// leader (rank 0) claims the tiles for all four CTAs. Launched with the
+// cluster dimension 2 * PAIRS as a launch attribute.
+template <int W, int PAIRS>
+__global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
@@ -532,10 +541,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   int* tile_ring = reinterpret_cast<int*>(tile_empty + kTileSlots);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
 
+  static_assert(PAIRS == 1 || (PAIRS == 2 && W == 512), "B-sharing clusters use 512-wide tiles");
+  constexpr int kCtas = 2 * PAIRS;
+  constexpr int kRowsT = 256 * PAIRS;  // rows of a (cluster) tile
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
+  const uint32_t prank = rank & 1;        // rank inside the pair
+  const int pair = static_cast<int>(rank >> 1);
+  const uint32_t pair_leader = rank & ~1u;
+  const bool leader = prank == 0;         // issues the pair's MMAs
+  const bool cleader = rank == 0;         // claims and publishes the tiles
+  // a stage is free once every pair has consumed it: each MMA commit that
+  // releases stages arrives in all CTAs of the cluster
+  constexpr uint16_t kFreeMask = static_cast<uint16_t>((1u << kCtas) - 1u);
   if (threadIdx.x == 0) trace_stamp(args, 0);
 
   if (warp == 0 && lane == 0) {
@@ -543,16 +562,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_b);
     if (args.tma_store) tma_prefetch_desc(&map_c);
     for (int s = 0; s < k2Stages; ++s) {
-      mbar_init(&full[s], 1);   // leader: its expect_tx arrive + both CTAs' bytes
-      mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both
+      mbar_init(&full[s], 1);   // pair leader: its expect_tx arrive + both CTAs' bytes
+      mbar_init(&empty[s], PAIRS);  // every pair leader's MMA commit, multicast to all CTAs
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 8);  // leader: 4 epilogue warps x 2 CTAs
     }
     for (int s = 0; s < kTileSlots; ++s) {
-      mbar_init(&tile_full[s], 1);    // the leader's producer (local or remote arrive)
-      mbar_init(&tile_empty[s], 10);  // leader: its MMA thread + peer producer + 2 x 4 epilogue warps
+      mbar_init(&tile_full[s], 1);  // the cluster leader's producer (local or remote arrive)
+      // cluster leader: the pairs' MMA threads + the other producers + 4
+      // epilogue warps per CTA
+      mbar_init(&tile_empty[s], PAIRS + (kCtas - 1) + 4 * kCtas);
     }
     fence_mbar_init();
   }
@@ -591,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int confirmed = -1;  // highest B panel seen ready
       uint64_t seen_lo = 0, seen_hi = 0;  // streamed link items seen ready
       while (t >= 0) {
-        if (leader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
+        if (cleader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
         ++wave;
         int t_next = 0;  // claimed once this tile's first loads are out
         int mb, nb, pnl, nbl;
@@ -616,9 +637,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           wait_panel_flag(args.panel_flags + pnl, args.panel_epoch);
           confirmed = pnl;
         }
-        const int row0 = mb * 256 + static_cast<int>(rank) * 128;
-        // this CTA's columns of each 256-column half: [h*256 + rank*128, +128)
-        const int col0 = nbl * W + static_cast<int>(rank) * 128;  // inside the panel
+        const int row0 = mb * kRowsT + pair * 256 + static_cast<int>(prank) * 128;
+        // this CTA's columns of each 256-column half: [h*256 + prank*128, +128)
+        const int col0 = nbl * W + static_cast<int>(prank) * 128;  // inside the panel
         // K serpentine: the tiles of a wave that follows one sweeping K
         // forwards start where it ended, on the K-slices still in L2
         const bool rev = args.kserp && ((t / step) & 1);
@@ -633,27 +654,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < W / 128; ++j) {  // 64-column chunks: half j/2, chunk j%2
             const int cj = col0 + (j >> 1) * 256 + (j & 1) * 64;
-            if (args.panels > 1)
+            if constexpr (PAIRS == 2) {  // my pair's half, to me and my twin in the other pair
+              if ((j >> 1) != pair) continue;
+              const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2u)));
+              if (args.panels > 1)
+                tma_load_3d_pair_mc(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, pnl, mask,
+                                    args.hint_b);
+              else
+                tma_load_2d_pair_mc(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, mask,
+                                    args.hint_b);
+            } else if (args.panels > 1) {
               tma_load_3d_pair(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, pnl,
                                args.hint_b);
-            else
+            } else {
               tma_load_2d_pair(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, args.hint_b);
+            }
           }
           if (wave == 1 && kb == 0) trace_stamp(args, 2);
-          if (kb == 0 && leader) t_next = claim_tile(args, next_static, step);  // behind the first loads
+          if (kb == 0 && cleader) t_next = claim_tile(args, next_static, step);  // behind the first loads
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        // hand the next tile to both CTAs' roles (the leader publishes)
-        if (leader) {
+        // hand the next tile to every CTA's roles (the cluster leader publishes)
+        if (cleader) {
           t = t_next < total ? t_next : -1;
           mbar_wait_cluster(&tile_empty[slot], tphase ^ 1);
           tile_ring[slot] = t;
-          st_shared_cluster(&tile_ring[slot], 1, t);
+#pragma unroll
+          for (uint32_t r = 1; r < kCtas; ++r) st_shared_cluster(&tile_ring[slot], r, t);
           mbar_arrive(&tile_full[slot]);
-          mbar_arrive_cluster(&tile_full[slot], 1);
+#pragma unroll
+          for (uint32_t r = 1; r < kCtas; ++r) mbar_arrive_cluster(&tile_full[slot], r);
         } else {
           mbar_wait_cluster(&tile_full[slot], tphase);
           t = tile_ring[slot];
@@ -665,7 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tphase ^= 1;
         }
       }
-      if (leader) release_counter(args, step);
+      if (cleader) release_counter(args, step);
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
@@ -708,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           issue(d_tmem, stage, kb, 0);
           if constexpr (W == 256) {
-            umma_commit_pair(&empty[stage], 0x3);
+            umma_commit_pair(&empty[stage], kFreeMask);
           } else {
             if (npend++ == 0) {
               pend_kb = kb;
@@ -724,7 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (h1) {
               for (int i = 0, st = pend_stage; i < npend; ++i) {
                 issue(d_tmem, st, pend_kb + i, 1);
-                umma_commit_pair(&empty[st], 0x3);
+                umma_commit_pair(&empty[st], kFreeMask);
                 if (++st == k2Stages) st = 0;
               }
               npend = 0;
@@ -741,12 +774,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             for (int i = 0, st = pend_stage; i < npend; ++i) {
               issue(d_tmem, st, pend_kb + i, 1);
-              umma_commit_pair(&empty[st], 0x3);
+              umma_commit_pair(&empty[st], kFreeMask);
               if (++st == k2Stages) st = 0;
             }
           }
         }
-        umma_commit_pair(&acc_full[acc], 0x3);
+        umma_commit_pair(&acc_full[acc], static_cast<uint16_t>(0x3u << pair_leader));
         if (args.trace) {  // the last commit of this worker overwrites
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
@@ -755,7 +788,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
         mbar_wait_cluster(&tile_full[slot], tphase);  // the next tile
         t = tile_ring[slot];
-        mbar_arrive(&tile_empty[slot]);
+        mbar_arrive_cluster(&tile_empty[slot], 0);  // the cluster leader's barrier
         if (++slot == kTileSlots) {
           slot = 0;
           tphase ^= 1;
@@ -797,7 +830,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         trace_stamp(args, 5);
         epi_traced = true;
       }
-      const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
+      const int row_base = mb * kRowsT + pair * 256 + static_cast<int>(prank) * 128 + quad * 32;
       if (args.tma_store) {
         // TMEM -> registers, 64 columns per step (two 32x32b.x32 loads, the
         // next step's in flight while this one is written) -> two 32-row x
@@ -855,7 +888,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0)  // the leader's barrier
-              mbar_arrive_cluster(&acc_empty[W == 256 ? acc : (c + 2) / 4 - 1], 0);
+              mbar_arrive_cluster(&acc_empty[W == 256 ? acc : (c + 2) / 4 - 1], pair_leader);
             if (args.trace && quad == 0 && lane == 0)
               trace_add(args, (c + 2) == 4 ? 12 : 13, gtimer() - te0);
           }
@@ -927,8 +960,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {  // the leader's barrier(s)
-        mbar_arrive_cluster(&acc_empty[W == 256 ? acc : 0], 0);
-        if (W == 512) mbar_arrive_cluster(&acc_empty[1], 0);
+        mbar_arrive_cluster(&acc_empty[W == 256 ? acc : 0], pair_leader);
+        if (W == 512) mbar_arrive_cluster(&acc_empty[1], pair_leader);
       }
       if (args.sblocks) {
         // direct stores (C pitch TMA cannot map): the same per-block count
@@ -1111,7 +1144,7 @@ namespace {
 // 1024^3: 16 tiles for 74 pairs) the single-SM kernel with 128 x 128 tiles
 // spreads the work over 4x as many CTAs. POAS_TC_KERNEL = 2cta512 | 2cta |
 // 1cta (128 x 256) | 1cta128 overrides.
-enum class TcVariant { pair512, pair, single256, single128 };
+enum class TcVariant { pair512x2, pair512, pair, single256, single128 };
 
 TcVariant choose_variant(int64_t M, int64_t N, int budget) {
   if (const char* v = std::getenv("POAS_TC_KERNEL")) {
@@ -1120,6 +1153,7 @@ TcVariant choose_variant(int64_t M, int64_t N, int budget) {
     if (s == "1cta128") return TcVariant::single128;
     if (s == "2cta") return TcVariant::pair;
     if (s == "2cta512") return TcVariant::pair512;
+    if (s == "2cta512x2") return TcVariant::pair512x2;
   }
   // Single-SM 128 x 128 tiles only when the pairs would be mostly idle (at
   // most a quarter busy): measured (profiles/r01_small_variants) 1024^3
@@ -1135,11 +1169,17 @@ const char* variant_name(TcVariant v) {
     case TcVariant::single256: return "tc_gemm_kernel";
     case TcVariant::single128: return "tc_gemm_kernel_n128";
     case TcVariant::pair512: return "tc_gemm_2cta_kernel<512>";
+    case TcVariant::pair512x2: return "tc_gemm_2cta_kernel<512,2>";
     case TcVariant::pair: break;
   }
   return "tc_gemm_2cta_kernel<256>";
 }
 }  // namespace
+
+// Clusters of two CTA pairs that fit on the device at once (a cluster of 4
+// must sit inside one GPC; GPCs with an SM count not divisible by 4 leave
+// SMs idle). Cached per device.
+int max_active_clusters_x2();
 
 cudaError_t tc_prepare_stream(cudaStream_t stream) {
   return next_tile_counter(stream) ? cudaSuccess : cudaErrorMemoryAllocation;
@@ -1192,7 +1232,7 @@ namespace {
 // launches plainly.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t stream,
-                       Args&&... args) {
+                       int cluster, Args&&... args) {
   static const bool pdl = [] {
     const char* e = std::getenv("POAS_TC_PDL");
     return !(e && std::string(e) == "0");
@@ -1202,11 +1242,22 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStre
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = static_cast<unsigned>(cluster);
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -1248,11 +1299,15 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Tile1<128, 6>::kSmem));
     if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<256>,
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<256, 1>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Pair<256>::kSmem));
     if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<512>,
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<512, 1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Pair<512>::kSmem));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<512, 2>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Pair<512>::kSmem));
   });
@@ -1268,11 +1323,14 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     // tables are in 256 x 256 tiles, panels take 512-wide tiles when every
     // panel is a whole number of them
     const char* v = std::getenv("POAS_TC_KERNEL");
-    if (v && std::string(v) != "2cta" && std::string(v) != "2cta512") return cudaErrorNotSupported;
-    const bool wide = variant == TcVariant::pair512 && !ss && np % 512 == 0;
-    variant = wide ? TcVariant::pair512 : TcVariant::pair;
+    if (v && std::string(v) != "2cta" && std::string(v) != "2cta512" && std::string(v) != "2cta512x2")
+      return cudaErrorNotSupported;
+    const bool wide = (variant == TcVariant::pair512 || variant == TcVariant::pair512x2) && !ss &&
+                      np % 512 == 0;
+    variant = wide ? variant : TcVariant::pair;
   }
-  const bool force_1cta = variant != TcVariant::pair && variant != TcVariant::pair512;
+  const bool force_1cta = variant != TcVariant::pair && variant != TcVariant::pair512 &&
+                          variant != TcVariant::pair512x2;
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -1318,7 +1376,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.tma_store = 0;
   args.trace = nullptr;
   args.panels = P;
-  args.tiles_n_panel = static_cast<int>(np / (variant == TcVariant::pair512 ? 512 : 256));
+  args.tiles_n_panel = static_cast<int>(np / (variant == TcVariant::pair ? 256 : 512));
   args.panel_flags = ps ? ps->flags : nullptr;
   args.panel_epoch = ps ? ps->epoch : 0;
   args.sblocks = nullptr;
@@ -1353,15 +1411,24 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     args.tma_store = !direct && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 &&
                      make_map_c(&mc, C, M, N, ldc);
     if (!args.tma_store) mc = ma;  // unused
-    const bool wide = variant == TcVariant::pair512;
+    // clusters of two pairs need a budget of at least one cluster
+    const bool x2 = variant == TcVariant::pair512x2 && std::min(budget / 4, max_active_clusters_x2()) >= 1;
+    const bool wide = x2 || variant == TcVariant::pair512;
     const int w = wide ? 512 : 256;
-    args.tiles_m = static_cast<int>((M + 255) / 256);
+    const int rows_t = x2 ? 512 : 256;
+    args.tiles_m = static_cast<int>((M + rows_t - 1) / rows_t);
     args.tiles_n = static_cast<int>((N + w - 1) / w);
     args.idesc = idesc_f16(t == AbType::bf16, 256, 256, false, true);  // per 256-column half
-    args.group = group_override > 0 ? group_override : kGroupM2;
+    args.group = group_override > 0 ? group_override : (x2 ? kGroupM2 / 2 : kGroupM2);
     const int tiles = args.tiles_m * args.tiles_n;
     int pairs = budget / 2;
-    if (pairs > tiles) pairs = tiles;
+    if (x2) {  // whole clusters of two pairs, no more than can be resident at once
+      int clusters = std::min(budget / 4, max_active_clusters_x2());
+      if (clusters > tiles) clusters = tiles;
+      pairs = 2 * clusters;
+    } else if (pairs > tiles) {
+      pairs = tiles;
+    }
     static unsigned long long* trace_buf = nullptr;
     const bool trace = std::getenv("POAS_TC_TRACE") != nullptr;
     if (trace) {
@@ -1371,8 +1438,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       args.trace = trace_buf;
     }
     const cudaError_t e =
-        wide ? launch_pdl(tc_gemm_2cta_kernel<512>, 2 * pairs, Pair<512>::kSmem, stream, ma, mb, mc, args)
-             : launch_pdl(tc_gemm_2cta_kernel<256>, 2 * pairs, Pair<256>::kSmem, stream, ma, mb, mc, args);
+        x2     ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kSmem, stream, 4, ma, mb, mc, args)
+        : wide ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kSmem, stream, 2, ma, mb, mc, args)
+               : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kSmem, stream, 2, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return e;
   }
@@ -1384,10 +1452,38 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
-  if (bn == 128) return launch_pdl(tc_gemm_kernel<128, 6>, grid, Tile1<128, 6>::kSmem, stream, ma, mb, args);
-  return launch_pdl(tc_gemm_kernel<256, 4>, grid, Tile1<256, 4>::kSmem, stream, ma, mb, args);
+  if (bn == 128) return launch_pdl(tc_gemm_kernel<128, 6>, grid, Tile1<128, 6>::kSmem, stream, 1, ma, mb, args);
+  return launch_pdl(tc_gemm_kernel<256, 4>, grid, Tile1<256, 4>::kSmem, stream, 1, ma, mb, args);
 }
 }  // namespace
+
+int max_active_clusters_x2() {
+  static std::mutex mu;
+  static std::map<int, int> by_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (auto it = by_dev.find(dev); it != by_dev.end()) return it->second;
+  int n = 0;
+  if (cudaFuncSetAttribute(tc_gemm_2cta_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(Pair<512>::kSmem)) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4 * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Pair<512>::kSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_2cta_kernel<512, 2>, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();
+  by_dev[dev] = n;
+  return n;
+}
 
 cudaError_t wait_flag(const int* flag, int value, cudaStream_t stream) {
   using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);

@@ -205,7 +205,7 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
-@pytest.mark.parametrize("variant", ["1cta", "2cta", "2cta512"])
+@pytest.mark.parametrize("variant", ["1cta", "2cta", "2cta512", "2cta512x2"])
 def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
     """POAS_TC_KSERP=0: every tile sweeps K forwards (the default alternates
     the direction per wave of tiles); both orders agree with the oracle and
@@ -232,7 +232,7 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 
 # (variant, epilogue): the single-SM kernels have one epilogue
 _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct"),
-                ("2cta512", "tma"), ("2cta512", "direct")]
+                ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512x2", "tma"), ("2cta512x2", "direct")]
 
 
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
@@ -265,7 +265,7 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
         assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL, (variant, ctas)
 
 
-@pytest.mark.parametrize("variant", [None, "2cta512"])
+@pytest.mark.parametrize("variant", [None, "2cta512", "2cta512x2"])
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_tc_epilogue_pitch_and_alignment(torch_cuda, poas, monkeypatch, accumulate, variant):
     """C inside a wider buffer: a padded pitch (TMA-store epilogue, tails
@@ -354,7 +354,7 @@ def _panel_major(torch, B16, panels):
     return torch.stack([B16[:, p * np_:(p + 1) * np_] for p in range(panels)]).contiguous()
 
 
-@pytest.mark.parametrize("variant", [None, "2cta512"])
+@pytest.mark.parametrize("variant", [None, "2cta512", "2cta512x2"])
 @pytest.mark.parametrize("panels", [2, 4])
 @pytest.mark.parametrize("shape", [(1000, 1024, 320), (300, 2048, 136)])
 def test_tc_gemm_panels(torch_cuda, poas, monkeypatch, shape, panels, variant):
@@ -387,7 +387,7 @@ def test_tc_gemm_panels(torch_cuda, poas, monkeypatch, shape, panels, variant):
         poas.tc_gemm_panels(2, m, 768, k, a.data_ptr(), k, bp.data_ptr(), 384, c.data_ptr(), n, 2)
 
 
-@pytest.mark.parametrize("variant", ["2cta", "2cta512"])
+@pytest.mark.parametrize("variant", ["2cta", "2cta512", "2cta512x2"])
 def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas, monkeypatch, variant):
     """The fused consumer: the GEMM is queued first with every flag clear;
     another stream delivers the panels later (a ~spin, then one flag per
@@ -450,21 +450,28 @@ def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
     assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel<256>"
     monkeypatch.setenv("POAS_TC_KERNEL", "2cta512")
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<512>"
+    monkeypatch.setenv("POAS_TC_KERNEL", "2cta512x2")
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<512,2>"
 
 
+@pytest.mark.parametrize("variant", ["2cta512", "2cta512x2"])
 @pytest.mark.parametrize("shape,ctas", [((2048, 4096, 2048), 4), ((1024, 2048, 64), 2),
-                                        ((777, 1536, 4104), 6), ((4096, 1000, 192), 148)])
+                                        ((777, 1536, 4104), 8), ((4096, 1000, 192), 148),
+                                        ((1300, 2560, 512), 12)])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_tc_wide_pair_half_release(torch_cuda, poas, monkeypatch, shape, ctas, accumulate):
+def test_tc_wide_pair_half_release(torch_cuda, poas, monkeypatch, shape, ctas, accumulate, variant):
     """256 x 512 pair tiles: the epilogue frees each 256-column half of the
     TMEM accumulator separately and the next tile's MMAs for half 1 trail
     half 0's by up to a ring of staged k-blocks. Many tiles per pair (long
     and short K -- one k-block: the end-of-tile catch-up), ragged N, and a
-    budget of every SM; exact vs the oracle, plain and accumulating."""
+    budget of every SM; exact vs the oracle, plain and accumulating. The
+    2cta512x2 clusters (two pairs sharing B by multicast) also run an odd
+    number of 256-row tiles (a half-empty cluster tile) and budgets below
+    one cluster (falls back to single pairs)."""
     import oracle
 
     torch = torch_cuda
-    monkeypatch.setenv("POAS_TC_KERNEL", "2cta512")
+    monkeypatch.setenv("POAS_TC_KERNEL", variant)
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 71), oracle.fill_uniform(k, n, 72)
     a = torch.from_numpy(A).cuda().bfloat16()
