@@ -4,7 +4,7 @@
 Metric (BASELINE.json): co-executed GEMM TFLOP/s at N=16384 on 1/2/4/8 B200,
 plus speedup vs the best single unit.
 
-Per rank (one process per GPU, torchrun for N > 1; weak scaling):
+Per rank (one process per GPU; `--gpus N` launches the N ranks itself; weak scaling):
   units      gpu<r>.tc   tensor cores (tcgen05 bf16 -> fp32) on TC_SMS SMs
              gpu<r>.simt CUDA cores (fp32 FFMA) on SIMT_SMS whole SMs
   predict    the POAS profiler probes both units on this box (C++, real
@@ -13,9 +13,11 @@ Per rank (one process per GPU, torchrun for N > 1; weak scaling):
   step       one co-executed GEMM of this rank's M=16384 rows x N=K=16384:
              every unit's share concurrently through the executor (C ABI);
              at N > 1 rank 0's B (bf16; fp32 too if the CUDA-core unit has
-             rows) is broadcast with NCCL inside the step, in column panels;
-             the tensor unit consumes them in ONE launch whose producers wait
-             per panel on a device flag written after that panel landed
+             rows) is delivered by the library's communicator inside the
+             step, in column panels (copy-engine chain over CUDA IPC by
+             default, NCCL optional); the tensor unit consumes them in ONE
+             launch whose producers wait per panel on a device flag
+             written after that panel landed
   value      whole-job TFLOP/s = 2*M_total*N*K / max-over-ranks device time
   e2e        the same GEMM through poas_b200_execute with HOST pinned buffers
              (bf16 A/B for the tensor unit, fp32 for the others, fp32 C):

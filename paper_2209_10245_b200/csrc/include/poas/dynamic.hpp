@@ -66,11 +66,22 @@ class DynamicScheduler {
   // the threshold. Returns true when it re-planned (schedule() replaced).
   bool observe(const SimulationResult& result);
 
+  // The fastest schedule measured so far (schedule() before any
+  // observation). schedule() after a re-plan has not been measured yet, and
+  // a plan derived from a re-fit can be worse than the one it replaces, so
+  // the adapt step hands this one to the run that follows.
+  const Schedule& best_schedule() const { return best_measured_ > 0.0 ? best_ : schedule_; }
+  double best_measured_makespan() const { return best_measured_; }
+  int best_observation() const { return best_observation_; }
+
  private:
   MachineProfile profile_;
   MatrixDims dims_;
   DynamicOptions options_;
   Schedule schedule_;
+  Schedule best_;
+  double best_measured_ = 0.0;
+  int best_observation_ = -1;
   int replans_ = 0;
   int observations_ = 0;
 };

@@ -167,6 +167,12 @@ DynamicScheduler::DynamicScheduler(MachineProfile prior, MatrixDims dims, Dynami
 }
 
 bool DynamicScheduler::observe(const SimulationResult& result) {
+  const double t = result.measured_makespan;
+  if (t > 0.0 && std::isfinite(t) && (best_measured_ <= 0.0 || t < best_measured_)) {
+    best_ = schedule_;
+    best_measured_ = t;
+    best_observation_ = observations_;
+  }
   profile_ = refit_profile(profile_, result.devices, options_.refit);
   ++observations_;
   if (!(std::fabs(result.makespan_error_pct) > options_.replan_threshold_pct)) return false;

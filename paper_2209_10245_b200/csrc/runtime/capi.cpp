@@ -490,7 +490,11 @@ int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t 
     }
     o += "  ],\n  \"replans\": " + std::to_string(dyn.replans()) + ",\n";
     o += "  \"profile\": \"" + json_escape(poas::format_profile(dyn.profile())) + "\",\n";
-    o += "  \"schedule\": " + poas::format_schedule(dyn.schedule()) + "}\n";
+    // the fastest measured plan (the last re-plan may be unmeasured, and a
+    // plan from a re-fit can be slower than the one it replaced)
+    o += "  \"best_iteration\": " + std::to_string(dyn.best_observation()) + ",\n";
+    o += "  \"last_schedule\": " + poas::format_schedule(dyn.schedule()) + ",\n";
+    o += "  \"schedule\": " + poas::format_schedule(dyn.best_schedule()) + "}\n";
     *out_json = dup_string(o);
   });
 }

@@ -393,8 +393,11 @@ int cmd_adapt(const Args& a) {
     poas::save_profile(a.get("out-profile"), dyn.profile());
     std::printf("wrote %s\n", a.get("out-profile").c_str());
   }
+  if (dyn.best_observation() >= 0)
+    std::printf("fastest measured plan: iteration %d (%.9f s)\n", dyn.best_observation(),
+                dyn.best_measured_makespan());
   if (a.has("out")) {
-    poas::save_schedule(a.get("out"), dyn.schedule());
+    poas::save_schedule(a.get("out"), dyn.best_schedule());
     std::printf("wrote %s\n", a.get("out").c_str());
   }
   return 0;
@@ -502,7 +505,7 @@ int cmd_evaluate(const Args& a) {
         dyn.observe(w);
       }
       live = dyn.profile();
-      s = dyn.schedule();
+      s = dyn.best_schedule();
     } else {
       ex.run(s, ops->io, 1);
     }

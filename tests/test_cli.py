@@ -82,7 +82,7 @@ def test_adapt_cpu_units(cli, tmp_path):
     units = "cpuA=cpu:threads=1;cpuB=cpu:threads=1"
     prof = tmp_path / "p.profile"
     r = run("profile", "--units", units, "--profiling",
-            "probes=3,repetitions=2,cpu_min_side=128,cpu_max_side=256", "--out", str(prof))
+            "probes=3,repetitions=3,cpu_min_side=192,cpu_max_side=448", "--out", str(prof))
     assert r.returncode == 0, r.stderr
     lines, cur = [], None
     for line in prof.read_text().splitlines():
@@ -120,7 +120,7 @@ def test_evaluate_adapt_cpu_units(cli, tmp_path):
                                   {"name": "b", "m": 300, "n": 200, "k": 128}]))
     out = tmp_path / "ev"
     r = run("evaluate", "--units", "cpuA=cpu:threads=1;cpuB=cpu:threads=1", "--inputs", str(inputs),
-            "--profiling", "probes=3,repetitions=2,cpu_min_side=128,cpu_max_side=256",
+            "--profiling", "probes=3,repetitions=3,cpu_min_side=192,cpu_max_side=448",
             "--repeats", "2", "--adapt", "3", "--out-dir", str(out))
     assert r.returncode == 0, r.stderr
     rep = json.loads((out / "report.json").read_text())
@@ -151,7 +151,7 @@ def test_evaluate_report_schema_is_the_reference(cli, tmp_path, ref, mach2_cfg):
     out = tmp_path / "ev"
     units = "cpu0=cpu:threads=1;cpu1=cpu:threads=1;cpu2=cpu:threads=1"
     r = run("evaluate", "--units", units, "--inputs", str(fin), "--profiling",
-            "probes=3,repetitions=2,cpu_min_side=128,cpu_max_side=256", "--repeats", "2",
+            "probes=3,repetitions=3,cpu_min_side=192,cpu_max_side=448", "--repeats", "2",
             "--out-dir", str(out))
     assert r.returncode == 0, r.stderr
     ours = json.loads((out / "report.json").read_text())

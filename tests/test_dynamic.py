@@ -151,7 +151,7 @@ def test_dynamic_loop_converges_on_host_units(poas):
     optimistic for one of them: the loop re-fits, re-plans, moves rows away
     and the prediction error shrinks; C stays exact."""
     units = "cpuA=cpu:threads=1;cpuB=cpu:threads=1"
-    prof = poas.profile_machine(units, "probes=3,repetitions=2,cpu_min_side=128,cpu_max_side=256")
+    prof = poas.profile_machine(units, "probes=3,repetitions=3,cpu_min_side=192,cpu_max_side=448")
     lines = []
     cur = None
     for line in prof.splitlines():
@@ -179,6 +179,12 @@ def test_dynamic_loop_converges_on_host_units(poas):
     assert abs(its[-1]["makespan_error_pct"]) < abs(its[0]["makespan_error_pct"])
     assert poas.machine_hash(out["profile"]) == poas.machine_hash(planted)
     assert out["schedule"]["machine_hash"] == ex.machine_hash
+    # the returned plan is the fastest MEASURED one (the last re-plan is
+    # unmeasured and a re-fit's plan can be slower than its predecessor)
+    best = out["best_iteration"]
+    assert its[best]["measured_makespan"] == min(i["measured_makespan"] for i in its)
+    assert {d["id"]: d["rows"] for d in out["schedule"]["devices"]} == its[best]["rows"]
+    assert out["last_schedule"]["machine_hash"] == ex.machine_hash
     ref = A.astype(np.float64) @ B.astype(np.float64)
     assert np.linalg.norm(C - ref) / np.linalg.norm(ref) < 2e-5
 
