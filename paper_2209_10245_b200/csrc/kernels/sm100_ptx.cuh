@@ -43,22 +43,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return done != 0;
 }
 
-// Watchdog for the spin loops: a wait that has not completed after ~16M
-// polls checks %globaltimer every ~1M polls and traps after 10 s, so a lost
-// signal fails the launch (a CUDA error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_watchdog(uint32_t& polls, unsigned long long& since) {
-  if (++polls < (1u << 24) || (polls & ((1u << 20) - 1)) != 0) return;
-  unsigned long long now;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-  if (since == 0) since = now;
-  else if (now - since > 10000000000ull) __trap();
-}
-
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // (no watchdog in the loop: a poll counter here cost the 256 x 256 pair
+  // kernel 10-13% at 2048^3-4096^3, profiles/r02_bisect)
   const uint32_t a = smem_addr(bar);
-  uint32_t polls = 0;
-  unsigned long long since = 0;
-  while (!mbar_try_wait(a, parity)) mbar_watchdog(polls, since);
+  while (!mbar_try_wait(a, parity)) {
+  }
 }
 
 // --------------------------------------------------------------------- TMA
@@ -239,8 +229,6 @@ __device__ __forceinline__ void st_shared_cluster(const void* p, uint32_t rank, 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
   uint32_t done;
-  uint32_t polls = 0;
-  unsigned long long since = 0;
   while (true) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -250,7 +238,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "r"(a), "r"(parity)
         : "memory");
     if (done) break;
-    mbar_watchdog(polls, since);
   }
 }
 // Non-blocking parity test (never suspends the thread), cluster-scope

@@ -59,6 +59,7 @@ struct TcArgs {
   int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
   unsigned long long* trace;  // dev: per-CTA %globaltimer stamps (POAS_TC_TRACE), or null
   int epi_skip;               // dev (POAS_TC_EPI_SKIP): TMA-store epilogue stages boxes, stores nothing
+  int direct8;                // 256 x 512 tiles: epilogue by 32-byte register stores (no smem staging)
   // Panel-major B (pair kernel): `panels` column panels of tiles_n_panel
   // N-tiles each, B loaded through a 3-D map {column, k, panel}; tiles are
   // ordered panel by panel. With panel_flags, a producer starts on panel p
@@ -492,8 +493,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 //            k-blocks stay staged, at most a ring's worth) once it is free.
 constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
-// Epilogue staging (TMA-store path): per epilogue warp two 32-row x 32-column
-// fp32 boxes, 128-byte swizzled rows (2 x 4 KB).
+// Epilogue staging (TMA-store path), per epilogue warp: W = 256 two 32-row x
+// 16-column fp32 boxes with 64-byte swizzled rows (2 x 2 KB); W = 512 two
+// 32-row x 32-column boxes with 128-byte swizzled rows (2 x 4 KB).
 
 template <int W>
 struct Pair {
@@ -502,7 +504,7 @@ struct Pair {
   static constexpr int kStages = W == 256 ? 6 : 4;
   static constexpr int kBBytes = (W / 2) * kBK * 2;  // this CTA's W/2 columns of B
   static constexpr int kStageBytes = k2ABytes + kBBytes;
-  static constexpr int kStagingBytes = 4 * 2 * 4096;
+  static constexpr int kStagingBytes = 4 * 2 * (W == 256 ? 2048 : 4096);
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 256;
   static_assert(kSmem <= 232448, "shared memory per CTA");
 };
@@ -514,10 +516,12 @@ struct Pair {
 // (1/3 fewer operand bytes per MAC than PAIRS = 1). A stage of a CTA is then
 // written by both pairs' producers: it is free once BOTH pairs' MMAs have
 // consumed it (every MMA commit is multicast to the four CTAs). The cluster
-// leader (rank 0) claims the tiles for all four CTAs. Launched with the
-// cluster dimension 2 * PAIRS as a launch attribute.
+// leader (rank 0) claims the tiles for all four CTAs. The cluster shape is
+// compiled in (__cluster_dims__): launching the same kernel with a runtime
+// cluster-dimension attribute instead ran the 256 x 256 tiles 10-15% slower
+// (profiles/r02_sizes).
 template <int W, int PAIRS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
@@ -831,45 +835,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi_traced = true;
       }
       const int row_base = mb * kRowsT + pair * 256 + static_cast<int>(prank) * 128 + quad * 32;
-      if (args.tma_store) {
-        // TMEM -> registers, 64 columns per step (two 32x32b.x32 loads, the
-        // next step's in flight while this one is written) -> two 32-row x
-        // 32-column staging boxes of this warp (128-byte rows, 128-byte
-        // swizzle: conflict-free, the TMA's layout) -> ONE proxy fence ->
-        // two TMA stores (or f32 add-reductions). The fence is the expensive
-        // part of a step, so a step covers 8 KB. Each 256-column half of
-        // the accumulator is released as soon as its last columns are in
-        // registers (TMEM reads, 64 B/clk/SM, are the floor of the drain).
-        uint8_t* slots = s_c + quad * 8192;
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(W == 256 ? acc * 256 : 0);
+      if (W == 512 && args.direct8) {
+        // 256 x 512 tiles, C 32-byte aligned with a pitch of whole 32-byte
+        // sectors: TMEM -> registers -> 256-bit st.global (each lane one
+        // full sector of its row), no staging, no proxy fence, no waits on
+        // store completion, so a half of the accumulator is free as soon as
+        // TMEM has been read. Masked rows / a ragged last sector fall back
+        // to scalar stores.
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+        const int row = row_base + lane;
+        float* crow = args.C + static_cast<long long>(row) * args.ldc;
         auto put = [&](const uint32_t* w, int c) {  // columns [c*64, c*64+64)
-          if (lane == 0) bulk_wait_read<0>();  // the previous step's stores have left smem
-          __syncwarp();
+          if (row >= args.M) return;
+          const int col0 = nb * W + c * 64;
 #pragma unroll
-          for (int bx = 0; bx < 2; ++bx) {
-            uint8_t* my_row = slots + bx * 4096 + lane * 128;
+          for (int q = 0; q < 8; ++q) {
+            const int col = col0 + q * 8;
+            if (col + 8 <= args.N) {
+              float o[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
-                  make_uint4(w[32 * bx + 4 * j], w[32 * bx + 4 * j + 1], w[32 * bx + 4 * j + 2],
-                             w[32 * bx + 4 * j + 3]);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && !args.epi_skip) {
+              for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(w[q * 8 + e]);
+              if (args.accumulate) {
+                float p[8];
+                asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=f"(p[0]), "=f"(p[1]), "=f"(p[2]), "=f"(p[3]), "=f"(p[4]),
+                               "=f"(p[5]), "=f"(p[6]), "=f"(p[7])
+                             : "l"(crow + col));
 #pragma unroll
-            for (int bx = 0; bx < 2; ++bx) {
-              const int col0 = nb * W + c * 64 + bx * 32;
-              uint8_t* box = slots + bx * 4096;
-              if (args.accumulate)
-                tma_reduce_add_2d(&map_c, box, col0, row_base);
-              else if (args.hint_c != kEvictNormal)
-                tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
-              else
-                tma_store_2d(&map_c, box, col0, row_base);
+                for (int e = 0; e < 8; ++e) o[e] += p[e];
+              }
+              asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + col),
+                           "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]), "f"(o[4]), "f"(o[5]),
+                           "f"(o[6]), "f"(o[7])
+                           : "memory");
+            } else {
+              for (int e = 0; e < 8 && col + e < args.N; ++e) {
+                float o = __uint_as_float(w[q * 8 + e]);
+                if (args.accumulate) o += crow[col + e];
+                crow[col + e] = o;
+              }
             }
-            bulk_commit();
           }
         };
         uint32_t va[64], vb[64];
@@ -887,14 +892,144 @@ __global__ void __launch_bounds__(kThreads, 1)
           if ((c + 2) % 4 == 0) {  // a 256-column half is in registers: free it
             tc_fence_before();
             __syncwarp();
-            if (lane == 0)  // the leader's barrier
-              mbar_arrive_cluster(&acc_empty[W == 256 ? acc : (c + 2) / 4 - 1], pair_leader);
+            if (lane == 0) mbar_arrive_cluster(&acc_empty[(c + 2) / 4 - 1], pair_leader);
             if (args.trace && quad == 0 && lane == 0)
               trace_add(args, (c + 2) == 4 ? 12 : 13, gtimer() - te0);
           }
           if (c + 2 < W / 64) load64(va, c + 2);
           put(vb, c + 1);
           tmem_wait_ld();
+        }
+        if (args.sblocks) {  // (streamed operands never use 512-wide tiles)
+          __trap();
+        }
+        if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
+        continue;
+      }
+      if (args.tma_store) {
+        if constexpr (W == 256) {
+          // 256 x 256 tiles (the accumulator is double buffered, so the
+          // drain overlaps the next tile's MMAs and only the completion of a
+          // short GEMM's last tile is exposed): TMEM -> registers -> a
+          // 32-row x 16-column staging box of this warp (64-byte swizzled
+          // rows) -> one TMA store (or f32 add-reduction) per box. Two boxes
+          // per warp, so a box's store drains while the next one fills; the
+          // TMEM load of the next 32 columns is in flight while the current
+          // ones are written. (With one fence per 2 KB this finishes a
+          // single-tile GEMM sooner than the wide tiles' 8 KB steps, which
+          // wait for the previous step's stores: 2048^3 922 vs 817 TFLOP/s,
+          // profiles/r02_sizes.)
+          uint8_t* boxes = s_c + quad * 4096;
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                 static_cast<uint32_t>(acc * 256);
+          auto put_box = [&](const uint32_t* w, int c) {  // 16 columns, box (c & 1)
+            uint8_t* box = boxes + (c & 1) * 2048;
+            if (lane == 0) bulk_wait_read<1>();  // the store two boxes back has left smem
+            __syncwarp();
+            uint8_t* my_row = box + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(my_row + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && !args.epi_skip) {
+              const int col0 = nb * W + c * 16;
+              if (args.accumulate)
+                tma_reduce_add_2d(&map_c, box, col0, row_base);
+              else if (args.hint_c != kEvictNormal)
+                tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
+              else
+                tma_store_2d(&map_c, box, col0, row_base);
+              bulk_commit();
+            }
+          };
+          uint32_t va[32], vb[32];
+          tmem_ld_32x32b_x32(taddr, va);
+          tmem_wait_ld();
+#pragma unroll 1
+          for (int c = 0; c < 8; c += 2) {
+            tmem_ld_32x32b_x32(taddr + (c + 1) * 32, vb);
+            put_box(va, 2 * c);
+            put_box(va + 16, 2 * c + 1);
+            tmem_wait_ld();
+            if (c + 2 < 8) {
+              tmem_ld_32x32b_x32(taddr + (c + 2) * 32, va);
+            } else {  // all 256 columns are in registers: free the accumulator
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], pair_leader);
+              if (args.trace && quad == 0 && lane == 0) trace_add(args, 12, gtimer() - te0);
+            }
+            put_box(vb, 2 * c + 2);
+            put_box(vb + 16, 2 * c + 3);
+            tmem_wait_ld();
+          }
+        } else {
+          // TMEM -> registers, 64 columns per step (two 32x32b.x32 loads, the
+          // next step's in flight while this one is written) -> two 32-row x
+          // 32-column staging boxes of this warp (128-byte rows, 128-byte
+          // swizzle: conflict-free, the TMA's layout) -> ONE proxy fence ->
+          // two TMA stores (or f32 add-reductions). The fence is the expensive
+          // part of a step, so a step covers 8 KB. Each 256-column half of
+          // the accumulator is released as soon as its last columns are in
+          // registers (TMEM reads, 64 B/clk/SM, are the floor of the drain).
+          uint8_t* slots = s_c + quad * 8192;
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                 static_cast<uint32_t>(W == 256 ? acc * 256 : 0);
+          auto put = [&](const uint32_t* w, int c) {  // columns [c*64, c*64+64)
+            if (lane == 0) bulk_wait_read<0>();  // the previous step's stores have left smem
+            __syncwarp();
+  #pragma unroll
+            for (int bx = 0; bx < 2; ++bx) {
+              uint8_t* my_row = slots + bx * 4096 + lane * 128;
+  #pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(w[32 * bx + 4 * j], w[32 * bx + 4 * j + 1], w[32 * bx + 4 * j + 2],
+                               w[32 * bx + 4 * j + 3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && !args.epi_skip) {
+  #pragma unroll
+              for (int bx = 0; bx < 2; ++bx) {
+                const int col0 = nb * W + c * 64 + bx * 32;
+                uint8_t* box = slots + bx * 4096;
+                if (args.accumulate)
+                  tma_reduce_add_2d(&map_c, box, col0, row_base);
+                else if (args.hint_c != kEvictNormal)
+                  tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
+                else
+                  tma_store_2d(&map_c, box, col0, row_base);
+              }
+              bulk_commit();
+            }
+          };
+          uint32_t va[64], vb[64];
+          auto load64 = [&](uint32_t (&v)[64], int c) {
+            tmem_ld_32x32b_x32(taddr + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+            tmem_ld_32x32b_x32(taddr + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          };
+          load64(va, 0);
+          tmem_wait_ld();
+  #pragma unroll 1
+          for (int c = 0; c < W / 64; c += 2) {
+            load64(vb, c + 1);
+            put(va, c);
+            tmem_wait_ld();
+            if ((c + 2) % 4 == 0) {  // a 256-column half is in registers: free it
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0)  // the leader's barrier
+                mbar_arrive_cluster(&acc_empty[W == 256 ? acc : (c + 2) / 4 - 1], pair_leader);
+              if (args.trace && quad == 0 && lane == 0)
+                trace_add(args, (c + 2) == 4 ? 12 : 13, gtimer() - te0);
+            }
+            if (c + 2 < W / 64) load64(va, c + 2);
+            put(vb, c + 1);
+            tmem_wait_ld();
+          }
         }
         if (args.trace && quad == 0 && lane == 0) {
           unsigned long long tt;
@@ -1048,17 +1183,17 @@ bool make_map_panels(CUtensorMap* map, AbType t, const void* base, int64_t K, in
 }
 
 // 2-D map over a row-major fp32 [rows x cols] C with leading dim `ld`
-// (elements): 32-column x 32-row boxes, 128-byte swizzle (the epilogue
-// staging layout).
-bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64_t ld) {
+// (elements): the epilogue's staging boxes -- 32 x 32 with 128-byte swizzle
+// for 256 x 512 tiles, 16 columns x 32 rows with 64-byte swizzle for 256 x 256.
+bool make_map_c(CUtensorMap* map, float* base, int64_t rows, int64_t cols, int64_t ld, bool wide) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t box[2] = {wide ? 32u : 16u, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1146,7 +1281,7 @@ namespace {
 // 1cta (128 x 256) | 1cta128 overrides.
 enum class TcVariant { pair512x2, pair512, pair, single256, single128 };
 
-TcVariant choose_variant(int64_t M, int64_t N, int budget) {
+TcVariant choose_variant(int64_t M, int64_t N, int64_t K, int budget) {
   if (const char* v = std::getenv("POAS_TC_KERNEL")) {
     const std::string s(v);
     if (s == "1cta") return TcVariant::single256;
@@ -1160,8 +1295,11 @@ TcVariant choose_variant(int64_t M, int64_t N, int budget) {
   // 16.1 -> 12.4 us, but 2048^3 22.3 -> 29.6 us (64 pair tiles for 74 pairs).
   const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
   if (4 * pair_tiles <= budget / 2) return TcVariant::single128;
+  // 256 x 512 tiles need two waves of them, and a long K: their
+  // accumulator drain is exposed once per tile (4096^3: 1343 -> 1190
+  // TFLOP/s with wide tiles; 8192^3 and up they win, profiles/r02_sizes4)
   const int64_t wide_tiles = ((M + 255) / 256) * ((N + 511) / 512);
-  return wide_tiles >= 2 * (budget / 2) ? TcVariant::pair512 : TcVariant::pair;
+  return wide_tiles >= 2 * (budget / 2) && K >= 6144 ? TcVariant::pair512 : TcVariant::pair;
 }
 
 const char* variant_name(TcVariant v) {
@@ -1185,8 +1323,8 @@ cudaError_t tc_prepare_stream(cudaStream_t stream) {
   return next_tile_counter(stream) ? cudaSuccess : cudaErrorMemoryAllocation;
 }
 
-const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t) {
-  return variant_name(choose_variant(M, N, device_sm_count()));
+const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t K) {
+  return variant_name(choose_variant(M, N, K, device_sm_count()));
 }
 
 const char* tc_gemm_scheduler_name(int64_t M, int64_t N, int64_t K) {
@@ -1317,7 +1455,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   // once its scheduler fits the size, profiles/r01_tile_scheduler).
   // POAS_TC_KERNEL=1cta|2cta overrides (A/B comparisons, tests).
   const int budget_all = num_ctas > 0 ? num_ctas : device_sm_count();
-  TcVariant variant = choose_variant(M, N, budget_all);
+  TcVariant variant = choose_variant(M, N, K, budget_all);
   if (P > 1 || ss) {
     // panels / streamed operands: the pair kernel only; streamed block
     // tables are in 256 x 256 tiles, panels take 512-wide tiles when every
@@ -1394,6 +1532,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     args.stream_epoch = ss->epoch;
   }
   args.epi_skip = std::getenv("POAS_TC_EPI_SKIP") != nullptr;
+  args.direct8 = 0;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
     args.tile_counter = next_tile_counter(stream);
@@ -1405,12 +1544,6 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     // Epilogue through TMA stores when C allows a tensor map (16-byte
     // aligned base and row pitch); POAS_TC_EPILOGUE=direct forces the
     // register -> global path.
-    CUtensorMap mc;
-    const char* epi = std::getenv("POAS_TC_EPILOGUE");
-    const bool direct = epi && std::string(epi) == "direct";
-    args.tma_store = !direct && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 &&
-                     make_map_c(&mc, C, M, N, ldc);
-    if (!args.tma_store) mc = ma;  // unused
     // clusters of two pairs need a budget of at least one cluster
     const bool x2 = variant == TcVariant::pair512x2 && std::min(budget / 4, max_active_clusters_x2()) >= 1;
     const bool wide = x2 || variant == TcVariant::pair512;
@@ -1418,6 +1551,16 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     const int rows_t = x2 ? 512 : 256;
     args.tiles_m = static_cast<int>((M + rows_t - 1) / rows_t);
     args.tiles_n = static_cast<int>((N + w - 1) / w);
+    CUtensorMap mc;
+    const char* epi = std::getenv("POAS_TC_EPILOGUE");
+    const bool direct = epi && std::string(epi) == "direct";
+    args.tma_store = !direct && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 &&
+                     make_map_c(&mc, C, M, N, ldc, wide);
+    if (!args.tma_store) mc = ma;  // unused
+    // 256 x 512 tiles: 256-bit register stores when C allows them
+    // (POAS_TC_EPILOGUE=direct8)
+    args.direct8 = wide && epi && std::string(epi) == "direct8" &&
+                   (reinterpret_cast<uintptr_t>(C) & 31) == 0 && ldc % 8 == 0;
     args.idesc = idesc_f16(t == AbType::bf16, 256, 256, false, true);  // per 256-column half
     args.group = group_override > 0 ? group_override : (x2 ? kGroupM2 / 2 : kGroupM2);
     const int tiles = args.tiles_m * args.tiles_n;
@@ -1438,9 +1581,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       args.trace = trace_buf;
     }
     const cudaError_t e =
-        x2     ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kSmem, stream, 4, ma, mb, mc, args)
-        : wide ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kSmem, stream, 2, ma, mb, mc, args)
-               : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kSmem, stream, 2, ma, mb, mc, args);
+        x2     ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
+        : wide ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
+               : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kSmem, stream, 1, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return e;
   }
@@ -1471,13 +1614,7 @@ int max_active_clusters_x2() {
     cfg.gridDim = dim3(4 * 64);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Pair<512>::kSmem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 4;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 0;  // the cluster shape (4) is compiled into the kernel
     if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_2cta_kernel<512, 2>, &cfg) != cudaSuccess) n = 0;
   }
   cudaGetLastError();

@@ -232,7 +232,8 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 
 # (variant, epilogue): the single-SM kernels have one epilogue
 _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct"),
-                ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512x2", "tma"), ("2cta512x2", "direct")]
+                ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512", "direct8"), ("2cta512x2", "tma"),
+                ("2cta512x2", "direct")]
 
 
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
@@ -249,8 +250,8 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
     torch = torch_cuda
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
     monkeypatch.setenv("POAS_TC_SCHED", sched)
-    if epilogue == "direct":
-        monkeypatch.setenv("POAS_TC_EPILOGUE", "direct")
+    if epilogue != "tma":
+        monkeypatch.setenv("POAS_TC_EPILOGUE", epilogue)
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 31), oracle.fill_uniform(k, n, 32)
     ldb = (n + 7) // 8 * 8
@@ -454,7 +455,7 @@ def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<512,2>"
 
 
-@pytest.mark.parametrize("variant", ["2cta512", "2cta512x2"])
+@pytest.mark.parametrize("variant", ["2cta512", "2cta512x2", "2cta512:direct8"])
 @pytest.mark.parametrize("shape,ctas", [((2048, 4096, 2048), 4), ((1024, 2048, 64), 2),
                                         ((777, 1536, 4104), 8), ((4096, 1000, 192), 148),
                                         ((1300, 2560, 512), 12)])
@@ -471,7 +472,10 @@ def test_tc_wide_pair_half_release(torch_cuda, poas, monkeypatch, shape, ctas, a
     import oracle
 
     torch = torch_cuda
+    variant, _, epilogue = variant.partition(":")
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
+    if epilogue:
+        monkeypatch.setenv("POAS_TC_EPILOGUE", epilogue)
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 71), oracle.fill_uniform(k, n, 72)
     a = torch.from_numpy(A).cuda().bfloat16()
