@@ -481,6 +481,8 @@ def main():
     ap.add_argument("--no-adapt", action="store_true",
                     help="warm-up runs the static plan (no model re-fit / re-plan)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip BASELINE configs C2 and C5 (rank 0 at N=1; ~30 s)")
     ap.add_argument("--ref-rows", type=int, default=None)
     ap.add_argument("--save", default=None, help="directory for profile/schedule/report artefacts")
     args = ap.parse_args()
@@ -990,6 +992,40 @@ def main():
             cpu_baseline = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                             "sample": f"unavailable: {exc}"}
 
+    # ---- BASELINE configs C2 and C5 (rank 0 at N=1 only; tools/sweep.py):
+    # C2 = 8192^3 co-executed by host CPU + fp32 CUDA cores + fp16 tensor
+    # cores; C5 = square sizes 1024..32768, the POAS plan (static prediction
+    # error, then the dynamic re-plan) vs tensor cores alone on every SM vs
+    # the cuBLAS timing reference vs the host-CPU unit. Reported, never fatal.
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        try:
+            sys.path.insert(0, str(ROOT / "tools"))
+            import sweep as sw
+
+            t_sw = time.perf_counter()
+            c5 = sw.c5([1024, 2048, 4096, 8192, 16384, 32768], args.preroll)
+            c2 = sw.c2()
+            sv = sw.simt_vs_cublas_fp32()
+            keep = ("n", "plan_rows", "static_error_pct", "poas_tflops", "adapted_error_pct",
+                    "tc_only_148sm_tflops", "cublas_bf16_fp32out_tflops", "host_cpu_tflops", "host_cores")
+            sweep = {
+                "c5": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items() if k in keep}
+                       for r in c5["rows"]],
+                "c5_note": "POAS = the plan after the dynamic warm-up (static_error_pct: the profile-only "
+                           "plan against its own timed steps); tc_only = our tensor kernel on every SM; "
+                           "cublas = torch.mm bf16->fp32 (timing reference only); resident operands, "
+                           "sustained regime (graph-replayed steps lasting >= 0.25 s)",
+                "c2": {"n": c2["n"], "tflops": round(c2["tflops"], 3), "plan_rows": c2["plan_rows"],
+                       "static_plan_rows": c2["static_plan"]["rows"],
+                       "static_error_pct": round(c2["static_plan"]["makespan_error_pct"], 3),
+                       "makespan_error_pct": round(c2["makespan_error_pct"], 3),
+                       "units": "host CPU (AVX-512) + fp32 CUDA cores (2 SMs) + fp16 tensor cores (146 SMs)"},
+                "simt_vs_cublas_fp32": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in sv.items()},
+                "seconds": round(time.perf_counter() - t_sw, 1)}
+        except Exception as exc:  # reported, never fatal
+            sweep = {"error": f"{type(exc).__name__}: {exc}"}
+
     # per step: one GEMM launch per busy unit (the tensor unit consumes all
     # B panels in one launch; a CUDA-core unit launches once per panel),
     # plus the executor's start-gate kernel on this GPU
@@ -1055,6 +1091,7 @@ def main():
                 "level1_link_gbs": round(link_bw / 1e9, 2) if link_bw else None,
                 "b_panels": P,
                 "c4": c4,
+                "sweep": sweep,
             },
             # the tensor kernel is timed inside a long back-to-back run under
             # the power cap: the measured SUSTAINED cuBLAS figure is its
