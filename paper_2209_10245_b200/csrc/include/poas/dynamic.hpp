@@ -70,7 +70,9 @@ class DynamicScheduler {
   // observation). schedule() after a re-plan has not been measured yet, and
   // a plan derived from a re-fit can be worse than the one it replaces, so
   // the adapt step hands this one to the run that follows.
-  const Schedule& best_schedule() const { return best_measured_ > 0.0 ? best_ : schedule_; }
+  // When the latest plan splits the rows exactly as the fastest one did, the
+  // latest is returned: same work, prediction from the latest re-fit.
+  const Schedule& best_schedule() const;
   double best_measured_makespan() const { return best_measured_; }
   int best_observation() const { return best_observation_; }
 

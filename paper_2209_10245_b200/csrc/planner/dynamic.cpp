@@ -166,6 +166,15 @@ DynamicScheduler::DynamicScheduler(MachineProfile prior, MatrixDims dims, Dynami
   schedule_ = plan_with_policy(profile_, dims_, options_.policy);
 }
 
+const Schedule& DynamicScheduler::best_schedule() const {
+  if (!(best_measured_ > 0.0)) return schedule_;
+  bool same = best_.devices.size() == schedule_.devices.size();
+  for (std::size_t i = 0; same && i < best_.devices.size(); ++i)
+    same = best_.devices[i].id == schedule_.devices[i].id &&
+           best_.devices[i].rows == schedule_.devices[i].rows;
+  return same ? schedule_ : best_;
+}
+
 bool DynamicScheduler::observe(const SimulationResult& result) {
   const double t = result.measured_makespan;
   if (t > 0.0 && std::isfinite(t) && (best_measured_ <= 0.0 || t < best_measured_)) {
