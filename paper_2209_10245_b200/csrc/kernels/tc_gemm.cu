@@ -545,7 +545,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
   int* tile_ring = reinterpret_cast<int*>(tile_empty + kTileSlots);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
 
-  static_assert(PAIRS == 1 || (PAIRS == 2 && W == 512), "B-sharing clusters use 512-wide tiles");
+  static_assert(PAIRS == 1 || PAIRS == 2, "one or two CTA pairs per cluster");
   constexpr int kCtas = 2 * PAIRS;
   constexpr int kRowsT = 256 * PAIRS;  // rows of a (cluster) tile
   const int warp = threadIdx.x >> 5;
@@ -658,8 +658,8 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < W / 128; ++j) {  // 64-column chunks: half j/2, chunk j%2
             const int cj = col0 + (j >> 1) * 256 + (j & 1) * 64;
-            if constexpr (PAIRS == 2) {  // my pair's half, to me and my twin in the other pair
-              if ((j >> 1) != pair) continue;
+            if constexpr (PAIRS == 2) {  // my pair's share of the chunks, to me and my twin
+              if (j / (W / 256) != pair) continue;
               const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2u)));
               if (args.panels > 1)
                 tma_load_3d_pair_mc(sb + j * kBChunkBytes, &map_b, &full[stage], cj, kc, pnl, mask,
@@ -1279,7 +1279,7 @@ namespace {
 // 1024^3: 16 tiles for 74 pairs) the single-SM kernel with 128 x 128 tiles
 // spreads the work over 4x as many CTAs. POAS_TC_KERNEL = 2cta512 | 2cta |
 // 1cta (128 x 256) | 1cta128 overrides.
-enum class TcVariant { pair512x2, pair512, pair, single256, single128 };
+enum class TcVariant { pair512x2, pair256x2, pair512, pair, single256, single128 };
 
 TcVariant choose_variant(int64_t M, int64_t N, int64_t K, int budget) {
   if (const char* v = std::getenv("POAS_TC_KERNEL")) {
@@ -1289,6 +1289,7 @@ TcVariant choose_variant(int64_t M, int64_t N, int64_t K, int budget) {
     if (s == "2cta") return TcVariant::pair;
     if (s == "2cta512") return TcVariant::pair512;
     if (s == "2cta512x2") return TcVariant::pair512x2;
+    if (s == "2cta256x2") return TcVariant::pair256x2;
   }
   // Single-SM 128 x 128 tiles only when the pairs would be mostly idle (at
   // most a quarter busy): measured (profiles/r01_small_variants) 1024^3
@@ -1308,6 +1309,7 @@ const char* variant_name(TcVariant v) {
     case TcVariant::single128: return "tc_gemm_kernel_n128";
     case TcVariant::pair512: return "tc_gemm_2cta_kernel<512>";
     case TcVariant::pair512x2: return "tc_gemm_2cta_kernel<512,2>";
+    case TcVariant::pair256x2: return "tc_gemm_2cta_kernel<256,2>";
     case TcVariant::pair: break;
   }
   return "tc_gemm_2cta_kernel<256>";
@@ -1445,6 +1447,10 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Pair<512>::kSmem));
     if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<256, 2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Pair<256>::kSmem));
+    if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<512, 2>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Pair<512>::kSmem));
@@ -1461,14 +1467,15 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     // tables are in 256 x 256 tiles, panels take 512-wide tiles when every
     // panel is a whole number of them
     const char* v = std::getenv("POAS_TC_KERNEL");
-    if (v && std::string(v) != "2cta" && std::string(v) != "2cta512" && std::string(v) != "2cta512x2")
+    if (v && std::string(v) != "2cta" && std::string(v) != "2cta512" && std::string(v) != "2cta512x2" &&
+        std::string(v) != "2cta256x2")
       return cudaErrorNotSupported;
     const bool wide = (variant == TcVariant::pair512 || variant == TcVariant::pair512x2) && !ss &&
                       np % 512 == 0;
-    variant = wide ? variant : TcVariant::pair;
+    if (!wide) variant = variant == TcVariant::pair256x2 && !ss ? variant : TcVariant::pair;
   }
   const bool force_1cta = variant != TcVariant::pair && variant != TcVariant::pair512 &&
-                          variant != TcVariant::pair512x2;
+                          variant != TcVariant::pair512x2 && variant != TcVariant::pair256x2;
   const char* group_env = std::getenv("POAS_TC_GROUP");  // raster experiments
   const int group_override = group_env ? std::atoi(group_env) : 0;
 
@@ -1514,7 +1521,8 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.tma_store = 0;
   args.trace = nullptr;
   args.panels = P;
-  args.tiles_n_panel = static_cast<int>(np / (variant == TcVariant::pair ? 256 : 512));
+  args.tiles_n_panel = static_cast<int>(
+      np / (variant == TcVariant::pair512 || variant == TcVariant::pair512x2 ? 512 : 256));
   args.panel_flags = ps ? ps->flags : nullptr;
   args.panel_epoch = ps ? ps->epoch : 0;
   args.sblocks = nullptr;
@@ -1545,8 +1553,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     // aligned base and row pitch); POAS_TC_EPILOGUE=direct forces the
     // register -> global path.
     // clusters of two pairs need a budget of at least one cluster
-    const bool x2 = variant == TcVariant::pair512x2 && std::min(budget / 4, max_active_clusters_x2()) >= 1;
-    const bool wide = x2 || variant == TcVariant::pair512;
+    const bool x2 = (variant == TcVariant::pair512x2 || variant == TcVariant::pair256x2) &&
+                    std::min(budget / 4, max_active_clusters_x2()) >= 1;
+    const bool wide = variant == TcVariant::pair512x2 || variant == TcVariant::pair512;
     const int w = wide ? 512 : 256;
     const int rows_t = x2 ? 512 : 256;
     args.tiles_m = static_cast<int>((M + rows_t - 1) / rows_t);
@@ -1581,9 +1590,10 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       args.trace = trace_buf;
     }
     const cudaError_t e =
-        x2     ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
-        : wide ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
-               : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kSmem, stream, 1, ma, mb, mc, args);
+        x2 && wide ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
+        : x2       ? launch_pdl(tc_gemm_2cta_kernel<256, 2>, 2 * pairs, Pair<256>::kSmem, stream, 1, ma, mb, mc, args)
+        : wide     ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
+                   : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kSmem, stream, 1, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return e;
   }

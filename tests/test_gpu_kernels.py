@@ -205,7 +205,7 @@ def test_full_size_tc_property(torch_cuda, poas):
     assert rel <= 1.5 * rel_cublas + 1e-6, (rel, rel_cublas)
 
 
-@pytest.mark.parametrize("variant", ["1cta", "2cta", "2cta512", "2cta512x2"])
+@pytest.mark.parametrize("variant", ["1cta", "2cta", "2cta512", "2cta512x2", "2cta256x2"])
 def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
     """POAS_TC_KSERP=0: every tile sweeps K forwards (the default alternates
     the direction per wave of tiles); both orders agree with the oracle and
@@ -233,7 +233,7 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 # (variant, epilogue): the single-SM kernels have one epilogue
 _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct"),
                 ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512", "direct8"), ("2cta512x2", "tma"),
-                ("2cta512x2", "direct")]
+                ("2cta512x2", "direct"), ("2cta256x2", "tma"), ("2cta256x2", "direct")]
 
 
 @pytest.mark.parametrize("sched", ["dynamic", "static", "wave"])
@@ -355,7 +355,7 @@ def _panel_major(torch, B16, panels):
     return torch.stack([B16[:, p * np_:(p + 1) * np_] for p in range(panels)]).contiguous()
 
 
-@pytest.mark.parametrize("variant", [None, "2cta512", "2cta512x2"])
+@pytest.mark.parametrize("variant", [None, "2cta512", "2cta512x2", "2cta256x2"])
 @pytest.mark.parametrize("panels", [2, 4])
 @pytest.mark.parametrize("shape", [(1000, 1024, 320), (300, 2048, 136)])
 def test_tc_gemm_panels(torch_cuda, poas, monkeypatch, shape, panels, variant):
@@ -388,7 +388,7 @@ def test_tc_gemm_panels(torch_cuda, poas, monkeypatch, shape, panels, variant):
         poas.tc_gemm_panels(2, m, 768, k, a.data_ptr(), k, bp.data_ptr(), 384, c.data_ptr(), n, 2)
 
 
-@pytest.mark.parametrize("variant", ["2cta", "2cta512", "2cta512x2"])
+@pytest.mark.parametrize("variant", ["2cta", "2cta512", "2cta512x2", "2cta256x2"])
 def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas, monkeypatch, variant):
     """The fused consumer: the GEMM is queued first with every flag clear;
     another stream delivers the panels later (a ~spin, then one flag per
@@ -453,6 +453,8 @@ def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<512>"
     monkeypatch.setenv("POAS_TC_KERNEL", "2cta512x2")
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<512,2>"
+    monkeypatch.setenv("POAS_TC_KERNEL", "2cta256x2")
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<256,2>"
 
 
 @pytest.mark.parametrize("variant", ["2cta512", "2cta512x2", "2cta512:direct8"])
