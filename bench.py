@@ -557,6 +557,25 @@ def main():
         link_bw = b_bytes / comm.time_broadcast(b_bytes, transport, 3)
     if save and rank == 0:
         (save / "profile_resident.txt").write_text(profile)
+    # The Optimize stage's SM-partition decision (B200 extension,
+    # poas_b200_plan_partitions): the CUDA-core unit's budget among
+    # candidates, from this profile scaled by SM counts. Budget 0 = the unit
+    # left out and its SMs lent to the tensor unit, which is what the
+    # executor does whenever the plan gives the unit no rows.
+    sm_partition = None
+    try:
+        cand = [0, 2, 4, 8, 16, 32]
+        pp = poas.plan_partitions(profile, m_total // world, n, k, tc_id, args.tc_sms, simt_id,
+                                  args.simt_sms, cand, args.policy)
+        sm_partition = {"candidates": [{"simt_sms": c["simt_sms"], "tc_sms": c["tc_sms"],
+                                        "predicted_ms": round(c["makespan"] * 1e3, 4), "rows": c["rows"]}
+                                       for c in pp["candidates"]],
+                        "chosen_simt_sms": pp["candidates"][pp["best"]]["simt_sms"],
+                        "model": "each GPU unit's compute slope scaled inversely with its SM count, the "
+                                 "CUDA-core unit's resident-operand bandwidth with its SM count; planned "
+                                 f"with policy {args.policy}"}
+    except Exception as exc:  # reported, never fatal
+        sm_partition = {"error": f"{type(exc).__name__}: {exc}"}
     sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
 
     def resident_run(label, m_all, n, k, steps, panels_req, adapt=True, full=True):
@@ -1091,6 +1110,7 @@ def main():
                 "level1_link_gbs": round(link_bw / 1e9, 2) if link_bw else None,
                 "b_panels": P,
                 "c4": c4,
+                "sm_partition": sm_partition,
                 "sweep": sweep,
             },
             # the tensor kernel is timed inside a long back-to-back run under

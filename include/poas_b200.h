@@ -76,6 +76,20 @@ int poas_b200_plan(const char* profile_text, int64_t m, int64_t n, int64_t k,
 int poas_b200_plan_policy(const char* profile_text, int64_t m, int64_t n, int64_t k,
                           const char* policy, char** schedule_json);
 
+/* SM partition of one GPU between its tensor unit and its CUDA-core unit,
+ * chosen by the planner (B200 extension; no reference counterpart: the
+ * reference's units are fixed devices). The profile describes the units at
+ * their measured budgets tc_sms / simt_sms; each candidate CUDA-core budget
+ * (simt_budgets[i], 0 = unit left out and its SMs lent to the tensor unit)
+ * scales the units' compute slopes inversely with their SM counts and the
+ * CUDA-core unit's resident-operand bandwidth with its budget, and is
+ * planned with `policy`. *out_json: {"best": index, "candidates": [{"simt_sms",
+ * "tc_sms", "makespan", "rows": {id: rows}}]}; free with poas_b200_free. */
+int poas_b200_plan_partitions(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                              const char* tc_id, int tc_sms, const char* simt_id, int simt_sms,
+                              const int* simt_budgets, int count, const char* policy,
+                              char** out_json);
+
 /* standalone_schedule (proj/include/poas/scheduler.hpp:40-41). */
 int poas_b200_plan_standalone(const char* profile_text, const char* device_id, int64_t m,
                               int64_t n, int64_t k, char** schedule_json);

@@ -98,4 +98,47 @@ Schedule plan_with_policy(const MachineProfile& machine, const MatrixDims& dims,
   fail(errc::invalid_argument, "unknown planner policy '" + policy + "'");
 }
 
+PartitionChoice plan_sm_partitions(const MachineProfile& machine, const MatrixDims& dims,
+                                   const std::string& tc_id, int tc_sms, const std::string& simt_id,
+                                   int simt_sms, const std::vector<int>& simt_budgets,
+                                   const std::string& policy) {
+  validate_machine(machine);
+  const DeviceProfile* tc = machine.find(tc_id);
+  const DeviceProfile* simt = machine.find(simt_id);
+  if (!tc || !simt) fail(errc::invalid_argument, "partition: unknown unit id");
+  if (tc_sms < 1 || simt_sms < 1) fail(errc::invalid_argument, "partition: SM budgets must be >= 1");
+  if (simt_budgets.empty()) fail(errc::invalid_argument, "partition: no candidate budgets");
+  const int total = tc_sms + simt_sms;
+  PartitionChoice out;
+  for (const int s : simt_budgets) {
+    if (s < 0 || s >= total) fail(errc::invalid_argument, "partition: candidate budget out of range");
+    MachineProfile m;
+    m.bus = machine.bus;
+    for (const DeviceProfile& d : machine.devices) {
+      if (d.id == simt_id) {
+        if (s == 0) continue;  // left out: its SMs go to the tensor unit
+        DeviceProfile x = d;
+        x.compute.slope *= static_cast<double>(simt_sms) / s;
+        if (x.bandwidth > 0.0) x.bandwidth *= static_cast<double>(s) / simt_sms;
+        m.devices.push_back(x);
+      } else if (d.id == tc_id) {
+        DeviceProfile x = d;
+        x.compute.slope *= static_cast<double>(tc_sms) / (total - s);
+        m.devices.push_back(x);
+      } else {
+        m.devices.push_back(d);
+      }
+    }
+    PartitionCandidate c;
+    c.simt_sms = s;
+    c.tc_sms = total - s;
+    c.schedule = plan_with_policy(m, dims, policy);
+    const double best = out.candidates.empty() ? 0.0 : out.candidates[out.best].schedule.makespan;
+    out.candidates.push_back(std::move(c));
+    if (out.candidates.size() == 1 || out.candidates.back().schedule.makespan < best)
+      out.best = out.candidates.size() - 1;
+  }
+  return out;
+}
+
 }  // namespace poas

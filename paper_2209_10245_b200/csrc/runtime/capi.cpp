@@ -212,6 +212,34 @@ int poas_b200_plan_policy(const char* profile_text, int64_t m, int64_t n, int64_
   });
 }
 
+int poas_b200_plan_partitions(const char* profile_text, int64_t m, int64_t n, int64_t k,
+                              const char* tc_id, int tc_sms, const char* simt_id, int simt_sms,
+                              const int* simt_budgets, int count, const char* policy,
+                              char** out_json) {
+  return guard([&] {
+    need_ptr(out_json, "out_json");
+    if (count < 1 || !simt_budgets) raise(POAS_E_INVALID_ARGUMENT, "no candidate budgets");
+    const poas::MachineProfile machine = poas::parse_profile(need_str(profile_text, "profile"));
+    const std::vector<int> budgets(simt_budgets, simt_budgets + count);
+    const poas::PartitionChoice c = poas::plan_sm_partitions(
+        machine, dims_of(m, n, k), need_str(tc_id, "tc_id"), tc_sms, need_str(simt_id, "simt_id"),
+        simt_sms, budgets, policy ? policy : "");
+    std::string o = "{\"best\": " + std::to_string(c.best) + ", \"candidates\": [";
+    for (std::size_t i = 0; i < c.candidates.size(); ++i) {
+      const poas::PartitionCandidate& x = c.candidates[i];
+      o += std::string(i ? ", " : "") + "{\"simt_sms\": " + std::to_string(x.simt_sms) +
+           ", \"tc_sms\": " + std::to_string(x.tc_sms) + ", \"makespan\": " + g17(x.schedule.makespan) +
+           ", \"rows\": {";
+      for (std::size_t j = 0; j < x.schedule.devices.size(); ++j)
+        o += std::string(j ? ", " : "") + "\"" + json_escape(x.schedule.devices[j].id) +
+             "\": " + std::to_string(x.schedule.devices[j].rows);
+      o += "}}";
+    }
+    o += "]}";
+    *out_json = dup_string(o);
+  });
+}
+
 int poas_b200_plan_standalone(const char* profile_text, const char* device_id, int64_t m,
                               int64_t n, int64_t k, char** schedule_json) {
   return guard([&] {

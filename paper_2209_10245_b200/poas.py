@@ -39,6 +39,16 @@ def plan_policy(profile: str, m: int, n: int, k: int, policy: str = "reference")
     return call_str(lib.poas_b200_plan_policy, _b(profile), m, n, k, _b(policy))
 
 
+def plan_partitions(profile: str, m: int, n: int, k: int, tc_id: str, tc_sms: int, simt_id: str,
+                    simt_sms: int, simt_budgets, policy: str = "best-subset") -> dict:
+    """The planner's choice of one GPU's SM partition between its tensor and
+    CUDA-core units (poas_b200_plan_partitions; B200 extension):
+    {"best": i, "candidates": [{"simt_sms", "tc_sms", "makespan", "rows"}]}."""
+    arr = (C.c_int * len(simt_budgets))(*[int(x) for x in simt_budgets])
+    return json.loads(call_str(lib.poas_b200_plan_partitions, _b(profile), m, n, k, _b(tc_id), int(tc_sms),
+                               _b(simt_id), int(simt_sms), arr, len(simt_budgets), _b(policy)))
+
+
 def refit_profile(profile: str, report: str | dict, alpha: float = 0.5) -> str:
     """Dynamic-scheduling model update (paper §3.4.2; B200 extension): the
     profile re-fitted from one execution report (Executor.execute's dict or
