@@ -78,6 +78,31 @@ def test_tc_full_size_sampled_rows(torch_cuda, poas, m, n, k):
     _check_rows(torch, C, a, b, oracle.sampled_rows(m), sa, sb, n, k, label)
 
 
+def test_c2_fp16_tensor_full_size_sampled_rows(torch_cuda, poas):
+    """C2's tensor share: fp16 operands at 8192^3 on the default (256 x 512
+    pair-tile) kernel, sampled rows vs the oracle in fp16 rounding."""
+    import oracle
+
+    torch = torch_cuda
+    n = k = m = 8192
+    sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
+    a32 = torch.empty(m, k, device="cuda")
+    b32 = torch.empty(k, n, device="cuda")
+    poas.fill_uniform(poas.DTYPE_F32, a32.data_ptr(), k, m, k, 0, 0, k, sa)
+    poas.fill_uniform(poas.DTYPE_F32, b32.data_ptr(), n, k, n, 0, 0, n, sb)
+    a, b = a32.half(), b32.half()
+    C = torch.full((m, n), float("nan"), device="cuda")
+    poas.tc_gemm(poas.DTYPE_F16, m, n, k, a.data_ptr(), k, b.data_ptr(), n, C.data_ptr(), n)
+    torch.cuda.synchronize()
+    rows = oracle.sampled_rows(m)
+    ref = oracle.full_size_rows_f64(rows, n, k, sa, sb, 1)
+    got = C.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    err = oracle.rel_frobenius(got, ref)
+    print(f"8192^3 fp16 {poas.tc_kernel_name(m, n, k)}: sampled-row rel err {err:.3e}")
+    assert poas.tc_kernel_name(m, n, k) == "tc_gemm_2cta_kernel<512>"
+    assert np.isfinite(got).all() and err <= tol_for(k), err
+
+
 def test_c3_poas_plan_full_size_sampled_rows(torch_cuda, poas):
     """C3 through the product path the bench times: profile the bench's two
     units, plan (best-subset), execute with resident operands; every sampled

@@ -69,12 +69,17 @@ TC_SHAPES = [(128, 256, 64), (1000, 1000, 1000), (129, 300, 72), (64, 4096, 512)
              (1, 1, 8), (7, 1000, 24), (255, 257, 136), (2048, 2048, 2048), (333, 1536, 4104)]
 
 
+@pytest.mark.parametrize("variant", [None, "2cta512"])
 @pytest.mark.parametrize("shape", TC_SHAPES)
 @pytest.mark.parametrize("dtype,mode", [(2, 2), (1, 1)])
-def test_tc_gemm_vs_oracle(torch_cuda, poas, shape, dtype, mode):
+def test_tc_gemm_vs_oracle(torch_cuda, poas, monkeypatch, shape, dtype, mode, variant):
+    """bf16 and fp16 operands, every shape through the size-chosen kernel and
+    through the 256 x 512 pair tiles (tiny, ragged and long-K shapes)."""
     import oracle
 
     torch = torch_cuda
+    if variant:
+        monkeypatch.setenv("POAS_TC_KERNEL", variant)
     m, n, k = shape
     A = oracle.fill_uniform(m, k, 11)
     B = oracle.fill_uniform(k, n, 12)
