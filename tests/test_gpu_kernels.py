@@ -93,7 +93,15 @@ def test_tc_gemm_vs_oracle(torch_cuda, poas, monkeypatch, shape, dtype, mode, va
     poas.tc_gemm(dtype, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), n)
     torch.cuda.synchronize()
     ref = oracle.gemm_rows_f64(A, B, mode)
-    assert oracle.rel_frobenius(c.cpu().numpy(), ref) <= TOL
+    got = c.cpu().numpy()
+    assert oracle.rel_frobenius(got, ref) <= TOL
+    # against the UNROUNDED fp32 inputs: the operand
+    # rounding dominates -- bf16 <= 8e-3, fp16 <= 2e-3; a statistical bound
+    # (rounding errors average over K), so only from K >= 64 (at K = 8 one
+    # 1x1 output can sit at 1.4e-2 for bf16)
+    if k >= 64:
+        exact = oracle.gemm_rows_f64(A, B, 0)
+        assert oracle.rel_frobenius(got, exact) <= (8e-3 if dtype == 2 else 2e-3)
 
 
 @pytest.mark.parametrize("ctas", [1, 2, 7, 146])
