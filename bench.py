@@ -314,7 +314,7 @@ def host_unit_baseline(poas, n: int) -> dict:
     out = {"cores": os.cpu_count()}
     # C1: the POAS pipeline on the host cores only
     units = "cpu0=cpu:threads=0"
-    prof = poas.profile_machine(units, "probes=5,repetitions=2,cpu_min_side=1000,cpu_max_side=2000", bus=True)
+    prof = poas.profile_machine(units, "probes=5,repetitions=2,cpu_min_side=1000,cpu_max_side=2000", bus=True, retries=2)
     c1 = 2048
     sched = poas.plan(prof, c1, c1, c1)
     sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
@@ -547,7 +547,7 @@ def main():
         # they see burst clocks the sustained run never gets).
         if args.probe_warmup > 0:
             warm_sustained(poas, torch, dev, args.probe_warmup)
-        profile = poas.profile_machine(units_res, PROFILING, bus=True)
+        profile = poas.profile_machine(units_res, PROFILING, bus=True, retries=2)
     t_prof = time.perf_counter() - t0
     link_bw = None
     if comm:
@@ -905,7 +905,7 @@ def main():
             policy = "overlap" if overlap else args.policy
             if tc_elem not in e2e_profiles:  # same units either way: probe once
                 e2e_profiles[tc_elem] = poas.profile_machine(
-                    units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048", bus=True)
+                    units_e2e, PROFILING + ",cpu_min_side=1024,cpu_max_side=2048", bus=True, retries=2)
             prof_e2e = e2e_profiles[tc_elem]
             ref_e2e = json.loads(poas.plan(prof_e2e, m, n, k))
             ex_e2e = poas.Executor(units_e2e + (";overlap=1" if overlap else "")
@@ -1013,8 +1013,15 @@ def main():
             tfl, sec, sample, cores = reference_cpu_path(args.n, sample_rows=args.ref_rows, reps=1)
             cpu_baseline = {"value": round(tfl, 4), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                             "sample": sample, "cpu_model": cpu_model()}
-            cpu_baseline["host_unit"] = host_unit_baseline(poas, args.n)
-            cpu_baseline["reference_planner"] = reference_planner_cost(profile, m, n, k)
+            # each extra reported on its own: a noisy host probe fit (the
+            # reference's fit_linear rejects a non-positive slope) must not
+            # take the reference CPU path's number with it
+            for key, fn in (("host_unit", lambda: host_unit_baseline(poas, args.n)),
+                            ("reference_planner", lambda: reference_planner_cost(profile, m, n, k))):
+                try:
+                    cpu_baseline[key] = fn()
+                except Exception as exc:
+                    cpu_baseline[key] = {"error": f"{type(exc).__name__}: {exc}"}
         except Exception as exc:  # reported, never fatal
             cpu_baseline = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                             "sample": f"unavailable: {exc}"}

@@ -169,10 +169,19 @@ class Unit:
     __del__ = close
 
 
-def profile_machine(units: str, profiling: str = "", bus: bool = True) -> str:
+def profile_machine(units: str, profiling: str = "", bus: bool = True, retries: int = 0) -> str:
     """profile_machine over real units -> "poas-profile v1" text
-    (reference proj/src/simulator.cpp:53-74 + proj/src/profiler.cpp:75-135)."""
-    return call_str(lib.poas_b200_profile_machine, _b(units), _b(profiling), int(bus))
+    (reference proj/src/simulator.cpp:53-74 + proj/src/profiler.cpp:75-135).
+    `retries`: re-measure up to that many times when the reference's
+    fit_linear rejects the samples (a non-positive slope: host-CPU probes
+    of small sides on a busy host); the fit itself is unchanged."""
+    for attempt in range(retries + 1):
+        try:
+            return call_str(lib.poas_b200_profile_machine, _b(units), _b(profiling), int(bus))
+        except PoasError as e:
+            if e.errc != "degenerate_samples" or attempt == retries:
+                raise
+    raise AssertionError("unreachable")
 
 
 GEMM_CB = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_int64)

@@ -123,7 +123,7 @@ def c5(sizes, preroll_ms=20, steps=10):
         d = operands(n)
         io = io_for(n, d)
         warm(0.5)
-        profile = poas.profile_machine(units, PROF, True)
+        profile = poas.profile_machine(units, PROF, True, retries=2)
         ex = poas.Executor(units)
         # timed runs last >= ~0.25 s back to back (the sustained regime the
         # pre-rolled probes were taken in; a 1 ms burst runs at boost clock)
@@ -196,7 +196,7 @@ def c2(n=8192):
     units = (f"cpu0=cpu:threads={threads};"
              "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048;"
              "gpu0.tc=xpu:dev=0:sms=146:dtype=f16:elem=2:link=hbm:probe=4096-8192")
-    profile = poas.profile_machine(units, PROF + ",cpu_min_side=512,cpu_max_side=1536", True)
+    profile = poas.profile_machine(units, PROF + ",cpu_min_side=512,cpu_max_side=1536", True, retries=2)
     d = operands(n, with_host=True)
     # fp16 operands for the fp16 tensor unit
     d["A16"] = d["A32"].half().view(torch.bfloat16)
