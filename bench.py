@@ -74,6 +74,14 @@ def measured_peaks():
     return 1590.0, 1400.0, "fallback"  # B200_PROFILING.md: 1.59 burst, ~1.4 sustained
 
 
+def hbm_peak():
+    """Measured HBM copy bandwidth (GB/s, MEASURED_PEAKS.json) or None."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clock + clock-event (throttle) reasons DURING the timed region.
 
@@ -1055,7 +1063,11 @@ def main():
                        "static_error_pct": round(c2["static_plan"]["makespan_error_pct"], 3),
                        "makespan_error_pct": round(c2["makespan_error_pct"], 3),
                        "units": "host CPU (AVX-512) + fp32 CUDA cores (2 SMs) + fp16 tensor cores (146 SMs)"},
-                "simt_vs_cublas_fp32": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in sv.items()},
+                "simt_vs_cublas_fp32": dict(
+                    {k: (round(v, 3) if isinstance(v, float) else v) for k, v in sv.items()},
+                    # FP32 pipe: 148 SMs x 128 lanes x 2 flop x 1965 MHz
+                    fp32_peak_tflops=round(148 * 128 * 2 * 1.965e9 / 1e12, 1),
+                    frac_of_fp32_peak=round(sv["simt_all_sms_tflops"] / (148 * 128 * 2 * 1.965e9 / 1e12), 3)),
                 "seconds": round(time.perf_counter() - t_sw, 1)}
         except Exception as exc:  # reported, never fatal
             sweep = {"error": f"{type(exc).__name__}: {exc}"}
@@ -1135,7 +1147,13 @@ def main():
                          "peak": peak_sust or peak_burst, "unit": "TFLOP/s",
                          "frac": round(achieved / (peak_sust or peak_burst), 4),
                          "peak_burst": peak_burst, "frac_burst": round(achieved / peak_burst, 4),
-                         "traffic": traffic, "kernel": f"{poas.tc_kernel_name(tc_rows, n, k)} "
+                         "traffic": traffic,
+                         # the ncu DRAM bytes per launch over this run's
+                         # launch time: the kernel's achieved HBM bandwidth
+                         "hbm_achieved_gbs": (round(traffic / tc_compute / 1e9, 1)
+                                              if traffic and tc_compute > 0 else None),
+                         "hbm_peak_gbs": hbm_peak(),
+                         "kernel": f"{poas.tc_kernel_name(tc_rows, n, k)} "
                                    f"({poas.tc_scheduler_name(tc_rows, n, k)} tile scheduler)",
                          "peak_kind": (f"of {peak_kind}: bf16 sustained (cuBLAS seconds-long loop under the "
                                        f"power cap), the kernel being timed inside {args.steps} back-to-back "
