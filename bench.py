@@ -1074,8 +1074,14 @@ def main():
 
     # per step: one GEMM launch per busy unit (the tensor unit consumes all
     # B panels in one launch; a CUDA-core unit launches once per panel),
-    # plus the executor's start-gate kernel on this GPU
-    launches_per_step = sum((1 if d["id"] == tc_id else P) for d in sched["devices"] if d["rows"] > 0) + 1
+    # plus the executor's start-gate kernel on this GPU -- except when the
+    # executor replays the steps as one CUDA graph (resident operands, one
+    # busy GPU unit, one panel, no communicator, <= 256 repeats: executor.cpp
+    # graph_mode), which has no gate
+    busy = [d for d in sched["devices"] if d["rows"] > 0]
+    graph_replay = (world == 1 and P <= 1 and len(busy) == 1 and args.steps <= 256
+                    and os.environ.get("POAS_EXEC_GRAPH") != "0")
+    launches_per_step = sum((1 if d["id"] == tc_id else P) for d in busy) + (0 if graph_replay else 1)
     meas_make, pred_job, pred_adapt = main_res["meas_job"], main_res["pred_job"], main_res["pred_adapt_job"]
     static_same = main_res["static_same"]
     if rank == 0:
