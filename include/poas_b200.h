@@ -312,7 +312,10 @@ int poas_b200_refit_profile(const char* profile_text, const char* report_json, d
  * |makespan error| > replan_threshold_pct, repeat. out_json:
  * {"iterations": [{iteration, replanned, rows{id: n}, predicted_makespan,
  * measured_makespan, makespan_error_pct}], "replans", "profile" (final,
- * poas-profile v1 text), "schedule" (final)}. */
+ * poas-profile v1 text), "best_iteration", "last_schedule" (the last
+ * re-plan, possibly never executed), "schedule" (the plan to run next: the
+ * fastest MEASURED one -- or the last plan when it splits the rows the same
+ * way, for its fresher prediction)}. */
 int poas_b200_run_dynamic(poas_executor_t ex, const char* profile_text, int64_t m, int64_t n,
                           int64_t k, const char* policy, const poas_gemm_io* io, int iterations,
                           int repeats, double alpha, double replan_threshold_pct,
