@@ -59,7 +59,6 @@ struct TcArgs {
   int tma_store;         // pair kernel: 1 = epilogue through smem + TMA store (map_c)
   unsigned long long* trace;  // dev: per-CTA %globaltimer stamps (POAS_TC_TRACE), or null
   int epi_skip;               // dev (POAS_TC_EPI_SKIP): TMA-store epilogue stages boxes, stores nothing
-  int direct8;                // 256 x 512 tiles: epilogue by 32-byte register stores (no smem staging)
   // Panel-major B (pair kernel): `panels` column panels of tiles_n_panel
   // N-tiles each, B loaded through a 3-D map {column, k, panel}; tiles are
   // ordered panel by panel. With panel_flags, a producer starts on panel p
@@ -835,77 +834,6 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
         epi_traced = true;
       }
       const int row_base = mb * kRowsT + pair * 256 + static_cast<int>(prank) * 128 + quad * 32;
-      if (W == 512 && args.direct8) {
-        // 256 x 512 tiles, C 32-byte aligned with a pitch of whole 32-byte
-        // sectors: TMEM -> registers -> 256-bit st.global (each lane one
-        // full sector of its row), no staging, no proxy fence, no waits on
-        // store completion, so a half of the accumulator is free as soon as
-        // TMEM has been read. Masked rows / a ragged last sector fall back
-        // to scalar stores.
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-        const int row = row_base + lane;
-        float* crow = args.C + static_cast<long long>(row) * args.ldc;
-        auto put = [&](const uint32_t* w, int c) {  // columns [c*64, c*64+64)
-          if (row >= args.M) return;
-          const int col0 = nb * W + c * 64;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int col = col0 + q * 8;
-            if (col + 8 <= args.N) {
-              float o[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(w[q * 8 + e]);
-              if (args.accumulate) {
-                float p[8];
-                asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=f"(p[0]), "=f"(p[1]), "=f"(p[2]), "=f"(p[3]), "=f"(p[4]),
-                               "=f"(p[5]), "=f"(p[6]), "=f"(p[7])
-                             : "l"(crow + col));
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[e] += p[e];
-              }
-              asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + col),
-                           "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3]), "f"(o[4]), "f"(o[5]),
-                           "f"(o[6]), "f"(o[7])
-                           : "memory");
-            } else {
-              for (int e = 0; e < 8 && col + e < args.N; ++e) {
-                float o = __uint_as_float(w[q * 8 + e]);
-                if (args.accumulate) o += crow[col + e];
-                crow[col + e] = o;
-              }
-            }
-          }
-        };
-        uint32_t va[64], vb[64];
-        auto load64 = [&](uint32_t (&v)[64], int c) {
-          tmem_ld_32x32b_x32(taddr + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-          tmem_ld_32x32b_x32(taddr + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        };
-        load64(va, 0);
-        tmem_wait_ld();
-#pragma unroll 1
-        for (int c = 0; c < W / 64; c += 2) {
-          load64(vb, c + 1);
-          put(va, c);
-          tmem_wait_ld();
-          if ((c + 2) % 4 == 0) {  // a 256-column half is in registers: free it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&acc_empty[(c + 2) / 4 - 1], pair_leader);
-            if (args.trace && quad == 0 && lane == 0)
-              trace_add(args, (c + 2) == 4 ? 12 : 13, gtimer() - te0);
-          }
-          if (c + 2 < W / 64) load64(va, c + 2);
-          put(vb, c + 1);
-          tmem_wait_ld();
-        }
-        if (args.sblocks) {  // (streamed operands never use 512-wide tiles)
-          __trap();
-        }
-        if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
-        continue;
-      }
       if (args.tma_store) {
         if constexpr (W == 256) {
           // 256 x 256 tiles (the accumulator is double buffered, so the
@@ -1540,7 +1468,6 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     args.stream_epoch = ss->epoch;
   }
   args.epi_skip = std::getenv("POAS_TC_EPI_SKIP") != nullptr;
-  args.direct8 = 0;
   args.wave_sync = sched == "wave";
   if (sched != "static") {
     args.tile_counter = next_tile_counter(stream);
@@ -1566,10 +1493,6 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     args.tma_store = !direct && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 &&
                      make_map_c(&mc, C, M, N, ldc, wide);
     if (!args.tma_store) mc = ma;  // unused
-    // 256 x 512 tiles: 256-bit register stores when C allows them
-    // (POAS_TC_EPILOGUE=direct8)
-    args.direct8 = wide && epi && std::string(epi) == "direct8" &&
-                   (reinterpret_cast<uintptr_t>(C) & 31) == 0 && ldc % 8 == 0;
     args.idesc = idesc_f16(t == AbType::bf16, 256, 256, false, true);  // per 256-column half
     args.group = group_override > 0 ? group_override : (x2 ? kGroupM2 / 2 : kGroupM2);
     const int tiles = args.tiles_m * args.tiles_n;

@@ -245,7 +245,7 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 
 # (variant, epilogue): the single-SM kernels have one epilogue
 _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct"),
-                ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512", "direct8"), ("2cta512x2", "tma"),
+                ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512x2", "tma"),
                 ("2cta512x2", "direct"), ("2cta256x2", "tma"), ("2cta256x2", "direct")]
 
 
@@ -470,7 +470,7 @@ def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<256,2>"
 
 
-@pytest.mark.parametrize("variant", ["2cta512", "2cta512x2", "2cta512:direct8"])
+@pytest.mark.parametrize("variant", ["2cta512", "2cta512x2", "2cta512:direct"])
 @pytest.mark.parametrize("shape,ctas", [((2048, 4096, 2048), 4), ((1024, 2048, 64), 2),
                                         ((777, 1536, 4104), 8), ((4096, 1000, 192), 148),
                                         ((1300, 2560, 512), 12)])
