@@ -493,8 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int k2ABytes = 128 * kBK * 2;  // this CTA's 128 rows of A: 16 KB
 constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
 // Epilogue staging (TMA-store path), per epilogue warp: W = 256 two 32-row x
-// 16-column fp32 boxes with 64-byte swizzled rows (2 x 2 KB); W = 512 two
-// 32-row x 32-column boxes with 128-byte swizzled rows (2 x 4 KB).
+// 16-column fp32 boxes with 64-byte swizzled rows (2 x 2 KB); W = 512 one
+// 32-row x 32-column box with 128-byte swizzled rows (4 KB).
 
 template <int W>
 struct Pair {
@@ -503,7 +503,12 @@ struct Pair {
   static constexpr int kStages = W == 256 ? 6 : 4;
   static constexpr int kBBytes = (W / 2) * kBK * 2;  // this CTA's W/2 columns of B
   static constexpr int kStageBytes = k2ABytes + kBBytes;
-  static constexpr int kStagingBytes = 4 * 2 * (W == 256 ? 2048 : 4096);
+  // epilogue warps: 4 (one per TMEM lane quarter) for 256 x 256 tiles,
+  // whose drain hides behind the other accumulator; 8 (two per quarter,
+  // alternate 32-column chunks) for 256 x 512 tiles, whose drain is exposed
+  static constexpr int kEpiWarps = W == 512 ? 8 : 4;
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kStagingBytes = W == 256 ? 4 * 2 * 2048 : kEpiWarps * 4096;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 256;
   static_assert(kSmem <= 232448, "shared memory per CTA");
 };
@@ -520,7 +525,7 @@ struct Pair {
 // cluster-dimension attribute instead ran the 256 x 256 tiles 10-15% slower
 // (profiles/r02_sizes).
 template <int W, int PAIRS>
-__global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
@@ -570,13 +575,13 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 8);  // leader: 4 epilogue warps x 2 CTAs
+      mbar_init(&acc_empty[b], 2 * P::kEpiWarps);  // pair leader: the epilogue warps of both CTAs
     }
     for (int s = 0; s < kTileSlots; ++s) {
       mbar_init(&tile_full[s], 1);  // the cluster leader's producer (local or remote arrive)
-      // cluster leader: the pairs' MMA threads + the other producers + 4
-      // epilogue warps per CTA
-      mbar_init(&tile_empty[s], PAIRS + (kCtas - 1) + 4 * kCtas);
+      // cluster leader: the pairs' MMA threads + the other producers + the
+      // epilogue warps of every CTA
+      mbar_init(&tile_empty[s], PAIRS + (kCtas - 1) + P::kEpiWarps * kCtas);
     }
     fence_mbar_init();
   }
@@ -799,7 +804,8 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int quad = warp & 3;
+    const int quad = warp & 3;          // the TMEM lane quarter this warp may access
+    const int sub = (warp - 2) >> 2;    // W = 512: which of the quarter's two warps
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool vec = (args.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
@@ -829,7 +835,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const unsigned long long te0 = args.trace ? gtimer() : 0;
-      if (quad == 0 && lane == 0 && !epi_traced) {
+      if (quad == 0 && sub == 0 && lane == 0 && !epi_traced) {
         trace_stamp(args, 5);
         epi_traced = true;
       }
@@ -894,72 +900,60 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
             tmem_wait_ld();
           }
         } else {
-          // TMEM -> registers, 64 columns per step (two 32x32b.x32 loads, the
-          // next step's in flight while this one is written) -> two 32-row x
-          // 32-column staging boxes of this warp (128-byte rows, 128-byte
-          // swizzle: conflict-free, the TMA's layout) -> ONE proxy fence ->
-          // two TMA stores (or f32 add-reductions). The fence is the expensive
-          // part of a step, so a step covers 8 KB. Each 256-column half of
-          // the accumulator is released as soon as its last columns are in
-          // registers (TMEM reads, 64 B/clk/SM, are the floor of the drain).
-          uint8_t* slots = s_c + quad * 8192;
-          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                                 static_cast<uint32_t>(W == 256 ? acc * 256 : 0);
-          auto put = [&](const uint32_t* w, int c) {  // columns [c*64, c*64+64)
-            if (lane == 0) bulk_wait_read<0>();  // the previous step's stores have left smem
+          // Two warps per TMEM lane quarter, alternate 32-column chunks:
+          // TMEM -> registers (the warp's next chunk in flight while this
+          // one is written) -> this warp's 32-row x 32-column staging box
+          // (128-byte rows, 128-byte swizzle: conflict-free, the TMA's
+          // layout) -> proxy fence -> TMA store (or f32 add-reduction). Each
+          // 256-column half of the accumulator is released as soon as both
+          // warps of every quarter hold their last chunks of it: the drain
+          // is exposed once per wide tile, and twice the warps read TMEM and
+          // issue stores concurrently.
+          uint8_t* box = s_c + (warp - 2) * 4096;
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+          auto put = [&](const uint32_t* w, int c) {  // columns [c*32, c*32+32)
+            if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has left smem
             __syncwarp();
-  #pragma unroll
-            for (int bx = 0; bx < 2; ++bx) {
-              uint8_t* my_row = slots + bx * 4096 + lane * 128;
-  #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
-                    make_uint4(w[32 * bx + 4 * j], w[32 * bx + 4 * j + 1], w[32 * bx + 4 * j + 2],
-                               w[32 * bx + 4 * j + 3]);
-            }
+            uint8_t* my_row = box + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && !args.epi_skip) {
-  #pragma unroll
-              for (int bx = 0; bx < 2; ++bx) {
-                const int col0 = nb * W + c * 64 + bx * 32;
-                uint8_t* box = slots + bx * 4096;
-                if (args.accumulate)
-                  tma_reduce_add_2d(&map_c, box, col0, row_base);
-                else if (args.hint_c != kEvictNormal)
-                  tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
-                else
-                  tma_store_2d(&map_c, box, col0, row_base);
-              }
+              const int col0 = nb * W + c * 32;
+              if (args.accumulate)
+                tma_reduce_add_2d(&map_c, box, col0, row_base);
+              else if (args.hint_c != kEvictNormal)
+                tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
+              else
+                tma_store_2d(&map_c, box, col0, row_base);
               bulk_commit();
             }
           };
-          uint32_t va[64], vb[64];
-          auto load64 = [&](uint32_t (&v)[64], int c) {
-            tmem_ld_32x32b_x32(taddr + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-            tmem_ld_32x32b_x32(taddr + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-          };
-          load64(va, 0);
+          uint32_t va[32], vb[32];
+          tmem_ld_32x32b_x32(taddr + sub * 32, va);
           tmem_wait_ld();
-  #pragma unroll 1
-          for (int c = 0; c < W / 64; c += 2) {
-            load64(vb, c + 1);
-            put(va, c);
+#pragma unroll 1
+          for (int i = 0; i < 8; i += 2) {  // this warp's chunks sub + 2i (8 of 16)
+            const int ca = sub + 2 * i;
+            tmem_ld_32x32b_x32(taddr + (ca + 2) * 32, vb);
+            put(va, ca);
             tmem_wait_ld();
-            if ((c + 2) % 4 == 0) {  // a 256-column half is in registers: free it
+            if (i == 2 || i == 6) {  // this warp's last chunk of a half is in registers
               tc_fence_before();
               __syncwarp();
-              if (lane == 0)  // the leader's barrier
-                mbar_arrive_cluster(&acc_empty[W == 256 ? acc : (c + 2) / 4 - 1], pair_leader);
-              if (args.trace && quad == 0 && lane == 0)
-                trace_add(args, (c + 2) == 4 ? 12 : 13, gtimer() - te0);
+              if (lane == 0) mbar_arrive_cluster(&acc_empty[i == 2 ? 0 : 1], pair_leader);
+              if (args.trace && quad == 0 && sub == 0 && lane == 0)
+                trace_add(args, i == 2 ? 12 : 13, gtimer() - te0);
             }
-            if (c + 2 < W / 64) load64(va, c + 2);
-            put(vb, c + 1);
+            if (i + 2 < 8) tmem_ld_32x32b_x32(taddr + (ca + 4) * 32, va);
+            put(vb, ca + 2);
             tmem_wait_ld();
           }
         }
-        if (args.trace && quad == 0 && lane == 0) {
+        if (args.trace && quad == 0 && sub == 0 && lane == 0) {
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           args.trace[blockIdx.x * 16 + 6] = tt;
@@ -983,7 +977,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = row_base + lane;
       float* crow = args.C + static_cast<long long>(row) * args.ldc;
 #pragma unroll 1
-      for (int c = 0; c < W / 32; ++c) {
+      for (int c = sub; c < W / 32; c += P::kEpiWarps / 4) {  // this warp's 32-column chunks
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                static_cast<uint32_t>((W == 256 ? acc * 256 : 0) + c * 32),
@@ -1299,15 +1293,15 @@ namespace {
 // and prologue overlap the previous kernel of its stream. POAS_TC_PDL=0
 // launches plainly.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, size_t smem, cudaStream_t stream,
-                       int cluster, Args&&... args) {
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int threads, size_t smem,
+                       cudaStream_t stream, int cluster, Args&&... args) {
   static const bool pdl = [] {
     const char* e = std::getenv("POAS_TC_PDL");
     return !(e && std::string(e) == "0");
   }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -1513,10 +1507,14 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
       args.trace = trace_buf;
     }
     const cudaError_t e =
-        x2 && wide ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
-        : x2       ? launch_pdl(tc_gemm_2cta_kernel<256, 2>, 2 * pairs, Pair<256>::kSmem, stream, 1, ma, mb, mc, args)
-        : wide     ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kSmem, stream, 1, ma, mb, mc, args)
-                   : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kSmem, stream, 1, ma, mb, mc, args);
+        x2 && wide ? launch_pdl(tc_gemm_2cta_kernel<512, 2>, 2 * pairs, Pair<512>::kThreads, Pair<512>::kSmem,
+                                stream, 1, ma, mb, mc, args)
+        : x2       ? launch_pdl(tc_gemm_2cta_kernel<256, 2>, 2 * pairs, Pair<256>::kThreads, Pair<256>::kSmem,
+                                stream, 1, ma, mb, mc, args)
+        : wide     ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kThreads, Pair<512>::kSmem,
+                                stream, 1, ma, mb, mc, args)
+                   : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kThreads, Pair<256>::kSmem,
+                                stream, 1, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return e;
   }
@@ -1528,8 +1526,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
-  if (bn == 128) return launch_pdl(tc_gemm_kernel<128, 6>, grid, Tile1<128, 6>::kSmem, stream, 1, ma, mb, args);
-  return launch_pdl(tc_gemm_kernel<256, 4>, grid, Tile1<256, 4>::kSmem, stream, 1, ma, mb, args);
+  if (bn == 128)
+    return launch_pdl(tc_gemm_kernel<128, 6>, grid, kThreads, Tile1<128, 6>::kSmem, stream, 1, ma, mb, args);
+  return launch_pdl(tc_gemm_kernel<256, 4>, grid, kThreads, Tile1<256, 4>::kSmem, stream, 1, ma, mb, args);
 }
 }  // namespace
 
@@ -1545,7 +1544,7 @@ int max_active_clusters_x2() {
                            static_cast<int>(Pair<512>::kSmem)) == cudaSuccess) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(4 * 64);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(Pair<512>::kThreads);
     cfg.dynamicSmemBytes = Pair<512>::kSmem;
     cfg.numAttrs = 0;  // the cluster shape (4) is compiled into the kernel
     if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_2cta_kernel<512, 2>, &cfg) != cudaSuccess) n = 0;

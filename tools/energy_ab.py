@@ -16,7 +16,7 @@ import threading
 import time
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, os.environ.get("POAS_TREE", str(Path(__file__).resolve().parent.parent)))
 
 import pynvml  # noqa: E402
 import torch  # noqa: E402

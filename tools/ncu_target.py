@@ -5,10 +5,11 @@
     python tools/ncu_target.py micro            # CUDA-event timings, prints JSON
 """
 import json
+import os
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, os.environ.get("POAS_TREE", str(Path(__file__).resolve().parent.parent)))
 
 import torch  # noqa: E402
 
