@@ -194,8 +194,12 @@ def c5(sizes, preroll_ms=20, steps=10):
 def c2(n=8192):
     threads = max(1, (os.cpu_count() or 2) - 2)
     units = (f"cpu0=cpu:threads={threads};"
-             "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048;"
-             "gpu0.tc=xpu:dev=0:sms=146:dtype=f16:elem=2:link=hbm:probe=4096-8192")
+             "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=512-2048:preroll=20;"
+             "gpu0.tc=xpu:dev=0:sms=146:dtype=f16:elem=2:link=hbm:probe=6144-8192:preroll=20")
+    # pre-rolled probes over the top quarter of the sizes the tensor unit
+    # runs (as C5): a cold 8192^3 probe after an idle gap runs ~15% slower
+    # than the back-to-back steps it predicts
+    warm(0.5)
     profile = poas.profile_machine(units, PROF + ",cpu_min_side=512,cpu_max_side=1536", True, retries=2)
     d = operands(n, with_host=True)
     # fp16 operands for the fp16 tensor unit
