@@ -563,8 +563,6 @@ def main():
         # delivered to every rank by the transport the steps use
         b_bytes = k * n * 2
         link_bw = b_bytes / comm.time_broadcast(b_bytes, transport, 3)
-    if save and rank == 0:
-        (save / "profile_resident.txt").write_text(profile)
     # The Optimize stage's SM-partition decision (B200 extension,
     # poas_b200_plan_partitions): the CUDA-core unit's budget among
     # candidates, from this profile scaled by SM counts. Budget 0 = the unit
@@ -584,6 +582,23 @@ def main():
                                  f"with policy {args.policy}"}
     except Exception as exc:  # reported, never fatal
         sm_partition = {"error": f"{type(exc).__name__}: {exc}"}
+    # Predict again after Optimize: with the CUDA-core unit left out, the
+    # executor lends its SMs to the tensor unit, so the tensor unit is probed
+    # on that budget and its model spliced into the profile (same machine,
+    # same hash). The static prediction then describes the grid that runs:
+    # at 8192^3 the 146- and 148-SM grids differ by a whole wave of tiles
+    # (8 vs 7), at 16384^3 by 29 vs 28.
+    if (not args.profile and isinstance(sm_partition, dict) and sm_partition.get("chosen_simt_sms") == 0
+            and not (world > 1 and transport == "nccl")):
+        lent_sms = args.tc_sms + args.simt_sms
+        units_lent = (f"{tc_id}=xpu:dev={g}:sms={lent_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384:"
+                      f"preroll={args.preroll}")
+        profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING, bus=True, retries=2),
+                                   tc_id)
+        sm_partition["tensor_unit_reprobed_on_sms"] = lent_sms
+    t_prof = time.perf_counter() - t0
+    if save and rank == 0:
+        (save / "profile_resident.txt").write_text(profile)
     sa, sb = poas.stream_seed(SEED, "A"), poas.stream_seed(SEED, "B")
 
     def resident_run(label, m_all, n, k, steps, panels_req, adapt=True, full=True):

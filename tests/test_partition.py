@@ -88,3 +88,24 @@ def test_partition_rejects_bad_arguments(poas):
         kw.update(bad)
         with pytest.raises(PoasError):
             poas.plan_partitions(prof, N, N, N, kw["tc_id"], 146, "gpu0.simt", kw["simt_sms"], kw["budgets"])
+
+
+def test_splice_unit_replaces_the_model_keeps_the_machine(poas):
+    """Predict after Optimize (bench.py): a unit re-probed on its decided SM
+    budget replaces its model in the machine profile; identity, priorities
+    and the machine hash stay, so schedules planned from either run on the
+    same executor."""
+    base = _b200(poas)
+    faster = _profile(2.0 / 1.37e15, 2.0 / 0.8e12)  # the tensor unit on 148 SMs
+    out = poas.splice_unit(base, faster, "gpu0.tc")
+    assert poas.machine_hash(out) == poas.machine_hash(base)
+    assert poas.profile_roundtrip(out) == out
+    tc = [ln for ln in out.split("device gpu0.tc")[1].splitlines() if ln.startswith("slope ")][0]
+    assert float(tc.split()[1]) == pytest.approx(2.0 / 1.37e15, rel=1e-15)
+    simt = [ln for ln in out.split("device gpu0.simt")[1].splitlines() if ln.startswith("slope ")][0]
+    assert float(simt.split()[1]) == pytest.approx(2.0 / 0.8e12, rel=1e-15)
+    s0 = json.loads(poas.plan_policy(base, N, N, N, "best-subset"))
+    s1 = json.loads(poas.plan_policy(out, N, N, N, "best-subset"))
+    assert s1["makespan"] < s0["makespan"]
+    with pytest.raises(ValueError):
+        poas.splice_unit(base, faster, "gpu9.tc")

@@ -124,6 +124,13 @@ def c5(sizes, preroll_ms=20, steps=10):
         io = io_for(n, d)
         warm(0.5)
         profile = poas.profile_machine(units, PROF, True, retries=2)
+        # Predict again after the partition decision (as bench.py): with the
+        # CUDA-core unit left out the tensor unit runs on its 2 SMs too
+        part = poas.plan_partitions(profile, n, n, n, "gpu0.tc", 146, "gpu0.simt", 2, [0, 2], POLICY)
+        reprobed = part["candidates"][part["best"]]["simt_sms"] == 0
+        if reprobed:
+            lent = f"gpu0.tc=xpu:dev=0:sms=148:dtype=bf16:elem=2:link=hbm:probe={lo}-{hi}:preroll={preroll_ms}"
+            profile = poas.splice_unit(profile, poas.profile_machine(lent, PROF, True, retries=2), "gpu0.tc")
         ex = poas.Executor(units)
         # timed runs last >= ~0.25 s back to back (the sustained regime the
         # pre-rolled probes were taken in; a 1 ms burst runs at boost clock)
@@ -164,7 +171,7 @@ def c5(sizes, preroll_ms=20, steps=10):
         poas_s = t_poas[mid]
         tc_s = sorted(t_tc)[1]
         cb_s = sorted(t_cb)[1]
-        row = {"n": n, "tc_probe": [lo, hi], "steps": it,
+        row = {"n": n, "tc_probe": [lo, hi], "tc_probed_on_sms": 148 if reprobed else 146, "steps": it,
                "static_plan_rows": {x["id"]: x["rows"] for x in json.loads(static)["devices"]},
                "static_predicted_ms": rep_s["predicted_makespan"] * 1e3,
                "static_measured_ms": rep_s["measured_makespan"] * 1e3,
