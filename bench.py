@@ -50,6 +50,11 @@ TC_SMS = 146
 TC_SMS_MULTI = 144  # N > 1: 4 SMs (with the idle CUDA-core unit's 2) stay free for NCCL's broadcast kernels
 SIMT_SMS = 2
 PROFILING = "probes=9,repetitions=3,bandwidth_payload=268435456"
+# the tensor unit re-probed on the budget the partition decision gives it:
+# the bottom and top of its range, 5 repetitions each, so the fitted line
+# passes through the measured top (the size the steps run); in between the
+# time is a staircase of whole waves of tiles (tools/sweep.py PROF_TC)
+PROFILING_TC = "probes=2,repetitions=5,bandwidth_payload=268435456"
 
 
 def log(*a):
@@ -593,7 +598,7 @@ def main():
         lent_sms = args.tc_sms + args.simt_sms
         units_lent = (f"{tc_id}=xpu:dev={g}:sms={lent_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384:"
                       f"preroll={args.preroll}")
-        profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING, bus=True, retries=2),
+        profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING_TC, bus=True, retries=2),
                                    tc_id)
         sm_partition["tensor_unit_reprobed_on_sms"] = lent_sms
     t_prof = time.perf_counter() - t0

@@ -22,6 +22,13 @@ from paper_2209_10245_b200 import poas  # noqa: E402
 
 SEED = 20261017
 PROF = "probes=9,repetitions=3,bandwidth_payload=268435456"
+# The tensor unit re-probed on its lent budget (see c5): two probe sides, the
+# bottom and the top of its range, five repetitions each -- the line then
+# passes through the measured time at the top, the size the plan runs.
+# Between the two the time is a staircase of whole waves of tiles, which a
+# line fitted through intermediate sides over-predicts at the top (4096 /
+# 8192: -11..-14%, profiles/r02_lent).
+PROF_TC = "probes=2,repetitions=5,bandwidth_payload=268435456"
 # the bench's planner policy: the reference's whole-row rounding hands its
 # residue to the slowest unit (at 32768^3 one row to the 2-SM CUDA-core
 # unit, whose B stream then outlasts the tensor unit: 67 vs 54 ms)
@@ -130,7 +137,7 @@ def c5(sizes, preroll_ms=20, steps=10):
         reprobed = part["candidates"][part["best"]]["simt_sms"] == 0
         if reprobed:
             lent = f"gpu0.tc=xpu:dev=0:sms=148:dtype=bf16:elem=2:link=hbm:probe={lo}-{hi}:preroll={preroll_ms}"
-            profile = poas.splice_unit(profile, poas.profile_machine(lent, PROF, True, retries=2), "gpu0.tc")
+            profile = poas.splice_unit(profile, poas.profile_machine(lent, PROF_TC, True, retries=2), "gpu0.tc")
         ex = poas.Executor(units)
         # timed runs last >= ~0.25 s back to back (the sustained regime the
         # pre-rolled probes were taken in; a 1 ms burst runs at boost clock)
