@@ -543,7 +543,7 @@ def main():
     # probes pre-rolled (preroll=<ms>: each timed probe follows back-to-back
     # launches of the same GEMM): the sustained, power-capped regime the
     # timed steps run in, not the boost clock of a launch after an idle gap
-    units_res = (f"{tc_id}=xpu:dev={g}:sms={args.tc_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384:"
+    units_res = (f"{tc_id}=xpu:dev={g}:sms={args.tc_sms}:dtype=bf16:elem=2:link=fused:probe=8192-16384:"
                  f"preroll={args.preroll};"
                  f"{simt_id}=gpu:dev={g}:sms={args.simt_sms}:exclusive=1:elem=4:link=hbm:probe=512-2048:"
                  f"preroll={args.preroll}")
@@ -596,7 +596,7 @@ def main():
     if (not args.profile and isinstance(sm_partition, dict) and sm_partition.get("chosen_simt_sms") == 0
             and not (world > 1 and transport == "nccl")):
         lent_sms = args.tc_sms + args.simt_sms
-        units_lent = (f"{tc_id}=xpu:dev={g}:sms={lent_sms}:dtype=bf16:elem=2:link=hbm:probe=8192-16384:"
+        units_lent = (f"{tc_id}=xpu:dev={g}:sms={lent_sms}:dtype=bf16:elem=2:link=fused:probe=8192-16384:"
                       f"preroll={args.preroll}")
         profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING_TC, bus=True, retries=2),
                                    tc_id)
@@ -922,7 +922,7 @@ def main():
         e2e_profiles = {}
 
         def run_e2e(tc_elem, overlap, pipeline=False):
-            units_e2e = units_res.replace("elem=2:link=hbm", f"elem={tc_elem}:link=pcie").replace(
+            units_e2e = units_res.replace("elem=2:link=fused", f"elem={tc_elem}:link=pcie").replace(
                 "elem=4:link=hbm", "elem=4:link=pcie")
             if not args.no_e2e_cpu:
                 # With host-resident operands the host cores are a unit too:

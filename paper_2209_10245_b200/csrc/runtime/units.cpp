@@ -81,12 +81,13 @@ UnitSpec parse_unit_spec(const std::string& text) {
     } else if (k == "link") {
       if (v == "pcie") u.link = Link::pcie;
       else if (v == "hbm") u.link = Link::hbm;
-      else poas::fail(poas::errc::invalid_argument, "unit spec: link must be pcie or hbm");
+      else if (v == "fused") u.link = Link::fused;
+      else poas::fail(poas::errc::invalid_argument, "unit spec: link must be pcie, hbm or fused");
     } else {
       poas::fail(poas::errc::invalid_argument, "unit spec '" + text + "': unknown option " + k);
     }
   }
-  if (u.kind == poas::DeviceKind::cpu && u.link == Link::hbm) u.link = Link::pcie;
+  if (u.kind == poas::DeviceKind::cpu && u.link != Link::pcie) u.link = Link::pcie;
   return u;
 }
 
@@ -294,8 +295,25 @@ double Unit::time_gemm(std::int64_t side) {
       const double r = static_cast<double>(side) / static_cast<double>(last_probe_side_);
       est = last_probe_s_ * r * r * r;
     }
-    const int pre = est > 0.0 ? static_cast<int>(spec_.preroll_ms * 1e-3 / est) + 1 : 2;
-    for (int i = 0; i < std::min(pre, 4096); ++i) one();
+    const int pre = std::min(est > 0.0 ? static_cast<int>(spec_.preroll_ms * 1e-3 / est) + 1 : 2, 4096);
+    // the pre-roll's own back-to-back launches give this side's launch time
+    // (the cubic extrapolation above misses by far for short, latency-bound
+    // GEMMs: from a 512^3 probe it puts 2048^3 at ~0.5 ms, ~25x too long,
+    // and the probe would time one isolated launch instead of the
+    // back-to-back regime the steps run in)
+    cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+    for (int i = 0; i < pre; ++i) one();
+    cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
+    float pre_ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&pre_ms, ev0_, ev1_), "cudaEventElapsedTime");
+    const double per = static_cast<double>(pre_ms) * 1e-3 / pre;
+    if (per > 0.0) est = per;
+    // a pre-roll shorter than asked (an over-estimate above): top it up
+    if (est > 0.0 && pre * est < spec_.preroll_ms * 1e-3)
+      for (int i = 0, more = std::min(static_cast<int>((spec_.preroll_ms * 1e-3 - pre * est) / est) + 1, 4096);
+           i < more; ++i)
+        one();
     if (est > 0.0) reps = std::clamp(static_cast<int>(100e-6 / est) + 1, 1, 32);
   }
   cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
@@ -311,6 +329,10 @@ double Unit::time_gemm(std::int64_t side) {
 
 double Unit::time_transfer(std::uint64_t bytes) {
   if (!on_gpu()) poas::fail(poas::errc::backend_failure, "cpu unit has no link");
+  // The operand stream is inside the probed GEMM: a nominal 1 PB/s keeps
+  // the model's copy phases (and the LP's bandwidth terms) at ~zero while
+  // staying a valid positive bandwidth of the reference profile format.
+  if (spec_.link == Link::fused) return static_cast<double>(bytes) / 1e15;
   DeviceGuard g(spec_.device);
   // Buffers first: allocation must stay outside the timed interval.
   if (spec_.link == Link::pcie) {

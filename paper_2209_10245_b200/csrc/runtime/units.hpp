@@ -22,7 +22,15 @@
 
 namespace poas_b200 {
 
-enum class Link { pcie, hbm };
+// What a unit's operands cross before it computes (what time_transfer
+// measures): pcie = pinned host memory over the unit's PCIe link; hbm =
+// resident operands streamed into the unit's own SMs (a streaming read on
+// its budget: what a few-row CUDA-core share pays to read all of B); fused
+// = resident operands whose stream is part of the probed GEMM itself (a
+// tensor unit's fat share reads A and B while it computes, which its
+// square-GEMM probes already time: a separate copy phase would count the
+// stream twice -- 2048^3: +32% predicted, profiles/r02_lent5).
+enum class Link { pcie, hbm, fused };
 
 struct UnitSpec {
   std::string id;

@@ -506,3 +506,45 @@ def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
             assert oracle.rel_frobenius(hC.numpy(), exp) <= TOL, reps
             assert torch.equal(hC, exp_host), reps
             assert rep["repeats"] == reps and rep["measured_makespan"] > 0
+
+
+def test_fused_link_unit_profile(torch_cuda, poas):
+    """link=fused (a tensor unit whose operand stream is inside its probed
+    GEMM): the profile's bandwidth is the nominal 1 PB/s, so the plan's copy
+    phases are ~0 and its prediction is the compute model alone; a resident
+    run through it is exact."""
+    import oracle
+
+    torch = torch_cuda
+    units = ("gpu0.tc=xpu:dev=0:sms=16:dtype=bf16:elem=2:link=fused:probe=512-1024;"
+             "gpu0.simt=gpu:dev=0:sms=2:exclusive=1:elem=4:link=hbm:probe=128-256")
+    prof = poas.profile_machine(units, "probes=3,repetitions=2,bandwidth_payload=4194304", True, retries=2)
+    bw = {}
+    cur = None
+    for line in prof.splitlines():
+        p = line.split()
+        if len(p) == 2 and p[0] == "device":
+            cur = p[1]
+        elif len(p) == 2 and p[0] == "bandwidth":
+            bw[cur] = float(p[1])
+    assert bw["gpu0.tc"] == pytest.approx(1e15, rel=1e-6)
+    assert 1e9 < bw["gpu0.simt"] < 1e13
+    m, n, k = 1024, 768, 512
+    s = json.loads(poas.plan_policy(prof, m, n, k, "best-subset"))
+    tc = [d for d in s["devices"] if d["id"] == "gpu0.tc"][0]
+    assert tc["rows"] > 0
+    ci, co = tc["copy_in"], tc["copy_out"]
+    assert ci[1] - ci[0] < 1e-7 and co[1] - co[0] < 1e-7
+    A, B = oracle.fill_uniform(m, k, 3), oracle.fill_uniform(k, n, 4)
+    a16 = torch.from_numpy(A).cuda().bfloat16()
+    b16 = torch.from_numpy(B).cuda().bfloat16()
+    a32 = torch.from_numpy(A).cuda()
+    b32 = torch.from_numpy(B).cuda()
+    C = torch.full((m, n), float("nan"), device="cuda")
+    io = poas.GemmIO(m=m, n=n, k=k, a_dev=a32.data_ptr(), lda_dev=k, b_dev=b32.data_ptr(), ldb_dev=n,
+                     a16_dev=a16.data_ptr(), lda16_dev=k, b16_dev=b16.data_ptr(), ldb16_dev=n,
+                     c_dev=C.data_ptr(), ldc_dev=n, resident=1)
+    poas.Executor(units).execute(json.dumps(s), io, 1)
+    torch.cuda.synchronize()
+    ref = oracle.expected_c(s, A, B, {"gpu0.tc": 2, "gpu0.simt": 0})
+    assert oracle.rel_frobenius(C.cpu().numpy(), ref) <= 2e-5
