@@ -145,7 +145,10 @@ int poas_b200_simplex(int num_vars, const double* objective, int n_eq, const dou
  *   gpu : dev=<cuda ordinal>, sms=<n>       (SM budget, 0 = all), exclusive=0|1
  *   xpu : dev=<ordinal>, sms=<n>, dtype=bf16|f16, elem=<bytes on the link>
  * and, for any kind: probe=MIN-MAX (the unit's own probe side range),
- * link=pcie|hbm (what time_transfer measures), align=<rows> (xpu);
+ * link=pcie|hbm|fused (what time_transfer measures: pinned host memory
+ * over PCIe; resident operands streamed into the unit's own SMs; or
+ * resident operands streamed inside the probed GEMM itself -- a tensor
+ * unit's fat share -- reported as a nominal 1 PB/s), align=<rows> (xpu);
  * GPU units: preroll=<ms> (each timed probe follows back-to-back launches
  * of the same GEMM worth that long: probes in the continuous-load, power-
  * capped regime a co-executed step runs in; default 0 = one launch).
