@@ -1,3 +1,11 @@
+"""Probe vs timed-step diagnosis at small sizes (dev tool; profiles/r02_fused).
+
+    python tools/dbg_probe.py
+
+For 2048^3 and 4096^3: the tensor unit's fitted model at its lent budget
+(two-point and nine-point probe sets) against executor runs of 1 / 42 / 256
+graph-replayed repeats and Python-loop launches.
+"""
 import sys, json, time
 sys.path.insert(0, '.')
 import torch
