@@ -598,9 +598,12 @@ def main():
         lent_sms = args.tc_sms + args.simt_sms
         units_lent = (f"{tc_id}=xpu:dev={g}:sms={lent_sms}:dtype=bf16:elem=2:link=fused:probe=8192-16384:"
                       f"preroll={args.preroll}")
-        profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING_TC, bus=True, retries=2),
-                                   tc_id)
-        sm_partition["tensor_unit_reprobed_on_sms"] = lent_sms
+        try:
+            profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING_TC, bus=True,
+                                                                     retries=2), tc_id)
+            sm_partition["tensor_unit_reprobed_on_sms"] = lent_sms
+        except Exception as exc:  # reported; the first profile stands
+            sm_partition["tensor_unit_reprobe_error"] = f"{type(exc).__name__}: {exc}"
     t_prof = time.perf_counter() - t0
     if save and rank == 0:
         (save / "profile_resident.txt").write_text(profile)
