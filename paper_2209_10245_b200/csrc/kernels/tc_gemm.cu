@@ -66,6 +66,7 @@ struct TcArgs {
   // delivers B, e.g. after each panel's broadcast).
   int panels;
   int tiles_n_panel;
+  int panel_order;  // 1: tiles panel by panel (else the grouped raster over all panels)
   const int* panel_flags;
   int panel_epoch;
   // Streamed operands (pair kernel; see tc_gemm_stream): tiles ordered by a
@@ -220,14 +221,25 @@ __device__ __forceinline__ int4 tile_coords_stream(const TcArgs& a, int t, int& 
 }
 
 // Tile t of a (possibly panel-major) problem: M-tile mb, global N-tile nb,
-// its panel p and N-tile inside the panel nbl (grouped raster per panel).
+// its panel p and N-tile inside the panel nbl. Default: the grouped raster
+// over the whole grid (the panels are only where B's columns live), so the
+// tiles in flight share A row panels through L2; with panel_order the tiles
+// go panel by panel (each panel consumed as soon as it lands, at the price
+// of re-reading every A row panel once per B panel: C4 per GPU at 8 GPUs,
+// 16 panels, 1381 vs 1551 TFLOP/s row-major, profiles/r02_panels).
 __device__ __forceinline__ void tile_coords_panel(const TcArgs& a, int t, int& mb, int& nb, int& p,
                                                   int& nbl) {
-  if (a.panels > 1) {
+  if (a.panels > 1 && a.panel_order) {
     const int per = a.tiles_m * a.tiles_n_panel;
     p = t / per;
     tile_coords(t - p * per, a.tiles_m, a.tiles_n_panel, a.group, mb, nbl, a.raster_n);
     nb = p * a.tiles_n_panel + nbl;
+    return;
+  }
+  if (a.panels > 1) {
+    tile_coords(t, a.tiles_m, a.tiles_n, a.group, mb, nb, a.raster_n);
+    p = nb / a.tiles_n_panel;
+    nbl = nb - p * a.tiles_n_panel;
     return;
   }
   p = 0;
@@ -617,7 +629,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kTh
       // later tiles; dynamic claims continue after the first wave.
       int t = first < total ? first : -1;
       next_static = first + step;
-      int confirmed = -1;  // highest B panel seen ready
+      uint64_t panels_seen = 0;  // B panels seen ready (P <= 64; more: checked per tile)
       uint64_t seen_lo = 0, seen_hi = 0;  // streamed link items seen ready
       while (t >= 0) {
         if (cleader && wave_on && wave > 0) wave_on = wave_barrier(args, wave, step, total, wave_target);
@@ -641,9 +653,9 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kTh
         } else {
           tile_coords_panel(args, t, mb, nb, pnl, nbl);
         }
-        if (args.panel_flags && pnl > confirmed) {  // flags are set in panel order
+        if (args.panel_flags && (pnl >= 64 || !(panels_seen & (1ull << pnl)))) {
           wait_panel_flag(args.panel_flags + pnl, args.panel_epoch);
-          confirmed = pnl;
+          if (pnl < 64) panels_seen |= 1ull << pnl;
         }
         const int row0 = mb * kRowsT + pair * 256 + static_cast<int>(prank) * 128;
         // this CTA's columns of each 256-column half: [h*256 + prank*128, +128)
@@ -1443,6 +1455,10 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.tma_store = 0;
   args.trace = nullptr;
   args.panels = P;
+  {
+    const char* po = std::getenv("POAS_TC_PANEL_ORDER");  // "panel": tiles panel by panel
+    args.panel_order = po && std::string(po) == "panel";
+  }
   args.tiles_n_panel = static_cast<int>(
       np / (variant == TcVariant::pair512 || variant == TcVariant::pair512x2 ? 512 : 256));
   args.panel_flags = ps ? ps->flags : nullptr;
