@@ -79,6 +79,40 @@ def measured_peaks():
     return 1590.0, 1400.0, "fallback"  # B200_PROFILING.md: 1.59 burst, ~1.4 sustained
 
 
+def concurrent_link_ms(torch, h2d_bytes: int, d2h_bytes: int) -> float | None:
+    """Best of 3: `h2d_bytes` host->device and `d2h_bytes` device->host at
+    the same time (pinned host memory, 64 MiB copies, one stream each), ms."""
+    try:
+        chunk = 64 << 20
+        hs = torch.empty(h2d_bytes, dtype=torch.uint8).pin_memory()
+        hd = torch.empty(d2h_bytes, dtype=torch.uint8).pin_memory()
+        ds = torch.empty(d2h_bytes, dtype=torch.uint8, device="cuda")
+        dd = torch.empty(h2d_bytes, dtype=torch.uint8, device="cuda")
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0, e1, e2 = (torch.cuda.Event(True) for _ in range(3))
+            e0.record()
+            s_in.wait_event(e0)
+            s_out.wait_event(e0)
+            with torch.cuda.stream(s_in):
+                for a in range(0, h2d_bytes, chunk):
+                    dd[a:a + chunk].copy_(hs[a:a + chunk], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for a in range(0, d2h_bytes, chunk):
+                    hd[a:a + chunk].copy_(ds[a:a + chunk], non_blocking=True)
+            e1.record(s_in)
+            e2.record(s_out)
+            torch.cuda.synchronize()
+            t = max(e0.elapsed_time(e1), e0.elapsed_time(e2))
+            best = t if best is None else min(best, t)
+        del hs, hd, ds, dd
+        return best
+    except Exception:
+        return None
+
+
 def hbm_peak():
     """Measured HBM copy bandwidth (GB/s, MEASURED_PEAKS.json) or None."""
     try:
@@ -1004,6 +1038,15 @@ def main():
                 link_s = max(h2d, d2h) / bw if overlap else (h2d + d2h) / bw
                 out["link_bound_ms"] = round(link_s * 1e3, 3)
                 out["link_bandwidth_gbs"] = round(bw / 1e9, 2)
+            if overlap and rank == 0:
+                # the link measured as the overlapped step uses it: this
+                # step's H2D and D2H bytes at once, contiguous 64 MiB copies
+                # (one stream per direction; more streams do not help,
+                # profiles/r02_pcie) -- the practical floor of the step
+                cl = concurrent_link_ms(torch, h2d, d2h)
+                if cl:
+                    out["link_concurrent_ms"] = round(cl, 3)
+                    out["link_frac"] = round(cl / out["ms_per_step"], 3)
             if save and rank == 0:
                 tag = ("e2e" if tc_elem == 2 else "e2e_fp32") + ("" if overlap else "_sync") + (
                     "_pipelined" if pipeline else "")
