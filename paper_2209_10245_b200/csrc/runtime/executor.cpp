@@ -516,10 +516,16 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     }
   const bool pipelined = overlapped && pipeline_ && !any_cpu && busy_gpu_units == 1 &&
                          sstate[busy_unit].item_flags != nullptr;
-  if (pipelined && repeats > 1) {  // the second C buffer, before any repeat is queued
+  // POAS_EXEC_PIPE_STAGING=1: one A / B staging set (each repeat's copy-in
+  // waits for the previous repeat's start gate, i.e. its GEMM's end)
+  const char* pipe_env = std::getenv("POAS_EXEC_PIPE_STAGING");
+  const bool two_sets = pipelined && !(pipe_env && std::string(pipe_env) == "1");
+  if (pipelined && repeats > 1) {  // the second C / A / B buffers, before any repeat is queued
     DeviceGuard g(unit[busy_unit]->spec().device);
-    unit[busy_unit]->scratch(6).ensure(
-        static_cast<std::size_t>(schedule.devices[busy_unit].rows * d.n) * 4);
+    const std::int64_t r = schedule.devices[busy_unit].rows;
+    unit[busy_unit]->scratch(6).ensure(static_cast<std::size_t>(r * d.n) * 4);
+    unit[busy_unit]->scratch(7).ensure(static_cast<std::size_t>(r * round_up(d.k, 8)) * 2);
+    unit[busy_unit]->scratch(8).ensure(static_cast<std::size_t>(d.k * round_up(d.n, 8)) * 2);
   }
 
   // One repeat of an overlapped link unit: host->device (A parts and B
@@ -540,8 +546,14 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     const std::size_t esz = link16 ? 2 : 4;
     const std::int64_t lda_l = link16 ? round_up(d.k, 8) : d.k;
     const std::int64_t ldb_l = link16 ? round_up(d.n, 8) : d.n;
-    char* a_l = static_cast<char*>(u->scratch(link16 ? 2 : 0).ensure(static_cast<std::size_t>(r * lda_l) * esz));
-    char* b_l = static_cast<char*>(u->scratch(link16 ? 3 : 1).ensure(static_cast<std::size_t>(d.k * ldb_l) * esz));
+    // pipelined (16-bit link, one streamed launch per repeat): odd repeats
+    // land their A / B in a second staging set, so a repeat's copy-in runs
+    // while the previous repeat still computes on the first
+    const bool second = two_sets && link16 && (rr & 1) && sstate[i].item_flags;
+    char* a_l = static_cast<char*>(
+        u->scratch(second ? 7 : (link16 ? 2 : 0)).ensure(static_cast<std::size_t>(r * lda_l) * esz));
+    char* b_l = static_cast<char*>(
+        u->scratch(second ? 8 : (link16 ? 3 : 1)).ensure(static_cast<std::size_t>(d.k * ldb_l) * esz));
     float* c = static_cast<float*>(u->scratch(4).ensure(static_cast<std::size_t>(r * d.n) * 4));
     const std::vector<std::int64_t>& rp = grid[i].parts;
     const std::vector<std::int64_t>& cp = grid[i].panels;
@@ -549,8 +561,14 @@ SimulationResult Executor::run(const Schedule& schedule, const GemmOperands& io,
     for (std::size_t p = 1; p < rp.size(); ++p) roff[p] = roff[p - 1] + rp[p - 1];
     for (std::size_t q = 1; q < cp.size(); ++q) coff[q] = coff[q - 1] + cp[q - 1];
 
-    // host -> device
-    cuda_check(cudaStreamWaitEvent(hs, t0[u->spec().device][rr], 0), "wait t0");
+    // host -> device: after this repeat's start -- or, pipelined with two
+    // staging sets, once the repeat that last used this set has computed
+    // (its GEMM read it), without waiting for the previous repeat
+    if (two_sets && link16 && sstate[i].item_flags && rr >= 1) {
+      if (rr >= 2) cuda_check(cudaStreamWaitEvent(hs, ev[rr - 2][i].cp1, 0), "wait staging set");
+    } else {
+      cuda_check(cudaStreamWaitEvent(hs, t0[u->spec().device][rr], 0), "wait t0");
+    }
     if (bus_ && prev_in != nd) cuda_check(cudaStreamWaitEvent(hs, ev[rr][prev_in].ci1, 0), "wait");
     cuda_check(cudaEventRecord(e.ci0, hs), "cudaEventRecord");
     for (std::size_t k = 0; k < link_order[i].size(); ++k) {

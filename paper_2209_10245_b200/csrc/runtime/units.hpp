@@ -144,7 +144,9 @@ class Unit : public poas::DeviceBackend {
   double last_probe_s_ = 0.0;  // the previous probe (pre-roll sizing)
   std::size_t xfer_warm_bytes_ = 0;  // link probe buffers warmed for this size
   std::int64_t last_probe_side_ = 0;
-  DeviceBuffer scratch_[7];  // 0-4 staging, 5 streamed-launch state, 6 second C (pipelined)
+  // 0-4 staging, 5 streamed-launch state, 6 second C (pipelined), 7-8 second
+  // 16-bit A / B staging (pipelined: repeat r+1 lands while r computes)
+  DeviceBuffer scratch_[9];
 };
 
 // RAII device selection.

@@ -34,17 +34,29 @@ ex = poas.Executor(units + ";overlap=1;pipeline=1")
 out = {"base_grid": None, "rows": []}
 tc = [d for d in base["devices"] if d["id"] == "gpu0.tc"][0]
 out["base_grid"] = [len({t["m"] for t in tc["tiles"]}), len(tc["tiles"])]
-for R, Q in ((4, 4), (8, 4), (4, 8), (8, 8), (16, 4), (16, 8), (8, 16), (16, 16), (32, 8)):
+import os  # noqa: E402
+
+grids = ((4, 4), (8, 4), (4, 8), (8, 8), (16, 4), (16, 8), (8, 16), (16, 16), (32, 8))
+if os.environ.get("E2E_GRID_STAGING_AB"):  # A/B one vs two staging sets, planner's and 16x4 grids
+    grids = ((4, 4), (16, 4)) * 3
+for R, Q in grids:
     s = json.loads(json.dumps(base))
     d = [x for x in s["devices"] if x["id"] == "gpu0.tc"][0]
     pr, pc = d["rows"] // R, n // Q
     d["tiles"] = [{"m": pr, "k": k, "n": pc} for _ in range(R) for _ in range(Q)]
     sched = poas.schedule_roundtrip(json.dumps(s))
-    ex.execute(sched, io, 3)
-    t0 = time.perf_counter()
-    ex.execute(sched, io, 20)
-    ms = (time.perf_counter() - t0) / 20 * 1e3
-    row = {"grid": [R, Q], "ms_per_step": round(ms, 3), "tflops": round(2 * n ** 3 / ms / 1e9, 1)}
+    variants = (("two_sets", None), ("one_set", "1")) if os.environ.get("E2E_GRID_STAGING_AB") else (("default", None),)
+    row = {"grid": [R, Q]}
+    for name, env in variants:
+        if env:
+            os.environ["POAS_EXEC_PIPE_STAGING"] = env
+        else:
+            os.environ.pop("POAS_EXEC_PIPE_STAGING", None)
+        ex.execute(sched, io, 3)
+        t0 = time.perf_counter()
+        ex.execute(sched, io, 20)
+        ms = (time.perf_counter() - t0) / 20 * 1e3
+        row[name] = {"ms_per_step": round(ms, 3), "tflops": round(2 * n ** 3 / ms / 1e9, 1)}
     out["rows"].append(row)
     print(json.dumps(row), file=sys.stderr, flush=True)
 print(json.dumps(out))
