@@ -139,7 +139,7 @@ def test_cpu_only_executor_run(poas, ref):
     import oracle
 
     units = "cpu0=cpu:threads=4"
-    profile = poas.profile_machine(units, "probes=4,repetitions=2,cpu_min_side=128,cpu_max_side=320")
+    profile = poas.profile_machine(units, "probes=4,repetitions=3,cpu_min_side=192,cpu_max_side=448", retries=3)
     m, n, k = 300, 256, 128
     sched = poas.plan(profile, m, n, k)
     assert sched == ref.plan(profile, m, n, k)

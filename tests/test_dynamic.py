@@ -151,7 +151,7 @@ def test_dynamic_loop_converges_on_host_units(poas):
     optimistic for one of them: the loop re-fits, re-plans, moves rows away
     and the prediction error shrinks; C stays exact."""
     units = "cpuA=cpu:threads=1;cpuB=cpu:threads=1"
-    prof = poas.profile_machine(units, "probes=3,repetitions=3,cpu_min_side=192,cpu_max_side=448")
+    prof = poas.profile_machine(units, "probes=3,repetitions=3,cpu_min_side=192,cpu_max_side=448", retries=3)
     lines = []
     cur = None
     for line in prof.splitlines():
