@@ -374,9 +374,15 @@ def host_unit_baseline(poas, n: int) -> dict:
     io = poas.GemmIO(m=c1, n=c1, k=c1, a_host=A.ctypes.data, lda_host=c1, b_host=B.ctypes.data, ldb_host=c1,
                      c_host=Cm.ctypes.data, ldc_host=c1, resident=0)
     ex.execute(sched, io, 1)
-    t0 = time.perf_counter()
-    rep = ex.execute(sched, io, 5)
-    sec = (time.perf_counter() - t0) / 5
+    # the median of three 5-repeat runs (the host's clock wanders after the
+    # reference path's 10 s of all-core load just before)
+    runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        r_ = ex.execute(sched, io, 5)
+        runs.append(((time.perf_counter() - t0) / 5, r_))
+    runs.sort(key=lambda x: x[0])
+    sec, rep = runs[1]
     ref = A.astype(np.float64) @ B.astype(np.float64)
     err = float(np.linalg.norm(Cm - ref) / np.linalg.norm(ref))
     out["c1"] = {"workload": "C1: 2048^3 fp32, POAS predict/plan/execute on a CPU-only machine (host_gemm)",

@@ -39,6 +39,8 @@ import os  # noqa: E402
 grids = ((4, 4), (8, 4), (4, 8), (8, 8), (16, 4), (16, 8), (8, 16), (16, 16), (32, 8))
 if os.environ.get("E2E_GRID_STAGING_AB"):  # A/B one vs two staging sets, planner's and 16x4 grids
     grids = ((4, 4), (16, 4)) * 3
+if os.environ.get("E2E_GRID_LIST"):  # e.g. "16x1,8x2"
+    grids = tuple(tuple(int(v) for v in g.split("x")) for g in os.environ["E2E_GRID_LIST"].split(","))
 for R, Q in grids:
     s = json.loads(json.dumps(base))
     d = [x for x in s["devices"] if x["id"] == "gpu0.tc"][0]
