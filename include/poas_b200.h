@@ -90,6 +90,15 @@ int poas_b200_plan_partitions(const char* profile_text, int64_t m, int64_t n, in
                               const int* simt_budgets, int count, const char* policy,
                               char** out_json);
 
+/* Predict again after the partition decision: `profile_text` with unit
+ * `unit_id`'s measured model (slope, intercept, bandwidth, ops window)
+ * replaced by the same unit's entry in `unit_profile_text` -- the unit
+ * re-probed on its decided SM budget (e.g. a poas_b200_profile_machine of
+ * that one unit). Identity, kind, priority, alignment and the machine hash
+ * are unchanged. *out_profile: poas-profile v1 text (poas_b200_free). */
+int poas_b200_profile_splice_unit(const char* profile_text, const char* unit_profile_text,
+                                  const char* unit_id, char** out_profile);
+
 /* standalone_schedule (proj/include/poas/scheduler.hpp:40-41). */
 int poas_b200_plan_standalone(const char* profile_text, const char* device_id, int64_t m,
                               int64_t n, int64_t k, char** schedule_json);

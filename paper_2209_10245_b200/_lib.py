@@ -27,6 +27,7 @@ SIGNATURES: dict[str, tuple] = {
     "poas_b200_plan": (C.c_int, [cp, i64, i64, i64, C.POINTER(vp)]),
     "poas_b200_plan_standalone": (C.c_int, [cp, cp, i64, i64, i64, C.POINTER(vp)]),
     "poas_b200_plan_policy": (C.c_int, [cp, i64, i64, i64, cp, C.POINTER(vp)]),
+    "poas_b200_profile_splice_unit": (C.c_int, [cp, cp, cp, C.POINTER(vp)]),
     "poas_b200_plan_partitions": (C.c_int, [cp, i64, i64, i64, cp, C.c_int, cp, C.c_int,
                                             C.POINTER(C.c_int), C.c_int, cp, C.POINTER(vp)]),
     "poas_b200_split": (C.c_int, [cp, i64, i64, i64, C.POINTER(vp)]),

@@ -471,6 +471,28 @@ int poas_b200_execute(poas_executor_t ex, const char* schedule_json, const poas_
   });
 }
 
+int poas_b200_profile_splice_unit(const char* profile_text, const char* unit_profile_text,
+                                  const char* unit_id, char** out_profile) {
+  return guard([&] {
+    need_ptr(out_profile, "out_profile");
+    poas::MachineProfile m = poas::parse_profile(need_str(profile_text, "profile"));
+    const poas::MachineProfile u = poas::parse_profile(need_str(unit_profile_text, "unit profile"));
+    const std::string id = need_str(unit_id, "unit_id");
+    const poas::DeviceProfile* src = u.find(id);
+    poas::DeviceProfile* dst = nullptr;
+    for (poas::DeviceProfile& d : m.devices)
+      if (d.id == id) dst = &d;
+    if (!src || !dst) raise(POAS_E_INVALID_ARGUMENT, "splice: unit '" + id + "' missing");
+    if (src->kind != dst->kind) raise(POAS_E_INVALID_ARGUMENT, "splice: unit kinds differ");
+    dst->compute = src->compute;
+    dst->bandwidth = src->bandwidth;
+    dst->ops_min = src->ops_min;
+    dst->ops_max = src->ops_max;
+    poas::validate_machine(m);
+    *out_profile = dup_string(poas::format_profile(m));
+  });
+}
+
 int poas_b200_refit_profile(const char* profile_text, const char* report_json, double alpha,
                             char** out_profile) {
   return guard([&] {

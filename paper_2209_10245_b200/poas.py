@@ -52,35 +52,10 @@ def plan_partitions(profile: str, m: int, n: int, k: int, tc_id: str, tc_sms: in
 def splice_unit(profile: str, unit_profile: str, unit_id: str) -> str:
     """`profile` with device `unit_id`'s measured model (slope, intercept,
     bandwidth, ops window) taken from `unit_profile` -- the same unit probed
-    again in another configuration, e.g. on the SM budget the partition
-    decision gives it. Identity, kind, priority and alignment stay, so the
-    machine hash is unchanged. Canonical text (profile_roundtrip)."""
-    keys = ("slope", "intercept", "bandwidth", "ops_min", "ops_max")
-
-    def fields(text):
-        out, cur = {}, None
-        for line in text.splitlines():
-            parts = line.split()
-            if len(parts) == 2 and parts[0] == "device":
-                cur = parts[1]
-            elif cur == unit_id and len(parts) == 2 and parts[0] in keys:
-                out[parts[0]] = parts[1]
-        return out
-
-    new = fields(unit_profile)
-    if set(new) != set(keys):
-        raise ValueError(f"splice_unit: {unit_id} not fully described in the unit profile")
-    lines, cur = [], None
-    for line in profile.splitlines():
-        parts = line.split()
-        if len(parts) == 2 and parts[0] == "device":
-            cur = parts[1]
-        elif cur == unit_id and len(parts) == 2 and parts[0] in keys:
-            line = f"{parts[0]} {new[parts[0]]}"
-        lines.append(line)
-    if unit_id not in fields(profile) and not any(l.split() == ["device", unit_id] for l in lines):
-        raise ValueError(f"splice_unit: no device {unit_id} in the profile")
-    return profile_roundtrip("\n".join(lines) + "\n")
+    again on the SM budget the partition decision gives it
+    (poas_b200_profile_splice_unit). Identity, kind, priority and alignment
+    stay, so the machine hash is unchanged."""
+    return call_str(lib.poas_b200_profile_splice_unit, _b(profile), _b(unit_profile), _b(unit_id))
 
 
 def refit_profile(profile: str, report: str | dict, alpha: float = 0.5) -> str:

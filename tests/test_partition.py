@@ -107,5 +107,7 @@ def test_splice_unit_replaces_the_model_keeps_the_machine(poas):
     s0 = json.loads(poas.plan_policy(base, N, N, N, "best-subset"))
     s1 = json.loads(poas.plan_policy(out, N, N, N, "best-subset"))
     assert s1["makespan"] < s0["makespan"]
-    with pytest.raises(ValueError):
+    from paper_2209_10245_b200 import PoasError
+
+    with pytest.raises(PoasError):
         poas.splice_unit(base, faster, "gpu9.tc")
