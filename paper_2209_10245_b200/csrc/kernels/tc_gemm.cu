@@ -5,14 +5,18 @@
 // Replaces the XPU-kind synthetic law of the reference (SyntheticBackend::
 // time_gemm, /root/reference/proj/src/simulator.cpp:30-34) with real work.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0  lane 0 : TMA producer  -- A tile [128 x 64] K-major, B tile
-//                    [64 x 256] N-major, both 128B-swizzled, STAGES-deep ring
-//   warp 1  lane 0 : MMA issuer    -- tcgen05.mma.cta_group::1.kind::f16
-//                    128x256x16, accumulator in TMEM (2 x 256 columns, double
-//                    buffered so the epilogue of tile i overlaps tile i+1)
-//   warps 2..5     : epilogue      -- tcgen05.ld 32x32b -> registers -> fp32 C
-// M/N/K tails come from TMA out-of-bounds zero fill plus masked stores.
+// Kernels (all persistent over output tiles, one CTA per SM):
+//   tc_gemm_2cta_kernel<W, PAIRS>  CTA pairs (cta_group::2), 256 x W tiles:
+//     W = 512 (default from K >= 6144; 4 x 48 KB stages, the accumulator
+//     fills TMEM and its halves are released separately, 8 epilogue warps),
+//     W = 256 (6 x 32 KB stages, double-buffered accumulator, 4 epilogue
+//     warps); PAIRS = 2 puts two pairs in a cluster sharing B by multicast.
+//   tc_gemm_kernel<BN, STAGES>     one SM, 128 x BN tiles (small GEMMs).
+// Roles: warp 0 lane 0 TMA producer (A K-major, B N-major, 128B-swizzled
+// ring), warp 1 lane 0 MMA issuer (tcgen05.mma .kind::f16, fp32 accumulator
+// in TMEM), the remaining warps the epilogue (tcgen05.ld -> registers ->
+// swizzled smem box -> TMA store / reduce-add). M/N/K tails come from TMA
+// out-of-bounds zero fill and clipped stores. See DESIGN.md section 2.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
