@@ -506,6 +506,19 @@ def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
             assert oracle.rel_frobenius(hC.numpy(), exp) <= TOL, reps
             assert torch.equal(hC, exp_host), reps
             assert rep["repeats"] == reps and rep["measured_makespan"] > 0
+        # new host operands between runs (odd repeats land in the second
+        # staging set): 2 x A is exact in bf16 and in the fp32 sums, so every
+        # run must give exactly 2 x C -- nothing stale from either set
+        hA16_2 = (hA16.float() * 2).bfloat16().contiguous().pin_memory()
+        io.a16_host = hA16_2.data_ptr()
+        for reps in (2, 3):
+            hC.fill_(float("nan"))
+            ex_p.execute(sched_text, io, reps)
+            assert torch.equal(hC, exp_host * 2), reps
+        io.a16_host = hA16.data_ptr()
+        hC.fill_(float("nan"))
+        ex_p.execute(sched_text, io, 4)
+        assert torch.equal(hC, exp_host)
 
 
 def test_fused_link_unit_profile(torch_cuda, poas):
