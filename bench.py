@@ -591,16 +591,35 @@ def main():
     units_exec = units_res + (";lend=0" if (world > 1 and transport == "nccl") else "")
 
     # ---- predict (this GPU's units, real kernels) + the level-1 link probe
-    t0 = time.perf_counter()
-    if args.profile:  # a profile measured earlier on this box (e.g. for an ncu pass)
-        profile = Path(args.profile.replace("{rank}", str(rank))).read_text()
-    else:
+    # Ranks that share a GPU (the multi-rank path exercised on a one-GPU
+    # box) probe in turn: concurrent probes would time each other's kernels
+    # and skew the level-1 split (one rank was left no rows).
+    shared_gpu = world > 1 and torch.cuda.device_count() < env_int("LOCAL_WORLD_SIZE", world)
+
+    def in_turn(fn):
+        if not shared_gpu:
+            return fn()
+        out_ = None
+        for r_ in range(world):
+            grp.barrier()
+            if r_ == rank:
+                out_ = fn()
+        grp.barrier()
+        return out_
+
+    def probe_units():
         # Bring the GPU to the power-capped steady state the timed region
         # runs in before probing (the probes are short GEMMs; on a cool GPU
         # they see burst clocks the sustained run never gets).
         if args.probe_warmup > 0:
             warm_sustained(poas, torch, dev, args.probe_warmup)
-        profile = poas.profile_machine(units_res, PROFILING, bus=True, retries=2)
+        return poas.profile_machine(units_res, PROFILING, bus=True, retries=2)
+
+    t0 = time.perf_counter()
+    if args.profile:  # a profile measured earlier on this box (e.g. for an ncu pass)
+        profile = Path(args.profile.replace("{rank}", str(rank))).read_text()
+    else:
+        profile = in_turn(probe_units)
     t_prof = time.perf_counter() - t0
     link_bw = None
     if comm:
@@ -638,12 +657,18 @@ def main():
         lent_sms = args.tc_sms + args.simt_sms
         units_lent = (f"{tc_id}=xpu:dev={g}:sms={lent_sms}:dtype=bf16:elem=2:link=fused:probe=8192-16384:"
                       f"preroll={args.preroll}")
-        try:
-            profile = poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING_TC, bus=True,
-                                                                     retries=2), tc_id)
+        def reprobe():
+            try:
+                return poas.splice_unit(profile, poas.profile_machine(units_lent, PROFILING_TC, bus=True,
+                                                                      retries=2), tc_id), None
+            except Exception as exc:  # reported; the first profile stands
+                return profile, f"{type(exc).__name__}: {exc}"
+
+        profile, err = in_turn(reprobe)
+        if err:
+            sm_partition["tensor_unit_reprobe_error"] = err
+        else:
             sm_partition["tensor_unit_reprobed_on_sms"] = lent_sms
-        except Exception as exc:  # reported; the first profile stands
-            sm_partition["tensor_unit_reprobe_error"] = f"{type(exc).__name__}: {exc}"
     t_prof = time.perf_counter() - t0
     if save and rank == 0:
         (save / "profile_resident.txt").write_text(profile)
