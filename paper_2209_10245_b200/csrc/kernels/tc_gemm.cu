@@ -1217,23 +1217,27 @@ namespace {
 // 1024^3: 16 tiles for 74 pairs) the single-SM kernel with 128 x 128 tiles
 // spreads the work over 4x as many CTAs. POAS_TC_KERNEL = 2cta512 | 2cta |
 // 1cta (128 x 256) | 1cta128 overrides.
-enum class TcVariant { pair512x2, pair256x2, pair512, pair, single256, single128 };
+enum class TcVariant { pair512x2, pair256x2, pair512, pair, single256, single128, single64 };
 
 TcVariant choose_variant(int64_t M, int64_t N, int64_t K, int budget) {
   if (const char* v = std::getenv("POAS_TC_KERNEL")) {
     const std::string s(v);
     if (s == "1cta") return TcVariant::single256;
     if (s == "1cta128") return TcVariant::single128;
+    if (s == "1cta64") return TcVariant::single64;
     if (s == "2cta") return TcVariant::pair;
     if (s == "2cta512") return TcVariant::pair512;
     if (s == "2cta512x2") return TcVariant::pair512x2;
     if (s == "2cta256x2") return TcVariant::pair256x2;
   }
-  // Single-SM 128 x 128 tiles only when the pairs would be mostly idle (at
-  // most a quarter busy): measured (profiles/r01_small_variants) 1024^3
-  // 16.1 -> 12.4 us, but 2048^3 22.3 -> 29.6 us (64 pair tiles for 74 pairs).
-  const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  if (4 * pair_tiles <= budget / 2) return TcVariant::single128;
+  // Single-SM tiles when the grid of 128 x 128 tiles fits in one wave of the
+  // budget: 128 x 64 tiles when even those would leave half the SMs idle
+  // (1024^3: 242 vs 213 TFLOP/s, cuBLAS 242-247), else 128 x 128 (1536^3:
+  // 497 vs 454 for pair tiles); pair tiles from there on (2048^3: 906 vs
+  // 682), profiles/r02_n64.
+  const int64_t t128 = ((M + 127) / 128) * ((N + 127) / 128);
+  if (2 * t128 <= budget) return TcVariant::single64;
+  if (t128 <= budget) return TcVariant::single128;
   // 256 x 512 tiles need two waves of them, and a long K: their
   // accumulator drain is exposed once per tile (4096^3: 1343 -> 1190
   // TFLOP/s with wide tiles; 8192^3 and up they win, profiles/r02_sizes4)
@@ -1245,6 +1249,7 @@ const char* variant_name(TcVariant v) {
   switch (v) {
     case TcVariant::single256: return "tc_gemm_kernel";
     case TcVariant::single128: return "tc_gemm_kernel_n128";
+    case TcVariant::single64: return "tc_gemm_kernel_n64";
     case TcVariant::pair512: return "tc_gemm_2cta_kernel<512>";
     case TcVariant::pair512x2: return "tc_gemm_2cta_kernel<512,2>";
     case TcVariant::pair256x2: return "tc_gemm_2cta_kernel<256,2>";
@@ -1372,6 +1377,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   std::call_once(once, [] {
     attr_err = cudaFuncSetAttribute(tc_gemm_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(Tile1<256, 4>::kSmem));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_kernel<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Tile1<64, 8>::kSmem));
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(tc_gemm_kernel<128, 6>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1538,7 +1546,7 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);
     return e;
   }
-  const int bn = variant == TcVariant::single128 ? 128 : 256;
+  const int bn = variant == TcVariant::single64 ? 64 : variant == TcVariant::single128 ? 128 : 256;
   args.tiles_m = static_cast<int>((M + kBM - 1) / kBM);
   args.tiles_n = static_cast<int>((N + bn - 1) / bn);
   args.idesc = idesc_f16(t == AbType::bf16, kBM, bn, false, true);
@@ -1546,6 +1554,8 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   int grid = budget;
   const int tiles = args.tiles_m * args.tiles_n;
   if (grid > tiles) grid = tiles;
+  if (bn == 64)
+    return launch_pdl(tc_gemm_kernel<64, 8>, grid, kThreads, Tile1<64, 8>::kSmem, stream, 1, ma, mb, args);
   if (bn == 128)
     return launch_pdl(tc_gemm_kernel<128, 6>, grid, kThreads, Tile1<128, 6>::kSmem, stream, 1, ma, mb, args);
   return launch_pdl(tc_gemm_kernel<256, 4>, grid, kThreads, Tile1<256, 4>::kSmem, stream, 1, ma, mb, args);

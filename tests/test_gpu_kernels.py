@@ -244,7 +244,7 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 
 
 # (variant, epilogue): the single-SM kernels have one epilogue
-_TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("2cta", "tma"), ("2cta", "direct"),
+_TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("1cta64", "tma"), ("2cta", "tma"), ("2cta", "direct"),
                 ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512x2", "tma"),
                 ("2cta512x2", "direct"), ("2cta256x2", "tma"), ("2cta256x2", "direct")]
 
@@ -448,17 +448,19 @@ def test_tc_gemm_panels_waits_for_flags(torch_cuda, poas, monkeypatch, variant):
 
 
 def test_tc_variant_choice(torch_cuda, poas, monkeypatch):
-    """256 x 512 pair tiles from two waves of them, 256 x 256 pair tiles
-    below, 128 x 128 single-SM tiles when at most a quarter of the pairs
-    would be busy; the env override wins."""
+    """256 x 512 pair tiles from two waves of them (and K >= 6144), 256 x 256
+    pair tiles below, single-SM tiles when the grid of 128 x 128 tiles fits
+    in one wave (128 x 64 when it fills at most half); the env override
+    wins."""
     monkeypatch.delenv("POAS_TC_KERNEL", raising=False)
     assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel<512>"
     assert poas.tc_kernel_name(65536, 8192, 8192) == "tc_gemm_2cta_kernel<512>"
     assert poas.tc_kernel_name(8192, 8192, 8192) == "tc_gemm_2cta_kernel<512>"
     assert poas.tc_kernel_name(4096, 4096, 4096) == "tc_gemm_2cta_kernel<256>"
-    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_kernel_n128"
+    assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_kernel_n64"
+    assert poas.tc_kernel_name(1536, 1536, 1536) == "tc_gemm_kernel_n128"
     assert poas.tc_kernel_name(2048, 2048, 2048) == "tc_gemm_2cta_kernel<256>"
-    assert poas.tc_kernel_name(256, 4096, 16384) == "tc_gemm_kernel_n128"
+    assert poas.tc_kernel_name(256, 4096, 16384) == "tc_gemm_kernel_n64"
     monkeypatch.setenv("POAS_TC_KERNEL", "2cta")
     assert poas.tc_kernel_name(1024, 1024, 1024) == "tc_gemm_2cta_kernel<256>"
     assert poas.tc_kernel_name(16384, 16384, 16384) == "tc_gemm_2cta_kernel<256>"
