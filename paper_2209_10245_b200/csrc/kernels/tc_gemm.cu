@@ -512,19 +512,22 @@ constexpr int kGroupM2 = 8;  // default raster group: 8 x 256 rows
 // 16-column fp32 boxes with 64-byte swizzled rows (2 x 2 KB); W = 512 one
 // 32-row x 32-column box with 128-byte swizzled rows (4 KB).
 
-template <int W>
+template <int W, int EPI = 0>
 struct Pair {
   static_assert(W == 256 || W == 512, "pair tile width");
   static constexpr int kHalves = W / 256;
   static constexpr int kStages = W == 256 ? 6 : 4;
   static constexpr int kBBytes = (W / 2) * kBK * 2;  // this CTA's W/2 columns of B
   static constexpr int kStageBytes = k2ABytes + kBBytes;
-  // epilogue warps: 4 (one per TMEM lane quarter) for 256 x 256 tiles,
-  // whose drain hides behind the other accumulator; 8 (two per quarter,
-  // alternate 32-column chunks) for 256 x 512 tiles, whose drain is exposed
-  static constexpr int kEpiWarps = W == 512 ? 8 : 4;
+  // epilogue warps: 8 (two per TMEM lane quarter, alternate 32-column
+  // chunks: twice the warps read TMEM and issue stores) where the drain is
+  // exposed -- every 256 x 512 tile, and 256 x 256 tiles when the GEMM is one
+  // wave of them (2048^3: drain 4.4 -> 3.45 us, +2%); 4 (one per quarter)
+  // for 256 x 256 tiles whose drain hides behind the other accumulator
+  // (there 8 cost 0.6-1%: 4096^3 1318 -> 1305 TFLOP/s, profiles/r02_epi256)
+  static constexpr int kEpiWarps = EPI ? EPI : (W == 512 ? 8 : 4);
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
-  static constexpr int kStagingBytes = W == 256 ? 4 * 2 * 2048 : kEpiWarps * 4096;
+  static constexpr int kStagingBytes = kEpiWarps * 4096;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kStagingBytes + 256;
   static_assert(kSmem <= 232448, "shared memory per CTA");
 };
@@ -540,12 +543,12 @@ struct Pair {
 // compiled in (__cluster_dims__): launching the same kernel with a runtime
 // cluster-dimension attribute instead ran the 256 x 256 tiles 10-15% slower
 // (profiles/r02_sizes).
-template <int W, int PAIRS>
-__global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kThreads, 1)
+template <int W, int PAIRS, int EPI = 0>
+__global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>::kThreads, 1)
     tc_gemm_2cta_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
-  using P = Pair<W>;
+  using P = Pair<W, EPI>;
   constexpr int k2StagingBytes = P::kStagingBytes;
   constexpr int k2Stages = P::kStages;
   constexpr int k2BBytes = P::kBBytes;
@@ -869,7 +872,9 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kTh
           // single-tile GEMM sooner than the wide tiles' 8 KB steps, which
           // wait for the previous step's stores: 2048^3 922 vs 817 TFLOP/s,
           // profiles/r02_sizes.)
-          uint8_t* boxes = s_c + quad * 4096;
+          constexpr int S = P::kEpiWarps / 4;  // warps per TMEM lane quarter
+          constexpr int kChunks = 8 / S;         // this warp's 32-column chunks
+          uint8_t* boxes = s_c + (warp - 2) * 4096;
           const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                  static_cast<uint32_t>(acc * 256);
           auto put_box = [&](const uint32_t* w, int c) {  // 16 columns, box (c & 1)
@@ -895,24 +900,26 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kTh
             }
           };
           uint32_t va[32], vb[32];
-          tmem_ld_32x32b_x32(taddr, va);
+          tmem_ld_32x32b_x32(taddr + sub * 32, va);
           tmem_wait_ld();
 #pragma unroll 1
-          for (int c = 0; c < 8; c += 2) {
-            tmem_ld_32x32b_x32(taddr + (c + 1) * 32, vb);
+          for (int i = 0; i < kChunks; i += 2) {  // chunks sub + S * i
+            const int c = sub + S * i;
+            tmem_ld_32x32b_x32(taddr + (c + S) * 32, vb);
             put_box(va, 2 * c);
             put_box(va + 16, 2 * c + 1);
             tmem_wait_ld();
-            if (c + 2 < 8) {
-              tmem_ld_32x32b_x32(taddr + (c + 2) * 32, va);
-            } else {  // all 256 columns are in registers: free the accumulator
+            if (i + 2 < kChunks) {
+              tmem_ld_32x32b_x32(taddr + (c + 2 * S) * 32, va);
+            } else {  // this warp's columns are in registers: free the accumulator
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(&acc_empty[acc], pair_leader);
-              if (args.trace && quad == 0 && lane == 0) trace_add(args, 12, gtimer() - te0);
+              if (args.trace && quad == 0 && sub == 0 && lane == 0)
+                trace_add(args, 12, gtimer() - te0);
             }
-            put_box(vb, 2 * c + 2);
-            put_box(vb + 16, 2 * c + 3);
+            put_box(vb, 2 * (c + S));
+            put_box(vb + 16, 2 * (c + S) + 1);
             tmem_wait_ld();
           }
         } else {
@@ -981,7 +988,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kTh
           bulk_wait_all();
           fence_proxy_async_global();
           __threadfence();
-          const int target = args.stream_epoch * blk_tiles * 8;
+          const int target = args.stream_epoch * blk_tiles * 2 * P::kEpiWarps;
           if (atomicAdd(args.block_count + blk, 1) + 1 == target) {
             __threadfence();
             atomicExch(args.block_flags + blk, args.stream_epoch);
@@ -1042,7 +1049,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W>::kTh
         __threadfence();
         __syncwarp();
         if (lane == 0) {
-          const int target = args.stream_epoch * blk_tiles * 8;
+          const int target = args.stream_epoch * blk_tiles * 2 * P::kEpiWarps;
           if (atomicAdd(args.block_count + blk, 1) + 1 == target) {
             __threadfence();
             atomicExch(args.block_flags + blk, args.stream_epoch);
@@ -1389,6 +1396,10 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Pair<256>::kSmem));
     if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<256, 1, 8>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Pair<256, 8>::kSmem));
+    if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(tc_gemm_2cta_kernel<512, 1>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Pair<512>::kSmem));
@@ -1526,6 +1537,10 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     } else if (pairs > tiles) {
       pairs = tiles;
     }
+    // 256 x 256 tiles: 8 epilogue warps when the GEMM is one wave of tiles
+    // (its drain is all exposed); POAS_TC_EPI=4|8 overrides
+    const char* epi_env = std::getenv("POAS_TC_EPI");
+    const bool epi8 = epi_env ? std::atoi(epi_env) == 8 : tiles <= pairs;
     static unsigned long long* trace_buf = nullptr;
     const bool trace = std::getenv("POAS_TC_TRACE") != nullptr;
     if (trace) {
@@ -1541,6 +1556,8 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
                                 stream, 1, ma, mb, mc, args)
         : wide     ? launch_pdl(tc_gemm_2cta_kernel<512, 1>, 2 * pairs, Pair<512>::kThreads, Pair<512>::kSmem,
                                 stream, 1, ma, mb, mc, args)
+        : epi8     ? launch_pdl(tc_gemm_2cta_kernel<256, 1, 8>, 2 * pairs, Pair<256, 8>::kThreads,
+                                Pair<256, 8>::kSmem, stream, 1, ma, mb, mc, args)
                    : launch_pdl(tc_gemm_2cta_kernel<256, 1>, 2 * pairs, Pair<256>::kThreads, Pair<256>::kSmem,
                                 stream, 1, ma, mb, mc, args);
     if (trace) print_trace(trace_buf, 2 * pairs, stream, M, N, K);

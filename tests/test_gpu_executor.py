@@ -454,7 +454,8 @@ def test_b_panels_with_flags_one_launch(torch_cuda, poas):
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("grid", ["aligned", "ragged", "aligned_n_not4", "aligned_1sm"])
 @pytest.mark.parametrize("link", ["bf16", "fp32"])
-def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
+@pytest.mark.parametrize("epi", [None, "8"])
+def test_overlapped_grid_ragged(torch_cuda, poas, monkeypatch, link, grid, epi):
     """Overlapped execution of a hand-made 3 x 3 grid of blocks (ragged row
     parts and column panels, the tiles of an "overlap" schedule): A parts
     and B panels interleaved host->device, each block's C back as soon as it
@@ -464,8 +465,15 @@ def test_overlapped_grid_ragged(torch_cuda, poas, link, grid):
     "aligned_n_not4": C's pitch (n = 1002) is not a TMA pitch, so the
     streamed launch writes C with direct stores and must still raise every
     block flag; "aligned_1sm": a one-SM budget cannot run the pair kernel, so
-    the streamed launch is not used (both used to hang)."""
+    the streamed launch is not used (both used to hang).
+    epi = "8": the streamed launch with 8 epilogue warps per CTA (16 block
+    arrivals per tile)."""
     import oracle
+
+    if epi:
+        if link != "bf16":
+            pytest.skip("the epilogue-warp choice is the streamed launch's")
+        monkeypatch.setenv("POAS_TC_EPI", epi)
 
     torch = torch_cuda
     elem = 2 if link == "bf16" else 4

@@ -245,6 +245,7 @@ def test_tc_kernel_forward_k_order(torch_cuda, poas, monkeypatch, variant):
 
 # (variant, epilogue): the single-SM kernels have one epilogue
 _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("1cta64", "tma"), ("2cta", "tma"), ("2cta", "direct"),
+                ("2cta", "tma-epi8"), ("2cta", "direct-epi8"), ("2cta", "tma-epi4"),
                 ("2cta512", "tma"), ("2cta512", "direct"), ("2cta512x2", "tma"),
                 ("2cta512x2", "direct"), ("2cta256x2", "tma"), ("2cta256x2", "direct")]
 
@@ -253,8 +254,8 @@ _TC_VARIANTS = [("1cta", "tma"), ("1cta128", "tma"), ("1cta64", "tma"), ("2cta",
 @pytest.mark.parametrize("variant,epilogue", _TC_VARIANTS)
 @pytest.mark.parametrize("shape", [(300, 520, 200), (256, 256, 64), (1000, 1000, 1000), (2049, 777, 136)])
 def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched, epilogue):
-    """The tensor kernels (single-SM 128x256 / 128x128, CTA-pair 256x256 and
-    256x512) under
+    """The tensor kernels (single-SM 128x256 / 128x128 / 128x64, CTA-pair
+    256x256 with 4 or 8 epilogue warps and 256x512) under
     every tile scheduler and both pair-kernel epilogues (TMA store; direct
     register stores) agree with the oracle, including partial pair tiles,
     odd SM budgets and a C pitch TMA cannot map (n = 777)."""
@@ -263,8 +264,11 @@ def test_tc_kernel_variants(torch_cuda, poas, monkeypatch, variant, shape, sched
     torch = torch_cuda
     monkeypatch.setenv("POAS_TC_KERNEL", variant)
     monkeypatch.setenv("POAS_TC_SCHED", sched)
+    epilogue, _, epi = epilogue.partition("-epi")  # the 256x256 kernel's epilogue warps
     if epilogue != "tma":
         monkeypatch.setenv("POAS_TC_EPILOGUE", epilogue)
+    if epi:
+        monkeypatch.setenv("POAS_TC_EPI", epi)
     m, n, k = shape
     A, B = oracle.fill_uniform(m, k, 31), oracle.fill_uniform(k, n, 32)
     ldb = (n + 7) // 8 * 8
