@@ -11,6 +11,8 @@
 //     fills TMEM and its halves are released separately, 8 epilogue warps),
 //     W = 256 (6 x 32 KB stages, double-buffered accumulator, 4 epilogue
 //     warps); PAIRS = 2 puts two pairs in a cluster sharing B by multicast.
+//     Opt-in (POAS_TC_SPLIT=1): a last wave of at most half a wave of tiles
+//     runs as two K-halves (store, then add-reduce after a ready flag).
 //   tc_gemm_kernel<BN, STAGES>     one SM, 128 x BN tiles (small GEMMs).
 // Roles: warp 0 lane 0 TMA producer (A K-major, B N-major, 128B-swizzled
 // ring), warp 1 lane 0 MMA issuer (tcgen05.mma .kind::f16, fp32 accumulator
@@ -85,7 +87,32 @@ struct TcArgs {
   int* block_count;
   int* block_flags;
   int stream_epoch;
+  // Last-wave K split (pair kernel, dynamic scheduler): tiles [split_base,
+  // tiles) run as two K-halves, work units split_base + 2j + part; part 0
+  // sweeps k-blocks [0, split_kb) and stores, part 1 sweeps the rest and
+  // add-reduces once part 0's boxes are in global memory. split_cnt: per
+  // split tile {part-0 warps done, ready flag, part-1 warps released, -},
+  // all zero again when the launch ends (so graph replays need no reset).
+  int split_base;
+  int split_kb;
+  int* split_cnt;
 };
+
+// Work unit u -> tile, k-block range [kb0, kb1) and split part (-1: whole tile).
+__device__ __forceinline__ int unit_tile(const TcArgs& a, int u, int k_blocks, int& kb0, int& kb1,
+                                         int& part) {
+  if (!a.split_cnt || u < a.split_base) {
+    kb0 = 0;
+    kb1 = k_blocks;
+    part = -1;
+    return u;
+  }
+  const int v = u - a.split_base;
+  part = v & 1;
+  kb0 = part ? a.split_kb : 0;
+  kb1 = part ? k_blocks : a.split_kb;
+  return a.split_base + (v >> 1);
+}
 
 // Spin (acquire, with backoff) until *flag >= epoch; traps after 10 s so a
 // missing signal fails the launch instead of hanging the GPU.
@@ -615,7 +642,9 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
   griddep_wait();
   if (threadIdx.x == 0) trace_stamp(args, 1);
 
-  const int total = args.tiles_m * args.tiles_n;
+  // work units: one per tile, two per last-wave split tile (unit_tile)
+  const int total = args.tiles_m * args.tiles_n +
+                    (args.split_cnt ? args.tiles_m * args.tiles_n - args.split_base : 0);
   const int k_blocks = (args.K + kBK - 1) / kBK;
   const int first = static_cast<int>(cluster_id_x());
   const int step = static_cast<int>(num_clusters_x());
@@ -643,6 +672,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
         ++wave;
         int t_next = 0;  // claimed once this tile's first loads are out
         int mb, nb, pnl, nbl;
+        int kb0 = 0, kb1 = k_blocks, part = -1;
         if (args.sblocks) {
           int blk;
           const int4 d = tile_coords_stream(args, t, mb, nb, blk);
@@ -658,7 +688,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
             }
           }
         } else {
-          tile_coords_panel(args, t, mb, nb, pnl, nbl);
+          tile_coords_panel(args, unit_tile(args, t, k_blocks, kb0, kb1, part), mb, nb, pnl, nbl);
         }
         if (args.panel_flags && (pnl >= 64 || !(panels_seen & (1ull << pnl)))) {
           wait_panel_flag(args.panel_flags + pnl, args.panel_epoch);
@@ -669,9 +699,9 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
         const int col0 = nbl * W + static_cast<int>(prank) * 128;  // inside the panel
         // K serpentine: the tiles of a wave that follows one sweeping K
         // forwards start where it ended, on the K-slices still in L2
-        const bool rev = args.kserp && ((t / step) & 1);
-        for (int kb = 0; kb < k_blocks; ++kb) {
-          const int kc = (rev ? k_blocks - 1 - kb : kb) * kBK;
+        const bool rev = args.kserp && part < 0 && ((t / step) & 1);
+        for (int kb = 0; kb < kb1 - kb0; ++kb) {
+          const int kc = (rev ? k_blocks - 1 - kb : kb0 + kb) * kBK;
           mbar_wait(&empty[stage], phase ^ 1);
           if (wave == 1 && kb == 0) trace_stamp(args, 9);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
@@ -759,7 +789,9 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
         // stage is released once both halves have consumed it)
         bool h1 = W == 256;
         int npend = 0, pend_kb = 0, pend_stage = 0;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int kb0, kb1, part;
+        unit_tile(args, t, k_blocks, kb0, kb1, part);
+        for (int kb = 0; kb < kb1 - kb0; ++kb) {  // local k-block: the first one overwrites D
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (!traced) {
@@ -845,14 +877,30 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
     for (int t = first < total ? first : -1; t >= 0; t = next_tile()) {
       int mb, nb;
       int pnl_unused, nbl_unused, blk = 0, blk_tiles = 0;
+      int kb0, kb1, part = -1;
       if (args.sblocks) {
         const int4 d = tile_coords_stream(args, t, mb, nb, blk);
         blk_tiles = (d.x >> 16) * (d.y >> 16);
       } else {
-        tile_coords_panel(args, t, mb, nb, pnl_unused, nbl_unused);
+        tile_coords_panel(args, unit_tile(args, t, k_blocks, kb0, kb1, part), mb, nb, pnl_unused,
+                          nbl_unused);
       }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
+      if (part == 1) {
+        // the tile's other K-half stores first; this half add-reduces onto it
+        // (a fixed order: C is the same for every run of this configuration)
+        int* sc = args.split_cnt + 4 * (unit_tile(args, t, k_blocks, kb0, kb1, part) - args.split_base);
+        if (lane == 0) {
+          wait_panel_flag(sc + 1, 1);
+          // the last part-1 warp past the flag clears it for the next launch
+          if (atomicAdd(sc + 2, 8 / P::kEpiWarps) + 8 / P::kEpiWarps == 16) {
+            atomicExch(sc + 2, 0);
+            atomicExch(sc + 1, 0);
+          }
+        }
+        __syncwarp();
+      }
       const unsigned long long te0 = args.trace ? gtimer() : 0;
       if (quad == 0 && sub == 0 && lane == 0 && !epi_traced) {
         trace_stamp(args, 5);
@@ -890,7 +938,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
             __syncwarp();
             if (lane == 0 && !args.epi_skip) {
               const int col0 = nb * W + c * 16;
-              if (args.accumulate)
+              if (args.accumulate || part == 1)
                 tma_reduce_add_2d(&map_c, box, col0, row_base);
               else if (args.hint_c != kEvictNormal)
                 tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
@@ -946,7 +994,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
             __syncwarp();
             if (lane == 0 && !args.epi_skip) {
               const int col0 = nb * W + c * 32;
-              if (args.accumulate)
+              if (args.accumulate || part == 1)
                 tma_reduce_add_2d(&map_c, box, col0, row_base);
               else if (args.hint_c != kEvictNormal)
                 tma_store_2d_hint(&map_c, box, col0, row_base, args.hint_c);
@@ -992,6 +1040,19 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(Pair<W, EPI>
           if (atomicAdd(args.block_count + blk, 1) + 1 == target) {
             __threadfence();
             atomicExch(args.block_flags + blk, args.stream_epoch);
+          }
+        }
+        if (part == 0 && lane == 0) {
+          // this warp's boxes of the first K-half are in global memory: the
+          // tile's last warp (16 shares per pair tile) raises its ready flag
+          bulk_wait_all();
+          fence_proxy_async_global();
+          __threadfence();
+          int* sc = args.split_cnt + 4 * (unit_tile(args, t, k_blocks, kb0, kb1, part) - args.split_base);
+          if (atomicAdd(sc, 8 / P::kEpiWarps) + 8 / P::kEpiWarps == 16) {
+            atomicExch(sc, 0);
+            __threadfence();
+            atomicExch(sc + 1, 1);
           }
         }
         if (W == 512 || (acc ^= 1) == 0) acc_phase ^= 1;
@@ -1186,6 +1247,28 @@ namespace {
 // streams may run at the same time and never do (a shared
 // per-device ring could hand two concurrent launches the same slot once one
 // stream had queued more launches than the ring had slots).
+// Last-wave split counters (TcArgs::split_cnt), 4 ints per split tile, one
+// zeroed block per (device, stream); every launch leaves them zero.
+constexpr int kSplitMax = 128;
+int* split_counters(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int*> by_stream;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(dev, stream);
+  if (auto it = by_stream.find(key); it != by_stream.end()) return it->second;
+  int* p = nullptr;
+  const size_t bytes = kSplitMax * 4 * sizeof(int);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(p);
+    return nullptr;
+  }
+  by_stream.emplace(key, p);
+  return p;
+}
+
 int* next_tile_counter(cudaStream_t stream) {
   constexpr int kBlock = 64;  // counters per allocation, 128 B apart
   static std::mutex mu;
@@ -1272,7 +1355,7 @@ const char* variant_name(TcVariant v) {
 int max_active_clusters_x2();
 
 cudaError_t tc_prepare_stream(cudaStream_t stream) {
-  return next_tile_counter(stream) ? cudaSuccess : cudaErrorMemoryAllocation;
+  return next_tile_counter(stream) && split_counters(stream) ? cudaSuccess : cudaErrorMemoryAllocation;
 }
 
 const char* tc_gemm_kernel_name(int64_t M, int64_t N, int64_t K) {
@@ -1492,6 +1575,9 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
   args.block_count = nullptr;
   args.block_flags = nullptr;
   args.stream_epoch = 0;
+  args.split_base = 0;
+  args.split_kb = 0;
+  args.split_cnt = nullptr;
   if (ss) {
     args.sblocks = reinterpret_cast<const int4*>(ss->blocks);
     args.nsblocks = ss->nblocks;
@@ -1541,6 +1627,31 @@ cudaError_t tc_gemm_impl(AbType t, int64_t M, int64_t N, int64_t K, const void* 
     // (its drain is all exposed); POAS_TC_EPI=4|8 overrides
     const char* epi_env = std::getenv("POAS_TC_EPI");
     const bool epi8 = epi_env ? std::atoi(epi_env) == 8 : tiles <= pairs;
+    // Last-wave K split (opt-in, POAS_TC_SPLIT=1): when the last wave holds
+    // at most half a wave of tiles, those tiles run as two K-halves on
+    // twice the pairs (4096^3 with 256 x 256 tiles: 256 tiles on 74 pairs,
+    // the last 34 as 68 halves). Measured, it does not pay: 4096^3-5120^3
+    // within +-0.5%, 2560^3 -6% (profiles/r02_split) -- a part-filled last
+    // wave already runs faster per tile than a full one. Dynamic scheduler
+    // only (a half's partner is claimed no later than itself), TMA-store
+    // epilogue, one pair per cluster, no panel flags / streamed blocks; never
+    // in the deterministic mode (POAS_TC_KSERP=0).
+    {
+      const int all_pairs = budget / 2;
+      const int rem = tiles % all_pairs;
+      const int kbl = static_cast<int>((K + kBK - 1) / kBK);
+      const char* split_env = std::getenv("POAS_TC_SPLIT");
+      const bool split_on = split_env && std::string(split_env) == "1";
+      if (split_on && args.kserp && !x2 && args.tma_store && !ss && !ps && P == 1 &&
+          args.tile_counter && !args.wave_sync && kbl >= 8 && rem > 0 && 2 * rem <= all_pairs &&
+          rem <= kSplitMax) {
+        args.split_cnt = split_counters(stream);
+        if (!args.split_cnt) return cudaErrorMemoryAllocation;
+        args.split_base = tiles - rem;
+        args.split_kb = kbl / 2;
+        pairs = std::min(all_pairs, tiles + rem);
+      }
+    }
     static unsigned long long* trace_buf = nullptr;
     const bool trace = std::getenv("POAS_TC_TRACE") != nullptr;
     if (trace) {

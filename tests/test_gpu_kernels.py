@@ -511,3 +511,51 @@ def test_tc_wide_pair_half_release(torch_cuda, poas, monkeypatch, shape, ctas, a
         torch.cuda.synchronize()
         got = c.cpu().numpy() - (1.0 if accumulate else 0.0)
         assert oracle.rel_frobenius(got, ref) <= TOL, (shape, ctas)
+
+
+# (shape, SM budget) where the last wave of pair tiles is at most half a
+# wave, so its tiles run as two K-halves (TcArgs::split_*): 1000^2 x 1000 on
+# 5 pairs (16 tiles: 15 whole + 1 split), 1024^2 x 768 on 32 pairs (all 16
+# tiles split: 32 halves), 4096^2 x 512 on the whole chip (256 tiles, the
+# last 34 split on 74 pairs), and a ragged K tail (K = 1000: 16 k-blocks,
+# the last one partial, in part 1; 24 tiles on 7 pairs).
+_SPLIT_CASES = [((1000, 1000, 1000), 10), ((1024, 1024, 768), 64), ((4096, 4096, 512), 0),
+                ((777, 1304, 1000), 14)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["2cta", "2cta512"])
+@pytest.mark.parametrize("accumulate", [False, True])
+@pytest.mark.parametrize("case", _SPLIT_CASES)
+def test_tc_last_wave_split(torch_cuda, poas, monkeypatch, variant, accumulate, case):
+    """Last-wave K split: the split tiles' first K-half stores, the second
+    add-reduces after the first's ready flag. C matches the oracle (plain and
+    accumulating), equals itself bitwise over repeated launches (the ready
+    flags and counters are left zero by every launch) and stays within the
+    tolerance of the unsplit kernel (POAS_TC_SPLIT=0)."""
+    import oracle
+
+    torch = torch_cuda
+    (m, n, k), ctas = case
+    monkeypatch.setenv("POAS_TC_KERNEL", variant)
+    monkeypatch.setenv("POAS_TC_SCHED", "dynamic")
+    A, B = oracle.fill_uniform(m, k, 51), oracle.fill_uniform(k, n, 52)
+    a = torch.from_numpy(A).cuda().bfloat16()
+    b = torch.from_numpy(B).cuda().bfloat16()
+    ref = oracle.gemm_rows_f64(A, B, 2)
+    c0 = np.random.default_rng(5).uniform(-1, 1, (m, n)).astype(np.float32) if accumulate else None
+    outs = []
+    for split in ("1", "1", "1", "0"):
+        monkeypatch.setenv("POAS_TC_SPLIT", split)
+        c = torch.from_numpy(c0).cuda() if accumulate else torch.full((m, n), float("nan"), device="cuda")
+        for _ in range(2 if split == "1" else 1):  # back-to-back launches on one stream
+            if accumulate:
+                c.copy_(torch.from_numpy(c0))
+            poas.tc_gemm(2, m, n, k, a.data_ptr(), k, b.data_ptr(), n, c.data_ptr(), n,
+                         accumulate=accumulate, num_ctas=ctas)
+        torch.cuda.synchronize()
+        got = c.cpu().numpy()
+        want = ref + (c0.astype(np.float64) if accumulate else 0)
+        assert oracle.rel_frobenius(got, want) <= TOL, (variant, split, case)
+        outs.append(got)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
