@@ -527,9 +527,18 @@ def main():
                     help="dynamic scheduling of the resident run: EWMA weight of the newest round")
     ap.add_argument("--warmup-seconds", type=float, default=1.0,
                     help="minimum length of the dynamic warm-up (steady power-capped state)")
-    ap.add_argument("--preroll", type=int, default=20,
-                    help="ms of back-to-back launches before each timed GPU-unit probe (0: cold probes)")
-    ap.add_argument("--probe-warmup", type=float, default=0.5,
+    # The resident steps run the tensor pipe continuously, in the deepest
+    # power-capped state: their probes follow 1.5 s of warm-up GEMMs and a
+    # 60 ms pre-roll each (C3 static error +5.1% -> +0.9%, C4 +8.1% -> +3.6%,
+    # two alternating runs each, profiles/r02_probe_regime). The e2e step is
+    # link-bound (the tensor unit idles between parts) and the C2/C5 sweep
+    # keeps the regime its errors were validated in: 20 ms.
+    ap.add_argument("--preroll", type=int, default=60,
+                    help="ms of back-to-back launches before each timed GPU-unit probe of the resident "
+                         "run (0: cold probes)")
+    ap.add_argument("--preroll-e2e", type=int, default=20,
+                    help="pre-roll of the e2e run's probes and of the C2/C5 sweep (ms)")
+    ap.add_argument("--probe-warmup", type=float, default=1.5,
                     help="seconds of tensor-core GEMMs before profiling (0: probe a cool GPU)")
     ap.add_argument("--no-adapt", action="store_true",
                     help="warm-up runs the static plan (no model re-fit / re-plan)")
@@ -991,7 +1000,8 @@ def main():
 
         def run_e2e(tc_elem, overlap, pipeline=False):
             units_e2e = units_res.replace("elem=2:link=fused", f"elem={tc_elem}:link=pcie").replace(
-                "elem=4:link=hbm", "elem=4:link=pcie")
+                "elem=4:link=hbm", "elem=4:link=pcie").replace(f"preroll={args.preroll}",
+                                                               f"preroll={args.preroll_e2e}")
             if not args.no_e2e_cpu:
                 # With host-resident operands the host cores are a unit too:
                 # they compute rows in place while the GPU units' copies hold
@@ -1143,7 +1153,7 @@ def main():
             import sweep as sw
 
             t_sw = time.perf_counter()
-            c5 = sw.c5([1024, 2048, 4096, 8192, 16384, 32768], args.preroll)
+            c5 = sw.c5([1024, 2048, 4096, 8192, 16384, 32768], args.preroll_e2e)
             c2 = sw.c2()
             sv = sw.simt_vs_cublas_fp32()
             keep = ("n", "plan_rows", "static_error_pct", "poas_tflops", "adapted_error_pct",
