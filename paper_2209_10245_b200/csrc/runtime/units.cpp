@@ -316,11 +316,42 @@ double Unit::time_gemm(std::int64_t side) {
         one();
     if (est > 0.0) reps = std::clamp(static_cast<int>(100e-6 / est) + 1, 1, 32);
   }
-  cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
-  for (int i = 0; i < reps; ++i) one();
-  cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
-  cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
   float ms = 0.f;
+  if (reps > 1 && std::getenv("POAS_PROBE_GRAPH") == nullptr) {
+    // A short GEMM is timed as the executor runs a resident plan's steps:
+    // consecutive launches replayed as one CUDA graph (host launch cost off
+    // the GPU's critical path), >= ~1 ms of them. POAS_PROBE_GRAPH (set)
+    // times stream launches instead.
+    const int greps = std::clamp(static_cast<int>(reps * 10), 2, 512);
+    if (tensor) cuda_check(tc_prepare_stream(stream_), "tc_prepare_stream");
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+    try {
+      for (int i = 0; i < greps; ++i) one();
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(stream_, &graph), "cudaStreamEndCapture");
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(ie, "cudaGraphInstantiate (probe)");
+    cuda_check(cudaGraphLaunch(exec, stream_), "cudaGraphLaunch");  // upload, steady state
+    cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+    cuda_check(cudaGraphLaunch(exec, stream_), "cudaGraphLaunch");
+    cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+    const cudaError_t se = cudaEventSynchronize(ev1_);
+    cudaGraphExecDestroy(exec);
+    cuda_check(se, "cudaEventSynchronize");
+    reps = greps;
+  } else {
+    cuda_check(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+    for (int i = 0; i < reps; ++i) one();
+    cuda_check(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
+  }
   cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "cudaEventElapsedTime");
   last_probe_s_ = static_cast<double>(ms) * 1e-3 / reps;
   last_probe_side_ = side;

@@ -233,8 +233,11 @@ def c2(n=8192):
     io = io_for(n, d, with_host=True)
     ex = poas.Executor(units)
     # back to the sustained regime the probes were taken in (building the
-    # host operands above left the GPU idle for a second: boost clocks)
-    warm(0.2)
+    # host operands above left the GPU idle for a second: boost clocks). As
+    # long as the warm-up before the probes: after 0.2 s the static
+    # iteration's 5 steps still ran up to 12% faster than predicted
+    # (profiles/r02_graph_probe)
+    warm(0.5)
     dyn = ex.run_dynamic(profile, n, n, n, io, iterations=6, alpha=1.0, replan_threshold_pct=2.0,
                          policy=POLICY, repeats=5)  # the timed run's duty cycle
     sched = poas.schedule_roundtrip(json.dumps(dyn["schedule"]))
